@@ -1,0 +1,164 @@
+/*
+ * smol_preproc.h -- C ABI of the B200-native Smol preprocessing hot path.
+ *
+ * The operation (§2 "Breakdown of end-to-end DNN inference",
+ * P:366-382, steps 1-4; §6.4 "Partial and Low-Fidelity Decoding",
+ * P:1037-1148): for each image of a batch of entropy-decoded baseline JPEGs
+ * (Huffman decoding stays on the host), compute
+ *
+ *   dequantize -> 8x8 IDCT at scale 1, 1/2, 1/4 or 1/8 (reduced-fidelity
+ *   decode, reading R1) -> level shift / round / clamp to u8 (R3) -> 4:2:0
+ *   centred triangle chroma upsample (R2) -> exact JFIF YCbCr->RGB (R6) ->
+ *   bilinear resize (half-pixel, no antialias, R8) to the short-side or exact
+ *   size (R7/R11) -> centre crop or per-image ROI
+ *    -> float, /255, -mean, /std -> NCHW
+ *    fp32 or fp16.
+ *
+ * Only the coefficient blocks under the bilinear tap footprint of the crop are
+ * read and transformed (ROI decoding).  Decoded pixels never go
+ * to HBM: one fused sm_100a kernel per (scale, output dtype).
+ *
+ * Conventions
+ *  - Every function returns an int32_t smol_status and never throws.  On
+ *    failure smol_last_error() returns a thread-local message naming the
+ *    failing image index and field where applicable.
+ *  - Pointer kinds are stated per field: DEVICE = cudaMalloc'd memory of the
+ *    plan's device; HOST = ordinary host memory.  Coefficient pointers given
+ *    to smol_preproc_run_host may be host memory that was pinned with
+ *    cudaHostRegister / cudaMallocHost (read by the kernel over PCIe).
+ *  - The caller owns every buffer it passes and must keep it alive until the
+ *    work on `stream` has finished.  The plan owns its own device scratch.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    Work is asynchronous; kernel faults surface at the caller's next sync.
+ *  - One run per plan may be in flight per stream; plans are not thread-safe.
+ */
+#ifndef SMOL_PREPROC_H
+#define SMOL_PREPROC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMOL_ABI_VERSION 1
+
+typedef enum {
+  SMOL_OK = 0,
+  SMOL_ERR_INVALID = 1,      /* bad argument / descriptor field             */
+  SMOL_ERR_UNSUPPORTED = 2,  /* valid but not implemented (e.g. 4:4:4)      */
+  SMOL_ERR_CUDA = 3,         /* CUDA runtime error (message has the name)   */
+  SMOL_ERR_NOMEM = 4,        /* device/host allocation failed               */
+  SMOL_ERR_CAPACITY = 5      /* n_images > plan capacity, or tile too large */
+} smol_status;
+
+typedef enum { SMOL_OUT_F32_NCHW = 0, SMOL_OUT_F16_NCHW = 1 } smol_out_dtype;
+typedef enum { SMOL_RESIZE_SHORT_SIDE = 0, SMOL_RESIZE_EXACT = 1 } smol_resize_mode;
+typedef enum { SMOL_LAYOUT_DENSE64 = 0 } smol_coef_layout;
+
+/* Plan parameters (fixed for the plan's lifetime). */
+typedef struct {
+  int32_t scale_denom;      /* k in {1,2,4,8}: decode at scale 1/k (R1)            */
+  int32_t resize_mode;      /* smol_resize_mode                                    */
+  int32_t resize_short;     /* SHORT_SIDE: short edge -> resize_short, long edge
+                               -> floor(resize_short*long/short) (torchvision)   */
+  int32_t resize_w, resize_h;  /* EXACT: resized size                            */
+  int32_t crop_w, crop_h;   /* centre crop in resized coordinates; 0,0 = none
+                               (required for SHORT_SIDE: fixed output size)      */
+  float mean[3], std[3];    /* RGB; y = (x/255 - mean)/std, std > 0              */
+  int32_t out_dtype;        /* smol_out_dtype                                      */
+  int32_t layout;           /* smol_coef_layout                                    */
+  int32_t tile_rows;        /* output rows per CTA tile; 0 = automatic           */
+} smol_preproc_params;
+
+/* One entropy-decoded 4:2:0 image. */
+typedef struct {
+  int32_t width, height;           /* SOF size in pixels, > 0                        */
+  int32_t subsampling;             /* 420 (anything else: SMOL_ERR_UNSUPPORTED)      */
+  int32_t qtable[3];               /* Y, Cb, Cr index into batch qtables             */
+  const int16_t* coef[3];          /* DEVICE (or pinned HOST for run_host):
+                                      [blocks_h][blocks_w][64] int16, natural
+                                      (row-major v*8+u) order, absolute DC;
+                                      16-byte aligned                               */
+  int32_t blocks_w[3], blocks_h[3];/* >= ceil(W/8), ceil(H/8) luma;
+                                      >= ceil(W/16), ceil(H/16) chroma              */
+  int32_t row_stride_bytes[3];     /* >= blocks_w*128, multiple of 16                 */
+  int32_t roi_left, roi_top;       /* optional ROI: crop window origin in resized
+                                      coordinates (window = crop_w x crop_h);
+                                      -1,-1 = centre crop                            */
+} smol_image_desc;
+
+typedef struct {
+  int32_t n_images;                /* 0 is allowed (no-op)                           */
+  const smol_image_desc* images;   /* HOST array of n_images                          */
+  const uint16_t* qtables;         /* DEVICE [n_qtables][64] natural order, 1..65535 */
+  int32_t n_qtables;               /* 1..4                                            */
+} smol_batch_desc;
+
+typedef struct smol_preproc_plan smol_preproc_plan_t;   /* opaque */
+
+/* Geometry of one image under a plan (test/introspection; host only). */
+typedef struct {
+  int32_t Wd, Hd;               /* decoded luma size at scale 1/k (R4)          */
+  int32_t Wc, Hc;               /* decoded chroma size                          */
+  int32_t Wr, Hr;               /* resized size                                  */
+  int32_t left, top;            /* crop origin in resized coordinates            */
+  int32_t OW, OH;               /* output size                                   */
+  int32_t lx0, lx1, ly0, ly1;   /* luma tap footprint (inclusive, decoded px)    */
+  int32_t cx0, cx1, cy0, cy1;   /* chroma footprint incl. upsample neighbours    */
+  int32_t bx0[3], bx1[3], by0[3], by1[3];  /* ROI block ranges per component   */
+  int64_t roi_blocks;           /* blocks under the footprint (sum over comps)  */
+  int64_t roi_coef_bytes;       /* algorithmic coefficient bytes of the image   */
+} smol_geometry;
+
+/* Create a plan on the current CUDA device for batches of <= max_images.
+ * Validates params, allocates all device scratch once (no allocation in
+ * run).  *out = NULL on failure. */
+int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
+                          smol_preproc_plan_t** out);
+
+/* Run the fused path on `stream`.  out: DEVICE [n][3][OH][OW] fp32/fp16.
+ * Validates every descriptor before any launch (status + smol_last_error). */
+int32_t smol_preproc_run(smol_preproc_plan_t* plan, const smol_batch_desc* batch,
+                         void* out, void* stream);
+
+/* Same as smol_preproc_run, but coefficient pointers (and qtables) may be
+ * pinned HOST memory: the fused kernel reads only the ROI blocks across PCIe
+ * (end-to-end path; no separate staging copy).  out: DEVICE. */
+int32_t smol_preproc_run_host(smol_preproc_plan_t* plan, const smol_batch_desc* batch,
+                              void* out, void* stream);
+
+void smol_preproc_destroy(smol_preproc_plan_t* plan);
+
+/* Output tensor shape (C=3, OH, OW) of the plan. */
+int32_t smol_preproc_output_shape(const smol_preproc_plan_t* plan, int32_t* c, int32_t* h,
+                                  int32_t* w);
+
+/* Number of kernel launches one smol_preproc_run issues (for accounting). */
+int32_t smol_preproc_launches_per_run(const smol_preproc_plan_t* plan);
+
+/* Host-only: geometry of one image under `params` (no CUDA needed). */
+int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_desc* image,
+                            smol_geometry* out);
+
+/* Test-only: run the SAME fused kernel with its debug store enabled: besides
+ * `out`, writes the u8 samples it decoded into DEVICE int16 planes
+ * (initialised by the caller to -1): y_dbg[n][Hd][Wd], cb_dbg/cr_dbg
+ * [n][Hc][Wc], rgb_dbg[n][Hd][Wd][3] (per-image slices of size
+ * dbg_stride_* elements).  Only samples inside each image's footprint are
+ * written. */
+int32_t smol_debug_run(smol_preproc_plan_t* plan, const smol_batch_desc* batch, void* out,
+                       int16_t* y_dbg, int16_t* cb_dbg, int16_t* cr_dbg, int16_t* rgb_dbg,
+                       int64_t dbg_stride_y, int64_t dbg_stride_c, int64_t dbg_stride_rgb,
+                       void* stream);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* smol_last_error(void);
+
+/* SMOL_ABI_VERSION of the loaded library. */
+int32_t smol_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMOL_PREPROC_H */

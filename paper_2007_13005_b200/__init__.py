@@ -1,0 +1,192 @@
+"""B200-native Smol preprocessing hot path (arXiv 2007.13005, §2 steps 1-4 and
+§6.4 partial / reduced-fidelity decoding) -- thin Python binding.
+
+The product is the C-ABI library ``libsmol_preproc.so`` (include/smol_preproc.h)
+built from ``csrc/`` for sm_100a.  This module only marshals arguments:
+coefficient planes live in a torch-allocated arena (device memory or pinned
+host memory), descriptors are ctypes structs, and every computation runs in
+the fused CUDA kernel.  There is no CPU fallback: without the library every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._native import (BatchDesc, Geometry, ImageDesc, Params, SmolError, build, check, lib,
+                      SMOL_OUT_F16_NCHW, SMOL_OUT_F32_NCHW, SMOL_RESIZE_EXACT,
+                      SMOL_RESIZE_SHORT_SIDE, SMOL_LAYOUT_DENSE64, EXPORTS, LIB_PATH)
+
+__all__ = ["make_params", "params_from_config", "geometry", "CoefBatch", "Plan", "SmolError",
+           "build", "lib", "EXPORTS", "LIB_PATH"]
+
+IMAGENET_MEAN = (0.485, 0.456, 0.406)
+IMAGENET_STD = (0.229, 0.224, 0.225)
+
+
+def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: int = 256,
+                resize_w: int = 0, resize_h: int = 0, crop_w: int = 0, crop_h: int = 0,
+                mean=IMAGENET_MEAN, std=IMAGENET_STD, out_dtype: str = "f32",
+                tile_rows: int = 0) -> Params:
+    p = Params()
+    p.scale_denom = scale_denom
+    p.resize_mode = SMOL_RESIZE_SHORT_SIDE if resize_mode == "short" else SMOL_RESIZE_EXACT
+    p.resize_short, p.resize_w, p.resize_h = resize_short, resize_w, resize_h
+    p.crop_w, p.crop_h = crop_w, crop_h
+    p.mean = (ctypes.c_float * 3)(*mean)
+    p.std = (ctypes.c_float * 3)(*std)
+    p.out_dtype = SMOL_OUT_F16_NCHW if out_dtype == "f16" else SMOL_OUT_F32_NCHW
+    p.layout = SMOL_LAYOUT_DENSE64
+    p.tile_rows = tile_rows
+    return p
+
+
+def params_from_config(cfg, **kw) -> Params:
+    """Params for a synth.Config (BASELINE.json workload)."""
+    args = dict(scale_denom=cfg.scale_denom, resize_mode=cfg.resize_mode,
+                resize_short=cfg.resize_short, resize_w=cfg.resize_w, resize_h=cfg.resize_h,
+                crop_w=cfg.crop_w, crop_h=cfg.crop_h, out_dtype=cfg.out_dtype)
+    args.update(kw)
+    return make_params(**args)
+
+
+def _desc_for(width, height, blocks_w, blocks_h, qidx=(0, 1, 1), roi=None) -> ImageDesc:
+    d = ImageDesc()
+    d.width, d.height, d.subsampling = width, height, 420
+    d.qtable = (ctypes.c_int32 * 3)(*qidx)
+    for c in range(3):
+        d.blocks_w[c], d.blocks_h[c] = blocks_w[c], blocks_h[c]
+        d.row_stride_bytes[c] = blocks_w[c] * 128
+    d.roi_left, d.roi_top = roi if roi is not None else (-1, -1)
+    return d
+
+
+def geometry(params: Params, width: int, height: int, roi=None) -> dict:
+    """Host-only geometry of one image (smol_debug_geometry)."""
+    d = _desc_for(width, height, [(width + 7) // 8, (width + 15) // 16, (width + 15) // 16],
+                  [(height + 7) // 8, (height + 15) // 16, (height + 15) // 16], roi=roi)
+    g = Geometry()
+    check(lib().smol_debug_geometry(ctypes.byref(params), ctypes.byref(d), ctypes.byref(g)))
+    return g.as_dict()
+
+
+class CoefBatch:
+    """Entropy-decoded coefficient planes of N images in one torch arena.
+
+    images: sequence of objects with .width, .height, .coef (3 int16 arrays
+    [bh][bw][64]) and .qidx; qtables: [nq][64] uint16.  location: "device"
+    (HBM, for smol_preproc_run) or "pinned" (page-locked host memory, for the
+    end-to-end smol_preproc_run_host path).
+    """
+
+    def __init__(self, images: Sequence, qtables: np.ndarray, location: str = "device",
+                 device: Optional[int] = None, rois: Optional[Sequence] = None):
+        import torch
+        self.n = len(images)
+        sizes = [[int(c.size) for c in im.coef] for im in images]
+        total = int(sum(sum(s) for s in sizes))
+        host = np.empty(max(total, 8), np.int16)
+        offs = []
+        o = 0
+        for im, s in zip(images, sizes):
+            oo = []
+            for ci in range(3):
+                host[o:o + s[ci]] = np.ascontiguousarray(im.coef[ci], dtype=np.int16).ravel()
+                oo.append(o)
+                o += s[ci]                      # every plane is a multiple of 64 elements
+            offs.append(oo)
+        qt = np.ascontiguousarray(qtables, dtype=np.uint16).view(np.int16)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        if location == "device":
+            self.arena = torch.from_numpy(host).to(dev)
+            self.qtables = torch.from_numpy(qt.copy()).to(dev)
+        elif location == "pinned":
+            self.arena = torch.from_numpy(host).pin_memory()
+            self.qtables = torch.from_numpy(qt.copy()).to(dev)
+        else:
+            raise ValueError(location)
+        self.location = location
+        self.coef_bytes = int(self.arena.numel()) * 2
+        base = self.arena.data_ptr()
+        self.descs = (ImageDesc * max(self.n, 1))()
+        for i, (im, oo) in enumerate(zip(images, offs)):
+            roi = rois[i] if rois is not None else None
+            d = _desc_for(im.width, im.height, [c.shape[1] for c in im.coef],
+                          [c.shape[0] for c in im.coef], tuple(im.qidx), roi)
+            for ci in range(3):
+                d.coef[ci] = base + 2 * oo[ci]
+            self.descs[i] = d
+        self.desc = BatchDesc()
+        self.desc.n_images = self.n
+        self.desc.images = ctypes.cast(self.descs, ctypes.POINTER(ImageDesc))
+        self.desc.qtables = self.qtables.data_ptr()
+        self.desc.n_qtables = int(qtables.shape[0])
+
+
+class Plan:
+    """smol_preproc_plan on the current CUDA device."""
+
+    def __init__(self, params: Params, max_images: int):
+        self.params = params
+        self._h = ctypes.c_void_p()
+        check(lib().smol_preproc_plan(ctypes.byref(params), int(max_images), ctypes.byref(self._h)))
+        c, h, w = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        check(lib().smol_preproc_output_shape(self._h, ctypes.byref(c), ctypes.byref(h), ctypes.byref(w)))
+        self.out_shape = (c.value, h.value, w.value)
+        self.max_images = max_images
+
+    @property
+    def out_dtype(self):
+        import torch
+        return torch.float16 if self.params.out_dtype == SMOL_OUT_F16_NCHW else torch.float32
+
+    def launches_per_run(self) -> int:
+        return int(lib().smol_preproc_launches_per_run(self._h))
+
+    def new_output(self, n: int):
+        import torch
+        return torch.empty((n,) + self.out_shape, dtype=self.out_dtype, device="cuda")
+
+    @staticmethod
+    def _stream(stream) -> int:
+        import torch
+        s = torch.cuda.current_stream() if stream is None else stream
+        return s.cuda_stream
+
+    def run(self, batch: CoefBatch, out=None, stream=None):
+        if out is None:
+            out = self.new_output(batch.n)
+        fn = lib().smol_preproc_run_host if batch.location == "pinned" else lib().smol_preproc_run
+        check(fn(self._h, ctypes.byref(batch.desc), out.data_ptr(), self._stream(stream)))
+        return out
+
+    def debug_run(self, batch: CoefBatch, geoms: Sequence[dict], out=None, stream=None):
+        """Fused kernel with its debug store: returns (out, Y, Cb, Cr, RGB) with
+        int16 planes (-1 where the kernel did not write)."""
+        import torch
+        if out is None:
+            out = self.new_output(batch.n)
+        g = geoms
+        sy = max(d["Wd"] * d["Hd"] for d in g)
+        sc = max(d["Wc"] * d["Hc"] for d in g)
+        y = torch.full((batch.n, sy), -1, dtype=torch.int16, device="cuda")
+        cb = torch.full((batch.n, sc), -1, dtype=torch.int16, device="cuda")
+        cr = torch.full((batch.n, sc), -1, dtype=torch.int16, device="cuda")
+        rgb = torch.full((batch.n, 3 * sy), -1, dtype=torch.int16, device="cuda")
+        check(lib().smol_debug_run(self._h, ctypes.byref(batch.desc), out.data_ptr(), y.data_ptr(),
+                                   cb.data_ptr(), cr.data_ptr(), rgb.data_ptr(), sy, sc, 3 * sy,
+                                   self._stream(stream)))
+        return out, y, cb, cr, rgb
+
+    def close(self):
+        if self._h:
+            lib().smol_preproc_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

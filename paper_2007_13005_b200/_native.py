@@ -1,0 +1,135 @@
+"""ctypes mirror of include/smol_preproc.h and the nvcc build of the library.
+
+Argument marshalling only: every step of the path runs in the CUDA library.
+There is no fallback: if the shared library is missing, loading raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "libsmol_preproc.so")
+HEADER = os.path.join(_ROOT, "include", "smol_preproc.h")
+SOURCES = [os.path.join(_PKG, "csrc", f) for f in
+           ("smol_preproc.cu", "smol_kernels.cuh", "smol_geom.cuh")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+
+# smol_status
+SMOL_OK, SMOL_ERR_INVALID, SMOL_ERR_UNSUPPORTED, SMOL_ERR_CUDA, SMOL_ERR_NOMEM, SMOL_ERR_CAPACITY = range(6)
+STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "UNSUPPORTED", 3: "CUDA", 4: "NOMEM", 5: "CAPACITY"}
+SMOL_OUT_F32_NCHW, SMOL_OUT_F16_NCHW = 0, 1
+SMOL_RESIZE_SHORT_SIDE, SMOL_RESIZE_EXACT = 0, 1
+SMOL_LAYOUT_DENSE64 = 0
+
+# every symbol include/smol_preproc.h declares (checked by tests/test_abi.py)
+EXPORTS = ["smol_preproc_plan", "smol_preproc_run", "smol_preproc_run_host", "smol_preproc_destroy",
+           "smol_preproc_output_shape", "smol_preproc_launches_per_run", "smol_debug_geometry",
+           "smol_debug_run", "smol_last_error", "smol_abi_version"]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("scale_denom", ctypes.c_int32), ("resize_mode", ctypes.c_int32),
+                ("resize_short", ctypes.c_int32), ("resize_w", ctypes.c_int32),
+                ("resize_h", ctypes.c_int32), ("crop_w", ctypes.c_int32), ("crop_h", ctypes.c_int32),
+                ("mean", ctypes.c_float * 3), ("std", ctypes.c_float * 3),
+                ("out_dtype", ctypes.c_int32), ("layout", ctypes.c_int32),
+                ("tile_rows", ctypes.c_int32)]
+
+
+class ImageDesc(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("subsampling", ctypes.c_int32), ("qtable", ctypes.c_int32 * 3),
+                ("coef", ctypes.c_void_p * 3), ("blocks_w", ctypes.c_int32 * 3),
+                ("blocks_h", ctypes.c_int32 * 3), ("row_stride_bytes", ctypes.c_int32 * 3),
+                ("roi_left", ctypes.c_int32), ("roi_top", ctypes.c_int32)]
+
+
+class BatchDesc(ctypes.Structure):
+    _fields_ = [("n_images", ctypes.c_int32), ("images", ctypes.POINTER(ImageDesc)),
+                ("qtables", ctypes.c_void_p), ("n_qtables", ctypes.c_int32)]
+
+
+class Geometry(ctypes.Structure):
+    _fields_ = ([(n, ctypes.c_int32) for n in ("Wd", "Hd", "Wc", "Hc", "Wr", "Hr", "left", "top",
+                                               "OW", "OH", "lx0", "lx1", "ly0", "ly1",
+                                               "cx0", "cx1", "cy0", "cy1")] +
+                [(n, ctypes.c_int32 * 3) for n in ("bx0", "bx1", "by0", "by1")] +
+                [("roi_blocks", ctypes.c_int64), ("roi_coef_bytes", ctypes.c_int64)])
+
+    def as_dict(self):
+        d = {}
+        for n, _ in self._fields_:
+            v = getattr(self, n)
+            d[n] = list(v) if isinstance(v, ctypes.Array) else v
+        return d
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB_PATH):
+        return True
+    t = os.path.getmtime(LIB_PATH)
+    return any(os.path.getmtime(s) > t for s in SOURCES + [HEADER])
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libsmol_preproc.so (in-tree)."""
+    if not force and not _stale():
+        return LIB_PATH
+    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(_ROOT, "include"), "-o", tmp, SOURCES[0]]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{r.stderr}")
+    if verbose:
+        print(r.stderr)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library; raises if it was not built (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                               "(the Smol path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        vp = ctypes.c_void_p
+        L.smol_preproc_plan.argtypes = [P(Params), ctypes.c_int32, P(vp)]
+        L.smol_preproc_run.argtypes = [vp, P(BatchDesc), vp, vp]
+        L.smol_preproc_run_host.argtypes = [vp, P(BatchDesc), vp, vp]
+        L.smol_preproc_destroy.argtypes = [vp]
+        L.smol_preproc_destroy.restype = None
+        L.smol_preproc_output_shape.argtypes = [vp] + [P(ctypes.c_int32)] * 3
+        L.smol_preproc_launches_per_run.argtypes = [vp]
+        L.smol_debug_geometry.argtypes = [P(Params), P(ImageDesc), P(Geometry)]
+        L.smol_debug_run.argtypes = [vp, P(BatchDesc), vp, vp, vp, vp, vp,
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, vp]
+        L.smol_last_error.argtypes = []
+        L.smol_last_error.restype = ctypes.c_char_p
+        L.smol_abi_version.argtypes = []
+        for name in EXPORTS:
+            f = getattr(L, name)
+            if f.restype is ctypes.c_int:           # ctypes default
+                f.restype = ctypes.c_int32
+        _lib = L
+    return _lib
+
+
+class SmolError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"smol status {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def check(status: int) -> None:
+    if status != SMOL_OK:
+        raise SmolError(status, lib().smol_last_error().decode())

@@ -1,0 +1,107 @@
+// smol_geom.cuh -- per-image and per-tile geometry of the fused Smol
+// preprocessing kernel, shared by the host runtime (validation, shared-memory
+// sizing, smol_debug_geometry) and the device kernels.  Part of the CUDA path
+// only; the oracle (oracle/) has its own, independent implementation.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define SMOL_HD __host__ __device__ __forceinline__
+#else
+#define SMOL_HD inline
+#endif
+
+namespace smol {
+
+constexpr int kThreads = 256;             // threads per CTA (8 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kScratchPitch = 9;          // floats per row of the IDCT transpose scratch
+
+SMOL_HD int ceil_div(int a, int b) { return (a + b - 1) / b; }
+SMOL_HD int imin(int a, int b) { return a < b ? a : b; }
+SMOL_HD int imax(int a, int b) { return a > b ? a : b; }
+
+// Device-side image descriptor (built by the host in smol_preproc_run).
+struct __align__(16) DevImage {
+  const int16_t* coef[3];   // block-raster [bh][bw][64] int16, natural order
+  int32_t stride[3];        // int16 elements per block row
+  int32_t qidx[3];          // quant table index per component
+  int32_t Wd, Hd;           // decoded luma size at scale 1/k (R4)
+  int32_t Wc, Hc;           // decoded chroma size
+  int32_t Wr, Hr;           // resized size
+  int32_t left, top;        // crop origin in resized coordinates
+};
+
+// Reading R9: the half-pixel bilinear source index of destination index d
+// (R8: src = max(0, (d + 1/2) in/out - 1/2)), from exact integers:
+//   num = max(0, (2d+1) in - out),  i0 = num div 2out,  w = (num mod 2out) / 2out,
+//   i1 = min(i0 + 1, in - 1).
+SMOL_HD void src_tap(int d, int in, int out, int& i0, int& i1, float& w) {
+  long long num = (long long)(2 * d + 1) * in - out;
+  if (num < 0) num = 0;
+  long long den = 2LL * out;
+  long long q = num / den;
+  i0 = (int)q;
+  w = (float)(num - q * den) / (float)den;   // both exact in fp32 (< 2^24)
+  if (i0 > in - 1) i0 = in - 1;
+  i1 = imin(i0 + 1, in - 1);
+}
+
+// Footprint of output rows [oy0, oy1) x all OW columns, and the shared-memory
+// carve-up of the CTA that processes it.
+struct TileLayout {
+  int ly0, ly1, lx0, lx1;          // luma (decoded) tap footprint, inclusive
+  int cy0, cy1, cx0, cx1;          // chroma footprint incl. triangle neighbours
+  int by0[3], by1[3], bx0[3], bx1[3];   // ROI block ranges per component
+  int pitch[3], rows[3];           // u8 plane geometry in smem (pitch in bytes)
+  int nly, nlx;                    // footprint size (RGB buffer)
+  // byte offsets in dynamic shared memory
+  int off_q, off_xt, off_yt, off_pl[3], off_rgb, total;
+};
+
+SMOL_HD int align16(int x) { return (x + 15) & ~15; }
+
+SMOL_HD void tile_layout(const DevImage& im, int K, int OW, int oy0, int oy1, TileLayout& L) {
+  const int P = 8 / K;
+  int a, b; float w;
+  src_tap(im.left, im.Wd, im.Wr, L.lx0, b, w);
+  src_tap(im.left + OW - 1, im.Wd, im.Wr, a, L.lx1, w);
+  src_tap(im.top + oy0, im.Hd, im.Hr, L.ly0, b, w);
+  src_tap(im.top + oy1 - 1, im.Hd, im.Hr, a, L.ly1, w);
+  // chroma rows/cols used by the centred triangle filter of luma rows
+  // [ly0, ly1]: floor((ly0-1)/2) .. floor((ly1+1)/2), clamped (reading R2)
+  L.cy0 = imax(0, (L.ly0 - 1) >> 1);
+  L.cy1 = imin(im.Hc - 1, (L.ly1 + 1) >> 1);
+  L.cx0 = imax(0, (L.lx0 - 1) >> 1);
+  L.cx1 = imin(im.Wc - 1, (L.lx1 + 1) >> 1);
+  L.by0[0] = L.ly0 / P; L.by1[0] = L.ly1 / P;
+  L.bx0[0] = L.lx0 / P; L.bx1[0] = L.lx1 / P;
+  for (int c = 1; c < 3; ++c) {
+    L.by0[c] = L.cy0 / P; L.by1[c] = L.cy1 / P;
+    L.bx0[c] = L.cx0 / P; L.bx1[c] = L.cx1 / P;
+  }
+  for (int c = 0; c < 3; ++c) {
+    L.pitch[c] = ((L.bx1[c] - L.bx0[c] + 1) * P + 3) & ~3;
+    L.rows[c] = (L.by1[c] - L.by0[c] + 1) * P;
+  }
+  L.nly = L.ly1 - L.ly0 + 1;
+  L.nlx = L.lx1 - L.lx0 + 1;
+  int off = 0;
+  L.off_q = off;   off += 3 * 64 * 4;                       // dequant table (float)
+  L.off_xt = off;  off += align16(OW * 8);                  // x taps: int2{i0|i1<<16, w}
+  L.off_yt = off;  off += align16((oy1 - oy0) * 8);         // y taps
+  for (int c = 0; c < 3; ++c) { L.off_pl[c] = off; off += align16(L.pitch[c] * L.rows[c]); }
+  L.off_rgb = off;
+  int rgb = L.nly * L.nlx * 4;
+  int scratch = kWarps * 4 * 8 * kScratchPitch * 4;         // IDCT transpose (aliases RGB)
+  off += align16(rgb > scratch ? rgb : scratch);
+  L.total = off;
+}
+
+SMOL_HD long long tile_roi_blocks(const TileLayout& L) {
+  long long n = 0;
+  for (int c = 0; c < 3; ++c) n += (long long)(L.by1[c] - L.by0[c] + 1) * (L.bx1[c] - L.bx0[c] + 1);
+  return n;
+}
+
+}  // namespace smol

@@ -1,0 +1,422 @@
+// smol_preproc.cu -- host runtime of the C ABI declared in
+// include/smol_preproc.h: parameter/descriptor validation, per-image
+// geometry, device descriptor upload (pinned ring, no allocation per run),
+// kernel selection per (scale, dtype) and launch.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "smol_preproc.h"
+#include "smol_geom.cuh"
+#include "smol_kernels.cuh"
+
+using namespace smol;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int32_t fail(int32_t code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define SMOL_CUDA(call)                                                             \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(SMOL_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),  \
+                  __FILE__, __LINE__);                                              \
+  } while (0)
+
+constexpr int kRing = 4;           // descriptor ring depth (runs in flight per plan)
+constexpr int kMaxDevices = 64;
+
+// ------------------------------------------------------------ basis upload --
+// Definitions in smol_kernels.cuh (struct Basis); reading R1.
+void init_basis(Basis& b) {
+  const double pi = 3.14159265358979323846;
+  double t[8][8];
+  for (int u = 0; u < 8; ++u)
+    for (int x = 0; x < 8; ++x) {
+      if (u == 0) t[u][x] = 1.0;
+      else if (u == 4) t[u][x] = ((2 * x + 1) % 8 == 1 || (2 * x + 1) % 8 == 7) ? 1.0 : -1.0;
+      else t[u][x] = std::sqrt(2.0) * std::cos((2 * x + 1) * u * pi / 16.0);
+    }
+  for (int u = 0; u < 8; ++u)
+    for (int x = 0; x < 4; ++x) b.t[u][x] = (float)t[u][x];
+  // box means; entries that vanish by the sum-of-cosines identity are exact 0
+  auto box = [&](int k, int u, int j) -> double {
+    if (u > 0 && ((k * u) % 16 == 0 || (k * u * (2 * j + 1)) % 16 == 8)) return 0.0;
+    double s = 0;
+    for (int x = j * k; x < j * k + k; ++x) s += t[u][x];
+    return s / k;
+  };
+  for (int j = 0; j < 2; ++j)
+    for (int u = 0; u < 8; ++u) b.a2[j][u] = (float)box(2, u, j);
+  for (int u = 0; u < 8; ++u) b.a4[u] = (float)box(4, u, 0);
+}
+
+std::mutex g_basis_mu;
+bool g_basis_done[kMaxDevices] = {};
+
+int32_t ensure_basis(int dev) {
+  std::lock_guard<std::mutex> lk(g_basis_mu);
+  if (dev < 0 || dev >= kMaxDevices) return fail(SMOL_ERR_CUDA, "device index %d out of range", dev);
+  if (g_basis_done[dev]) return SMOL_OK;
+  Basis b;
+  init_basis(b);
+  SMOL_CUDA(cudaMemcpyToSymbol(c_basis, &b, sizeof(Basis)));
+  g_basis_done[dev] = true;
+  return SMOL_OK;
+}
+
+// ------------------------------------------------------------- validation --
+int32_t validate_params(const smol_preproc_params* p) {
+  if (!p) return fail(SMOL_ERR_INVALID, "params is NULL");
+  if (p->scale_denom != 1 && p->scale_denom != 2 && p->scale_denom != 4 && p->scale_denom != 8)
+    return fail(SMOL_ERR_INVALID, "params.scale_denom=%d not in {1,2,4,8}", p->scale_denom);
+  if (p->resize_mode == SMOL_RESIZE_SHORT_SIDE) {
+    if (p->resize_short <= 0) return fail(SMOL_ERR_INVALID, "params.resize_short=%d <= 0", p->resize_short);
+    if (p->crop_w <= 0 || p->crop_h <= 0)
+      return fail(SMOL_ERR_INVALID, "SHORT_SIDE resize needs crop_w, crop_h > 0 (fixed output size)");
+  } else if (p->resize_mode == SMOL_RESIZE_EXACT) {
+    if (p->resize_w <= 0 || p->resize_h <= 0)
+      return fail(SMOL_ERR_INVALID, "params.resize_w/h=%d/%d must be > 0", p->resize_w, p->resize_h);
+    if ((p->crop_w > 0) != (p->crop_h > 0) || p->crop_w < 0 || p->crop_h < 0)
+      return fail(SMOL_ERR_INVALID, "params.crop_w/h=%d/%d: both > 0 or both 0", p->crop_w, p->crop_h);
+    if (p->crop_w > p->resize_w || p->crop_h > p->resize_h)
+      return fail(SMOL_ERR_INVALID, "crop %dx%d larger than resize %dx%d", p->crop_w, p->crop_h,
+                  p->resize_w, p->resize_h);
+  } else {
+    return fail(SMOL_ERR_INVALID, "params.resize_mode=%d", p->resize_mode);
+  }
+  for (int c = 0; c < 3; ++c) {
+    if (!(p->std[c] > 0.f) || !std::isfinite(p->std[c]) || !std::isfinite(p->mean[c]))
+      return fail(SMOL_ERR_INVALID, "params.std[%d]=%g must be finite and > 0", c, (double)p->std[c]);
+  }
+  if (p->out_dtype != SMOL_OUT_F32_NCHW && p->out_dtype != SMOL_OUT_F16_NCHW)
+    return fail(SMOL_ERR_INVALID, "params.out_dtype=%d", p->out_dtype);
+  if (p->layout != SMOL_LAYOUT_DENSE64)
+    return fail(SMOL_ERR_UNSUPPORTED, "params.layout=%d (only DENSE64)", p->layout);
+  if (p->tile_rows < 0 || p->tile_rows > 4096)
+    return fail(SMOL_ERR_INVALID, "params.tile_rows=%d", p->tile_rows);
+  return SMOL_OK;
+}
+
+// Per-image geometry (readings R4, R7, R11); fills the device descriptor's
+// size fields.  idx is the image index for error messages.
+int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, int idx, DevImage& g) {
+  const int k = p->scale_denom;
+  if (d->width <= 0 || d->height <= 0)
+    return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d must be > 0", idx, d->width, d->height);
+  if (d->width > 65535 || d->height > 65535)
+    return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d > 65535 (JPEG limit)", idx, d->width, d->height);
+  if (d->subsampling != 420)
+    return fail(SMOL_ERR_UNSUPPORTED, "image %d: subsampling=%d (only 420)", idx, d->subsampling);
+  g.Wd = ceil_div(d->width, k);
+  g.Hd = ceil_div(d->height, k);
+  g.Wc = ceil_div(d->width, 2 * k);
+  g.Hc = ceil_div(d->height, 2 * k);
+  int OW, OH;
+  if (p->resize_mode == SMOL_RESIZE_SHORT_SIDE) {
+    const long long S = p->resize_short;
+    if (g.Wd <= g.Hd) { g.Wr = (int)S; g.Hr = (int)(S * g.Hd / g.Wd); }
+    else              { g.Hr = (int)S; g.Wr = (int)(S * g.Wd / g.Hd); }
+  } else {
+    g.Wr = p->resize_w; g.Hr = p->resize_h;
+  }
+  if (p->crop_w > 0) { OW = p->crop_w; OH = p->crop_h; } else { OW = g.Wr; OH = g.Hr; }
+  if (OW > g.Wr || OH > g.Hr)
+    return fail(SMOL_ERR_INVALID, "image %d: crop %dx%d larger than resized %dx%d", idx, OW, OH, g.Wr, g.Hr);
+  if (d->roi_left < 0 && d->roi_top < 0) {
+    // torchvision centre crop: round((Wr - cw) / 2) with round-half-to-even
+    auto half_even = [](int v) { return (v % 2 == 0) ? v / 2 : (((v - 1) / 2) % 2 == 0 ? (v - 1) / 2 : (v + 1) / 2); };
+    g.left = half_even(g.Wr - OW);
+    g.top = half_even(g.Hr - OH);
+  } else {
+    if (d->roi_left < 0 || d->roi_top < 0 || d->roi_left + OW > g.Wr || d->roi_top + OH > g.Hr)
+      return fail(SMOL_ERR_INVALID, "image %d: roi origin (%d,%d) + %dx%d outside resized %dx%d", idx,
+                  d->roi_left, d->roi_top, OW, OH, g.Wr, g.Hr);
+    g.left = d->roi_left;
+    g.top = d->roi_top;
+  }
+  return SMOL_OK;
+}
+
+int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, int idx, int n_qtables,
+                       DevImage& g) {
+  int32_t rc = image_geometry(p, d, idx, g);
+  if (rc) return rc;
+  const int need_w[3] = {ceil_div(d->width, 8), ceil_div(d->width, 16), ceil_div(d->width, 16)};
+  const int need_h[3] = {ceil_div(d->height, 8), ceil_div(d->height, 16), ceil_div(d->height, 16)};
+  static const char* names[3] = {"Y", "Cb", "Cr"};
+  for (int c = 0; c < 3; ++c) {
+    if (!d->coef[c]) return fail(SMOL_ERR_INVALID, "image %d: coef[%d] (%s) is NULL", idx, c, names[c]);
+    if (reinterpret_cast<uintptr_t>(d->coef[c]) % 16)
+      return fail(SMOL_ERR_INVALID, "image %d: coef[%d] not 16-byte aligned", idx, c);
+    if (d->blocks_w[c] < need_w[c] || d->blocks_h[c] < need_h[c])
+      return fail(SMOL_ERR_INVALID, "image %d: blocks_w[%d]=%d / blocks_h[%d]=%d < required %d / %d", idx, c,
+                  d->blocks_w[c], c, d->blocks_h[c], need_w[c], need_h[c]);
+    if (d->row_stride_bytes[c] < d->blocks_w[c] * 128 || d->row_stride_bytes[c] % 16)
+      return fail(SMOL_ERR_INVALID, "image %d: row_stride_bytes[%d]=%d (need >= %d, multiple of 16)", idx, c,
+                  d->row_stride_bytes[c], d->blocks_w[c] * 128);
+    if (d->qtable[c] < 0 || d->qtable[c] >= n_qtables)
+      return fail(SMOL_ERR_INVALID, "image %d: qtable[%d]=%d not in [0,%d)", idx, c, d->qtable[c], n_qtables);
+    g.coef[c] = d->coef[c];
+    g.stride[c] = d->row_stride_bytes[c] / 2;
+    g.qidx[c] = d->qtable[c];
+  }
+  return SMOL_OK;
+}
+
+int auto_tile_rows(int K) {
+  switch (K) {
+    case 1: return 16;
+    case 2: return 32;
+    case 4: return 32;
+    default: return 64;
+  }
+}
+
+using KernelFn = void (*)(const KParams);
+
+template <int K>
+KernelFn pick_kernel(bool f16, bool dbg) {
+  if (dbg) return f16 ? smol_fused_kernel<K, true, true> : smol_fused_kernel<K, false, true>;
+  return f16 ? smol_fused_kernel<K, true, false> : smol_fused_kernel<K, false, false>;
+}
+
+KernelFn select_kernel(int K, bool f16, bool dbg) {
+  switch (K) {
+    case 1: return pick_kernel<1>(f16, dbg);
+    case 2: return pick_kernel<2>(f16, dbg);
+    case 4: return pick_kernel<4>(f16, dbg);
+    default: return pick_kernel<8>(f16, dbg);
+  }
+}
+
+}  // namespace
+
+struct smol_preproc_plan {
+  smol_preproc_params p;
+  int max_images = 0;
+  int device = 0;
+  int OW = 0, OH = 0;          // 0 when the output size is image dependent (never: validated)
+  int tile_rows = 0;
+  int smem_optin = 0;
+  DevImage* d_desc = nullptr;  // [kRing][max_images]
+  DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
+  cudaEvent_t ev[kRing] = {};
+  int ring = 0;
+  float na[3], nb[3];
+};
+
+extern "C" {
+
+int32_t smol_abi_version(void) { return SMOL_ABI_VERSION; }
+
+const char* smol_last_error(void) { return g_last_error.c_str(); }
+
+int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_desc* image,
+                            smol_geometry* out) {
+  g_last_error.clear();
+  int32_t rc = validate_params(params);
+  if (rc) return rc;
+  if (!image || !out) return fail(SMOL_ERR_INVALID, "image/out is NULL");
+  DevImage g{};
+  rc = image_geometry(params, image, 0, g);
+  if (rc) return rc;
+  memset(out, 0, sizeof(*out));
+  out->Wd = g.Wd; out->Hd = g.Hd; out->Wc = g.Wc; out->Hc = g.Hc;
+  out->Wr = g.Wr; out->Hr = g.Hr; out->left = g.left; out->top = g.top;
+  out->OW = params->crop_w > 0 ? params->crop_w : g.Wr;
+  out->OH = params->crop_w > 0 ? params->crop_h : g.Hr;
+  TileLayout L;
+  tile_layout(g, params->scale_denom, out->OW, 0, out->OH, L);
+  out->lx0 = L.lx0; out->lx1 = L.lx1; out->ly0 = L.ly0; out->ly1 = L.ly1;
+  out->cx0 = L.cx0; out->cx1 = L.cx1; out->cy0 = L.cy0; out->cy1 = L.cy1;
+  for (int c = 0; c < 3; ++c) {
+    out->bx0[c] = L.bx0[c]; out->bx1[c] = L.bx1[c]; out->by0[c] = L.by0[c]; out->by1[c] = L.by1[c];
+  }
+  out->roi_blocks = tile_roi_blocks(L);
+  out->roi_coef_bytes = out->roi_blocks * 128;
+  return SMOL_OK;
+}
+
+int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images, smol_preproc_plan_t** out) {
+  g_last_error.clear();
+  if (!out) return fail(SMOL_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  int32_t rc = validate_params(params);
+  if (rc) return rc;
+  if (max_images <= 0 || max_images > (1 << 20))
+    return fail(SMOL_ERR_INVALID, "max_images=%d not in [1, 2^20]", max_images);
+  int dev = 0;
+  SMOL_CUDA(cudaGetDevice(&dev));
+  rc = ensure_basis(dev);
+  if (rc) return rc;
+  smol_preproc_plan_t* pl = new (std::nothrow) smol_preproc_plan_t();
+  if (!pl) return fail(SMOL_ERR_NOMEM, "plan allocation");
+  pl->p = *params;
+  pl->max_images = max_images;
+  pl->device = dev;
+  if (params->crop_w > 0) { pl->OW = params->crop_w; pl->OH = params->crop_h; }
+  else { pl->OW = params->resize_w; pl->OH = params->resize_h; }
+  pl->tile_rows = params->tile_rows > 0 ? params->tile_rows : auto_tile_rows(params->scale_denom);
+  for (int c = 0; c < 3; ++c) {
+    pl->na[c] = (float)(1.0 / (255.0 * (double)params->std[c]));
+    pl->nb[c] = (float)(-(double)params->mean[c] / (double)params->std[c]);
+  }
+  cudaError_t e = cudaDeviceGetAttribute(&pl->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_desc, sizeof(DevImage) * (size_t)max_images * kRing);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
+  for (int i = 0; i < kRing && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) {
+    // opt every instantiation of this plan's (scale, dtype) in to large smem
+    const bool f16 = params->out_dtype == SMOL_OUT_F16_NCHW;
+    for (int dbg = 0; dbg < 2 && e == cudaSuccess; ++dbg)
+      e = cudaFuncSetAttribute(select_kernel(params->scale_denom, f16, dbg),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, pl->smem_optin);
+  }
+  if (e != cudaSuccess) {
+    smol_preproc_destroy(pl);
+    return fail(e == cudaErrorMemoryAllocation ? SMOL_ERR_NOMEM : SMOL_ERR_CUDA, "plan setup: %s",
+                cudaGetErrorString(e));
+  }
+  *out = pl;
+  return SMOL_OK;
+}
+
+void smol_preproc_destroy(smol_preproc_plan_t* pl) {
+  if (!pl) return;
+  for (int i = 0; i < kRing; ++i)
+    if (pl->ev[i]) { cudaEventSynchronize(pl->ev[i]); cudaEventDestroy(pl->ev[i]); }
+  if (pl->d_desc) cudaFree(pl->d_desc);
+  if (pl->h_desc) cudaFreeHost(pl->h_desc);
+  delete pl;
+}
+
+int32_t smol_preproc_output_shape(const smol_preproc_plan_t* pl, int32_t* c, int32_t* h, int32_t* w) {
+  if (!pl || !c || !h || !w) return fail(SMOL_ERR_INVALID, "NULL argument");
+  *c = 3; *h = pl->OH; *w = pl->OW;
+  return SMOL_OK;
+}
+
+int32_t smol_preproc_launches_per_run(const smol_preproc_plan_t* pl) {
+  return pl ? 1 : 0;
+}
+
+}  // extern "C"
+
+namespace {
+
+int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream_v,
+                 const KParams* dbg) {
+  g_last_error.clear();
+  if (!pl) return fail(SMOL_ERR_INVALID, "plan is NULL");
+  if (!b) return fail(SMOL_ERR_INVALID, "batch is NULL");
+  if (b->n_images < 0) return fail(SMOL_ERR_INVALID, "n_images=%d < 0", b->n_images);
+  if (b->n_images == 0) return SMOL_OK;
+  if (b->n_images > pl->max_images)
+    return fail(SMOL_ERR_CAPACITY, "n_images=%d > plan capacity %d", b->n_images, pl->max_images);
+  if (!b->images) return fail(SMOL_ERR_INVALID, "batch.images is NULL");
+  if (!b->qtables || b->n_qtables < 1 || b->n_qtables > 4)
+    return fail(SMOL_ERR_INVALID, "batch.qtables NULL or n_qtables=%d not in [1,4]", b->n_qtables);
+  if (!out) return fail(SMOL_ERR_INVALID, "out is NULL");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_v);
+  const int K = pl->p.scale_denom;
+
+  // ring slot: wait until the run that last used it has consumed its descriptors
+  const int slot = pl->ring;
+  pl->ring = (pl->ring + 1) % kRing;
+  SMOL_CUDA(cudaEventSynchronize(pl->ev[slot]));
+  DevImage* h = pl->h_desc + (size_t)slot * pl->max_images;
+  DevImage* d = pl->d_desc + (size_t)slot * pl->max_images;
+
+  // validate + build descriptors; shared memory = max over distinct geometries
+  int smem = 0;
+  int prev_w = -1, prev_h = -1, prev_l = -2, prev_t = -2;
+  const int ntiles = ceil_div(pl->OH, pl->tile_rows);
+  for (int i = 0; i < b->n_images; ++i) {
+    const smol_image_desc* di = &b->images[i];
+    DevImage g{};
+    int32_t rc = validate_image(&pl->p, di, i, b->n_qtables, g);
+    if (rc) return rc;
+    if (di->width != prev_w || di->height != prev_h || di->roi_left != prev_l || di->roi_top != prev_t) {
+      for (int t = 0; t < ntiles; ++t) {
+        TileLayout L;
+        tile_layout(g, K, pl->OW, t * pl->tile_rows, min(pl->OH, (t + 1) * pl->tile_rows), L);
+        if (L.total > smem) smem = L.total;
+      }
+      prev_w = di->width; prev_h = di->height; prev_l = di->roi_left; prev_t = di->roi_top;
+    }
+    h[i] = g;
+  }
+  if (smem > pl->smem_optin)
+    return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
+
+  SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * b->n_images, cudaMemcpyHostToDevice, stream));
+  KParams kp = dbg ? *dbg : KParams{};
+  kp.imgs = d;
+  kp.qtables = b->qtables;
+  kp.out = out;
+  kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = pl->tile_rows;
+  for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
+  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr);
+  dim3 grid(ntiles, b->n_images);
+  fn<<<grid, kThreads, smem, stream>>>(kp);
+  SMOL_CUDA(cudaGetLastError());
+  SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
+  return SMOL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t smol_preproc_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream) {
+  return run_impl(pl, b, out, stream, nullptr);
+}
+
+int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream) {
+  // Pinned host coefficient memory is device-addressable under UVA: the
+  // fused kernel reads only the ROI blocks across PCIe.
+  // Probe image 0's planes (a batch normally comes from one pinned arena).
+  if (b && b->images && b->n_images > 0) {
+    for (int c = 0; c < 3; ++c) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, b->images[0].coef[c]) != cudaSuccess ||
+          (a.type != cudaMemoryTypeHost && a.type != cudaMemoryTypeDevice &&
+           a.type != cudaMemoryTypeManaged)) {
+        cudaGetLastError();
+        return fail(SMOL_ERR_INVALID, "image 0: coef[%d] is neither pinned host nor device memory", c);
+      }
+    }
+  }
+  return run_impl(pl, b, out, stream, nullptr);
+}
+
+int32_t smol_debug_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, int16_t* y_dbg,
+                       int16_t* cb_dbg, int16_t* cr_dbg, int16_t* rgb_dbg, int64_t sy, int64_t sc,
+                       int64_t srgb, void* stream) {
+  if (!y_dbg || !cb_dbg || !cr_dbg || !rgb_dbg) return fail(SMOL_ERR_INVALID, "debug buffer is NULL");
+  KParams kp{};
+  kp.dbg_pl[0] = y_dbg; kp.dbg_pl[1] = cb_dbg; kp.dbg_pl[2] = cr_dbg; kp.dbg_rgb = rgb_dbg;
+  kp.dbg_stride_y = sy; kp.dbg_stride_c = sc; kp.dbg_stride_rgb = srgb;
+  return run_impl(pl, b, out, stream, &kp);
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+"""Test-side helpers: oracle references and the reading-R3 tie band.
+
+Only calls oracle/ (and synth/); never the CUDA path.  Tie-free corpora are
+built here (not in synth, which holds no decoder arithmetic) by rejecting
+blocks whose oracle samples lie within delta_b of a rounding tie.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+import synth
+
+
+def block_delta(coef: np.ndarray, q: np.ndarray) -> np.ndarray:
+    """Reading R3 tie band per block: delta_b = max(2^-12, 2^-23 * sum |D|).
+    coef [bh][bw][64] -> [bh][bw]."""
+    D = np.abs(coef.astype(np.int64) * q.astype(np.int64)).sum(axis=-1)
+    return np.maximum(2.0 ** -12, 2.0 ** -23 * D)
+
+
+def tie_distance(v: np.ndarray) -> np.ndarray:
+    """Distance of v + 128 from the nearest half-integer (a rounding tie)."""
+    x = v + 128.0
+    return np.abs(x - (np.floor(x) + 0.5))
+
+
+def plane_band(coef, q, k, v):
+    """Boolean [h][w]: sample within delta_b of a tie but not exactly on it."""
+    P = 8 // k
+    h, w = v.shape
+    delta = block_delta(coef, q)
+    dl = np.repeat(np.repeat(delta, P, axis=0), P, axis=1)[:h, :w]
+    d = tie_distance(v)
+    return (d <= dl) & (d > 0)
+
+
+def oracle_planes(p, im, qt):
+    """[(v, u8, band_mask)] for Y, Cb, Cr at the params' scale."""
+    res = []
+    for ci, (v, u8) in enumerate(oracle.decode_image_planes(p, im, qt, with_v=True)):
+        q = qt[im.qidx[ci]]
+        res.append((v, u8, plane_band(im.coef[ci], q, p.scale_denom, v)))
+    return res
+
+
+def make_tie_free(im, qt, k: int, max_iter: int = 50):
+    """Perturb AC coefficients of blocks having a sample within delta_b of a
+    tie (exact ties excluded as well) until none does, at decode scale 1/k."""
+    P = 8 // k
+    coef = [c.copy() for c in im.coef]
+    rng = np.random.default_rng(12345)
+    for ci in range(3):
+        q = qt[im.qidx[ci]]
+        bh, bw = coef[ci].shape[:2]
+        for _ in range(max_iter):
+            v, _ = oracle.decode_plane(coef[ci], q, k, bw * P, bh * P)
+            delta = block_delta(coef[ci], q)
+            d = tie_distance(v).reshape(bh, P, bw, P).min(axis=(1, 3))
+            bad = d <= delta
+            if not bad.any():
+                break
+            idx = np.argwhere(bad)
+            for (by, bx) in idx:
+                # an odd-u AC nudge shifts samples by irrational amounts
+                j = int(rng.choice([1, 3, 8, 24, 9]))
+                coef[ci][by, bx, j] += 1 if rng.random() < 0.5 else -1
+        else:
+            raise RuntimeError("tie-free regeneration did not converge")
+    return synth.CoefImage(im.width, im.height, coef, im.qidx)
+
+
+def rgb_from_planes(Y, Cb, Cr):
+    return oracle.upsample_color(Y, Cb, Cr)[1]

@@ -1,0 +1,304 @@
+"""GPU parity of the fused sm_100a kernel against the CPU oracle, through the
+C ABI (smol_preproc_run / smol_debug_run).
+
+Bar (north_star):
+  * u8 Y/Cb/Cr samples bit-exact, except samples whose oracle value lies
+    within delta_b of a rounding tie but not on it (reading R3): there +-1;
+    tie-free corpora must be bit-exact everywhere;
+  * u8 RGB bit-exact given the kernel's own Y/Cb/Cr (upsample + colour are
+    exact integer steps, R2/R6);
+  * output within 1e-4 (fp32) / 2e-3 (fp16) of the oracle's resize +
+    normalize of the kernel's RGB, and of the oracle's end-to-end output
+    (widened only for images with a band flip).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2007_13005_b200 as smol
+import synth
+from tests import helpers
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "f16": 2e-3}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _setup():
+    smol.build()
+    oracle.build()
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.init()
+
+
+def _cfg_params(cfg, **kw):
+    return smol.params_from_config(cfg, **kw), oracle.params_from_config(cfg)
+
+
+def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=None):
+    n = len(imgs)
+    plan = smol.Plan(ps, n)
+    batch = smol.CoefBatch(imgs, qt, rois=rois)
+    geoms = [smol.geometry(ps, im.width, im.height, roi=None if rois is None else rois[i])
+             for i, im in enumerate(imgs)]
+    if debug:
+        out, y, cb, cr, rgb = plan.debug_run(batch, geoms)
+    else:
+        out = plan.run(batch)
+    torch.cuda.synchronize()
+    out = out.float().cpu().numpy()
+    tol = TOL[cfg.out_dtype]
+    flips = 0
+    for i, im in enumerate(imgs):
+        g = geoms[i]
+        roi = None if rois is None else rois[i]
+        ref = oracle.run_image(po, im, qt, roi).astype(np.float64)
+        widen = 0.0
+        if debug:
+            planes = [t[i].cpu().numpy() for t in (y, cb, cr)]
+            dims = [(g["Hd"], g["Wd"]), (g["Hc"], g["Wc"]), (g["Hc"], g["Wc"])]
+            gp = []
+            for ci, (v, u8, band) in enumerate(helpers.oracle_planes(po, im, qt)):
+                h, w = dims[ci]
+                gpl = planes[ci][:h * w].reshape(h, w)
+                m = gpl >= 0
+                assert m.sum() > 0
+                d = gpl[m].astype(np.int32) - u8[m].astype(np.int32)
+                bad = d != 0
+                if strict:
+                    assert not bad.any(), f"image {i} comp {ci}: {bad.sum()} u8 mismatches (tie-free)"
+                else:
+                    assert np.all(np.abs(d) <= 1), f"image {i} comp {ci}: u8 off by >1"
+                    assert np.all(band[m][bad]), f"image {i} comp {ci}: mismatch outside tie band"
+                flips += int(bad.sum())
+                gp.append(np.where(m, gpl, 0).astype(np.uint8))
+            # RGB exact given the kernel's own planes
+            grgb = rgb[i].cpu().numpy()[:3 * g["Hd"] * g["Wd"]].reshape(g["Hd"], g["Wd"], 3)
+            mrgb = grgb[..., 0] >= 0
+            exp_rgb = helpers.rgb_from_planes(*gp)
+            assert np.array_equal(grgb[mrgb], exp_rgb[mrgb].astype(np.int16)), f"image {i}: RGB mismatch"
+            # resize/normalize given the kernel's own RGB
+            full = np.where(mrgb[..., None], grgb, 0).astype(np.uint8)
+            stage, _ = oracle.resize_crop_normalize(full, g["Wr"], g["Hr"], g["left"], g["top"],
+                                                   g["OW"], g["OH"], out_dtype=cfg.out_dtype)
+            assert np.max(np.abs(out[i] - stage.astype(np.float64))) <= tol, f"image {i}: resize stage"
+            if flips:
+                widen = 2.0 / (255 * min(synth.IMAGENET_STD))
+        err = np.max(np.abs(out[i] - ref))
+        assert err <= tol + widen, f"image {i}: max |gpu - oracle| = {err}"
+    if report is not None:
+        report["flips"] = report.get("flips", 0) + flips
+    plan.close()
+    return out
+
+
+@pytest.mark.parametrize("mode", ["natural", "stress"])
+def test_c1_full(mode):
+    cfg = synth.CONFIGS["c1"]
+    imgs, qt = synth.distinct_images(cfg, mode=mode)
+    ps, po = _cfg_params(cfg)
+    _check(cfg, imgs, qt, ps, po)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3a", "c3b", "c4", "c5"])
+@pytest.mark.parametrize("quality", [75, 95])
+def test_config_subset_natural(name, quality):
+    cfg = synth.CONFIGS[name]
+    n = {"c2": 6, "c3a": 6, "c3b": 6, "c4": 24, "c5": 2}[name]
+    imgs, qt = synth.distinct_images(cfg, quality=quality, n_distinct=n)
+    ps, po = _cfg_params(cfg)
+    rep = {}
+    _check(cfg, imgs, qt, ps, po, report=rep)
+    # band flips are rare: <= 1e-4 of decoded samples
+    assert rep["flips"] <= 1e-4 * n * cfg.width * cfg.height * 1.5 + 3
+
+
+@pytest.mark.parametrize("name", ["c2", "c3a", "c3b", "c4"])
+def test_config_subset_stress(name):
+    cfg = synth.CONFIGS[name]
+    imgs, qt = synth.distinct_images(cfg, mode="stress", n_distinct=3)
+    ps, po = _cfg_params(cfg)
+    _check(cfg, imgs, qt, ps, po)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_tie_free_strict(k):
+    cfg = synth.CONFIGS["c2"]
+    imgs, qt = synth.distinct_images(cfg, quality=95, n_distinct=2)
+    imgs = [helpers.make_tie_free(im, qt, k) for im in imgs]
+    import dataclasses
+    c = dataclasses.replace(cfg, scale_denom=k, resize_short=256 // k if k > 2 else 256,
+                            crop_w=224 // k if k > 2 else 224, crop_h=224 // k if k > 2 else 224)
+    ps, po = _cfg_params(c)
+    _check(c, imgs, qt, ps, po, strict=True)
+
+
+def test_dc_only_closed_form_all_scales():
+    # DC-only blocks, Q = 1: every decoded sample = clamp(floor(DC/8 + 128.5)).
+    qt = np.ones((2, 64), np.uint16)
+    rng = np.random.default_rng(5)
+    for k in (1, 2, 4, 8):
+        w, h = 128, 128
+        coef = []
+        for (bh, bw) in ((16, 16), (8, 8), (8, 8)):
+            c = np.zeros((bh, bw, 64), np.int16)
+            c[..., 0] = rng.integers(-2048, 2048, size=(bh, bw))
+            coef.append(c)
+        im = synth.CoefImage(w, h, coef)
+        P = 8 // k
+        ps = smol.make_params(scale_denom=k, resize_mode="exact", resize_w=w // k, resize_h=h // k)
+        plan = smol.Plan(ps, 1)
+        batch = smol.CoefBatch([im], qt)
+        g = smol.geometry(ps, w, h)
+        _, y, cb, cr, _ = plan.debug_run(batch, [g])
+        torch.cuda.synchronize()
+        for ci, t in enumerate((y, cb, cr)):
+            hh, ww = (g["Hd"], g["Wd"]) if ci == 0 else (g["Hc"], g["Wc"])
+            got = t[0].cpu().numpy()[:hh * ww].reshape(hh, ww)
+            exp = np.clip(np.floor(coef[ci][..., 0] / 8 + 128.5), 0, 255)
+            exp = np.repeat(np.repeat(exp, P, 0), P, 1)[:hh, :ww]
+            m = got >= 0
+            assert np.array_equal(got[m], exp[m].astype(np.int16)), (k, ci)
+        plan.close()
+
+
+def test_roi_poison_invariance():
+    # Blocks outside the ROI ranges must not influence the output at all.
+    for name in ("c2", "c3a", "c3b", "c4", "c5"):
+        cfg = synth.CONFIGS[name]
+        imgs, qt = synth.distinct_images(cfg, n_distinct=2)
+        ps, _ = _cfg_params(cfg)
+        plan = smol.Plan(ps, 2)
+        clean = plan.run(smol.CoefBatch(imgs, qt)).clone()
+        poisoned = []
+        for im in imgs:
+            g = smol.geometry(ps, im.width, im.height)
+            coef = []
+            for ci in range(3):
+                c = im.coef[ci].copy()
+                keep = np.zeros(c.shape[:2], bool)
+                keep[g["by0"][ci]:g["by1"][ci] + 1, g["bx0"][ci]:g["bx1"][ci] + 1] = True
+                c[~keep] = np.where(np.random.default_rng(ci).random((int((~keep).sum()), 64)) < 0.5,
+                                    32767, -32768)
+                coef.append(c)
+            poisoned.append(synth.CoefImage(im.width, im.height, coef))
+        dirty = plan.run(smol.CoefBatch(poisoned, qt))
+        torch.cuda.synchronize()
+        assert torch.equal(clean, dirty), name
+        plan.close()
+
+
+def test_heterogeneous_sizes_and_permutation():
+    rng = np.random.default_rng(77)
+    qt = synth.quant_tables(75)
+    sizes = [(500, 375), (375, 500), (333, 500), (97, 61), (61, 97), (256, 256), (231, 240), (640, 480)]
+    imgs = [synth.make_image(rng, w, h, qt) for (w, h) in sizes]
+    cfg = synth.Config("het", len(imgs), 0, 0, 2, "short", resize_short=128, crop_w=96, crop_h=96)
+    ps, po = _cfg_params(cfg)
+    out = _check(cfg, imgs, qt, ps, po)
+    perm = [5, 2, 7, 0, 1, 6, 3, 4]
+    plan = smol.Plan(ps, len(imgs))
+    out2 = plan.run(smol.CoefBatch([imgs[i] for i in perm], qt)).cpu().numpy()
+    assert np.array_equal(out2, out[perm])
+    plan.close()
+
+
+def test_explicit_roi_and_upscale():
+    rng = np.random.default_rng(78)
+    qt = synth.quant_tables(90)
+    imgs = [synth.make_image(rng, 120, 90, qt) for _ in range(3)]
+    cfg = synth.Config("roi", 3, 120, 90, 1, "exact", resize_w=300, resize_h=200, crop_w=64, crop_h=48)
+    ps, po = _cfg_params(cfg)
+    rois = [(0, 0), (236, 152), (101, 77)]
+    _check(cfg, imgs, qt, ps, po, rois=rois)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_tiny_and_odd_images(k):
+    rng = np.random.default_rng(79 + k)
+    qt = synth.quant_tables(75)
+    sizes = [(1, 1), (8, 8), (15, 9), (17, 33), (16, 1), (3, 40)]
+    imgs = [synth.make_image(rng, w, h, qt, "stress") for (w, h) in sizes]
+    cfg = synth.Config("tiny", len(imgs), 0, 0, k, "exact", resize_w=7, resize_h=5)
+    ps, po = _cfg_params(cfg)
+    _check(cfg, imgs, qt, ps, po)
+
+
+@pytest.mark.parametrize("tile_rows", [1, 7, 64, 224])
+def test_tile_rows_invariance(tile_rows):
+    cfg = synth.CONFIGS["c2"]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=2)
+    ps0, _ = _cfg_params(cfg)
+    ref = smol.Plan(ps0, 2).run(smol.CoefBatch(imgs, qt))
+    ps, _ = _cfg_params(cfg, tile_rows=tile_rows)
+    try:
+        out = smol.Plan(ps, 2).run(smol.CoefBatch(imgs, qt))
+    except smol.SmolError as e:
+        assert e.status == 5 and tile_rows == 224      # too much smem for a 224-row tile
+        return
+    torch.cuda.synchronize()
+    assert torch.equal(ref, out)
+
+
+def test_run_host_pinned_equals_device():
+    cfg = synth.CONFIGS["c2"]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=4)
+    ps, _ = _cfg_params(cfg)
+    plan = smol.Plan(ps, 4)
+    a = plan.run(smol.CoefBatch(imgs, qt, location="device"))
+    b = plan.run(smol.CoefBatch(imgs, qt, location="pinned"))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_errors_and_empty():
+    cfg = synth.CONFIGS["c1"]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=3)
+    ps, _ = _cfg_params(cfg)
+    plan = smol.Plan(ps, 2)
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(smol.CoefBatch(imgs, qt))
+    assert e.value.status == 5
+    b = smol.CoefBatch(imgs[:2], qt)
+    b.descs[1].blocks_w[1] = 1
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(b)
+    assert e.value.status == 1 and "image 1" in str(e.value)
+    b0 = smol.CoefBatch(imgs[:2], qt)
+    b0.desc.n_images = 0
+    out = plan.new_output(1)
+    plan.run(b0, out=out)            # no-op
+
+
+def _sample_check(name, n_sample, quality=75):
+    """Full BASELINE.json size in the bench's launch configuration; the oracle
+    checks sampled images one by one."""
+    cfg = synth.CONFIGS[name]
+    imgs, qt = synth.batch_images(cfg, quality=quality)
+    ps, po = _cfg_params(cfg)
+    plan = smol.Plan(ps, cfg.n)
+    out = plan.run(smol.CoefBatch(imgs, qt))
+    torch.cuda.synchronize()
+    assert tuple(out.shape) == (cfg.n, 3) + cfg.out_hw
+    assert torch.isfinite(out.float()).all()
+    idx = np.linspace(0, cfg.n - 1, n_sample).astype(int)
+    tol = TOL[cfg.out_dtype] + 2.0 / (255 * min(synth.IMAGENET_STD))   # band-widened
+    strict_ok = 0
+    for i in idx:
+        ref = oracle.run_image(po, imgs[i], qt).astype(np.float64)
+        err = float(np.max(np.abs(out[i].float().cpu().numpy() - ref)))
+        assert err <= tol, (name, i, err)
+        strict_ok += err <= TOL[cfg.out_dtype]
+    assert strict_ok >= len(idx) - 1
+    # replicated images must produce identical outputs anywhere in the batch
+    d = len({id(im) for im in imgs})
+    if cfg.n > d:
+        assert torch.equal(out[0], out[d])
+    plan.close()
+
+
+@pytest.mark.parametrize("name,n_sample", [("c2", 8), ("c3a", 8), ("c3b", 8), ("c4", 64), ("c5", 3)])
+def test_full_size_sampled(name, n_sample):
+    _sample_check(name, n_sample)
