@@ -113,14 +113,14 @@ def _cpu_baseline(cfg, imgs, qt, budget_s: float, max_images: int):
     t0 = time.perf_counter()
     oracle.run_image(po, imgs[0], qt)
     t1 = time.perf_counter() - t0
-    n = int(max(1, min(max_images, round(budget_s * cores / max(t1, 1e-6)))))
+    n = int(max(1, min(max_images, round(budget_s * cores / max(t1, 1e-6)))))   # ~budget_s of CPU work
     sample = [imgs[i % len(imgs)] for i in range(n)]
     t0 = time.perf_counter()
     with ThreadPoolExecutor(cores) as ex:
         list(ex.map(lambda im: oracle.run_image(po, im, qt), sample))
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} of the {cfg.n} {cfg.name} images ({cfg.width}x{cfg.height}), "
+            "sample": f"{n} {cfg.name} images ({cfg.width}x{cfg.height}, cycling the batch), "
                       f"thread pool of {cores} over images, {dt:.1f} s wall",
             "seconds": dt}
 
@@ -311,7 +311,7 @@ def main():
             line["clocks"] = c
         if world == 1 and not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = _cpu_baseline(cfg, imgs[:64], qt, args.cpu_budget, cfg.n)
+                line["cpu_baseline"] = _cpu_baseline(cfg, imgs[:64], qt, args.cpu_budget, 16 * cfg.n)
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)

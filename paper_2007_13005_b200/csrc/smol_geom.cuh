@@ -15,7 +15,10 @@ namespace smol {
 
 constexpr int kThreads = 256;             // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
-constexpr int kScratchPitch = 9;          // floats per row of the IDCT transpose scratch
+constexpr int kStepRows = 16;             // decoded luma rows per rolling step (one MCU row at scale 1)
+constexpr int kYRing = 32;                // luma rows kept in smem (two steps)
+constexpr int kCRing = 16;                // chroma rows kept per component (two steps)
+constexpr int kRgbRing = 32;              // RGB rows kept
 
 SMOL_HD int ceil_div(int a, int b) { return (a + b - 1) / b; }
 SMOL_HD int imin(int a, int b) { return a < b ? a : b; }
@@ -26,6 +29,7 @@ struct __align__(16) DevImage {
   const int16_t* coef[3];   // block-raster [bh][bw][64] int16, natural order
   int32_t stride[3];        // int16 elements per block row
   int32_t qidx[3];          // quant table index per component
+  int32_t nbw[3];           // valid block columns per component: ceil(W/8), ceil(W/16)
   int32_t Wd, Hd;           // decoded luma size at scale 1/k (R4)
   int32_t Wc, Hc;           // decoded chroma size
   int32_t Wr, Hr;           // resized size
@@ -47,25 +51,29 @@ SMOL_HD void src_tap(int d, int in, int out, int& i0, int& i1, float& w) {
   i1 = imin(i0 + 1, in - 1);
 }
 
-// Footprint of output rows [oy0, oy1) x all OW columns, and the shared-memory
-// carve-up of the CTA that processes it.
+SMOL_HD int align16(int x) { return (x + 15) & ~15; }
+
+// Footprint of the output tile rows [oy0, oy1) x cols [ox0, ox1) and the
+// shared-memory carve-up of the CTA that processes it.
 struct TileLayout {
+  int oy0, oy1, ox0, ox1;          // output tile
   int ly0, ly1, lx0, lx1;          // luma (decoded) tap footprint, inclusive
-  int cy0, cy1, cx0, cx1;          // chroma footprint incl. triangle neighbours
+  int cy0, cy1, cx0, cx1;          // chroma footprint incl. triangle neighbours (R2)
   int by0[3], by1[3], bx0[3], bx1[3];   // ROI block ranges per component
-  int pitch[3], rows[3];           // u8 plane geometry in smem (pitch in bytes)
-  int nly, nlx;                    // footprint size (RGB buffer)
+  int pitch[3];                    // bytes per ring row of the u8 planes
+  int xbase[3];                    // decoded column of ring byte 0 (= bx0 * P)
+  int rgb_x0, rgb_w;               // RGB ring: first column (even) and width (even), u32 units
+  int r0, nsteps;                  // first rolling-step row (16-aligned) and step count
   // byte offsets in dynamic shared memory
   int off_q, off_xt, off_yt, off_pl[3], off_rgb, total;
 };
 
-SMOL_HD int align16(int x) { return (x + 15) & ~15; }
-
-SMOL_HD void tile_layout(const DevImage& im, int K, int OW, int oy0, int oy1, TileLayout& L) {
+SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, int ox1, TileLayout& L) {
   const int P = 8 / K;
   int a, b; float w;
-  src_tap(im.left, im.Wd, im.Wr, L.lx0, b, w);
-  src_tap(im.left + OW - 1, im.Wd, im.Wr, a, L.lx1, w);
+  L.oy0 = oy0; L.oy1 = oy1; L.ox0 = ox0; L.ox1 = ox1;
+  src_tap(im.left + ox0, im.Wd, im.Wr, L.lx0, b, w);
+  src_tap(im.left + ox1 - 1, im.Wd, im.Wr, a, L.lx1, w);
   src_tap(im.top + oy0, im.Hd, im.Hr, L.ly0, b, w);
   src_tap(im.top + oy1 - 1, im.Hd, im.Hr, a, L.ly1, w);
   // chroma rows/cols used by the centred triangle filter of luma rows
@@ -74,27 +82,32 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int OW, int oy0, int oy1, Ti
   L.cy1 = imin(im.Hc - 1, (L.ly1 + 1) >> 1);
   L.cx0 = imax(0, (L.lx0 - 1) >> 1);
   L.cx1 = imin(im.Wc - 1, (L.lx1 + 1) >> 1);
+  // luma columns are processed in even/odd pairs: widen to even alignment
+  // (never beyond the image's valid block columns)
   L.by0[0] = L.ly0 / P; L.by1[0] = L.ly1 / P;
-  L.bx0[0] = L.lx0 / P; L.bx1[0] = L.lx1 / P;
+  L.bx0[0] = (L.lx0 & ~1) / P;
+  L.bx1[0] = imin((L.lx1 | 1) / P, im.nbw[0] - 1);
   for (int c = 1; c < 3; ++c) {
     L.by0[c] = L.cy0 / P; L.by1[c] = L.cy1 / P;
     L.bx0[c] = L.cx0 / P; L.bx1[c] = L.cx1 / P;
   }
   for (int c = 0; c < 3; ++c) {
-    L.pitch[c] = ((L.bx1[c] - L.bx0[c] + 1) * P + 3) & ~3;
-    L.rows[c] = (L.by1[c] - L.by0[c] + 1) * P;
+    L.xbase[c] = L.bx0[c] * P;
+    L.pitch[c] = (((L.bx1[c] - L.bx0[c] + 1) * P + 2) + 7) & ~7;   // + pair slack, 8-B rows
   }
-  L.nly = L.ly1 - L.ly0 + 1;
-  L.nlx = L.lx1 - L.lx0 + 1;
+  L.rgb_x0 = L.lx0 & ~1;
+  L.rgb_w = ((L.lx1 | 1) - L.rgb_x0 + 1);
+  L.r0 = L.ly0 & ~(kStepRows - 1);
+  // the last step must cover luma row ly1 and chroma row cy1 (luma 2 cy1)
+  L.nsteps = ((imax(L.ly1, 2 * L.cy1) - L.r0) / kStepRows) + 1;
   int off = 0;
-  L.off_q = off;   off += 3 * 64 * 4;                       // dequant table (float)
-  L.off_xt = off;  off += align16(OW * 8);                  // x taps: int2{i0|i1<<16, w}
-  L.off_yt = off;  off += align16((oy1 - oy0) * 8);         // y taps
-  for (int c = 0; c < 3; ++c) { L.off_pl[c] = off; off += align16(L.pitch[c] * L.rows[c]); }
-  L.off_rgb = off;
-  int rgb = L.nly * L.nlx * 4;
-  int scratch = kWarps * 4 * 8 * kScratchPitch * 4;         // IDCT transpose (aliases RGB)
-  off += align16(rgb > scratch ? rgb : scratch);
+  L.off_q = off;   off += 3 * 64 * 4;                         // dequant tables (float)
+  L.off_xt = off;  off += align16((ox1 - ox0) * 8);           // x taps: {x0 | x1<<16, w}
+  L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {y0 | y1<<16, w}
+  L.off_pl[0] = off; off += align16(L.pitch[0] * kYRing);
+  L.off_pl[1] = off; off += align16(L.pitch[1] * kCRing);
+  L.off_pl[2] = off; off += align16(L.pitch[2] * kCRing);
+  L.off_rgb = off;   off += align16(L.rgb_w * 4 * kRgbRing);
   L.total = off;
 }
 
@@ -103,5 +116,22 @@ SMOL_HD long long tile_roi_blocks(const TileLayout& L) {
   for (int c = 0; c < 3; ++c) n += (long long)(L.by1[c] - L.by0[c] + 1) * (L.bx1[c] - L.bx0[c] + 1);
   return n;
 }
+
+// Last RGB row computable after rolling step s (decoded luma rows
+// [r0 + 16 s, r0 + 16 s + 16) and chroma rows [.. /2, +8) are decoded):
+// luma row L needs chroma rows L>>1 and, for odd L, min(L>>1 + 1, Hc - 1).
+SMOL_HD int ready_after(const TileLayout& L, int Hc, int s) {
+  const int R = L.r0 + kStepRows * s;
+  const int chi = imin(L.cy1, (R >> 1) + kStepRows / 2 - 1);
+  int r = imin(L.ly1, R + kStepRows - 1);
+  if (chi < Hc - 1) r = imin(r, 2 * chi);
+  return r;
+}
+
+// Magic-number division for 0 <= n < 2^16, 1 <= d < 2^16.
+struct FastDiv {
+  uint32_t d, m;
+};
+SMOL_HD FastDiv make_fastdiv(uint32_t d) { return FastDiv{d, d <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / d) + 1u}; }
 
 }  // namespace smol

@@ -1,18 +1,20 @@
 // smol_kernels.cuh -- the fused sm_100a kernel of the Smol preprocessing hot
 // path: dequantize -> scaled IDCT -> u8 -> 4:2:0 upsample -> YCbCr->RGB ->
-// bilinear resize + crop -> normalize -> NCHW, one CTA per (image, tile of
-// output rows).  Decoded pixels live only in shared memory.
+// bilinear resize + crop -> normalize -> NCHW.  One CTA per (image, output
+// tile); decoded pixels live only in shared memory.
 //
-// Per CTA (256 threads):
-//   stage 0  tile geometry, dequant table (Q/8 in fp32), per-column and
-//            per-row bilinear taps (exact-integer coordinates, R9)
-//   stage 1  every ROI block of the tile (Y, Cb, Cr): 8 lanes per block, lane
-//            = coefficient row; one 128-bit load per lane (a warp reads 4
-//            consecutive blocks = 512 contiguous bytes); row pass in
-//            registers; transpose through smem; column pass; round/clamp to
-//            u8 with one F2I.U8.FLOOR (reading R3) into the u8 planes
-//   stage 2  upsample + colour for every footprint pixel -> packed RGBx u32
-//   stage 3  bilinear + normalize per output pixel, coalesced NCHW stores
+// Each CTA walks its tile's decoded-row footprint in 16-row steps (one MCU
+// row at scale 1) with rolling shared-memory windows, so every coefficient
+// block under the footprint is read and transformed once per tile:
+//   step s:  IDCT   the ROI blocks of luma rows [R, R+16) and chroma rows
+//                   [R/2, R/2+8) (thread per block; warp-uniform pruning of
+//                   all-zero high rows/columns) -> u8 Y / Cb / Cr rings
+//            sync
+//            colour RGB rows (ready_{s-1}, ready_s]: 4:2:0 triangle upsample
+//                   of an even/odd luma pair + exact JFIF -> packed RGBx ring
+//            sync
+//            output every output row whose lower tap row is ready: bilinear
+//                   + FMA normalize, 2 pixels per thread, NCHW stores
 #pragma once
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -27,63 +29,62 @@ namespace smol {
 //   a2[j][u] = 1/2 sum_{x=2j}^{2j+1} t[u][x], j < 2    (a2[j][0] = 1, a2[j][4] = 0 exactly)
 //   a4[u]    = 1/4 sum_{x=0}^{3} t[u][x]               (a4[0] = 1; 0 for u = 2, 4, 6)
 // Output j and P-1-j are mirror images: t[u][7-x] = (-1)^u t[u][x] (same for a_k).
+// Colour: kR, kB = fl32(1.402/16), fl32(1.772/16); cR, cB = fl32(1/2 - 2048 kR),
+// fl32(1/2 - 2048 kB) + 2^-13 (see colour()).
 struct Basis {
   float t[8][4];
   float a2[2][8];
   float a4[8];
+  float kR, kB, cR, cB;
 };
 
 __constant__ Basis c_basis;
 
-// 1-D transforms (reading R1, Definition A; separable form of the oracle's
-// sum).  in[u], u = 0..7  ->  out[j], j = 0..P-1.  The FMA chains start from
-// in[0] (weight exactly 1) and the exact +-1 / 0 entries so that DC-only and
-// {0,4}-only inputs are transformed exactly.
-template <int K> struct Idct1D;
-
-template <> struct Idct1D<1> {
-  static __device__ __forceinline__ void run(const float (&d)[8], float (&o)[8]) {
+// ------------------------------------------------------------ 1-D IDCTs ---
+// Reading R1 (Definition A), separable form of the oracle's sum.  in[u],
+// u < W nonzero (u >= W known zero, compile-time)  ->  out[j], j < P.  The
+// FMA chains start from in[0] (weight exactly 1) and the exact +-1 / 0
+// entries so that DC-only and {0,4}-only inputs are transformed exactly.
+template <int W>
+__device__ __forceinline__ void idct8(const float (&d)[8], float (&o)[8]) {
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      float e = fmaf(d[4], c_basis.t[4][x], d[0]);
-      e = fmaf(d[2], c_basis.t[2][x], e);
-      e = fmaf(d[6], c_basis.t[6][x], e);
-      float od = d[1] * c_basis.t[1][x];
-      od = fmaf(d[3], c_basis.t[3][x], od);
-      od = fmaf(d[5], c_basis.t[5][x], od);
-      od = fmaf(d[7], c_basis.t[7][x], od);
-      o[x] = e + od;
-      o[7 - x] = e - od;
-    }
+  for (int x = 0; x < 4; ++x) {
+    float e = d[0];
+    if (W > 4) e = fmaf(d[4], c_basis.t[4][x], e);
+    if (W > 2) e = fmaf(d[2], c_basis.t[2][x], e);
+    if (W > 6) e = fmaf(d[6], c_basis.t[6][x], e);
+    float od = 0.f;
+    if (W > 1) od = d[1] * c_basis.t[1][x];
+    if (W > 3) od = fmaf(d[3], c_basis.t[3][x], od);
+    if (W > 5) od = fmaf(d[5], c_basis.t[5][x], od);
+    if (W > 7) od = fmaf(d[7], c_basis.t[7][x], od);
+    if (W > 1) { o[x] = e + od; o[7 - x] = e - od; }
+    else { o[x] = e; o[7 - x] = e; }
   }
-};
+}
 
-template <> struct Idct1D<2> {
-  static __device__ __forceinline__ void run(const float (&d)[8], float (&o)[4]) {
+__device__ __forceinline__ void idct4(const float (&d)[8], float (&o)[4]) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      float e = fmaf(d[2], c_basis.a2[j][2], d[0]);
-      e = fmaf(d[6], c_basis.a2[j][6], e);
-      float od = d[1] * c_basis.a2[j][1];
-      od = fmaf(d[3], c_basis.a2[j][3], od);
-      od = fmaf(d[5], c_basis.a2[j][5], od);
-      od = fmaf(d[7], c_basis.a2[j][7], od);
-      o[j] = e + od;
-      o[3 - j] = e - od;
-    }
+  for (int j = 0; j < 2; ++j) {
+    float e = fmaf(d[2], c_basis.a2[j][2], d[0]);
+    e = fmaf(d[6], c_basis.a2[j][6], e);
+    float od = d[1] * c_basis.a2[j][1];
+    od = fmaf(d[3], c_basis.a2[j][3], od);
+    od = fmaf(d[5], c_basis.a2[j][5], od);
+    od = fmaf(d[7], c_basis.a2[j][7], od);
+    o[j] = e + od;
+    o[3 - j] = e - od;
   }
-};
+}
 
-template <> struct Idct1D<4> {
-  static __device__ __forceinline__ void run(const float (&d)[8], float (&o)[2]) {
-    float od = d[1] * c_basis.a4[1];
-    od = fmaf(d[3], c_basis.a4[3], od);
-    od = fmaf(d[5], c_basis.a4[5], od);
-    od = fmaf(d[7], c_basis.a4[7], od);
-    o[0] = d[0] + od;
-    o[1] = d[0] - od;
-  }
-};
+__device__ __forceinline__ void idct2(const float (&d)[8], float (&o)[2]) {
+  float od = d[1] * c_basis.a4[1];
+  od = fmaf(d[3], c_basis.a4[3], od);
+  od = fmaf(d[5], c_basis.a4[5], od);
+  od = fmaf(d[7], c_basis.a4[7], od);
+  o[0] = d[0] + od;
+  o[1] = d[0] - od;
+}
 
 // Reading R3: clamp(floor(v + 128 + 1/2), 0, 255) in one F2I.U8.FLOOR (cvt
 // saturates to the u8 range).
@@ -92,230 +93,407 @@ __device__ __forceinline__ uint32_t round_u8(float v) {
   asm("cvt.rmi.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(v + 128.5f));
   return r;
 }
+__device__ __forceinline__ uint32_t floor_u8(float v) {
+  uint32_t r;
+  asm("cvt.rmi.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+
+__device__ __forceinline__ void unpack_row(const int4 r, float (&d)[8]) {
+  d[0] = (float)(int16_t)(r.x & 0xffff); d[1] = (float)(r.x >> 16);
+  d[2] = (float)(int16_t)(r.y & 0xffff); d[3] = (float)(r.y >> 16);
+  d[4] = (float)(int16_t)(r.z & 0xffff); d[5] = (float)(r.z >> 16);
+  d[6] = (float)(int16_t)(r.w & 0xffff); d[7] = (float)(r.w >> 16);
+}
+
+// Full-scale block: row pass over the H nonzero rows (warp max), column pass
+// with the H-row input set; W = warp max nonzero column + 1.
+template <int W>
+__device__ __forceinline__ void idct_rows(const int4 (&raw)[8], const float* q, int H, float (&m)[8][8]) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    if (v < H) {
+      float d[8];
+      unpack_row(raw[v], d);
+      const float4 q0 = *reinterpret_cast<const float4*>(q + v * 8);
+      const float4 q1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
+      d[0] *= q0.x; d[1] *= q0.y; d[2] *= q0.z; d[3] *= q0.w;
+      d[4] *= q1.x; d[5] *= q1.y; d[6] *= q1.z; d[7] *= q1.w;
+      idct8<W>(d, m[v]);
+    }
+  }
+}
+
+template <int H>
+__device__ __forceinline__ void idct_cols_store(const float (&m)[8][8], uint8_t* dst, int pitch, int row0,
+                                                int rmask) {
+  uint32_t px[8][2];
+#pragma unroll
+  for (int x = 0; x < 8; ++x) {
+    float col[8], f[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) col[v] = (v < H) ? m[v][x] : 0.f;
+    idct8<H>(col, f);
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const uint32_t b = round_u8(f[y]);
+      if (x == 0) px[y][0] = b;
+      else if (x < 4) px[y][0] |= b << (8 * x);
+      else if (x == 4) px[y][1] = b;
+      else px[y][1] |= b << (8 * (x - 4));
+    }
+  }
+#pragma unroll
+  for (int y = 0; y < 8; ++y)
+    *reinterpret_cast<uint2*>(dst + ((row0 + y) & rmask) * pitch) = make_uint2(px[y][0], px[y][1]);
+}
+
+// Decode one block at scale 1/K into the ring plane (ring of `ring` rows).
+// `act` = this lane has a block; every lane of the warp must call it (warp
+// reductions pick the nonzero row/column extents).
+template <int K>
+__device__ __forceinline__ void decode_block(bool act, const int16_t* src, const float* q, uint8_t* plane,
+                                             int pitch, int ring, int row0, int col0) {
+  constexpr int P = 8 / K;
+  if constexpr (K == 8) {
+    if (act) plane[(row0 & (ring - 1)) * pitch + col0] = (uint8_t)round_u8((float)__ldg(src) * q[0]);
+  } else if constexpr (K == 1) {
+    int4 raw[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      raw[v] = act ? __ldg(reinterpret_cast<const int4*>(src) + v) : make_int4(0, 0, 0, 0);
+    uint32_t rows = 0;
+    int4 acc = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      rows |= ((raw[v].x | raw[v].y | raw[v].z | raw[v].w) != 0) << v;
+      acc.x |= raw[v].x; acc.y |= raw[v].y; acc.z |= raw[v].z; acc.w |= raw[v].w;
+    }
+    const int wcol = acc.w ? ((acc.w >> 16) ? 8 : 7) : acc.z ? ((acc.z >> 16) ? 6 : 5)
+                   : acc.y ? ((acc.y >> 16) ? 4 : 3) : ((acc.x >> 16) ? 2 : 1);
+    const int H = max(1, (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows)));
+    const int W = (int)__reduce_max_sync(0xffffffffu, (uint32_t)wcol);
+    float m[8][8];
+    switch (W) {
+      case 1: idct_rows<1>(raw, q, H, m); break;
+      case 2: idct_rows<2>(raw, q, H, m); break;
+      case 3: idct_rows<3>(raw, q, H, m); break;
+      case 4: idct_rows<4>(raw, q, H, m); break;
+      case 5: idct_rows<5>(raw, q, H, m); break;
+      case 6: idct_rows<6>(raw, q, H, m); break;
+      case 7: idct_rows<7>(raw, q, H, m); break;
+      default: idct_rows<8>(raw, q, H, m); break;
+    }
+    if (act) {
+      uint8_t* dst = plane + col0;
+      switch (H) {
+        case 1: idct_cols_store<1>(m, dst, pitch, row0, ring - 1); break;
+        case 2: idct_cols_store<2>(m, dst, pitch, row0, ring - 1); break;
+        case 3: idct_cols_store<3>(m, dst, pitch, row0, ring - 1); break;
+        case 4: idct_cols_store<4>(m, dst, pitch, row0, ring - 1); break;
+        case 5: idct_cols_store<5>(m, dst, pitch, row0, ring - 1); break;
+        case 6: idct_cols_store<6>(m, dst, pitch, row0, ring - 1); break;
+        case 7: idct_cols_store<7>(m, dst, pitch, row0, ring - 1); break;
+        default: idct_cols_store<8>(m, dst, pitch, row0, ring - 1); break;
+      }
+    }
+  } else {
+    // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7})
+    float g[8][P];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      if ((K == 2 && v == 4) || (K == 4 && (v == 2 || v == 4 || v == 6))) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) g[v][j] = 0.f;
+        continue;
+      }
+      float d[8];
+      unpack_row(act ? __ldg(reinterpret_cast<const int4*>(src) + v) : make_int4(0, 0, 0, 0), d);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d[u] *= q[v * 8 + u];
+      float o[P];
+      if constexpr (K == 2) idct4(d, o); else idct2(d, o);
+#pragma unroll
+      for (int j = 0; j < P; ++j) g[v][j] = o[j];
+    }
+    if (act) {
+      uint32_t px[P];
+#pragma unroll
+      for (int x = 0; x < P; ++x) {
+        float col[8], f[P];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) col[v] = g[v][x];
+        if constexpr (K == 2) idct4(col, f); else idct2(col, f);
+#pragma unroll
+        for (int y = 0; y < P; ++y) {
+          const uint32_t b = round_u8(f[y]);
+          px[y] = (x == 0) ? b : (px[y] | (b << (8 * x)));
+        }
+      }
+#pragma unroll
+      for (int y = 0; y < P; ++y) {
+        uint8_t* d = plane + ((row0 + y) & (ring - 1)) * pitch + col0;
+        if constexpr (K == 2) *reinterpret_cast<uint32_t*>(d) = px[y];
+        else *reinterpret_cast<uint16_t*>(d) = (uint16_t)px[y];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- colour -----
+// Reading R6.  R and B in fp32: t = c16 * k + (Y + c), floor+clamp in one
+// F2I.U8.FLOOR.  Exactness: the fractional parts of the exact values are
+// multiples of 1/8000 (R) and 1/4000 (B); the fp32 evaluation error is
+// < 6.1e-5 and cB carries a +2^-13 bias so that B's two exact ties
+// (Cb - 128 = +-125) round up; both bounds are verified exhaustively over all
+// (Y, c16) by tests/test_color_fp32.py.  G = Y + floor((K1 - 43017 cb16 -
+// 89267 cr16) / 2e6) - 136 in exact unsigned integers (K1 = 543917632).
+__device__ __forceinline__ uint32_t colour(int Y, int cb16, int cr16) {
+  const float yf = (float)Y;
+  const uint32_t R = floor_u8(fmaf((float)cr16, c_basis.kR, yf + c_basis.cR));
+  const uint32_t B = floor_u8(fmaf((float)cb16, c_basis.kB, yf + c_basis.cB));
+  const uint32_t u = 543917632u - 43017u * (uint32_t)cb16 - 89267u * (uint32_t)cr16;
+  const int G = min(max(Y + (int)(u / 2000000u) - 136, 0), 255);
+  return R | ((uint32_t)G << 8) | (B << 16);
+}
+
+__device__ __forceinline__ int ldu8(const uint8_t* p) { return *p; }
 
 struct KParams {
   const DevImage* imgs;
   const uint16_t* qtables;
   void* out;
-  int OW, OH, tile_rows;
+  int OW, OH, tile_rows, tile_cols, n_col_tiles;
   float na[3], nb[3];              // y = x * na + nb = (x/255 - mean)/std
   int16_t* dbg_pl[3];              // debug planes (DEBUG instantiation only)
   int16_t* dbg_rgb;
   long long dbg_stride_y, dbg_stride_c, dbg_stride_rgb;
 };
 
-// Reading R6, exact JFIF in integers: with chroma c16 in 1/16 units and
-// d = c16 - 2048,  R = Y + floor((175250 dR + 10^6) / (2*10^6)),
-// G = Y + floor((-43017 dB - 89267 dR + 10^6) / (2*10^6)),
-// B = Y + floor((221500 dB + 10^6) / (2*10^6))   (1.402/16 = 175250/2e6 ...).
-// floor division of a possibly negative numerator via an unsigned bias of
-// 256 * 2e6 (all numerators stay below 2^31).
-__device__ __forceinline__ int jfif_offset(int num) {
-  return (int)((uint32_t)(num + 1000000 + 512000000) / 2000000u) - 256;
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return f.d <= 1 ? n : __umulhi(n, f.m);
 }
-__device__ __forceinline__ uint32_t clamp255(int x) { return (uint32_t)min(max(x, 0), 255); }
+
+// byte b of x as float, via the 2^23 magic (ALU + FMA pipes, no I2F)
+__device__ __forceinline__ float byte_f(uint32_t x, int b) {
+  return __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540 + b)) - 8388608.f;
+}
 
 template <int K, bool F16, bool DEBUG>
 __global__ void __launch_bounds__(kThreads, 2)
 smol_fused_kernel(const KParams kp) {
   constexpr int P = 8 / K;                 // decoded samples per block side
   extern __shared__ __align__(16) uint8_t smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int n = blockIdx.y;
-  const int oy0 = blockIdx.x * kp.tile_rows;
-  const int oy1 = min(kp.OH, oy0 + kp.tile_rows);
-  const int OW = kp.OW;
+  const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
+  const int oy0 = trow * kp.tile_rows, oy1 = min(kp.OH, oy0 + kp.tile_rows);
+  const int ox0 = tcol * kp.tile_cols, ox1 = min(kp.OW, ox0 + kp.tile_cols);
 
-  // Descriptor and tile geometry live in shared memory: per-component fields
-  // are indexed with a runtime component id (no local-memory arrays).
   __shared__ DevImage im;
   __shared__ TileLayout L;
   if (tid == 0) {
     im = kp.imgs[n];
-    tile_layout(im, K, OW, oy0, oy1, L);
+    tile_layout(im, K, oy0, oy1, ox0, ox1, L);
   }
   __syncthreads();
   float* qf = reinterpret_cast<float*>(smem + L.off_q);
   int2* xt = reinterpret_cast<int2*>(smem + L.off_xt);
   int2* yt = reinterpret_cast<int2*>(smem + L.off_yt);
+  uint8_t* ypl = smem + L.off_pl[0];
+  uint8_t* cbpl = smem + L.off_pl[1];
+  uint8_t* crpl = smem + L.off_pl[2];
   uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + L.off_rgb);
-  float* scratch = reinterpret_cast<float*>(smem + L.off_rgb);   // aliases rgb (stage 1 only)
+  const int ntw = ox1 - ox0, nth = oy1 - oy0;
 
-  // ---- stage 0: dequant table and taps ----------------------------------
-  for (int i = tid; i < 3 * 64; i += kThreads) {
-    const int c = i >> 6;
-    qf[i] = (float)kp.qtables[im.qidx[c] * 64 + (i & 63)] * 0.125f;   // Q/8 (exact)
-  }
-  for (int ox = tid; ox < OW; ox += kThreads) {
+  // ---- prologue: dequant tables (Q/8, exact) and bilinear taps ----------
+  for (int i = tid; i < 3 * 64; i += kThreads)
+    qf[i] = (float)kp.qtables[im.qidx[i >> 6] * 64 + (i & 63)] * 0.125f;
+  for (int i = tid; i < ntw; i += kThreads) {
     int i0, i1; float w;
-    src_tap(im.left + ox, im.Wd, im.Wr, i0, i1, w);
-    xt[ox] = make_int2((i0 - L.lx0) | ((i1 - L.lx0) << 16), __float_as_int(w));
+    src_tap(im.left + ox0 + i, im.Wd, im.Wr, i0, i1, w);
+    xt[i] = make_int2((i0 - L.rgb_x0) | ((i1 - L.rgb_x0) << 16), __float_as_int(w));
   }
-  for (int r = tid; r < oy1 - oy0; r += kThreads) {
+  for (int i = tid; i < nth; i += kThreads) {
     int i0, i1; float w;
-    src_tap(im.top + oy0 + r, im.Hd, im.Hr, i0, i1, w);
-    yt[r] = make_int2((i0 - L.ly0) | ((i1 - L.ly0) << 16), __float_as_int(w));
+    src_tap(im.top + oy0 + i, im.Hd, im.Hr, i0, i1, w);
+    yt[i] = make_int2(i0 | (i1 << 16), __float_as_int(w));
   }
+  const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
+  const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
+  const int npairs = L.rgb_w >> 1;
+  const FastDiv fd_pairs = make_fastdiv(npairs);
+  const int nopairs = (ntw + 1) >> 1;
+  const FastDiv fd_opairs = make_fastdiv(nopairs);
+  const size_t plane_sz = (size_t)kp.OH * kp.OW;
+  int ready_prev = L.ly0 - 1;
+  int done_prev = 0;                       // output rows of the tile finished
   __syncthreads();
 
-  // ---- stage 1: dequantize + scaled IDCT of every ROI block --------------
-  const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nby0 = L.by1[0] - L.by0[0] + 1;
-  const int nbxc = L.bx1[1] - L.bx0[1] + 1, nbyc = L.by1[1] - L.by0[1] + 1;
-  const int nY = nbx0 * nby0, nC = nbxc * nbyc;
-  const int total = nY + 2 * nC;
-  if constexpr (K == 8) {
-    // DC only: v = D(0,0)/8 (all AC basis means vanish exactly), 1 lane/block
-    for (int t = tid; t < total; t += kThreads) {
-      int c, tt, nbx;
-      if (t < nY) { c = 0; tt = t; nbx = nbx0; }
-      else { c = 1 + (t - nY) / nC; tt = (t - nY) - (c - 1) * nC; nbx = nbxc; }
-      const int by = tt / nbx, bx = tt - by * nbx;
-      const int16_t* src = im.coef[c] + (size_t)(L.by0[c] + by) * im.stride[c] + (size_t)(L.bx0[c] + bx) * 64;
-      const float d0 = (float)__ldg(src) * qf[c * 64];
-      smem[L.off_pl[c] + by * L.pitch[c] + bx] = (uint8_t)round_u8(d0);
-    }
-  } else {
-    const int slot = lane >> 3, r = lane & 7;
-    float* sc = scratch + (warp * 4 + slot) * 8 * kScratchPitch;
-    for (int base = warp * 4; base < total; base += kWarps * 4) {
-      const int t = base + slot;
-      const bool act = t < total;
-      int c = 0, by = 0, bx = 0;
-      float d[8];
-      if (act) {
-        int tt, nbx;
-        if (t < nY) { c = 0; tt = t; nbx = nbx0; }
-        else { c = 1 + (t - nY) / nC; tt = (t - nY) - (c - 1) * nC; nbx = nbxc; }
-        by = tt / nbx; bx = tt - by * nbx;
-        const int16_t* src = im.coef[c] + (size_t)(L.by0[c] + by) * im.stride[c] +
-                             (size_t)(L.bx0[c] + bx) * 64 + r * 8;
-        const int4 raw = __ldg(reinterpret_cast<const int4*>(src));
-        const float4 q0 = *reinterpret_cast<const float4*>(qf + c * 64 + r * 8);
-        const float4 q1 = *reinterpret_cast<const float4*>(qf + c * 64 + r * 8 + 4);
-        d[0] = (float)(int16_t)(raw.x & 0xffff) * q0.x; d[1] = (float)(raw.x >> 16) * q0.y;
-        d[2] = (float)(int16_t)(raw.y & 0xffff) * q0.z; d[3] = (float)(raw.y >> 16) * q0.w;
-        d[4] = (float)(int16_t)(raw.z & 0xffff) * q1.x; d[5] = (float)(raw.z >> 16) * q1.y;
-        d[6] = (float)(int16_t)(raw.w & 0xffff) * q1.z; d[7] = (float)(raw.w >> 16) * q1.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) d[i] = 0.f;
+  for (int s = 0; s < L.nsteps; ++s) {
+    const int R = L.r0 + kStepRows * s;
+    // ---- IDCT of this step's ROI blocks --------------------------------
+    const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
+    const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P);
+    const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
+    const int ny = max(0, yb1 - yb0 + 1) * nbx0;
+    const int ncr = max(0, cb1 - cb0 + 1);
+    const int nc = ncr * nbxc;
+    const int ntask = ny + 2 * nc;
+    for (int base = tid & ~31; base < ntask; base += kThreads) {
+      const int t = base + (tid & 31);
+      const bool act = t < ntask;
+      int c = 0, brow = 0, bcol = 0;
+      if (t < ny) {
+        brow = (int)fdiv((uint32_t)t, fd_y);
+        bcol = t - brow * nbx0;
+        brow += yb0;
+      } else if (act) {
+        int tt = t - ny;
+        c = 1 + (tt >= nc);
+        tt -= (c - 1) * nc;
+        brow = (int)fdiv((uint32_t)tt, fd_c);
+        bcol = tt - brow * nbxc;
+        brow += cb0;
       }
-      // row pass: lane r transforms coefficient row v = r along u
-      float g[P];
-      if constexpr (K == 1) Idct1D<1>::run(d, g);
-      else if constexpr (K == 2) Idct1D<2>::run(d, g);
-      else Idct1D<4>::run(d, g);
-#pragma unroll
-      for (int x = 0; x < P; ++x) sc[r * kScratchPitch + x] = g[x];
-      __syncwarp();
-      // column pass: lane r < P owns output column x = r
-      if (act && r < P) {
-        float col[8];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) col[v] = sc[v * kScratchPitch + r];
-        float f[P];
-        if constexpr (K == 1) Idct1D<1>::run(col, f);
-        else if constexpr (K == 2) Idct1D<2>::run(col, f);
-        else Idct1D<4>::run(col, f);
-        uint8_t* dst = smem + L.off_pl[c] + (by * P) * L.pitch[c] + bx * P + r;
-#pragma unroll
-        for (int y = 0; y < P; ++y) dst[y * L.pitch[c]] = (uint8_t)round_u8(f[y]);
-      }
-      __syncwarp();
+      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * 64;
+      uint8_t* plane = smem + L.off_pl[c];
+      const int ring = c ? kCRing : kYRing;
+      decode_block<K>(act, src, qf + c * 64, plane, L.pitch[c], ring, brow * P, bcol * P);
     }
-  }
-  __syncthreads();
+    __syncthreads();
 
-  if constexpr (DEBUG) {
-    for (int c = 0; c < 3; ++c) {
-      const int W = c ? im.Wc : im.Wd, H = c ? im.Hc : im.Hd;
-      const int y0 = c ? L.cy0 : L.ly0, y1 = c ? L.cy1 : L.ly1;
-      const int x0 = c ? L.cx0 : L.lx0, x1 = c ? L.cx1 : L.lx1;
-      int16_t* dst = kp.dbg_pl[c] + n * (c ? kp.dbg_stride_c : kp.dbg_stride_y);
-      for (int y = y0 + warp; y <= y1; y += kWarps)
-        for (int x = x0 + lane; x <= x1; x += 32)
-          if (y < H && x < W)
-            dst[(size_t)y * W + x] = smem[L.off_pl[c] + (y - L.by0[c] * P) * L.pitch[c] + (x - L.bx0[c] * P)];
-    }
-  }
-
-  // ---- stage 2: 4:2:0 triangle upsample + YCbCr->RGB over the footprint --
-  {
-    const uint8_t* Yp = smem + L.off_pl[0];
-    const uint8_t* Cbp = smem + L.off_pl[1];
-    const uint8_t* Crp = smem + L.off_pl[2];
-    const int yorg = L.by0[0] * P, xorg = L.bx0[0] * P;
-    const int cyorg = L.by0[1] * P, cxorg = L.bx0[1] * P;
-    const int cp = L.pitch[1];
-    for (int ry = warp; ry < L.nly; ry += kWarps) {
-      const int ly = L.ly0 + ry;
-      const int j = ly >> 1;
-      const int j2 = min(max((ly & 1) ? j + 1 : j - 1, 0), im.Hc - 1);
-      const int rj = (j - cyorg) * cp, rj2 = (j2 - cyorg) * cp;
-      const uint8_t* yrow = Yp + (ly - yorg) * L.pitch[0] - xorg;
-      uint32_t* orow = rgb + ry * L.nlx - L.lx0;
-      for (int lx = L.lx0 + lane; lx <= L.lx1; lx += 32) {
-        const int i = lx >> 1;
-        const int i2 = min(max((lx & 1) ? i + 1 : i - 1, 0), im.Wc - 1);
-        const int ci = i - cxorg, ci2 = i2 - cxorg;
-        const int cb = 9 * Cbp[rj + ci] + 3 * (Cbp[rj + ci2] + Cbp[rj2 + ci]) + Cbp[rj2 + ci2];
-        const int cr = 9 * Crp[rj + ci] + 3 * (Crp[rj + ci2] + Crp[rj2 + ci]) + Crp[rj2 + ci2];
-        const int Y = yrow[lx];
-        const int dB = cb - 2048, dR = cr - 2048;
-        const uint32_t R = clamp255(Y + jfif_offset(175250 * dR));
-        const uint32_t G = clamp255(Y + jfif_offset(-43017 * dB - 89267 * dR));
-        const uint32_t B = clamp255(Y + jfif_offset(221500 * dB));
-        orow[lx] = R | (G << 8) | (B << 16);
+    if constexpr (DEBUG) {
+      // decoded samples of this step's block rows, clipped to the footprint
+      for (int c = 0; c < 3; ++c) {
+        const int W = c ? im.Wc : im.Wd, Hh = c ? im.Hc : im.Hd;
+        const int rlo = c ? max(cb0 * P, L.cy0) : max(yb0 * P, L.ly0);
+        const int rhi = c ? min((cb1 + 1) * P - 1, L.cy1) : min((yb1 + 1) * P - 1, L.ly1);
+        const int x0 = c ? L.cx0 : L.lx0, x1 = c ? L.cx1 : L.lx1;
+        const int ring = c ? kCRing : kYRing;
+        int16_t* dst = kp.dbg_pl[c] + n * (c ? kp.dbg_stride_c : kp.dbg_stride_y);
+        for (int y = rlo; y <= rhi; ++y)
+          for (int x = x0 + tid; x <= x1; x += kThreads)
+            if (y < Hh && x < W)
+              dst[(size_t)y * W + x] = smem[L.off_pl[c] + (y & (ring - 1)) * L.pitch[c] + (x - L.xbase[c])];
       }
     }
-  }
-  __syncthreads();
 
-  if constexpr (DEBUG) {
-    int16_t* dst = kp.dbg_rgb + n * kp.dbg_stride_rgb;
-    for (int ry = warp; ry < L.nly; ry += kWarps)
-      for (int rx = lane; rx < L.nlx; rx += 32) {
-        const uint32_t v = rgb[ry * L.nlx + rx];
-        const size_t o = ((size_t)(L.ly0 + ry) * im.Wd + (L.lx0 + rx)) * 3;
-        dst[o] = v & 255; dst[o + 1] = (v >> 8) & 255; dst[o + 2] = (v >> 16) & 255;
+    // ---- upsample + colour of the RGB rows that became ready -------------
+    const int ready = max(ready_prev, ready_after(L, im.Hc, s));
+    {
+      const int nrows = ready - ready_prev;
+      const int ntaskc = max(0, nrows) * npairs;
+      const int cxlo = L.cx0, cxhi = L.cx1;
+      for (int t = tid; t < ntaskc; t += kThreads) {
+        const int rr = (int)fdiv((uint32_t)t, fd_pairs);
+        const int p = t - rr * npairs;
+        const int ly = ready_prev + 1 + rr;
+        const int i = (L.rgb_x0 >> 1) + p;                     // chroma column of the pair
+        const int j = ly >> 1;
+        const int j2 = (ly & 1) ? min(j + 1, L.cy1) : max(j - 1, L.cy0);
+        const int im1 = max(i - 1, cxlo) - L.xbase[1], ip1 = min(i + 1, cxhi) - L.xbase[1];
+        const int ic = i - L.xbase[1];
+        const uint8_t* cb_j = cbpl + (j & (kCRing - 1)) * L.pitch[1];
+        const uint8_t* cb_k = cbpl + (j2 & (kCRing - 1)) * L.pitch[1];
+        const uint8_t* cr_j = crpl + (j & (kCRing - 1)) * L.pitch[2];
+        const uint8_t* cr_k = crpl + (j2 & (kCRing - 1)) * L.pitch[2];
+        const int b0 = 3 * ldu8(cb_j + ic), b1 = 3 * ldu8(cb_k + ic);
+        const int cbE = 3 * (b0 + ldu8(cb_j + im1)) + (b1 + ldu8(cb_k + im1));
+        const int cbO = 3 * (b0 + ldu8(cb_j + ip1)) + (b1 + ldu8(cb_k + ip1));
+        const int r0 = 3 * ldu8(cr_j + ic), r1 = 3 * ldu8(cr_k + ic);
+        const int crE = 3 * (r0 + ldu8(cr_j + im1)) + (r1 + ldu8(cr_k + im1));
+        const int crO = 3 * (r0 + ldu8(cr_j + ip1)) + (r1 + ldu8(cr_k + ip1));
+        const uint32_t yy = *reinterpret_cast<const uint16_t*>(
+            ypl + (ly & (kYRing - 1)) * L.pitch[0] + (2 * i - L.xbase[0]));
+        const uint32_t pe = colour(yy & 255, cbE, crE);
+        const uint32_t po = colour(yy >> 8, cbO, crO);
+        *reinterpret_cast<uint2*>(rgb + (ly & (kRgbRing - 1)) * L.rgb_w + 2 * p) = make_uint2(pe, po);
       }
-  }
+    }
+    __syncthreads();
 
-  // ---- stage 3: bilinear + normalize + NCHW store -------------------------
-  {
-    const float na0 = kp.na[0], na1 = kp.na[1], na2 = kp.na[2];
-    const float nb0 = kp.nb[0], nb1 = kp.nb[1], nb2 = kp.nb[2];
-    const size_t plane = (size_t)kp.OH * OW;
-    for (int r = warp; r < oy1 - oy0; r += kWarps) {
-      const int2 ty = yt[r];
-      const float wy = __int_as_float(ty.y);
-      const uint32_t* row0 = rgb + (ty.x & 0xffff) * L.nlx;
-      const uint32_t* row1 = rgb + (ty.x >> 16) * L.nlx;
-      const size_t obase = ((size_t)n * 3 * kp.OH + (oy0 + r)) * OW;
-      for (int ox = lane; ox < OW; ox += 32) {
-        const int2 tx = xt[ox];
-        const float wx = __int_as_float(tx.y);
-        const int x0 = tx.x & 0xffff, x1 = tx.x >> 16;
-        const uint32_t p00 = row0[x0], p01 = row0[x1], p10 = row1[x0], p11 = row1[x1];
-        float v[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const float a = (float)((p00 >> (8 * ch)) & 255), b = (float)((p01 >> (8 * ch)) & 255);
-          const float cc = (float)((p10 >> (8 * ch)) & 255), dd = (float)((p11 >> (8 * ch)) & 255);
-          const float top = fmaf(wx, b - a, a);
-          const float bot = fmaf(wx, dd - cc, cc);
-          v[ch] = fmaf(wy, bot - top, top);
+    if constexpr (DEBUG) {
+      int16_t* dst = kp.dbg_rgb + n * kp.dbg_stride_rgb;
+      for (int y = ready_prev + 1; y <= ready; ++y)
+        for (int x = L.lx0 + tid; x <= L.lx1; x += kThreads) {
+          const uint32_t v = rgb[(y & (kRgbRing - 1)) * L.rgb_w + (x - L.rgb_x0)];
+          const size_t o = ((size_t)y * im.Wd + x) * 3;
+          dst[o] = v & 255; dst[o + 1] = (v >> 8) & 255; dst[o + 2] = (v >> 16) & 255;
         }
-        const float y0 = fmaf(v[0], na0, nb0), y1 = fmaf(v[1], na1, nb1), y2 = fmaf(v[2], na2, nb2);
+    }
+
+    // ---- bilinear + normalize + NCHW store of the rows now complete -------
+    int done = done_prev;
+    {
+      // rows with lower tap <= ready (taps are monotone): binary search
+      int lo = done_prev, hi = nth;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int)((uint32_t)yt[mid].x >> 16) <= ready) lo = mid + 1; else hi = mid;
+      }
+      done = lo;
+    }
+    {
+      const int nr = done - done_prev;
+      const int ntasko = nr * nopairs;
+      const float na0 = kp.na[0], na1 = kp.na[1], na2 = kp.na[2];
+      const float nb0 = kp.nb[0], nb1 = kp.nb[1], nb2 = kp.nb[2];
+      for (int t = tid; t < ntasko; t += kThreads) {
+        const int rr = (int)fdiv((uint32_t)t, fd_opairs);
+        const int r = done_prev + rr;
+        const int ox = 2 * (t - rr * nopairs);
+        const int2 ty = yt[r];
+        const float wy = __int_as_float(ty.y);
+        const uint32_t* row0 = rgb + ((ty.x & 0xffff) & (kRgbRing - 1)) * L.rgb_w;
+        const uint32_t* row1 = rgb + (((uint32_t)ty.x >> 16) & (kRgbRing - 1)) * L.rgb_w;
+        float y[2][3];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int2 tx = xt[min(ox + e, ntw - 1)];
+          const float wx = __int_as_float(tx.y);
+          const int x0 = tx.x & 0xffff, x1 = (int)((uint32_t)tx.x >> 16);
+          const uint32_t p00 = row0[x0], p01 = row0[x1], p10 = row1[x0], p11 = row1[x1];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float a = byte_f(p00, ch), b = byte_f(p01, ch);
+            const float c = byte_f(p10, ch), d = byte_f(p11, ch);
+            const float top = fmaf(wx, b - a, a);
+            const float bot = fmaf(wx, d - c, c);
+            y[e][ch] = fmaf(wy, bot - top, top);
+          }
+          y[e][0] = fmaf(y[e][0], na0, nb0);
+          y[e][1] = fmaf(y[e][1], na1, nb1);
+          y[e][2] = fmaf(y[e][2], na2, nb2);
+        }
+        const int oy = oy0 + r, oxg = ox0 + ox;
+        const size_t o = ((size_t)n * 3 * kp.OH + oy) * kp.OW + oxg;
+        const bool pair = (ox + 1 < ntw) && ((kp.OW & 1) == 0);
         if constexpr (F16) {
-          __half* o = reinterpret_cast<__half*>(kp.out) + obase + ox;
-          o[0] = __float2half_rn(y0); o[plane] = __float2half_rn(y1); o[2 * plane] = __float2half_rn(y2);
+          __half* ob = reinterpret_cast<__half*>(kp.out) + o;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            if (pair) *reinterpret_cast<__half2*>(ob + ch * plane_sz) = __floats2half2_rn(y[0][ch], y[1][ch]);
+            else {
+              ob[ch * plane_sz] = __float2half_rn(y[0][ch]);
+              if (ox + 1 < ntw) ob[ch * plane_sz + 1] = __float2half_rn(y[1][ch]);
+            }
+          }
         } else {
-          float* o = reinterpret_cast<float*>(kp.out) + obase + ox;
-          __stcs(o, y0); __stcs(o + plane, y1); __stcs(o + 2 * plane, y2);
+          float* ob = reinterpret_cast<float*>(kp.out) + o;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            if (pair) __stcs(reinterpret_cast<float2*>(ob + ch * plane_sz), make_float2(y[0][ch], y[1][ch]));
+            else {
+              __stcs(ob + ch * plane_sz, y[0][ch]);
+              if (ox + 1 < ntw) __stcs(ob + ch * plane_sz + 1, y[1][ch]);
+            }
+          }
         }
       }
     }
+    ready_prev = max(ready_prev, ready);
+    done_prev = done;
   }
 }
 

@@ -67,6 +67,12 @@ void init_basis(Basis& b) {
   for (int j = 0; j < 2; ++j)
     for (int u = 0; u < 8; ++u) b.a2[j][u] = (float)box(2, u, j);
   for (int u = 0; u < 8; ++u) b.a4[u] = (float)box(4, u, 0);
+  // JFIF R and B (reading R6) in fp32; the exhaustive check of these exact
+  // recipes is tests/test_color_fp32.py
+  b.kR = (float)(1.402 / 16.0);
+  b.kB = (float)(1.772 / 16.0);
+  b.cR = (float)(0.5 - 2048.0 * 1.402 / 16.0);
+  b.cB = (float)(0.5 - 2048.0 * 1.772 / 16.0 + 1.0 / 8192.0);
 }
 
 std::mutex g_basis_mu;
@@ -178,17 +184,18 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
     g.coef[c] = d->coef[c];
     g.stride[c] = d->row_stride_bytes[c] / 2;
     g.qidx[c] = d->qtable[c];
+    g.nbw[c] = need_w[c];
   }
   return SMOL_OK;
 }
 
-int auto_tile_rows(int K) {
-  switch (K) {
-    case 1: return 16;
-    case 2: return 32;
-    case 4: return 32;
-    default: return 64;
-  }
+// Tiles per image: enough CTAs for ~6 resident per SM across the batch
+// (148 SMs; hardware scheduling balances the tail), each tile at least 8
+// output rows.
+int auto_tile_rows(int OH, int n_images) {
+  const int want = ceil_div(148 * 6, n_images > 0 ? n_images : 1);
+  const int ntiles = imax(1, imin(want, ceil_div(OH, 8)));
+  return ceil_div(OH, ntiles);
 }
 
 using KernelFn = void (*)(const KParams);
@@ -215,7 +222,7 @@ struct smol_preproc_plan {
   int max_images = 0;
   int device = 0;
   int OW = 0, OH = 0;          // 0 when the output size is image dependent (never: validated)
-  int tile_rows = 0;
+  int tile_rows = 0;               // 0 = automatic per batch size
   int smem_optin = 0;
   DevImage* d_desc = nullptr;  // [kRing][max_images]
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
@@ -244,8 +251,10 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
   out->Wr = g.Wr; out->Hr = g.Hr; out->left = g.left; out->top = g.top;
   out->OW = params->crop_w > 0 ? params->crop_w : g.Wr;
   out->OH = params->crop_w > 0 ? params->crop_h : g.Hr;
+  g.nbw[0] = ceil_div(image->width, 8);
+  g.nbw[1] = g.nbw[2] = ceil_div(image->width, 16);
   TileLayout L;
-  tile_layout(g, params->scale_denom, out->OW, 0, out->OH, L);
+  tile_layout(g, params->scale_denom, 0, out->OH, 0, out->OW, L);
   out->lx0 = L.lx0; out->lx1 = L.lx1; out->ly0 = L.ly0; out->ly1 = L.ly1;
   out->cx0 = L.cx0; out->cx1 = L.cx1; out->cy0 = L.cy0; out->cy1 = L.cy1;
   for (int c = 0; c < 3; ++c) {
@@ -275,7 +284,7 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   pl->device = dev;
   if (params->crop_w > 0) { pl->OW = params->crop_w; pl->OH = params->crop_h; }
   else { pl->OW = params->resize_w; pl->OH = params->resize_h; }
-  pl->tile_rows = params->tile_rows > 0 ? params->tile_rows : auto_tile_rows(params->scale_denom);
+  pl->tile_rows = params->tile_rows;
   for (int c = 0; c < 3; ++c) {
     pl->na[c] = (float)(1.0 / (255.0 * (double)params->std[c]));
     pl->nb[c] = (float)(-(double)params->mean[c] / (double)params->std[c]);
@@ -285,11 +294,20 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   for (int i = 0; i < kRing && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
   if (e == cudaSuccess) {
-    // opt every instantiation of this plan's (scale, dtype) in to large smem
+    // opt every instantiation of this plan's (scale, dtype) in to the largest
+    // dynamic smem the device allows next to the kernel's static smem
     const bool f16 = params->out_dtype == SMOL_OUT_F16_NCHW;
-    for (int dbg = 0; dbg < 2 && e == cudaSuccess; ++dbg)
-      e = cudaFuncSetAttribute(select_kernel(params->scale_denom, f16, dbg),
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, pl->smem_optin);
+    int limit = pl->smem_optin;
+    for (int dbg = 0; dbg < 2 && e == cudaSuccess; ++dbg) {
+      cudaFuncAttributes fa;
+      KernelFn fn = select_kernel(params->scale_denom, f16, dbg);
+      e = cudaFuncGetAttributes(&fa, fn);
+      if (e != cudaSuccess) break;
+      const int dyn = pl->smem_optin - (int)fa.sharedSizeBytes;
+      if (dyn < limit) limit = dyn;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    }
+    pl->smem_optin = limit;
   }
   if (e != cudaSuccess) {
     smol_preproc_destroy(pl);
@@ -347,23 +365,39 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   DevImage* d = pl->d_desc + (size_t)slot * pl->max_images;
 
   // validate + build descriptors; shared memory = max over distinct geometries
-  int smem = 0;
-  int prev_w = -1, prev_h = -1, prev_l = -2, prev_t = -2;
-  const int ntiles = ceil_div(pl->OH, pl->tile_rows);
+  const int tile_rows = pl->tile_rows > 0 ? imin(pl->tile_rows, pl->OH) : auto_tile_rows(pl->OH, b->n_images);
+  const int ntiles = ceil_div(pl->OH, tile_rows);
+  // validate every descriptor once
   for (int i = 0; i < b->n_images; ++i) {
-    const smol_image_desc* di = &b->images[i];
-    DevImage g{};
-    int32_t rc = validate_image(&pl->p, di, i, b->n_qtables, g);
+    int32_t rc = validate_image(&pl->p, &b->images[i], i, b->n_qtables, h[i]);
     if (rc) return rc;
-    if (di->width != prev_w || di->height != prev_h || di->roi_left != prev_l || di->roi_top != prev_t) {
-      for (int t = 0; t < ntiles; ++t) {
-        TileLayout L;
-        tile_layout(g, K, pl->OW, t * pl->tile_rows, min(pl->OH, (t + 1) * pl->tile_rows), L);
-        if (L.total > smem) smem = L.total;
-      }
+  }
+  // shared memory of the largest tile over the batch's distinct geometries
+  auto max_smem = [&](int n_col_tiles) {
+    const int tile_cols = ceil_div(pl->OW, n_col_tiles);
+    int m = 0;
+    int prev_w = -1, prev_h = -1, prev_l = -2, prev_t = -2;
+    for (int i = 0; i < b->n_images; ++i) {
+      const smol_image_desc* di = &b->images[i];
+      if (di->width == prev_w && di->height == prev_h && di->roi_left == prev_l && di->roi_top == prev_t)
+        continue;
+      for (int t = 0; t < ntiles; ++t)
+        for (int u = 0; u < n_col_tiles; ++u) {
+          TileLayout L;
+          tile_layout(h[i], K, t * tile_rows, imin(pl->OH, (t + 1) * tile_rows), u * tile_cols,
+                      imin(pl->OW, (u + 1) * tile_cols), L);
+          m = imax(m, L.total);
+        }
       prev_w = di->width; prev_h = di->height; prev_l = di->roi_left; prev_t = di->roi_top;
     }
-    h[i] = g;
+    return m;
+  };
+  // column tiles only when a full-width tile would not leave 2 CTAs per SM
+  int n_col_tiles = 1;
+  int smem = max_smem(1);
+  while (smem > pl->smem_optin / 2 && n_col_tiles < 64 && 2 * n_col_tiles <= pl->OW) {
+    n_col_tiles *= 2;
+    smem = max_smem(n_col_tiles);
   }
   if (smem > pl->smem_optin)
     return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
@@ -373,10 +407,11 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   kp.imgs = d;
   kp.qtables = b->qtables;
   kp.out = out;
-  kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = pl->tile_rows;
+  kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;
+  kp.n_col_tiles = n_col_tiles; kp.tile_cols = ceil_div(pl->OW, n_col_tiles);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr);
-  dim3 grid(ntiles, b->n_images);
+  dim3 grid(ntiles * n_col_tiles, b->n_images);
   fn<<<grid, kThreads, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));

@@ -62,8 +62,9 @@ def make_tie_free(im, qt, k: int, max_iter: int = 50):
                 break
             idx = np.argwhere(bad)
             for (by, bx) in idx:
-                # an odd-u AC nudge shifts samples by irrational amounts
-                j = int(rng.choice([1, 3, 8, 24, 9]))
+                # an odd-u AC nudge shifts samples by irrational amounts; at
+                # scale 1/8 only the DC matters
+                j = 0 if k == 8 else int(rng.choice([1, 3, 8, 24, 9]))
                 coef[ci][by, bx, j] += 1 if rng.random() < 0.5 else -1
         else:
             raise RuntimeError("tie-free regeneration did not converge")
@@ -72,3 +73,27 @@ def make_tie_free(im, qt, k: int, max_iter: int = 50):
 
 def rgb_from_planes(Y, Cb, Cr):
     return oracle.upsample_color(Y, Cb, Cr)[1]
+
+
+def _taps(n_out, offset, n_in, n_res):
+    """R8 taps (i0, i1) of output indices offset..offset+n_out-1 in exact ints."""
+    d = np.arange(n_out, dtype=np.int64) + offset
+    num = np.maximum(0, (2 * d + 1) * n_in - n_res)
+    i0 = np.minimum(num // (2 * n_res), n_in - 1)
+    i1 = np.minimum(i0 + 1, n_in - 1)
+    return i0, i1
+
+
+def affected_outputs(po, im, qt, roi=None):
+    """Boolean [OH][OW]: outputs whose bilinear taps touch an RGB pixel that
+    depends on a decoded sample inside the reading-R3 tie band (where the
+    kernel may legitimately differ by one u8 level)."""
+    g = oracle.geometry(po, im.width, im.height)
+    left, top = (g.left, g.top) if roi is None else roi
+    bands = [b for (_, _, b) in oracle_planes(po, im, qt)]
+    c16, _ = oracle.upsample_color(np.zeros((g.Hd, g.Wd), np.uint8),
+                                   bands[1].astype(np.uint8), bands[2].astype(np.uint8))
+    pix = bands[0] | (c16[..., 0] > 0) | (c16[..., 1] > 0)
+    y0, y1 = _taps(g.OH, top, g.Hd, g.Hr)
+    x0, x1 = _taps(g.OW, left, g.Wd, g.Wr)
+    return (pix[y0][:, x0] | pix[y0][:, x1] | pix[y1][:, x0] | pix[y1][:, x1])

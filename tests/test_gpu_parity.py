@@ -274,7 +274,8 @@ def test_errors_and_empty():
 
 def _sample_check(name, n_sample, quality=75):
     """Full BASELINE.json size in the bench's launch configuration; the oracle
-    checks sampled images one by one."""
+    checks sampled images one by one.  Strict tolerance except on outputs
+    whose taps depend on a decoded sample inside the tie band (reading R3)."""
     cfg = synth.CONFIGS[name]
     imgs, qt = synth.batch_images(cfg, quality=quality)
     ps, po = _cfg_params(cfg)
@@ -284,14 +285,14 @@ def _sample_check(name, n_sample, quality=75):
     assert tuple(out.shape) == (cfg.n, 3) + cfg.out_hw
     assert torch.isfinite(out.float()).all()
     idx = np.linspace(0, cfg.n - 1, n_sample).astype(int)
-    tol = TOL[cfg.out_dtype] + 2.0 / (255 * min(synth.IMAGENET_STD))   # band-widened
-    strict_ok = 0
+    tol = TOL[cfg.out_dtype]
+    widen = 2.0 / (255 * min(synth.IMAGENET_STD))
     for i in idx:
         ref = oracle.run_image(po, imgs[i], qt).astype(np.float64)
-        err = float(np.max(np.abs(out[i].float().cpu().numpy() - ref)))
-        assert err <= tol, (name, i, err)
-        strict_ok += err <= TOL[cfg.out_dtype]
-    assert strict_ok >= len(idx) - 1
+        err = np.abs(out[i].float().cpu().numpy() - ref).max(axis=0)
+        aff = helpers.affected_outputs(po, imgs[i], qt)
+        assert err[~aff].max(initial=0) <= tol, (name, i, err[~aff].max())
+        assert err.max() <= tol + widen, (name, i, err.max())
     # replicated images must produce identical outputs anywhere in the batch
     d = len({id(im) for im in imgs})
     if cfg.n > d:
