@@ -97,10 +97,11 @@ def lib():
     """Load the CUDA library; raises if it was not built (no CPU fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+        path = os.environ.get("SMOL_LIB", LIB_PATH)      # experiment override (same ABI)
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build() "
                                "(the Smol path has no CPU fallback)")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         P = ctypes.POINTER
         vp = ctypes.c_void_p
         L.smol_preproc_plan.argtypes = [P(Params), ctypes.c_int32, P(vp)]

@@ -53,19 +53,29 @@ SMOL_HD void src_tap(int d, int in, int out, int& i0, int& i1, float& w) {
 
 SMOL_HD int align16(int x) { return (x + 15) & ~15; }
 
-// Footprint of the output tile rows [oy0, oy1) x cols [ox0, ox1) and the
-// shared-memory carve-up of the CTA that processes it.
+// Shared-memory rings (fixed pitches so neighbour loads use immediate offsets):
+//   Y   : kYRing slots x kYP bytes, column = x - xbase[0]
+//   Cb/Cr: kCSlots = 16 + 2 slots x kCP bytes each; row r lives in slot
+//          (r & 15) + 1, slot 0 mirrors slot 16 and slot 17 mirrors slot 1, so
+//          rows j-1, j, j+1 are always at constant stride; column
+//          c - xbase[c] + kCPad (image-edge columns replicated into the pad)
+//   RGB : kRgbRing + 1 slots (slot 32 mirrors slot 0) x rgb_p u32
+constexpr int kYP = 512;
+constexpr int kCP = 256;
+constexpr int kCPad = 8;
+constexpr int kCSlots = 18;
+
 struct TileLayout {
   int oy0, oy1, ox0, ox1;          // output tile
   int ly0, ly1, lx0, lx1;          // luma (decoded) tap footprint, inclusive
   int cy0, cy1, cx0, cx1;          // chroma footprint incl. triangle neighbours (R2)
   int by0[3], by1[3], bx0[3], bx1[3];   // ROI block ranges per component
-  int pitch[3];                    // bytes per ring row of the u8 planes
-  int xbase[3];                    // decoded column of ring byte 0 (= bx0 * P)
-  int rgb_x0, rgb_w;               // RGB ring: first column (even) and width (even), u32 units
+  int xbase[3];                    // decoded column of ring column 0 (= bx0 * P)
+  int rgb_x0, rgb_w, rgb_p;        // RGB ring: first column (even), width (even), pitch (u32)
   int r0, nsteps;                  // first rolling-step row (16-aligned) and step count
+  int fits;                        // footprint fits the fixed ring pitches
   // byte offsets in dynamic shared memory
-  int off_q, off_xt, off_yt, off_pl[3], off_rgb, total;
+  int off_q, off_xt, off_yt, off_y, off_c, off_rgb, total;
 };
 
 SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, int ox1, TileLayout& L) {
@@ -91,23 +101,21 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
     L.by0[c] = L.cy0 / P; L.by1[c] = L.cy1 / P;
     L.bx0[c] = L.cx0 / P; L.bx1[c] = L.cx1 / P;
   }
-  for (int c = 0; c < 3; ++c) {
-    L.xbase[c] = L.bx0[c] * P;
-    L.pitch[c] = (((L.bx1[c] - L.bx0[c] + 1) * P + 2) + 7) & ~7;   // + pair slack, 8-B rows
-  }
+  for (int c = 0; c < 3; ++c) L.xbase[c] = L.bx0[c] * P;
   L.rgb_x0 = L.lx0 & ~1;
   L.rgb_w = ((L.lx1 | 1) - L.rgb_x0 + 1);
+  L.rgb_p = L.rgb_w + 2;
   L.r0 = L.ly0 & ~(kStepRows - 1);
   // the last step must cover luma row ly1 and chroma row cy1 (luma 2 cy1)
   L.nsteps = ((imax(L.ly1, 2 * L.cy1) - L.r0) / kStepRows) + 1;
+  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 2 <= kYP) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= kCP);
   int off = 0;
   L.off_q = off;   off += 3 * 64 * 4;                         // dequant tables (float)
-  L.off_xt = off;  off += align16((ox1 - ox0) * 8);           // x taps: {x0 | x1<<16, w}
+  L.off_xt = off;  off += align16((ox1 - ox0 + 3) * 8);       // x taps: {4 x0, w}
   L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {y0 | y1<<16, w}
-  L.off_pl[0] = off; off += align16(L.pitch[0] * kYRing);
-  L.off_pl[1] = off; off += align16(L.pitch[1] * kCRing);
-  L.off_pl[2] = off; off += align16(L.pitch[2] * kCRing);
-  L.off_rgb = off;   off += align16(L.rgb_w * 4 * kRgbRing);
+  L.off_y = off;   off += kYRing * kYP;
+  L.off_c = off;   off += 2 * kCSlots * kCP;
+  L.off_rgb = off; off += align16(L.rgb_p * 4 * (kRgbRing + 1));
   L.total = off;
 }
 

@@ -41,23 +41,40 @@ struct Basis {
 __constant__ Basis c_basis;
 
 // ------------------------------------------------------------ 1-D IDCTs ---
-// Reading R1 (Definition A), separable form of the oracle's sum.  in[u],
-// u < W nonzero (u >= W known zero, compile-time)  ->  out[j], j < P.  The
-// FMA chains start from in[0] (weight exactly 1) and the exact +-1 / 0
-// entries so that DC-only and {0,4}-only inputs are transformed exactly.
+// Reading R1 (Definition A), separable form of the oracle's sum.  The
+// scale-1 basis t(u,x) = sqrt2 C(u) cos((2x+1) u pi/16) is compiled in as
+// immediates (FFMA immediate form; init_basis checks these literals against
+// the double-precision formula at plan creation):  c_k = sqrt2 cos(k pi/16).
+constexpr float kC1 = 1.387039845322f, kC2 = 1.306562964876f, kC3 = 1.175875602419f,
+                kC5 = 0.785694958387f, kC6 = 0.541196100146f, kC7 = 0.275899379283f;
+__host__ __device__ constexpr float basis_t(int u, int x) {
+  // t(u, x) for x < 4 (t(u, 7-x) = (-1)^u t(u, x)); t(0,x) = 1, t(4,x) = +-1 exactly
+  return u == 0 ? 1.f
+       : u == 1 ? (x == 0 ? kC1 : x == 1 ? kC3 : x == 2 ? kC5 : kC7)
+       : u == 2 ? (x == 0 ? kC2 : x == 1 ? kC6 : x == 2 ? -kC6 : -kC2)
+       : u == 3 ? (x == 0 ? kC3 : x == 1 ? -kC7 : x == 2 ? -kC1 : -kC5)
+       : u == 4 ? ((x == 0 || x == 3) ? 1.f : -1.f)
+       : u == 5 ? (x == 0 ? kC5 : x == 1 ? -kC1 : x == 2 ? kC7 : kC3)
+       : u == 6 ? (x == 0 ? kC6 : x == 1 ? -kC2 : x == 2 ? kC2 : -kC6)
+       :          (x == 0 ? kC7 : x == 1 ? -kC5 : x == 2 ? kC3 : -kC1);
+}
+
+// 8-point IDCT, inputs u >= W known zero (compile time).  The FMA chains
+// start from d[0] (weight exactly 1) and the exact +-1 entries of u = 4, so
+// DC-only and {0,4}-only inputs are transformed exactly (reading R3).
 template <int W>
 __device__ __forceinline__ void idct8(const float (&d)[8], float (&o)[8]) {
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
     float e = d[0];
-    if (W > 4) e = fmaf(d[4], c_basis.t[4][x], e);
-    if (W > 2) e = fmaf(d[2], c_basis.t[2][x], e);
-    if (W > 6) e = fmaf(d[6], c_basis.t[6][x], e);
+    if (W > 4) e = (x == 0 || x == 3) ? e + d[4] : e - d[4];
+    if (W > 2) e = fmaf(d[2], basis_t(2, x), e);
+    if (W > 6) e = fmaf(d[6], basis_t(6, x), e);
     float od = 0.f;
-    if (W > 1) od = d[1] * c_basis.t[1][x];
-    if (W > 3) od = fmaf(d[3], c_basis.t[3][x], od);
-    if (W > 5) od = fmaf(d[5], c_basis.t[5][x], od);
-    if (W > 7) od = fmaf(d[7], c_basis.t[7][x], od);
+    if (W > 1) od = d[1] * basis_t(1, x);
+    if (W > 3) od = fmaf(d[3], basis_t(3, x), od);
+    if (W > 5) od = fmaf(d[5], basis_t(5, x), od);
+    if (W > 7) od = fmaf(d[7], basis_t(7, x), od);
     if (W > 1) { o[x] = e + od; o[7 - x] = e - od; }
     else { o[x] = e; o[7 - x] = e; }
   }
@@ -106,28 +123,33 @@ __device__ __forceinline__ void unpack_row(const int4 r, float (&d)[8]) {
   d[6] = (float)(int16_t)(r.w & 0xffff); d[7] = (float)(r.w >> 16);
 }
 
-// Full-scale block: row pass over the H nonzero rows (warp max), column pass
-// with the H-row input set; W = warp max nonzero column + 1.
-template <int W>
-__device__ __forceinline__ void idct_rows(const int4 (&raw)[8], const float* q, int H, float (&m)[8][8]) {
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// Full-scale block, row pass: rows v < HR (rows >= HR are all-zero in the
+// whole warp), inputs u < W.  Level shift and rounding offset (+128 + 1/2,
+// reading R3) ride on the DC term: t(0, .) = 1 exactly, so adding it to
+// D(0,0) adds it to every output sample.
+template <int W, int HR>
+__device__ __forceinline__ void idct_rows(const int4 (&raw)[8], const float* q, float (&m)[8][8]) {
 #pragma unroll
-  for (int v = 0; v < 8; ++v) {
-    if (v < H) {
-      float d[8];
-      unpack_row(raw[v], d);
-      const float4 q0 = *reinterpret_cast<const float4*>(q + v * 8);
-      const float4 q1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
-      d[0] *= q0.x; d[1] *= q0.y; d[2] *= q0.z; d[3] *= q0.w;
-      d[4] *= q1.x; d[5] *= q1.y; d[6] *= q1.z; d[7] *= q1.w;
-      idct8<W>(d, m[v]);
-    }
+  for (int v = 0; v < HR; ++v) {
+    float d[8];
+    unpack_row(raw[v], d);
+    const float4 q0 = *reinterpret_cast<const float4*>(q + v * 8);
+    const float4 q1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
+    d[0] *= q0.x; d[1] *= q0.y; d[2] *= q0.z; d[3] *= q0.w;
+    d[4] *= q1.x; d[5] *= q1.y; d[6] *= q1.z; d[7] *= q1.w;
+    if (v == 0) d[0] += 128.5f;
+    idct8<W>(d, m[v]);
   }
 }
 
 template <int H>
-__device__ __forceinline__ void idct_cols_store(const float (&m)[8][8], uint8_t* dst, int pitch, int row0,
-                                                int rmask) {
-  uint32_t px[8][2];
+__device__ __forceinline__ void idct_cols(const float (&m)[8][8], uint32_t (&px)[8][2]) {
+  // column x's bytes are merged into the row words as they are produced
+  // (one PRMT per byte; keeps the live set at m + px)
 #pragma unroll
   for (int x = 0; x < 8; ++x) {
     float col[8], f[8];
@@ -136,27 +158,24 @@ __device__ __forceinline__ void idct_cols_store(const float (&m)[8][8], uint8_t*
     idct8<H>(col, f);
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
-      const uint32_t b = round_u8(f[y]);
-      if (x == 0) px[y][0] = b;
-      else if (x < 4) px[y][0] |= b << (8 * x);
-      else if (x == 4) px[y][1] = b;
-      else px[y][1] |= b << (8 * (x - 4));
+      const uint32_t b = floor_u8(f[y]);
+      uint32_t& w = px[y][x >> 2];
+      if ((x & 3) == 0) w = b;
+      else w = __byte_perm(w, b, (x & 3) == 1 ? 0x3240 : (x & 3) == 2 ? 0x3410 : 0x4210);
     }
   }
-#pragma unroll
-  for (int y = 0; y < 8; ++y)
-    *reinterpret_cast<uint2*>(dst + ((row0 + y) & rmask) * pitch) = make_uint2(px[y][0], px[y][1]);
 }
 
-// Decode one block at scale 1/K into the ring plane (ring of `ring` rows).
-// `act` = this lane has a block; every lane of the warp must call it (warp
-// reductions pick the nonzero row/column extents).
+// Decode one block at scale 1/K: px[y] holds the P samples of output row y
+// (little-endian bytes, 2 words per row at K = 1).  `act` = this lane has a
+// block; every lane of the warp must call it (warp reductions pick the
+// nonzero row/column extents).
 template <int K>
-__device__ __forceinline__ void decode_block(bool act, const int16_t* src, const float* q, uint8_t* plane,
-                                             int pitch, int ring, int row0, int col0) {
+__device__ __forceinline__ void decode_block(bool act, const int16_t* src, const float* q,
+                                             uint32_t (&px)[8][2]) {
   constexpr int P = 8 / K;
   if constexpr (K == 8) {
-    if (act) plane[(row0 & (ring - 1)) * pitch + col0] = (uint8_t)round_u8((float)__ldg(src) * q[0]);
+    px[0][0] = act ? round_u8((float)__ldg(src) * q[0]) : 0u;
   } else if constexpr (K == 1) {
     int4 raw[8];
 #pragma unroll
@@ -171,32 +190,15 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     }
     const int wcol = acc.w ? ((acc.w >> 16) ? 8 : 7) : acc.z ? ((acc.z >> 16) ? 6 : 5)
                    : acc.y ? ((acc.y >> 16) ? 4 : 3) : ((acc.x >> 16) ? 2 : 1);
-    const int H = max(1, (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows)));
+    const int H = (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows));
     const int W = (int)__reduce_max_sync(0xffffffffu, (uint32_t)wcol);
     float m[8][8];
-    switch (W) {
-      case 1: idct_rows<1>(raw, q, H, m); break;
-      case 2: idct_rows<2>(raw, q, H, m); break;
-      case 3: idct_rows<3>(raw, q, H, m); break;
-      case 4: idct_rows<4>(raw, q, H, m); break;
-      case 5: idct_rows<5>(raw, q, H, m); break;
-      case 6: idct_rows<6>(raw, q, H, m); break;
-      case 7: idct_rows<7>(raw, q, H, m); break;
-      default: idct_rows<8>(raw, q, H, m); break;
+    if (W <= 5) {
+      if (H <= 6) idct_rows<5, 6>(raw, q, m); else idct_rows<5, 8>(raw, q, m);
+    } else {
+      if (H <= 6) idct_rows<8, 6>(raw, q, m); else idct_rows<8, 8>(raw, q, m);
     }
-    if (act) {
-      uint8_t* dst = plane + col0;
-      switch (H) {
-        case 1: idct_cols_store<1>(m, dst, pitch, row0, ring - 1); break;
-        case 2: idct_cols_store<2>(m, dst, pitch, row0, ring - 1); break;
-        case 3: idct_cols_store<3>(m, dst, pitch, row0, ring - 1); break;
-        case 4: idct_cols_store<4>(m, dst, pitch, row0, ring - 1); break;
-        case 5: idct_cols_store<5>(m, dst, pitch, row0, ring - 1); break;
-        case 6: idct_cols_store<6>(m, dst, pitch, row0, ring - 1); break;
-        case 7: idct_cols_store<7>(m, dst, pitch, row0, ring - 1); break;
-        default: idct_cols_store<8>(m, dst, pitch, row0, ring - 1); break;
-      }
-    }
+    if (H <= 6) idct_cols<6>(m, px); else idct_cols<8>(m, px);
   } else {
     // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7})
     float g[8][P];
@@ -211,30 +213,22 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
       unpack_row(act ? __ldg(reinterpret_cast<const int4*>(src) + v) : make_int4(0, 0, 0, 0), d);
 #pragma unroll
       for (int u = 0; u < 8; ++u) d[u] *= q[v * 8 + u];
+      if (v == 0) d[0] += 128.5f;           // level shift + rounding offset (DC weight is exactly 1)
       float o[P];
       if constexpr (K == 2) idct4(d, o); else idct2(d, o);
 #pragma unroll
       for (int j = 0; j < P; ++j) g[v][j] = o[j];
     }
-    if (act) {
-      uint32_t px[P];
 #pragma unroll
-      for (int x = 0; x < P; ++x) {
-        float col[8], f[P];
+    for (int x = 0; x < P; ++x) {
+      float col[8], f[P];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) col[v] = g[v][x];
-        if constexpr (K == 2) idct4(col, f); else idct2(col, f);
-#pragma unroll
-        for (int y = 0; y < P; ++y) {
-          const uint32_t b = round_u8(f[y]);
-          px[y] = (x == 0) ? b : (px[y] | (b << (8 * x)));
-        }
-      }
+      for (int v = 0; v < 8; ++v) col[v] = g[v][x];
+      if constexpr (K == 2) idct4(col, f); else idct2(col, f);
 #pragma unroll
       for (int y = 0; y < P; ++y) {
-        uint8_t* d = plane + ((row0 + y) & (ring - 1)) * pitch + col0;
-        if constexpr (K == 2) *reinterpret_cast<uint32_t*>(d) = px[y];
-        else *reinterpret_cast<uint16_t*>(d) = (uint16_t)px[y];
+        const uint32_t b = floor_u8(f[y]);
+        px[y][0] = (x == 0) ? b : (px[y][0] | (b << (8 * x)));
       }
     }
   }
@@ -274,17 +268,34 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   return f.d <= 1 ? n : __umulhi(n, f.m);
 }
 
-// byte b of x as float, via the 2^23 magic (ALU + FMA pipes, no I2F)
+// byte b of x as float: PRMT (zero-extend) + I2FP (no XU-pipe I2F)
 __device__ __forceinline__ float byte_f(uint32_t x, int b) {
-  return __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540 + b)) - 8388608.f;
+  return __uint2float_rn(__byte_perm(x, 0u, 0x4440 + b));
+}
+
+
+#ifndef SMOL_MIN_BLOCKS
+#define SMOL_MIN_BLOCKS 3
+#endif
+
+template <int P>
+__device__ __forceinline__ void put_row(uint8_t* d, const uint32_t (&w)[2]) {
+  if constexpr (P == 8) *reinterpret_cast<uint2*>(d) = make_uint2(w[0], w[1]);
+  else if constexpr (P == 4) *reinterpret_cast<uint32_t*>(d) = w[0];
+  else if constexpr (P == 2) *reinterpret_cast<uint16_t*>(d) = (uint16_t)w[0];
+  else *d = (uint8_t)w[0];
+}
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[2], int e) {
+  return (w[e >> 2] >> (8 * (e & 3))) & 255u;
 }
 
 template <int K, bool F16, bool DEBUG>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, SMOL_MIN_BLOCKS)
 smol_fused_kernel(const KParams kp) {
   constexpr int P = 8 / K;                 // decoded samples per block side
   extern __shared__ __align__(16) uint8_t smem[];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int n = blockIdx.y;
   const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
   const int oy0 = trow * kp.tile_rows, oy1 = min(kp.OH, oy0 + kp.tile_rows);
@@ -292,56 +303,60 @@ smol_fused_kernel(const KParams kp) {
 
   __shared__ DevImage im;
   __shared__ TileLayout L;
+  __shared__ int ctr[2];                   // dynamic work counters (colour, output)
   if (tid == 0) {
     im = kp.imgs[n];
     tile_layout(im, K, oy0, oy1, ox0, ox1, L);
+    ctr[0] = 0;
+    ctr[1] = 0;
   }
   __syncthreads();
   float* qf = reinterpret_cast<float*>(smem + L.off_q);
   int2* xt = reinterpret_cast<int2*>(smem + L.off_xt);
   int2* yt = reinterpret_cast<int2*>(smem + L.off_yt);
-  uint8_t* ypl = smem + L.off_pl[0];
-  uint8_t* cbpl = smem + L.off_pl[1];
-  uint8_t* crpl = smem + L.off_pl[2];
+  uint8_t* yring = smem + L.off_y;
+  uint8_t* cring = smem + L.off_c;
   uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + L.off_rgb);
+  constexpr int kCStride = kCSlots * kCP;  // Cr ring follows the Cb ring
   const int ntw = ox1 - ox0, nth = oy1 - oy0;
+  const int rgb_p = L.rgb_p;
 
   // ---- prologue: dequant tables (Q/8, exact) and bilinear taps ----------
+  // Taps use exact-integer coordinates (R9).  Where the upper tap is clamped
+  // (i1 == i0) its weight is zeroed so the kernel may always read i0 + 1.
   for (int i = tid; i < 3 * 64; i += kThreads)
     qf[i] = (float)kp.qtables[im.qidx[i >> 6] * 64 + (i & 63)] * 0.125f;
-  for (int i = tid; i < ntw; i += kThreads) {
+  for (int i = tid; i < ntw + 3; i += kThreads) {
     int i0, i1; float w;
-    src_tap(im.left + ox0 + i, im.Wd, im.Wr, i0, i1, w);
-    xt[i] = make_int2((i0 - L.rgb_x0) | ((i1 - L.rgb_x0) << 16), __float_as_int(w));
+    src_tap(im.left + ox0 + min(i, ntw - 1), im.Wd, im.Wr, i0, i1, w);
+    xt[i] = make_int2(i0 - L.rgb_x0, __float_as_int(i1 == i0 ? 0.f : w));
   }
   for (int i = tid; i < nth; i += kThreads) {
     int i0, i1; float w;
     src_tap(im.top + oy0 + i, im.Hd, im.Hr, i0, i1, w);
-    yt[i] = make_int2(i0 | (i1 << 16), __float_as_int(w));
+    yt[i] = make_int2(i0 | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
   }
   const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
   const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
   const int npairs = L.rgb_w >> 1;
   const FastDiv fd_pairs = make_fastdiv(npairs);
-  const int nopairs = (ntw + 1) >> 1;
-  const FastDiv fd_opairs = make_fastdiv(nopairs);
+  const int nq4 = (ntw + 3) >> 2;
+  const FastDiv fd_q4 = make_fastdiv(nq4);
+  const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0);
   const size_t plane_sz = (size_t)kp.OH * kp.OW;
-  int ready_prev = L.ly0 - 1;
-  int done_prev = 0;                       // output rows of the tile finished
   __syncthreads();
 
-  for (int s = 0; s < L.nsteps; ++s) {
+  // ---- IDCT of one rolling step's ROI blocks (static: thread per block) --
+  auto idct_step = [&](int s) {
     const int R = L.r0 + kStepRows * s;
-    // ---- IDCT of this step's ROI blocks --------------------------------
     const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
     const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P);
     const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
     const int ny = max(0, yb1 - yb0 + 1) * nbx0;
-    const int ncr = max(0, cb1 - cb0 + 1);
-    const int nc = ncr * nbxc;
+    const int nc = max(0, cb1 - cb0 + 1) * nbxc;
     const int ntask = ny + 2 * nc;
     for (int base = tid & ~31; base < ntask; base += kThreads) {
-      const int t = base + (tid & 31);
+      const int t = base + lane;
       const bool act = t < ntask;
       int c = 0, brow = 0, bcol = 0;
       if (t < ny) {
@@ -357,76 +372,134 @@ smol_fused_kernel(const KParams kp) {
         brow += cb0;
       }
       const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * 64;
-      uint8_t* plane = smem + L.off_pl[c];
-      const int ring = c ? kCRing : kYRing;
-      decode_block<K>(act, src, qf + c * 64, plane, L.pitch[c], ring, brow * P, bcol * P);
+      uint32_t px[8][2];
+      decode_block<K>(act, src, qf + c * 64, px);
+      if (!act) continue;
+      if (c == 0) {
+        uint8_t* d = yring + bcol * P;
+#pragma unroll
+        for (int y = 0; y < P; ++y) put_row<P>(d + ((brow * P + y) & (kYRing - 1)) * kYP, px[y]);
+      } else {
+        uint8_t* d = cring + (c - 1) * kCStride + bcol * P + kCPad;
+        const int gx0 = (L.bx0[c] + bcol) * P;
+        const bool edge = (gx0 == 0) || (gx0 <= im.Wc - 1 && im.Wc - 1 < gx0 + P);
+#pragma unroll
+        for (int y = 0; y < P; ++y) {
+          const int r = brow * P + y;
+          const int rs = r & (kCRing - 1);
+          // slot rs+1, plus the guard mirrors (slot 0 = 16, slot 17 = 1)
+          for (int k = 0; k < 1 + (rs == 15 || rs == 0); ++k) {
+            uint8_t* row = d + (k == 0 ? rs + 1 : (rs == 15 ? 0 : kCSlots - 1)) * kCP;
+            put_row<P>(row, px[y]);
+            if (edge) {
+              // replicate image-edge chroma columns into the neighbours the
+              // triangle filter reads (reading R2: indices clamp at the edges)
+              if (gx0 == 0) row[-1] = (uint8_t)byte_of(px[y], 0);
+              const int e = im.Wc - 1 - gx0;
+              if (e >= 0 && e < P) row[e + 1] = (uint8_t)byte_of(px[y], e);
+            }
+          }
+        }
+      }
     }
-    __syncthreads();
+  };
+
+  int ready_prev = L.ly0 - 1;
+  int done_prev = 0;                       // output rows of the tile finished
+  idct_step(0);
+  __syncthreads();
+
+  for (int s = 0; s < L.nsteps; ++s) {
+    const int ready = max(ready_prev, ready_after(L, im.Hc, s));
+    if (tid == 0) ctr[1] = 0;
 
     if constexpr (DEBUG) {
       // decoded samples of this step's block rows, clipped to the footprint
+      const int R = L.r0 + kStepRows * s;
       for (int c = 0; c < 3; ++c) {
         const int W = c ? im.Wc : im.Wd, Hh = c ? im.Hc : im.Hd;
-        const int rlo = c ? max(cb0 * P, L.cy0) : max(yb0 * P, L.ly0);
-        const int rhi = c ? min((cb1 + 1) * P - 1, L.cy1) : min((yb1 + 1) * P - 1, L.ly1);
+        int rlo, rhi;
+        if (c == 0) { rlo = max(max(L.by0[0], R / P) * P, L.ly0); rhi = min(min(L.by1[0], (R + kStepRows) / P - 1) * P + P - 1, L.ly1); }
+        else {
+          rlo = max(((s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P)) * P, L.cy0);
+          rhi = min(min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1) * P + P - 1, L.cy1);
+        }
         const int x0 = c ? L.cx0 : L.lx0, x1 = c ? L.cx1 : L.lx1;
-        const int ring = c ? kCRing : kYRing;
         int16_t* dst = kp.dbg_pl[c] + n * (c ? kp.dbg_stride_c : kp.dbg_stride_y);
         for (int y = rlo; y <= rhi; ++y)
           for (int x = x0 + tid; x <= x1; x += kThreads)
             if (y < Hh && x < W)
-              dst[(size_t)y * W + x] = smem[L.off_pl[c] + (y & (ring - 1)) * L.pitch[c] + (x - L.xbase[c])];
+              dst[(size_t)y * W + x] = c == 0 ? yring[(y & (kYRing - 1)) * kYP + (x - L.xbase[0])]
+                                              : cring[(c - 1) * kCStride + ((y & (kCRing - 1)) + 1) * kCP +
+                                                      (x - L.xbase[c] + kCPad)];
       }
     }
 
     // ---- upsample + colour of the RGB rows that became ready -------------
-    const int ready = max(ready_prev, ready_after(L, im.Hc, s));
+    // 2x2 luma quads (rows 2j, 2j+1; cols 2i, 2i+1) share one 3x3 chroma
+    // neighbourhood.  Quads start at even rows: a row already produced may
+    // be recomputed (same result) and an odd row past `ready` may be
+    // computed early from incomplete chroma (recomputed next step and never
+    // read before: outputs only read rows <= ready).
     {
-      const int nrows = ready - ready_prev;
-      const int ntaskc = max(0, nrows) * npairs;
-      const int cxlo = L.cx0, cxhi = L.cx1;
-      for (int t = tid; t < ntaskc; t += kThreads) {
+      const int j0 = (ready_prev + 1) >> 1;
+      const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
+      const int ntaskc = nq * npairs;
+      for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&ctr[0], 32);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (chunk >= ntaskc) break;
+        const int t = chunk + lane;
+        if (t >= ntaskc) continue;
         const int rr = (int)fdiv((uint32_t)t, fd_pairs);
         const int p = t - rr * npairs;
-        const int ly = ready_prev + 1 + rr;
-        const int i = (L.rgb_x0 >> 1) + p;                     // chroma column of the pair
-        const int j = ly >> 1;
-        const int j2 = (ly & 1) ? min(j + 1, L.cy1) : max(j - 1, L.cy0);
-        const int im1 = max(i - 1, cxlo) - L.xbase[1], ip1 = min(i + 1, cxhi) - L.xbase[1];
-        const int ic = i - L.xbase[1];
-        const uint8_t* cb_j = cbpl + (j & (kCRing - 1)) * L.pitch[1];
-        const uint8_t* cb_k = cbpl + (j2 & (kCRing - 1)) * L.pitch[1];
-        const uint8_t* cr_j = crpl + (j & (kCRing - 1)) * L.pitch[2];
-        const uint8_t* cr_k = crpl + (j2 & (kCRing - 1)) * L.pitch[2];
-        const int b0 = 3 * ldu8(cb_j + ic), b1 = 3 * ldu8(cb_k + ic);
-        const int cbE = 3 * (b0 + ldu8(cb_j + im1)) + (b1 + ldu8(cb_k + im1));
-        const int cbO = 3 * (b0 + ldu8(cb_j + ip1)) + (b1 + ldu8(cb_k + ip1));
-        const int r0 = 3 * ldu8(cr_j + ic), r1 = 3 * ldu8(cr_k + ic);
-        const int crE = 3 * (r0 + ldu8(cr_j + im1)) + (r1 + ldu8(cr_k + im1));
-        const int crO = 3 * (r0 + ldu8(cr_j + ip1)) + (r1 + ldu8(cr_k + ip1));
-        const uint32_t yy = *reinterpret_cast<const uint16_t*>(
-            ypl + (ly & (kYRing - 1)) * L.pitch[0] + (2 * i - L.xbase[0]));
-        const uint32_t pe = colour(yy & 255, cbE, crE);
-        const uint32_t po = colour(yy >> 8, cbO, crO);
-        *reinterpret_cast<uint2*>(rgb + (ly & (kRgbRing - 1)) * L.rgb_w + 2 * p) = make_uint2(pe, po);
+        const int j = j0 + rr;                               // chroma row of the quad
+        const int i = (L.rgb_x0 >> 1) + p;                   // chroma column of the quad
+        const uint8_t* c1 = cring + ((j & (kCRing - 1)) + 1) * kCP + (i - L.xbase[1] + kCPad);
+        const uint8_t* c0 = c1 + (j > 0 ? -kCP : 0);               // row j-1 (clamped at the top)
+        const uint8_t* c2 = c1 + (j < im.Hc - 1 ? kCP : 0);        // row j+1 (clamped at the bottom)
+        int cbq[4], crq[4];
+#pragma unroll
+        for (int comp = 0; comp < 2; ++comp) {
+          const int o = comp * kCStride;
+          const int m0 = 3 * ldu8(c0 + o), m1 = 3 * ldu8(c1 + o), m2 = 3 * ldu8(c2 + o);
+          const int e0 = m0 + ldu8(c0 + o - 1), e1 = m1 + ldu8(c1 + o - 1), e2 = m2 + ldu8(c2 + o - 1);
+          const int d0 = m0 + ldu8(c0 + o + 1), d1 = m1 + ldu8(c1 + o + 1), d2 = m2 + ldu8(c2 + o + 1);
+          int* qv = comp ? crq : cbq;
+          qv[0] = 3 * e1 + e0;     // (2j,   2i)
+          qv[1] = 3 * d1 + d0;     // (2j,   2i+1)
+          qv[2] = 3 * e1 + e2;     // (2j+1, 2i)
+          qv[3] = 3 * d1 + d2;     // (2j+1, 2i+1)
+        }
+        const uint8_t* yr = yring + ((2 * j) & (kYRing - 1)) * kYP + (2 * i - L.xbase[0]);
+        const uint32_t y0 = *reinterpret_cast<const uint16_t*>(yr);
+        const uint32_t y1 = *reinterpret_cast<const uint16_t*>(yr + kYP);
+        const int slot = (2 * j) & (kRgbRing - 1);
+        uint32_t* r0p = rgb + slot * rgb_p + 2 * p;
+        const uint2 top = make_uint2(colour(y0 & 255, cbq[0], crq[0]), colour(y0 >> 8, cbq[1], crq[1]));
+        *reinterpret_cast<uint2*>(r0p) = top;
+        *reinterpret_cast<uint2*>(r0p + rgb_p) =
+            make_uint2(colour(y1 & 255, cbq[2], crq[2]), colour(y1 >> 8, cbq[3], crq[3]));
+        if (slot == 0) *reinterpret_cast<uint2*>(r0p + kRgbRing * rgb_p) = top;   // guard row
       }
     }
     __syncthreads();
+    if (tid == 0) ctr[0] = 0;
 
     if constexpr (DEBUG) {
       int16_t* dst = kp.dbg_rgb + n * kp.dbg_stride_rgb;
       for (int y = ready_prev + 1; y <= ready; ++y)
         for (int x = L.lx0 + tid; x <= L.lx1; x += kThreads) {
-          const uint32_t v = rgb[(y & (kRgbRing - 1)) * L.rgb_w + (x - L.rgb_x0)];
+          const uint32_t v = rgb[(y & (kRgbRing - 1)) * rgb_p + (x - L.rgb_x0)];
           const size_t o = ((size_t)y * im.Wd + x) * 3;
           dst[o] = v & 255; dst[o + 1] = (v >> 8) & 255; dst[o + 2] = (v >> 16) & 255;
         }
     }
 
-    // ---- bilinear + normalize + NCHW store of the rows now complete -------
-    int done = done_prev;
+    // rows whose lower tap row is ready (taps are monotone): binary search
+    int done;
     {
-      // rows with lower tap <= ready (taps are monotone): binary search
       int lo = done_prev, hi = nth;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -434,65 +507,78 @@ smol_fused_kernel(const KParams kp) {
       }
       done = lo;
     }
+
+    // ---- next step's IDCT (writes only Y/chroma rings: no reader now) ----
+    if (s + 1 < L.nsteps) idct_step(s + 1);
+
+    // ---- bilinear + normalize + NCHW store, 4 output pixels per task -----
     {
-      const int nr = done - done_prev;
-      const int ntasko = nr * nopairs;
+      const int ntasko = (done - done_prev) * nq4;
       const float na0 = kp.na[0], na1 = kp.na[1], na2 = kp.na[2];
       const float nb0 = kp.nb[0], nb1 = kp.nb[1], nb2 = kp.nb[2];
-      for (int t = tid; t < ntasko; t += kThreads) {
-        const int rr = (int)fdiv((uint32_t)t, fd_opairs);
+      for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&ctr[1], 32);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (chunk >= ntasko) break;
+        const int t = chunk + lane;
+        if (t >= ntasko) continue;
+        const int rr = (int)fdiv((uint32_t)t, fd_q4);
         const int r = done_prev + rr;
-        const int ox = 2 * (t - rr * nopairs);
+        const int ox = 4 * (t - rr * nq4);
         const int2 ty = yt[r];
         const float wy = __int_as_float(ty.y);
-        const uint32_t* row0 = rgb + ((ty.x & 0xffff) & (kRgbRing - 1)) * L.rgb_w;
-        const uint32_t* row1 = rgb + (((uint32_t)ty.x >> 16) & (kRgbRing - 1)) * L.rgb_w;
-        float y[2][3];
+        const uint32_t* row0 = rgb + ((ty.x & 0xffff) & (kRgbRing - 1)) * rgb_p;
+        float y[3][4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int2 tx = xt[min(ox + e, ntw - 1)];
+        for (int e = 0; e < 4; ++e) {
+          const int2 tx = xt[ox + e];                        // padded: ox + e <= ntw + 2
           const float wx = __int_as_float(tx.y);
-          const int x0 = tx.x & 0xffff, x1 = (int)((uint32_t)tx.x >> 16);
-          const uint32_t p00 = row0[x0], p01 = row0[x1], p10 = row1[x0], p11 = row1[x1];
+          const uint32_t* a = row0 + tx.x;
+          const uint32_t p00 = a[0], p01 = a[1], p10 = a[rgb_p], p11 = a[rgb_p + 1];
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            const float a = byte_f(p00, ch), b = byte_f(p01, ch);
-            const float c = byte_f(p10, ch), d = byte_f(p11, ch);
-            const float top = fmaf(wx, b - a, a);
-            const float bot = fmaf(wx, d - c, c);
-            y[e][ch] = fmaf(wy, bot - top, top);
+            const float fa = byte_f(p00, ch), fb = byte_f(p01, ch);
+            const float fc = byte_f(p10, ch), fd = byte_f(p11, ch);
+            const float tp = fmaf(wx, fb - fa, fa);
+            const float bt = fmaf(wx, fd - fc, fc);
+            y[ch][e] = fmaf(wy, bt - tp, tp);
           }
-          y[e][0] = fmaf(y[e][0], na0, nb0);
-          y[e][1] = fmaf(y[e][1], na1, nb1);
-          y[e][2] = fmaf(y[e][2], na2, nb2);
+          y[0][e] = fmaf(y[0][e], na0, nb0);
+          y[1][e] = fmaf(y[1][e], na1, nb1);
+          y[2][e] = fmaf(y[2][e], na2, nb2);
         }
-        const int oy = oy0 + r, oxg = ox0 + ox;
-        const size_t o = ((size_t)n * 3 * kp.OH + oy) * kp.OW + oxg;
-        const bool pair = (ox + 1 < ntw) && ((kp.OW & 1) == 0);
-        if constexpr (F16) {
-          __half* ob = reinterpret_cast<__half*>(kp.out) + o;
+        const size_t o = ((size_t)n * 3 * kp.OH + (oy0 + r)) * kp.OW + (ox0 + ox);
+        if (vec4 && ox + 4 <= ntw) {
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            if (pair) *reinterpret_cast<__half2*>(ob + ch * plane_sz) = __floats2half2_rn(y[0][ch], y[1][ch]);
-            else {
-              ob[ch * plane_sz] = __float2half_rn(y[0][ch]);
-              if (ox + 1 < ntw) ob[ch * plane_sz + 1] = __float2half_rn(y[1][ch]);
+            if constexpr (F16) {
+              const __half2 h0 = __floats2half2_rn(y[ch][0], y[ch][1]);
+              const __half2 h1 = __floats2half2_rn(y[ch][2], y[ch][3]);
+              uint2 v;
+              v.x = *reinterpret_cast<const uint32_t*>(&h0);
+              v.y = *reinterpret_cast<const uint32_t*>(&h1);
+              __stcs(reinterpret_cast<uint2*>(reinterpret_cast<__half*>(kp.out) + o + ch * plane_sz), v);
+            } else {
+              __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(kp.out) + o + ch * plane_sz),
+                     make_float4(y[ch][0], y[ch][1], y[ch][2], y[ch][3]));
             }
           }
         } else {
-          float* ob = reinterpret_cast<float*>(kp.out) + o;
 #pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            if (pair) __stcs(reinterpret_cast<float2*>(ob + ch * plane_sz), make_float2(y[0][ch], y[1][ch]));
-            else {
-              __stcs(ob + ch * plane_sz, y[0][ch]);
-              if (ox + 1 < ntw) __stcs(ob + ch * plane_sz + 1, y[1][ch]);
+          for (int e = 0; e < 4; ++e) {
+            if (ox + e >= ntw) break;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              if constexpr (F16) reinterpret_cast<__half*>(kp.out)[o + e + ch * plane_sz] = __float2half_rn(y[ch][e]);
+              else reinterpret_cast<float*>(kp.out)[o + e + ch * plane_sz] = y[ch][e];
             }
           }
         }
       }
     }
-    ready_prev = max(ready_prev, ready);
+    __syncthreads();
+    ready_prev = ready;
     done_prev = done;
   }
 }

@@ -373,8 +373,11 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
     if (rc) return rc;
   }
   // shared memory of the largest tile over the batch's distinct geometries
+  // (a tile whose footprint exceeds the fixed ring pitches reports INT_MAX/2)
+  auto cols_of = [&](int n_col_tiles) { return (ceil_div(pl->OW, n_col_tiles) + 3) & ~3; };  // multiple of 4
   auto max_smem = [&](int n_col_tiles) {
-    const int tile_cols = ceil_div(pl->OW, n_col_tiles);
+    const int tile_cols = cols_of(n_col_tiles);
+    n_col_tiles = ceil_div(pl->OW, tile_cols);
     int m = 0;
     int prev_w = -1, prev_h = -1, prev_l = -2, prev_t = -2;
     for (int i = 0; i < b->n_images; ++i) {
@@ -386,7 +389,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
           TileLayout L;
           tile_layout(h[i], K, t * tile_rows, imin(pl->OH, (t + 1) * tile_rows), u * tile_cols,
                       imin(pl->OW, (u + 1) * tile_cols), L);
-          m = imax(m, L.total);
+          m = imax(m, L.fits ? L.total : (1 << 30));
         }
       prev_w = di->width; prev_h = di->height; prev_l = di->roi_left; prev_t = di->roi_top;
     }
@@ -395,7 +398,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   // column tiles only when a full-width tile would not leave 2 CTAs per SM
   int n_col_tiles = 1;
   int smem = max_smem(1);
-  while (smem > pl->smem_optin / 2 && n_col_tiles < 64 && 2 * n_col_tiles <= pl->OW) {
+  while (smem > pl->smem_optin / 2 && n_col_tiles < 64 && 8 * n_col_tiles <= pl->OW) {
     n_col_tiles *= 2;
     smem = max_smem(n_col_tiles);
   }
@@ -408,7 +411,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   kp.qtables = b->qtables;
   kp.out = out;
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;
-  kp.n_col_tiles = n_col_tiles; kp.tile_cols = ceil_div(pl->OW, n_col_tiles);
+  kp.tile_cols = cols_of(n_col_tiles);
+  kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr);
   dim3 grid(ntiles * n_col_tiles, b->n_images);
