@@ -205,20 +205,26 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     cfg = synth.CONFIGS[args.config]
-    imgs, qt = synth.batch_images(cfg)
     params = smol.params_from_config(cfg, tile_rows=args.tile_rows)
-    plan = smol.Plan(params, cfg.n)
+    # weak scaling: a global batch of cfg.n images per GPU, partitioned into
+    # contiguous ROI-balanced ranges (one per rank); no data-path collective
+    from paper_2007_13005_b200 import shard
+    all_imgs, qt = synth.batch_images(cfg, n=cfg.n * world)
+    lo, hi = shard.partition(shard.roi_weights(params, all_imgs), world)[rank]
+    imgs = all_imgs[lo:hi]
+    nloc = len(imgs)
+    plan = smol.Plan(params, max(nloc, 1))
     arena_bytes = sum(im.nbytes() for im in imgs)
     reps = args.replicas or max(2, int(np.ceil(1.5 * L2_BYTES / max(arena_bytes, 1))) + 1)
     batches = [smol.CoefBatch(imgs, qt) for _ in range(reps)]
-    out = plan.new_output(cfg.n)
+    out = plan.new_output(nloc)
     stream = torch.cuda.Stream()
 
     # algorithmic bytes per image: ROI coefficients + output tensor
     g = smol.geometry(params, cfg.width, cfg.height)
     out_bytes = 3 * g["OH"] * g["OW"] * (2 if cfg.out_dtype == "f16" else 4)
     alg_bytes_img = g["roi_coef_bytes"] + out_bytes
-    alg_bytes_launch = alg_bytes_img * cfg.n
+    alg_bytes_launch = alg_bytes_img * nloc
 
     def step(k, o=out):
         plan.run(batches[k % reps], out=o, stream=stream)
@@ -241,12 +247,8 @@ def main():
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = cfg.n * args.steps * world / (ms_max / 1e3)
+    ms_max = shard.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
+    value = len(all_imgs) * args.steps / (ms_max / 1e3)
 
     # ---- per-launch kernel duration (events bracket each launch) ------------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -272,11 +274,8 @@ def main():
             res_host.copy_(out[:1], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-    te = torch.tensor([e2e_ms], device="cuda")
-    if dist:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = cfg.n * world / (float(te.item()) / 1e3)
+    e2e_ms = shard.max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, device="cuda")
+    e2e_value = len(all_imgs) / (e2e_ms / 1e3)
 
     if rank == 0:
         peak, peak_src = _peaks()
@@ -286,8 +285,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": cfg.out_dtype if False else "f32",
             "data": "synthetic (seeded natural-image JPEG coefficients, synth/)",
-            "config": {"workload": _workload_name(cfg), "batch_per_gpu": cfg.n,
-                       "global_batch": cfg.n * world, "parallelism": f"image shards x{world}, no collective",
+            "config": {"workload": _workload_name(cfg), "batch_per_gpu": nloc,
+                       "global_batch": len(all_imgs), "parallelism": f"image shards x{world}, no collective",
                        "l2": f"inputs larger than L2: {reps} rotating replicas of the "
                              f"{arena_bytes / 1e6:.0f} MB coefficient arena",
                        "alg_bytes_per_image": alg_bytes_img,
@@ -299,8 +298,8 @@ def main():
                          "kernel": "smol_fused_kernel", "launch_ms": launch_ms,
                          "alg_bytes_per_launch": alg_bytes_launch},
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": g["roi_coef_bytes"] * cfg.n,
-                    "d2h_bytes_per_step": int(res_host.numel() * res_host.element_size()),
+                    "h2d_bytes_per_step": g["roi_coef_bytes"] * len(all_imgs),
+                    "d2h_bytes_per_step": int(res_host.numel() * res_host.element_size()) * world,
                     "path": "smol_preproc_run_host: kernel reads ROI blocks from pinned host memory "
                             "over PCIe; D2H of one image's output as the step's result read"},
             "gpu_launches": args.steps * plan.launches_per_run(),
