@@ -71,7 +71,7 @@ struct TileLayout {
   int cy0, cy1, cx0, cx1;          // chroma footprint incl. triangle neighbours (R2)
   int by0[3], by1[3], bx0[3], bx1[3];   // ROI block ranges per component
   int xbase[3];                    // decoded column of ring column 0 (= bx0 * P)
-  int rgb_x0, rgb_w, rgb_p;        // RGB ring: first column (even), width (even), pitch (u32)
+  int rgb_x0, rgb_w, rgb_p;        // RGB ring: first column, width, pitch (u32; multiples of 4)
   int r0, nsteps;                  // first rolling-step row (16-aligned) and step count
   int fits;                        // footprint fits the fixed ring pitches
   // byte offsets in dynamic shared memory
@@ -92,23 +92,23 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.cy1 = imin(im.Hc - 1, (L.ly1 + 1) >> 1);
   L.cx0 = imax(0, (L.lx0 - 1) >> 1);
   L.cx1 = imin(im.Wc - 1, (L.lx1 + 1) >> 1);
-  // luma columns are processed in even/odd pairs: widen to even alignment
-  // (never beyond the image's valid block columns)
+  // luma columns are processed 4 at a time (two 2x2 quads): widen to
+  // 4-alignment (never beyond the image's valid block columns)
   L.by0[0] = L.ly0 / P; L.by1[0] = L.ly1 / P;
-  L.bx0[0] = (L.lx0 & ~1) / P;
-  L.bx1[0] = imin((L.lx1 | 1) / P, im.nbw[0] - 1);
+  L.bx0[0] = (L.lx0 & ~3) / P;
+  L.bx1[0] = imin((L.lx1 | 3) / P, im.nbw[0] - 1);
   for (int c = 1; c < 3; ++c) {
     L.by0[c] = L.cy0 / P; L.by1[c] = L.cy1 / P;
     L.bx0[c] = L.cx0 / P; L.bx1[c] = L.cx1 / P;
   }
   for (int c = 0; c < 3; ++c) L.xbase[c] = L.bx0[c] * P;
-  L.rgb_x0 = L.lx0 & ~1;
-  L.rgb_w = ((L.lx1 | 1) - L.rgb_x0 + 1);
-  L.rgb_p = L.rgb_w + 2;
+  L.rgb_x0 = L.lx0 & ~3;
+  L.rgb_w = ((L.lx1 | 3) - L.rgb_x0 + 1);
+  L.rgb_p = L.rgb_w + 4;
   L.r0 = L.ly0 & ~(kStepRows - 1);
   // the last step must cover luma row ly1 and chroma row cy1 (luma 2 cy1)
   L.nsteps = ((imax(L.ly1, 2 * L.cy1) - L.r0) / kStepRows) + 1;
-  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 2 <= kYP) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= kCP);
+  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= kYP) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= kCP);
   int off = 0;
   L.off_q = off;   off += 3 * 64 * 4;                         // dequant tables (float)
   L.off_xt = off;  off += align16((ox1 - ox0 + 3) * 8);       // x taps: {4 x0, w}
@@ -125,14 +125,16 @@ SMOL_HD long long tile_roi_blocks(const TileLayout& L) {
   return n;
 }
 
-// Last RGB row computable after rolling step s (decoded luma rows
+// Last RGB row produced after rolling step s (decoded luma rows
 // [r0 + 16 s, r0 + 16 s + 16) and chroma rows [.. /2, +8) are decoded):
 // luma row L needs chroma rows L>>1 and, for odd L, min(L>>1 + 1, Hc - 1).
+// While chroma is the limit the step ends on an odd row (2 chi - 1), so the
+// next step starts on an even row and 2x2 quads never straddle steps.
 SMOL_HD int ready_after(const TileLayout& L, int Hc, int s) {
   const int R = L.r0 + kStepRows * s;
   const int chi = imin(L.cy1, (R >> 1) + kStepRows / 2 - 1);
   int r = imin(L.ly1, R + kStepRows - 1);
-  if (chi < Hc - 1) r = imin(r, 2 * chi);
+  if (chi < Hc - 1) r = imin(r, chi < L.cy1 ? 2 * chi - 1 : 2 * chi);
   return r;
 }
 

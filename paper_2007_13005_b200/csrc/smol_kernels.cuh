@@ -338,8 +338,8 @@ smol_fused_kernel(const KParams kp) {
   }
   const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
   const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
-  const int npairs = L.rgb_w >> 1;
-  const FastDiv fd_pairs = make_fastdiv(npairs);
+  const int ntask4 = L.rgb_w >> 2;          // 4-column colour tasks per quad row
+  const FastDiv fd_t4 = make_fastdiv(ntask4);
   const int nq4 = (ntw + 3) >> 2;
   const FastDiv fd_q4 = make_fastdiv(nq4);
   const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0);
@@ -436,15 +436,14 @@ smol_fused_kernel(const KParams kp) {
     }
 
     // ---- upsample + colour of the RGB rows that became ready -------------
-    // 2x2 luma quads (rows 2j, 2j+1; cols 2i, 2i+1) share one 3x3 chroma
-    // neighbourhood.  Quads start at even rows: a row already produced may
-    // be recomputed (same result) and an odd row past `ready` may be
-    // computed early from incomplete chroma (recomputed next step and never
-    // read before: outputs only read rows <= ready).
+    // A task is 2x4 luma pixels (rows 2j, 2j+1; cols 2i .. 2i+3) sharing a
+    // 3x4 chroma neighbourhood.  Steps end on odd rows (ready_after), so
+    // quads never straddle steps; at the footprint's first/last row a quad
+    // may include one row outside it (computed, never read).
     {
       const int j0 = (ready_prev + 1) >> 1;
       const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
-      const int ntaskc = nq * npairs;
+      const int ntaskc = nq * ntask4;
       for (;;) {
         int chunk = 0;
         if (lane == 0) chunk = atomicAdd(&ctr[0], 32);
@@ -452,36 +451,47 @@ smol_fused_kernel(const KParams kp) {
         if (chunk >= ntaskc) break;
         const int t = chunk + lane;
         if (t >= ntaskc) continue;
-        const int rr = (int)fdiv((uint32_t)t, fd_pairs);
-        const int p = t - rr * npairs;
-        const int j = j0 + rr;                               // chroma row of the quad
-        const int i = (L.rgb_x0 >> 1) + p;                   // chroma column of the quad
+        const int rr = (int)fdiv((uint32_t)t, fd_t4);
+        const int p = t - rr * ntask4;
+        const int j = j0 + rr;                               // chroma row of the quads
+        const int i = (L.rgb_x0 >> 1) + 2 * p;               // chroma column of the left quad
         const uint8_t* c1 = cring + ((j & (kCRing - 1)) + 1) * kCP + (i - L.xbase[1] + kCPad);
         const uint8_t* c0 = c1 + (j > 0 ? -kCP : 0);               // row j-1 (clamped at the top)
         const uint8_t* c2 = c1 + (j < im.Hc - 1 ? kCP : 0);        // row j+1 (clamped at the bottom)
-        int cbq[4], crq[4];
+        int cbq[8], crq[8];                                  // [row 0: 4 cols][row 1: 4 cols]
 #pragma unroll
         for (int comp = 0; comp < 2; ++comp) {
           const int o = comp * kCStride;
-          const int m0 = 3 * ldu8(c0 + o), m1 = 3 * ldu8(c1 + o), m2 = 3 * ldu8(c2 + o);
-          const int e0 = m0 + ldu8(c0 + o - 1), e1 = m1 + ldu8(c1 + o - 1), e2 = m2 + ldu8(c2 + o - 1);
-          const int d0 = m0 + ldu8(c0 + o + 1), d1 = m1 + ldu8(c1 + o + 1), d2 = m2 + ldu8(c2 + o + 1);
+          int h[3][4];                                       // horizontal 3/1 taps per chroma row
+          const uint8_t* rows[3] = {c0, c1, c2};
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const int a = ldu8(rows[r] + o - 1), m = ldu8(rows[r] + o), n2 = ldu8(rows[r] + o + 1),
+                      z = ldu8(rows[r] + o + 2);
+            h[r][0] = 3 * m + a;     // col 2i
+            h[r][1] = 3 * m + n2;    // col 2i+1
+            h[r][2] = 3 * n2 + m;    // col 2i+2
+            h[r][3] = 3 * n2 + z;    // col 2i+3
+          }
           int* qv = comp ? crq : cbq;
-          qv[0] = 3 * e1 + e0;     // (2j,   2i)
-          qv[1] = 3 * d1 + d0;     // (2j,   2i+1)
-          qv[2] = 3 * e1 + e2;     // (2j+1, 2i)
-          qv[3] = 3 * d1 + d2;     // (2j+1, 2i+1)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            qv[x] = 3 * h[1][x] + h[0][x];       // row 2j
+            qv[4 + x] = 3 * h[1][x] + h[2][x];   // row 2j+1
+          }
         }
         const uint8_t* yr = yring + ((2 * j) & (kYRing - 1)) * kYP + (2 * i - L.xbase[0]);
-        const uint32_t y0 = *reinterpret_cast<const uint16_t*>(yr);
-        const uint32_t y1 = *reinterpret_cast<const uint16_t*>(yr + kYP);
+        const uint32_t y0 = *reinterpret_cast<const uint32_t*>(yr);
+        const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
         const int slot = (2 * j) & (kRgbRing - 1);
-        uint32_t* r0p = rgb + slot * rgb_p + 2 * p;
-        const uint2 top = make_uint2(colour(y0 & 255, cbq[0], crq[0]), colour(y0 >> 8, cbq[1], crq[1]));
-        *reinterpret_cast<uint2*>(r0p) = top;
-        *reinterpret_cast<uint2*>(r0p + rgb_p) =
-            make_uint2(colour(y1 & 255, cbq[2], crq[2]), colour(y1 >> 8, cbq[3], crq[3]));
-        if (slot == 0) *reinterpret_cast<uint2*>(r0p + kRgbRing * rgb_p) = top;   // guard row
+        uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
+        const uint4 top = make_uint4(colour(y0 & 255, cbq[0], crq[0]), colour((y0 >> 8) & 255, cbq[1], crq[1]),
+                                     colour((y0 >> 16) & 255, cbq[2], crq[2]), colour(y0 >> 24, cbq[3], crq[3]));
+        *reinterpret_cast<uint4*>(r0p) = top;
+        *reinterpret_cast<uint4*>(r0p + rgb_p) =
+            make_uint4(colour(y1 & 255, cbq[4], crq[4]), colour((y1 >> 8) & 255, cbq[5], crq[5]),
+                       colour((y1 >> 16) & 255, cbq[6], crq[6]), colour(y1 >> 24, cbq[7], crq[7]));
+        if (slot == 0) *reinterpret_cast<uint4*>(r0p + kRgbRing * rgb_p) = top;   // guard row
       }
     }
     __syncthreads();
@@ -530,9 +540,12 @@ smol_fused_kernel(const KParams kp) {
         const float wy = __int_as_float(ty.y);
         const uint32_t* row0 = rgb + ((ty.x & 0xffff) & (kRgbRing - 1)) * rgb_p;
         float y[3][4];
+        const int4 txa = *reinterpret_cast<const int4*>(xt + ox);      // taps of ox, ox+1
+        const int4 txb = *reinterpret_cast<const int4*>(xt + ox + 2);  // taps of ox+2, ox+3 (padded)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int2 tx = xt[ox + e];                        // padded: ox + e <= ntw + 2
+          const int2 tx = e == 0 ? make_int2(txa.x, txa.y) : e == 1 ? make_int2(txa.z, txa.w)
+                        : e == 2 ? make_int2(txb.x, txb.y) : make_int2(txb.z, txb.w);
           const float wx = __int_as_float(tx.y);
           const uint32_t* a = row0 + tx.x;
           const uint32_t p00 = a[0], p01 = a[1], p10 = a[rgb_p], p11 = a[rgb_p + 1];

@@ -72,9 +72,9 @@ def test_geometry_matches_oracle_and_rationals(native, oracle_mod, k):
             ly1 = _src_tap(g["top"] + g["OH"] - 1, g["Hd"], g["Hr"])[1]
             assert (g["lx0"], g["lx1"], g["ly0"], g["ly1"]) == (lx0, lx1, ly0, ly1)
             P = 8 // k
-            # luma columns are decoded in even/odd pairs (widened to even
-            # alignment, within the image's valid block columns)
-            assert (g["bx0"][0], g["bx1"][0]) == ((lx0 & ~1) // P, min((lx1 | 1) // P, -(-w // 8) - 1))
+            # luma columns are decoded in groups of 4 (2x2 quads, widened to
+            # 4-alignment, within the image's valid block columns)
+            assert (g["bx0"][0], g["bx1"][0]) == ((lx0 & ~3) // P, min((lx1 | 3) // P, -(-w // 8) - 1))
             cx0, cx1 = max(0, (lx0 - 1) // 2), min(g["Wc"] - 1, (lx1 + 1) // 2)
             assert (g["bx0"][1], g["bx1"][1]) == (cx0 // P, cx1 // P)
 
