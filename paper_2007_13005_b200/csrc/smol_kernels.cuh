@@ -435,6 +435,24 @@ smol_fused_kernel(const KParams kp) {
       }
     }
 
+    // ---- prefetch step s+1's ROI block rows into L2 (TMA bulk prefetch) --
+    // one contiguous segment per (component, block row); the IDCT of step
+    // s+1 (next phase) then hits L2 instead of waiting on HBM.
+    if (s + 1 < L.nsteps && tid < 32) {
+      const int R = L.r0 + kStepRows * (s + 1);
+      const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
+      const int cb0 = max(L.by0[1], (R >> 1) / P);
+      const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
+      const int ny = max(0, yb1 - yb0 + 1), nc = max(0, cb1 - cb0 + 1);
+      for (int k = tid; k < ny + 2 * nc; k += 32) {
+        int c = 0, brow = yb0 + k;
+        if (k >= ny) { c = 1 + (k - ny >= nc); brow = cb0 + (k - ny) - (c - 1) * nc; }
+        const int16_t* p = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)L.bx0[c] * 64;
+        const uint32_t bytes = (uint32_t)(L.bx1[c] - L.bx0[c] + 1) * 128u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+      }
+    }
+
     // ---- upsample + colour of the RGB rows that became ready -------------
     // A task is 2x4 luma pixels (rows 2j, 2j+1; cols 2i .. 2i+3) sharing a
     // 3x4 chroma neighbourhood.  Steps end on odd rows (ready_after), so
