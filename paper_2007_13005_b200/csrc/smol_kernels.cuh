@@ -258,8 +258,6 @@ struct KParams {
   const uint16_t* qtables;
   void* out;
   int OW, OH, tile_rows, tile_cols, n_col_tiles;
-  int n_items, tiles_per_image;    // work items = (image, tile), strided over CTAs
-  int max_tw, max_th, rgb_pmax;    // per-item table sizes / RGB ring pitch (u32)
   float na[3], nb[3];              // y = x * na + nb = (x/255 - mean)/std
   int16_t* dbg_pl[3];              // debug planes (DEBUG instantiation only)
   int16_t* dbg_rgb;
@@ -276,6 +274,10 @@ __device__ __forceinline__ float byte_f(uint32_t x, int b) {
 }
 
 
+#ifndef SMOL_MIN_BLOCKS
+#define SMOL_MIN_BLOCKS 3
+#endif
+
 template <int P>
 __device__ __forceinline__ void put_row(uint8_t* d, const uint32_t (&w)[2]) {
   if constexpr (P == 8) *reinterpret_cast<uint2*>(d) = make_uint2(w[0], w[1]);
@@ -288,430 +290,328 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[2], int e) {
   return (w[e >> 2] >> (8 * (e & 3))) & 255u;
 }
 
-// =========================================================================
-// Warp-specialised persistent pipeline (one CTA per SM).
-//
-//   IDCT warps (producer)   for each rolling step g of the CTA's work items:
-//                           wait cdone[g - kLag]; decode the step's ROI blocks
-//                           into the Y / Cb / Cr rings; arrive full[g].
-//   consumer warps          phase g: wait full[g]; colour(g) (upsample + JFIF
-//                           into the RGB ring) together with output(g-1)
-//                           (bilinear + normalize + NCHW stores); consumer-only
-//                           named barrier; arrive cdone[g].
-// No CTA-wide barrier after setup.  Rings are indexed by *virtual* rows that
-// continue across work items, so the producer can start item k+1 while the
-// consumers finish item k (item contexts are double-buffered, released by the
-// consumers through ctxfree[]).
-// =========================================================================
-#ifndef SMOL_DISABLE_PIPELINE
-constexpr int kPY = 64;          // Y ring rows (4 steps)
-constexpr int kPC = 64;          // chroma ring rows per component (+2 guard slots)
-constexpr int kPR = 64;          // RGB ring rows (+1 guard slot)
-constexpr int kLag = 2;          // producer may run this many steps ahead
-constexpr int kDepth = 4;        // mbarrier ring depth (> kLag)
-constexpr int kPCStride = (kPC + 2) * kCP;   // Cr ring follows the Cb ring
-
-template <int K> struct Roles { static constexpr int NI = 2, NC = 14; };
-template <> struct Roles<1> { static constexpr int NI = 4, NC = 12; };
-
-struct ItemCtx {
-  DevImage im;
-  TileLayout L;
-  int gstart;                     // CTA-global index of the item's first step
-  int k;                          // CTA-local item index (chroma spare slot)
-  int n, oy0, ox0, ntw, nth;
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "SMOL_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra SMOL_WAIT_%=;\n}"
-      :: "r"(smem_u32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
-}
-
 template <int K, bool F16, bool DEBUG>
-__global__ void __launch_bounds__((Roles<K>::NI + Roles<K>::NC) * 32, 1)
-smol_pipeline_kernel(const KParams kp) {
-  constexpr int P = 8 / K;
-  constexpr int NI = Roles<K>::NI, NC = Roles<K>::NC;
-  constexpr int NIT = NI * 32, NCT = NC * 32;
+__global__ void __launch_bounds__(kThreads, SMOL_MIN_BLOCKS)
+smol_fused_kernel(const KParams kp) {
+  constexpr int P = 8 / K;                 // decoded samples per block side
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ ItemCtx ctx[2];
-  __shared__ __align__(8) uint64_t full[kDepth], cdone[kDepth], ctxfree[2];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int n = blockIdx.y;
+  const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
+  const int oy0 = trow * kp.tile_rows, oy1 = min(kp.OH, oy0 + kp.tile_rows);
+  const int ox0 = tcol * kp.tile_cols, ox1 = min(kp.OW, ox0 + kp.tile_cols);
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // dynamic smem: [ctx tables x2][Y ring][Cb ring][Cr ring][RGB ring]
-  const int tab_q = 3 * 64 * 4, tab_x = align16((kp.max_tw + 4) * 8), tab_y = align16(kp.max_th * 8);
-  const int tab = tab_q + tab_x + tab_y;
-  uint8_t* yring = smem + 2 * tab;
-  uint8_t* cring = yring + kPY * kYP;
-  uint32_t* rgb = reinterpret_cast<uint32_t*>(cring + 2 * kPCStride);
-  const int rgb_p = kp.rgb_pmax;
-  auto tq = [&](int c) { return reinterpret_cast<float*>(smem + c * tab); };
-  auto tx = [&](int c) { return reinterpret_cast<int2*>(smem + c * tab + tab_q); };
-  auto tyt = [&](int c) { return reinterpret_cast<int2*>(smem + c * tab + tab_q + tab_x); };
-
+  __shared__ DevImage im;
+  __shared__ TileLayout L;
+  __shared__ int ctr[2];                   // dynamic work counters (colour, output)
   if (tid == 0) {
-    for (int i = 0; i < kDepth; ++i) { mbar_init(&full[i], NI); mbar_init(&cdone[i], NC); }
-    mbar_init(&ctxfree[0], NC);
-    mbar_init(&ctxfree[1], NC);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    im = kp.imgs[n];
+    tile_layout(im, K, oy0, oy1, ox0, ox1, L);
+    ctr[0] = 0;
+    ctr[1] = 0;
   }
   __syncthreads();
-  const int G = gridDim.x;
+  float* qf = reinterpret_cast<float*>(smem + L.off_q);
+  int2* xt = reinterpret_cast<int2*>(smem + L.off_xt);
+  int2* yt = reinterpret_cast<int2*>(smem + L.off_yt);
+  uint8_t* yring = smem + L.off_y;
+  uint8_t* cring = smem + L.off_c;
+  uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + L.off_rgb);
+  constexpr int kCStride = kCSlots * kCP;  // Cr ring follows the Cb ring
+  const int ntw = ox1 - ox0, nth = oy1 - oy0;
+  const int rgb_p = L.rgb_p;
 
-  if (warp < NI) {
-    // =========================== producer: IDCT ===========================
-    const int it = tid;                    // 0 .. NIT-1
-    int g = 0;
-    for (int k = 0;; ++k) {
-      const int item = blockIdx.x + k * G;
-      if (item >= kp.n_items) break;
-      const int c = k & 1;
-      if (k >= 2) mbar_wait(&ctxfree[c], ((k - 2) >> 1) & 1);
-      if (it == 0) {
-        ItemCtx& x = ctx[c];
-        const int n = item / kp.tiles_per_image, t = item - n * kp.tiles_per_image;
-        const int trow = t / kp.n_col_tiles, tcol = t - trow * kp.n_col_tiles;
-        x.n = n;
-        x.oy0 = trow * kp.tile_rows;
-        x.ox0 = tcol * kp.tile_cols;
-        x.nth = min(kp.OH, x.oy0 + kp.tile_rows) - x.oy0;
-        x.ntw = min(kp.OW, x.ox0 + kp.tile_cols) - x.ox0;
-        x.im = kp.imgs[n];
-        tile_layout(x.im, K, x.oy0, x.oy0 + x.nth, x.ox0, x.ox0 + x.ntw, x.L);
-        x.gstart = g;
-        x.k = k;
+  // ---- prologue: dequant tables (Q/8, exact) and bilinear taps ----------
+  // Taps use exact-integer coordinates (R9).  Where the upper tap is clamped
+  // (i1 == i0) its weight is zeroed so the kernel may always read i0 + 1.
+  for (int i = tid; i < 3 * 64; i += kThreads)
+    qf[i] = (float)kp.qtables[im.qidx[i >> 6] * 64 + (i & 63)] * 0.125f;
+  for (int i = tid; i < ntw + 3; i += kThreads) {
+    int i0, i1; float w;
+    src_tap(im.left + ox0 + min(i, ntw - 1), im.Wd, im.Wr, i0, i1, w);
+    xt[i] = make_int2(i0 - L.rgb_x0, __float_as_int(i1 == i0 ? 0.f : w));
+  }
+  for (int i = tid; i < nth; i += kThreads) {
+    int i0, i1; float w;
+    src_tap(im.top + oy0 + i, im.Hd, im.Hr, i0, i1, w);
+    yt[i] = make_int2(i0 | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
+  }
+  const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
+  const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
+  const int ntask4 = L.rgb_w >> 2;          // 4-column colour tasks per quad row
+  const FastDiv fd_t4 = make_fastdiv(ntask4);
+  const int nq4 = (ntw + 3) >> 2;
+  const FastDiv fd_q4 = make_fastdiv(nq4);
+  const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0);
+  const size_t plane_sz = (size_t)kp.OH * kp.OW;
+  __syncthreads();
+
+  // ---- IDCT of one rolling step's ROI blocks (static: thread per block) --
+  auto idct_step = [&](int s) {
+    const int R = L.r0 + kStepRows * s;
+    const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
+    const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P);
+    const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
+    const int ny = max(0, yb1 - yb0 + 1) * nbx0;
+    const int nc = max(0, cb1 - cb0 + 1) * nbxc;
+    const int ntask = ny + 2 * nc;
+    for (int base = tid & ~31; base < ntask; base += kThreads) {
+      const int t = base + lane;
+      const bool act = t < ntask;
+      int c = 0, brow = 0, bcol = 0;
+      if (t < ny) {
+        brow = (int)fdiv((uint32_t)t, fd_y);
+        bcol = t - brow * nbx0;
+        brow += yb0;
+      } else if (act) {
+        int tt = t - ny;
+        c = 1 + (tt >= nc);
+        tt -= (c - 1) * nc;
+        brow = (int)fdiv((uint32_t)tt, fd_c);
+        bcol = tt - brow * nbxc;
+        brow += cb0;
       }
-      named_bar(2, NIT);
-      const ItemCtx& x = ctx[c];
-      {
-        float* qf = tq(c);
-        int2* xt = tx(c);
-        int2* yt = tyt(c);
-        for (int i = it; i < 3 * 64; i += NIT)
-          qf[i] = (float)kp.qtables[x.im.qidx[i >> 6] * 64 + (i & 63)] * 0.125f;
-        for (int i = it; i < x.ntw + 4; i += NIT) {
-          int i0, i1; float w;
-          src_tap(x.im.left + x.ox0 + min(i, x.ntw - 1), x.im.Wd, x.im.Wr, i0, i1, w);
-          xt[i] = make_int2(i0 - x.L.rgb_x0, __float_as_int(i1 == i0 ? 0.f : w));
-        }
-        for (int i = it; i < x.nth; i += NIT) {
-          int i0, i1; float w;
-          src_tap(x.im.top + x.oy0 + i, x.im.Hd, x.im.Hr, i0, i1, w);
-          yt[i] = make_int2(i0 | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
-        }
-      }
-      named_bar(2, NIT);
-      const TileLayout& L = x.L;
-      const float* qf = tq(c);
-      const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
-      const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
-      const int ybase = 16 * x.gstart - L.r0;                    // Y vrow = ybase + image row
-      const int cbase = 8 * (x.gstart + x.k + 1) - (L.r0 >> 1);  // chroma vrow = cbase + chroma row
-      for (int s = 0; s < L.nsteps; ++s, ++g) {
-        const int R = L.r0 + kStepRows * s;
-        const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
-        const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P);
-        const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
-        const int ny = max(0, yb1 - yb0 + 1) * nbx0;
-        const int nc = max(0, cb1 - cb0 + 1) * nbxc;
-        const int ntask = ny + 2 * nc;
-        // L2 prefetch of the next step's block rows (TMA bulk prefetch)
-        if (s + 1 < L.nsteps && it < 32) {
-          const int R2 = R + kStepRows;
-          const int y0 = max(L.by0[0], R2 / P), y1 = min(L.by1[0], (R2 + kStepRows) / P - 1);
-          const int c0 = max(L.by0[1], (R2 >> 1) / P), c1 = min(L.by1[1], ((R2 >> 1) + kStepRows / 2) / P - 1);
-          const int py = max(0, y1 - y0 + 1), pc = max(0, c1 - c0 + 1);
-          for (int kk = it; kk < py + 2 * pc; kk += 32) {
-            int cc = 0, brow = y0 + kk;
-            if (kk >= py) { cc = 1 + (kk - py >= pc); brow = c0 + (kk - py) - (cc - 1) * pc; }
-            const int16_t* p = x.im.coef[cc] + (size_t)brow * x.im.stride[cc] + (size_t)L.bx0[cc] * 64;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                         :: "l"(p), "r"((uint32_t)(L.bx1[cc] - L.bx0[cc] + 1) * 128u) : "memory");
-          }
-        }
-        if (g >= kLag) mbar_wait(&cdone[(g - kLag) % kDepth], ((g - kLag) / kDepth) & 1);
-        for (int base = warp * 32; base < ntask; base += NIT) {
-          const int t = base + lane;
-          const bool act = t < ntask;
-          int cc = 0, brow = 0, bcol = 0;
-          if (t < ny) {
-            brow = (int)fdiv((uint32_t)t, fd_y);
-            bcol = t - brow * nbx0;
-            brow += yb0;
-          } else if (act) {
-            int tt = t - ny;
-            cc = 1 + (tt >= nc);
-            tt -= (cc - 1) * nc;
-            brow = (int)fdiv((uint32_t)tt, fd_c);
-            bcol = tt - brow * nbxc;
-            brow += cb0;
-          }
-          const int16_t* src = x.im.coef[cc] + (size_t)brow * x.im.stride[cc] + (size_t)(L.bx0[cc] + bcol) * 64;
-          uint32_t px[8][2];
-          decode_block<K>(act, src, qf + cc * 64, px);
-          if (!act) continue;
-          if (cc == 0) {
-            uint8_t* d = yring + bcol * P;
+      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * 64;
+      uint32_t px[8][2];
+      decode_block<K>(act, src, qf + c * 64, px);
+      if (!act) continue;
+      if (c == 0) {
+        uint8_t* d = yring + bcol * P;
 #pragma unroll
-            for (int y = 0; y < P; ++y) put_row<P>(d + ((ybase + brow * P + y) & (kPY - 1)) * kYP, px[y]);
-          } else {
-            uint8_t* d = cring + (cc - 1) * kPCStride + bcol * P + kCPad;
-            const int gx0 = (L.bx0[cc] + bcol) * P;
-            const int e = x.im.Wc - 1 - gx0;
-            const bool edge = (gx0 == 0) || (e >= 0 && e < P);
+        for (int y = 0; y < P; ++y) put_row<P>(d + ((brow * P + y) & (kYRing - 1)) * kYP, px[y]);
+      } else {
+        uint8_t* d = cring + (c - 1) * kCStride + bcol * P + kCPad;
+        const int gx0 = (L.bx0[c] + bcol) * P;
+        const bool edge = (gx0 == 0) || (gx0 <= im.Wc - 1 && im.Wc - 1 < gx0 + P);
 #pragma unroll
-            for (int y = 0; y < P; ++y) {
-              const int pos = (cbase + brow * P + y) & (kPC - 1);
-              // slot pos+1, plus the guard mirrors (slot 0 = slot kPC, slot kPC+1 = slot 1)
-              const int nmir = (pos == kPC - 1 || pos == 0) ? 2 : 1;
-              for (int m = 0; m < nmir; ++m) {
-                uint8_t* row = d + (m == 0 ? pos + 1 : (pos == 0 ? kPC + 1 : 0)) * kCP;
-                put_row<P>(row, px[y]);
-                if (edge) {
-                  // replicate image-edge chroma columns into the neighbours the
-                  // triangle filter reads (reading R2: indices clamp at the edges)
-                  if (gx0 == 0) row[-1] = (uint8_t)byte_of(px[y], 0);
-                  if (e >= 0 && e < P) row[e + 1] = (uint8_t)byte_of(px[y], e);
-                }
-              }
+        for (int y = 0; y < P; ++y) {
+          const int r = brow * P + y;
+          const int rs = r & (kCRing - 1);
+          // slot rs+1, plus the guard mirrors (slot 0 = 16, slot 17 = 1)
+          for (int k = 0; k < 1 + (rs == 15 || rs == 0); ++k) {
+            uint8_t* row = d + (k == 0 ? rs + 1 : (rs == 15 ? 0 : kCSlots - 1)) * kCP;
+            put_row<P>(row, px[y]);
+            if (edge) {
+              // replicate image-edge chroma columns into the neighbours the
+              // triangle filter reads (reading R2: indices clamp at the edges)
+              if (gx0 == 0) row[-1] = (uint8_t)byte_of(px[y], 0);
+              const int e = im.Wc - 1 - gx0;
+              if (e >= 0 && e < P) row[e + 1] = (uint8_t)byte_of(px[y], e);
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[g % kDepth]);
       }
     }
-    return;
-  }
+  };
 
-  // ============================ consumers ================================
-  const int ct = tid - NIT;                // 0 .. NCT-1
-  const float na0 = kp.na[0], na1 = kp.na[1], na2 = kp.na[2];
-  const float nb0 = kp.nb[0], nb1 = kp.nb[1], nb2 = kp.nb[2];
-  const size_t plane_sz = (size_t)kp.OH * kp.OW;
-  // pending output: rows [olo, ohi) of item context oc (colour finished)
-  bool have_out = false, out_last = false;
-  int oc = 0, olo = 0, ohi = 0, o_rlo = 0, o_rhi = 0;
-  int g = 0;
-  int ready_prev = 0, done_prev = 0;
-  for (int k = 0;; ++k) {
-    const int item = blockIdx.x + k * G;
-    const bool has_item = item < kp.n_items;
-    const int c = k & 1;
-    int nsteps = 1;
-    for (int s = 0; s < nsteps || !has_item; ++s) {
-      const bool has_step = has_item;
-      if (has_step) mbar_wait(&full[g % kDepth], (g / kDepth) & 1);
-      const ItemCtx& x = ctx[c];
-      const TileLayout& L = x.L;
-      if (has_step && s == 0) { nsteps = L.nsteps; ready_prev = L.ly0 - 1; done_prev = 0; }
-      int ready = ready_prev, done = done_prev;
-      int ntaskc = 0, j0 = 0, ntask4 = 1;
-      if (has_step) {
-        ready = max(ready_prev, ready_after(L, x.im.Hc, s));
-        j0 = (ready_prev + 1) >> 1;
-        const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
-        ntask4 = L.rgb_w >> 2;
-        ntaskc = nq * ntask4;
-        const int2* yt = tyt(c);
-        int lo = done_prev, hi = x.nth;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if ((int)((uint32_t)yt[mid].x >> 16) <= ready) lo = mid + 1; else hi = mid;
+  int ready_prev = L.ly0 - 1;
+  int done_prev = 0;                       // output rows of the tile finished
+  idct_step(0);
+  __syncthreads();
+
+  for (int s = 0; s < L.nsteps; ++s) {
+    const int ready = max(ready_prev, ready_after(L, im.Hc, s));
+    if (tid == 0) ctr[1] = 0;
+
+    if constexpr (DEBUG) {
+      // decoded samples of this step's block rows, clipped to the footprint
+      const int R = L.r0 + kStepRows * s;
+      for (int c = 0; c < 3; ++c) {
+        const int W = c ? im.Wc : im.Wd, Hh = c ? im.Hc : im.Hd;
+        int rlo, rhi;
+        if (c == 0) { rlo = max(max(L.by0[0], R / P) * P, L.ly0); rhi = min(min(L.by1[0], (R + kStepRows) / P - 1) * P + P - 1, L.ly1); }
+        else {
+          rlo = max(((s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P)) * P, L.cy0);
+          rhi = min(min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1) * P + P - 1, L.cy1);
         }
-        done = lo;
+        const int x0 = c ? L.cx0 : L.lx0, x1 = c ? L.cx1 : L.lx1;
+        int16_t* dst = kp.dbg_pl[c] + n * (c ? kp.dbg_stride_c : kp.dbg_stride_y);
+        for (int y = rlo; y <= rhi; ++y)
+          for (int x = x0 + tid; x <= x1; x += kThreads)
+            if (y < Hh && x < W)
+              dst[(size_t)y * W + x] = c == 0 ? yring[(y & (kYRing - 1)) * kYP + (x - L.xbase[0])]
+                                              : cring[(c - 1) * kCStride + ((y & (kCRing - 1)) + 1) * kCP +
+                                                      (x - L.xbase[c] + kCPad)];
       }
+    }
 
-      if constexpr (DEBUG) {
-        if (has_step) {
-          const int R = L.r0 + kStepRows * s;
-          const int ybase = 16 * x.gstart - L.r0, cbase = 8 * (x.gstart + x.k + 1) - (L.r0 >> 1);
-          for (int cc = 0; cc < 3; ++cc) {
-            const int W = cc ? x.im.Wc : x.im.Wd, Hh = cc ? x.im.Hc : x.im.Hd;
-            int rlo, rhi;
-            if (cc == 0) {
-              rlo = max(max(L.by0[0], R / P) * P, L.ly0);
-              rhi = min(min(L.by1[0], (R + kStepRows) / P - 1) * P + P - 1, L.ly1);
+    // ---- prefetch step s+1's ROI block rows into L2 (TMA bulk prefetch) --
+    // one contiguous segment per (component, block row); the IDCT of step
+    // s+1 (next phase) then hits L2 instead of waiting on HBM.
+    if (s + 1 < L.nsteps && tid < 32) {
+      const int R = L.r0 + kStepRows * (s + 1);
+      const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
+      const int cb0 = max(L.by0[1], (R >> 1) / P);
+      const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
+      const int ny = max(0, yb1 - yb0 + 1), nc = max(0, cb1 - cb0 + 1);
+      for (int k = tid; k < ny + 2 * nc; k += 32) {
+        int c = 0, brow = yb0 + k;
+        if (k >= ny) { c = 1 + (k - ny >= nc); brow = cb0 + (k - ny) - (c - 1) * nc; }
+        const int16_t* p = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)L.bx0[c] * 64;
+        const uint32_t bytes = (uint32_t)(L.bx1[c] - L.bx0[c] + 1) * 128u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+      }
+    }
+
+    // ---- upsample + colour of the RGB rows that became ready -------------
+    // A task is 2x4 luma pixels (rows 2j, 2j+1; cols 2i .. 2i+3) sharing a
+    // 3x4 chroma neighbourhood.  Steps end on odd rows (ready_after), so
+    // quads never straddle steps; at the footprint's first/last row a quad
+    // may include one row outside it (computed, never read).
+    {
+      const int j0 = (ready_prev + 1) >> 1;
+      const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
+      const int ntaskc = nq * ntask4;
+      for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&ctr[0], 32);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (chunk >= ntaskc) break;
+        const int t = chunk + lane;
+        if (t >= ntaskc) continue;
+        const int rr = (int)fdiv((uint32_t)t, fd_t4);
+        const int p = t - rr * ntask4;
+        const int j = j0 + rr;                               // chroma row of the quads
+        const int i = (L.rgb_x0 >> 1) + 2 * p;               // chroma column of the left quad
+        const uint8_t* c1 = cring + ((j & (kCRing - 1)) + 1) * kCP + (i - L.xbase[1] + kCPad);
+        const uint8_t* c0 = c1 + (j > 0 ? -kCP : 0);               // row j-1 (clamped at the top)
+        const uint8_t* c2 = c1 + (j < im.Hc - 1 ? kCP : 0);        // row j+1 (clamped at the bottom)
+        int cbq[8], crq[8];                                  // [row 0: 4 cols][row 1: 4 cols]
+#pragma unroll
+        for (int comp = 0; comp < 2; ++comp) {
+          const int o = comp * kCStride;
+          int h[3][4];                                       // horizontal 3/1 taps per chroma row
+          const uint8_t* rows[3] = {c0, c1, c2};
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const int a = ldu8(rows[r] + o - 1), m = ldu8(rows[r] + o), n2 = ldu8(rows[r] + o + 1),
+                      z = ldu8(rows[r] + o + 2);
+            h[r][0] = 3 * m + a;     // col 2i
+            h[r][1] = 3 * m + n2;    // col 2i+1
+            h[r][2] = 3 * n2 + m;    // col 2i+2
+            h[r][3] = 3 * n2 + z;    // col 2i+3
+          }
+          int* qv = comp ? crq : cbq;
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            qv[x] = 3 * h[1][x] + h[0][x];       // row 2j
+            qv[4 + x] = 3 * h[1][x] + h[2][x];   // row 2j+1
+          }
+        }
+        const uint8_t* yr = yring + ((2 * j) & (kYRing - 1)) * kYP + (2 * i - L.xbase[0]);
+        const uint32_t y0 = *reinterpret_cast<const uint32_t*>(yr);
+        const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
+        const int slot = (2 * j) & (kRgbRing - 1);
+        uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
+        const uint4 top = make_uint4(colour(y0 & 255, cbq[0], crq[0]), colour((y0 >> 8) & 255, cbq[1], crq[1]),
+                                     colour((y0 >> 16) & 255, cbq[2], crq[2]), colour(y0 >> 24, cbq[3], crq[3]));
+        *reinterpret_cast<uint4*>(r0p) = top;
+        *reinterpret_cast<uint4*>(r0p + rgb_p) =
+            make_uint4(colour(y1 & 255, cbq[4], crq[4]), colour((y1 >> 8) & 255, cbq[5], crq[5]),
+                       colour((y1 >> 16) & 255, cbq[6], crq[6]), colour(y1 >> 24, cbq[7], crq[7]));
+        if (slot == 0) *reinterpret_cast<uint4*>(r0p + kRgbRing * rgb_p) = top;   // guard row
+      }
+    }
+    __syncthreads();
+    if (tid == 0) ctr[0] = 0;
+
+    if constexpr (DEBUG) {
+      int16_t* dst = kp.dbg_rgb + n * kp.dbg_stride_rgb;
+      for (int y = ready_prev + 1; y <= ready; ++y)
+        for (int x = L.lx0 + tid; x <= L.lx1; x += kThreads) {
+          const uint32_t v = rgb[(y & (kRgbRing - 1)) * rgb_p + (x - L.rgb_x0)];
+          const size_t o = ((size_t)y * im.Wd + x) * 3;
+          dst[o] = v & 255; dst[o + 1] = (v >> 8) & 255; dst[o + 2] = (v >> 16) & 255;
+        }
+    }
+
+    // rows whose lower tap row is ready (taps are monotone): binary search
+    int done;
+    {
+      int lo = done_prev, hi = nth;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int)((uint32_t)yt[mid].x >> 16) <= ready) lo = mid + 1; else hi = mid;
+      }
+      done = lo;
+    }
+
+    // ---- next step's IDCT (writes only Y/chroma rings: no reader now) ----
+    if (s + 1 < L.nsteps) idct_step(s + 1);
+
+    // ---- bilinear + normalize + NCHW store, 4 output pixels per task -----
+    {
+      const int ntasko = (done - done_prev) * nq4;
+      const float na0 = kp.na[0], na1 = kp.na[1], na2 = kp.na[2];
+      const float nb0 = kp.nb[0], nb1 = kp.nb[1], nb2 = kp.nb[2];
+      for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&ctr[1], 32);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (chunk >= ntasko) break;
+        const int t = chunk + lane;
+        if (t >= ntasko) continue;
+        const int rr = (int)fdiv((uint32_t)t, fd_q4);
+        const int r = done_prev + rr;
+        const int ox = 4 * (t - rr * nq4);
+        const int2 ty = yt[r];
+        const float wy = __int_as_float(ty.y);
+        const uint32_t* row0 = rgb + ((ty.x & 0xffff) & (kRgbRing - 1)) * rgb_p;
+        float y[3][4];
+        const int4 txa = *reinterpret_cast<const int4*>(xt + ox);      // taps of ox, ox+1
+        const int4 txb = *reinterpret_cast<const int4*>(xt + ox + 2);  // taps of ox+2, ox+3 (padded)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int2 tx = e == 0 ? make_int2(txa.x, txa.y) : e == 1 ? make_int2(txa.z, txa.w)
+                        : e == 2 ? make_int2(txb.x, txb.y) : make_int2(txb.z, txb.w);
+          const float wx = __int_as_float(tx.y);
+          const uint32_t* a = row0 + tx.x;
+          const uint32_t p00 = a[0], p01 = a[1], p10 = a[rgb_p], p11 = a[rgb_p + 1];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float fa = byte_f(p00, ch), fb = byte_f(p01, ch);
+            const float fc = byte_f(p10, ch), fd = byte_f(p11, ch);
+            const float tp = fmaf(wx, fb - fa, fa);
+            const float bt = fmaf(wx, fd - fc, fc);
+            y[ch][e] = fmaf(wy, bt - tp, tp);
+          }
+          y[0][e] = fmaf(y[0][e], na0, nb0);
+          y[1][e] = fmaf(y[1][e], na1, nb1);
+          y[2][e] = fmaf(y[2][e], na2, nb2);
+        }
+        const size_t o = ((size_t)n * 3 * kp.OH + (oy0 + r)) * kp.OW + (ox0 + ox);
+        if (vec4 && ox + 4 <= ntw) {
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            if constexpr (F16) {
+              const __half2 h0 = __floats2half2_rn(y[ch][0], y[ch][1]);
+              const __half2 h1 = __floats2half2_rn(y[ch][2], y[ch][3]);
+              uint2 v;
+              v.x = *reinterpret_cast<const uint32_t*>(&h0);
+              v.y = *reinterpret_cast<const uint32_t*>(&h1);
+              __stcs(reinterpret_cast<uint2*>(reinterpret_cast<__half*>(kp.out) + o + ch * plane_sz), v);
             } else {
-              rlo = max(((s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P)) * P, L.cy0);
-              rhi = min(min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1) * P + P - 1, L.cy1);
-            }
-            const int x0 = cc ? L.cx0 : L.lx0, x1 = cc ? L.cx1 : L.lx1;
-            int16_t* dst = kp.dbg_pl[cc] + x.n * (cc ? kp.dbg_stride_c : kp.dbg_stride_y);
-            for (int y = rlo; y <= rhi; ++y)
-              for (int xx = x0 + ct; xx <= x1; xx += NCT)
-                if (y < Hh && xx < W)
-                  dst[(size_t)y * W + xx] =
-                      cc == 0 ? yring[((ybase + y) & (kPY - 1)) * kYP + (xx - L.xbase[0])]
-                              : cring[(cc - 1) * kPCStride + (((cbase + y) & (kPC - 1)) + 1) * kCP +
-                                      (xx - L.xbase[cc] + kCPad)];
-          }
-        }
-        if (have_out) {
-          // RGB rows of the previous step (colour finished before the last barrier)
-          const ItemCtx& ox = ctx[oc];
-          const int ybase = 16 * ox.gstart - ox.L.r0;
-          int16_t* dst = kp.dbg_rgb + ox.n * kp.dbg_stride_rgb;
-          for (int y = o_rlo; y <= o_rhi; ++y)
-            for (int xx = ox.L.lx0 + ct; xx <= ox.L.lx1; xx += NCT) {
-              const uint32_t v = rgb[((ybase + y) & (kPR - 1)) * rgb_p + (xx - ox.L.rgb_x0)];
-              const size_t o = ((size_t)y * ox.im.Wd + xx) * 3;
-              dst[o] = v & 255; dst[o + 1] = (v >> 8) & 255; dst[o + 2] = (v >> 16) & 255;
-            }
-        }
-      }
-
-      // ---- colour(g): 2x4-pixel tasks (see ready_after for the alignment) --
-      if (has_step) {
-        const FastDiv fd_t4 = make_fastdiv(ntask4);
-        const int ybase = 16 * x.gstart - L.r0;
-        const int cbase = 8 * (x.gstart + x.k + 1) - (L.r0 >> 1);
-        for (int t = ct; t < ntaskc; t += NCT) {
-          const int rr = (int)fdiv((uint32_t)t, fd_t4);
-          const int p = t - rr * ntask4;
-          const int j = j0 + rr;
-          const int i = (L.rgb_x0 >> 1) + 2 * p;
-          const uint8_t* c1 = cring + (((cbase + j) & (kPC - 1)) + 1) * kCP + (i - L.xbase[1] + kCPad);
-          const uint8_t* c0 = c1 + (j > 0 ? -kCP : 0);
-          const uint8_t* c2 = c1 + (j < x.im.Hc - 1 ? kCP : 0);
-          int cbq[8], crq[8];
-#pragma unroll
-          for (int comp = 0; comp < 2; ++comp) {
-            const int o = comp * kPCStride;
-            int h[3][4];
-            const uint8_t* rows[3] = {c0, c1, c2};
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-              const int a = ldu8(rows[r] + o - 1), m = ldu8(rows[r] + o), n2 = ldu8(rows[r] + o + 1),
-                        z = ldu8(rows[r] + o + 2);
-              h[r][0] = 3 * m + a;
-              h[r][1] = 3 * m + n2;
-              h[r][2] = 3 * n2 + m;
-              h[r][3] = 3 * n2 + z;
-            }
-            int* qv = comp ? crq : cbq;
-#pragma unroll
-            for (int xx = 0; xx < 4; ++xx) {
-              qv[xx] = 3 * h[1][xx] + h[0][xx];
-              qv[4 + xx] = 3 * h[1][xx] + h[2][xx];
+              __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(kp.out) + o + ch * plane_sz),
+                     make_float4(y[ch][0], y[ch][1], y[ch][2], y[ch][3]));
             }
           }
-          const int vy = (ybase + 2 * j) & (kPY - 1);
-          const uint8_t* yr = yring + vy * kYP + (2 * i - L.xbase[0]);
-          const uint32_t y0 = *reinterpret_cast<const uint32_t*>(yr);
-          const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
-          const int slot = (ybase + 2 * j) & (kPR - 1);
-          uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
-          const uint4 top = make_uint4(colour(y0 & 255, cbq[0], crq[0]), colour((y0 >> 8) & 255, cbq[1], crq[1]),
-                                       colour((y0 >> 16) & 255, cbq[2], crq[2]), colour(y0 >> 24, cbq[3], crq[3]));
-          *reinterpret_cast<uint4*>(r0p) = top;
-          *reinterpret_cast<uint4*>(r0p + rgb_p) =
-              make_uint4(colour(y1 & 255, cbq[4], crq[4]), colour((y1 >> 8) & 255, cbq[5], crq[5]),
-                         colour((y1 >> 16) & 255, cbq[6], crq[6]), colour(y1 >> 24, cbq[7], crq[7]));
-          if (slot == 0) *reinterpret_cast<uint4*>(r0p + kPR * rgb_p) = top;   // guard row
-        }
-      }
-
-      // ---- output(g-1): bilinear + normalize + NCHW, 4 pixels per task ----
-      if (have_out) {
-        const ItemCtx& ox = ctx[oc];
-        const int2* xt = tx(oc);
-        const int2* yt = tyt(oc);
-        const int nq4 = (ox.ntw + 3) >> 2;
-        const FastDiv fd_q4 = make_fastdiv(nq4);
-        const int ybase = 16 * ox.gstart - ox.L.r0;
-        const bool vec4 = ((kp.OW & 3) == 0) && ((ox.ox0 & 3) == 0);
-        const int ntasko = (ohi - olo) * nq4;
-        for (int t = ct; t < ntasko; t += NCT) {
-          const int rr = (int)fdiv((uint32_t)t, fd_q4);
-          const int r = olo + rr;
-          const int oxx = 4 * (t - rr * nq4);
-          const int2 ty = yt[r];
-          const float wy = __int_as_float(ty.y);
-          const uint32_t* row0 = rgb + ((ybase + (ty.x & 0xffff)) & (kPR - 1)) * rgb_p;
-          float y[3][4];
-          const int4 txa = *reinterpret_cast<const int4*>(xt + oxx);
-          const int4 txb = *reinterpret_cast<const int4*>(xt + oxx + 2);
+        } else {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int2 tt = e == 0 ? make_int2(txa.x, txa.y) : e == 1 ? make_int2(txa.z, txa.w)
-                          : e == 2 ? make_int2(txb.x, txb.y) : make_int2(txb.z, txb.w);
-            const float wx = __int_as_float(tt.y);
-            const uint32_t* a = row0 + tt.x;
-            const uint32_t p00 = a[0], p01 = a[1], p10 = a[rgb_p], p11 = a[rgb_p + 1];
+            if (ox + e >= ntw) break;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-              const float fa = byte_f(p00, ch), fb = byte_f(p01, ch);
-              const float fc = byte_f(p10, ch), fd = byte_f(p11, ch);
-              const float tp = fmaf(wx, fb - fa, fa);
-              const float bt = fmaf(wx, fd - fc, fc);
-              y[ch][e] = fmaf(wy, bt - tp, tp);
-            }
-            y[0][e] = fmaf(y[0][e], na0, nb0);
-            y[1][e] = fmaf(y[1][e], na1, nb1);
-            y[2][e] = fmaf(y[2][e], na2, nb2);
-          }
-          const size_t o = ((size_t)ox.n * 3 * kp.OH + (ox.oy0 + r)) * kp.OW + (ox.ox0 + oxx);
-          if (vec4 && oxx + 4 <= ox.ntw) {
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              if constexpr (F16) {
-                const __half2 h0 = __floats2half2_rn(y[ch][0], y[ch][1]);
-                const __half2 h1 = __floats2half2_rn(y[ch][2], y[ch][3]);
-                uint2 v;
-                v.x = *reinterpret_cast<const uint32_t*>(&h0);
-                v.y = *reinterpret_cast<const uint32_t*>(&h1);
-                __stcs(reinterpret_cast<uint2*>(reinterpret_cast<__half*>(kp.out) + o + ch * plane_sz), v);
-              } else {
-                __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(kp.out) + o + ch * plane_sz),
-                       make_float4(y[ch][0], y[ch][1], y[ch][2], y[ch][3]));
-              }
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              if (oxx + e >= ox.ntw) break;
-#pragma unroll
-              for (int ch = 0; ch < 3; ++ch) {
-                if constexpr (F16) reinterpret_cast<__half*>(kp.out)[o + e + ch * plane_sz] = __float2half_rn(y[ch][e]);
-                else reinterpret_cast<float*>(kp.out)[o + e + ch * plane_sz] = y[ch][e];
-              }
+              if constexpr (F16) reinterpret_cast<__half*>(kp.out)[o + e + ch * plane_sz] = __float2half_rn(y[ch][e]);
+              else reinterpret_cast<float*>(kp.out)[o + e + ch * plane_sz] = y[ch][e];
             }
           }
         }
       }
-
-      named_bar(1, NCT);
-      if (has_step && lane == 0) mbar_arrive(&cdone[g % kDepth]);
-      if (have_out && out_last && lane == 0) mbar_arrive(&ctxfree[oc]);
-      if (!has_step) { have_out = false; break; }
-      // colour(g) done: its rows are output in the next phase
-      have_out = true;
-      out_last = (s == nsteps - 1);
-      oc = c; olo = done_prev; ohi = done; o_rlo = ready_prev + 1; o_rhi = ready;
-      ready_prev = ready;
-      done_prev = done;
-      ++g;
     }
-    if (!has_item) break;
+    __syncthreads();
+    ready_prev = ready;
+    done_prev = done;
   }
 }
-#endif  // SMOL_DISABLE_PIPELINE
 
 }  // namespace smol

@@ -192,8 +192,8 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
 // Tiles per image: enough CTAs for ~6 resident per SM across the batch
 // (148 SMs; hardware scheduling balances the tail), each tile at least 8
 // output rows.
-int auto_tile_rows(int OH, int n_images, int num_sms) {
-  const int want = ceil_div(num_sms * 6, n_images > 0 ? n_images : 1);
+int auto_tile_rows(int OH, int n_images) {
+  const int want = ceil_div(148 * 6, n_images > 0 ? n_images : 1);
   const int ntiles = imax(1, imin(want, ceil_div(OH, 8)));
   return ceil_div(OH, ntiles);
 }
@@ -202,8 +202,8 @@ using KernelFn = void (*)(const KParams);
 
 template <int K>
 KernelFn pick_kernel(bool f16, bool dbg) {
-  if (dbg) return f16 ? smol_pipeline_kernel<K, true, true> : smol_pipeline_kernel<K, false, true>;
-  return f16 ? smol_pipeline_kernel<K, true, false> : smol_pipeline_kernel<K, false, false>;
+  if (dbg) return f16 ? smol_fused_kernel<K, true, true> : smol_fused_kernel<K, false, true>;
+  return f16 ? smol_fused_kernel<K, true, false> : smol_fused_kernel<K, false, false>;
 }
 
 KernelFn select_kernel(int K, bool f16, bool dbg) {
@@ -215,21 +215,6 @@ KernelFn select_kernel(int K, bool f16, bool dbg) {
   }
 }
 
-int pipeline_threads(int K) {
-  switch (K) {
-    case 1: return (Roles<1>::NI + Roles<1>::NC) * 32;
-    case 2: return (Roles<2>::NI + Roles<2>::NC) * 32;
-    case 4: return (Roles<4>::NI + Roles<4>::NC) * 32;
-    default: return (Roles<8>::NI + Roles<8>::NC) * 32;
-  }
-}
-
-// dynamic shared memory of the pipeline kernel (layout in smol_pipeline_kernel)
-int pipeline_smem(int max_tw, int max_th, int rgb_pmax) {
-  const int tab = 3 * 64 * 4 + align16((max_tw + 4) * 8) + align16(max_th * 8);
-  return 2 * tab + kPY * kYP + 2 * kPCStride + align16((kPR + 1) * rgb_pmax * 4);
-}
-
 }  // namespace
 
 struct smol_preproc_plan {
@@ -239,7 +224,6 @@ struct smol_preproc_plan {
   int OW = 0, OH = 0;          // 0 when the output size is image dependent (never: validated)
   int tile_rows = 0;               // 0 = automatic per batch size
   int smem_optin = 0;
-  int num_sms = 148;
   DevImage* d_desc = nullptr;  // [kRing][max_images]
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
   cudaEvent_t ev[kRing] = {};
@@ -306,7 +290,6 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     pl->nb[c] = (float)(-(double)params->mean[c] / (double)params->std[c]);
   }
   cudaError_t e = cudaDeviceGetAttribute(&pl->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   for (int i = 0; i < kRing && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
@@ -382,21 +365,20 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   DevImage* d = pl->d_desc + (size_t)slot * pl->max_images;
 
   // validate + build descriptors; shared memory = max over distinct geometries
-  const int tile_rows = pl->tile_rows > 0 ? imin(pl->tile_rows, pl->OH) : auto_tile_rows(pl->OH, b->n_images, pl->num_sms);
+  const int tile_rows = pl->tile_rows > 0 ? imin(pl->tile_rows, pl->OH) : auto_tile_rows(pl->OH, b->n_images);
   const int ntiles = ceil_div(pl->OH, tile_rows);
   // validate every descriptor once
   for (int i = 0; i < b->n_images; ++i) {
     int32_t rc = validate_image(&pl->p, &b->images[i], i, b->n_qtables, h[i]);
     if (rc) return rc;
   }
-  // widest RGB ring row over the batch's distinct tile geometries; a tile whose
-  // footprint exceeds the fixed ring pitches forces more column tiles
+  // shared memory of the largest tile over the batch's distinct geometries
+  // (a tile whose footprint exceeds the fixed ring pitches reports INT_MAX/2)
   auto cols_of = [&](int n_col_tiles) { return (ceil_div(pl->OW, n_col_tiles) + 3) & ~3; };  // multiple of 4
-  auto scan = [&](int n_col_tiles, int& rgb_pmax) {
+  auto max_smem = [&](int n_col_tiles) {
     const int tile_cols = cols_of(n_col_tiles);
     n_col_tiles = ceil_div(pl->OW, tile_cols);
-    bool fits = true;
-    rgb_pmax = 4;
+    int m = 0;
     int prev_w = -1, prev_h = -1, prev_l = -2, prev_t = -2;
     for (int i = 0; i < b->n_images; ++i) {
       const smol_image_desc* di = &b->images[i];
@@ -407,22 +389,21 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
           TileLayout L;
           tile_layout(h[i], K, t * tile_rows, imin(pl->OH, (t + 1) * tile_rows), u * tile_cols,
                       imin(pl->OW, (u + 1) * tile_cols), L);
-          fits = fits && L.fits;
-          rgb_pmax = imax(rgb_pmax, L.rgb_p);
+          m = imax(m, L.fits ? L.total : (1 << 30));
         }
       prev_w = di->width; prev_h = di->height; prev_l = di->roi_left; prev_t = di->roi_top;
     }
-    return fits ? pipeline_smem(tile_cols, tile_rows, rgb_pmax) : (1 << 30);
+    return m;
   };
-  int n_col_tiles = 1, rgb_pmax = 4;
-  int smem = scan(1, rgb_pmax);
-  while (smem > pl->smem_optin && n_col_tiles < 64 && 8 * n_col_tiles <= pl->OW) {
+  // column tiles only when a full-width tile would not leave 2 CTAs per SM
+  int n_col_tiles = 1;
+  int smem = max_smem(1);
+  while (smem > pl->smem_optin / 2 && n_col_tiles < 64 && 8 * n_col_tiles <= pl->OW) {
     n_col_tiles *= 2;
-    smem = scan(n_col_tiles, rgb_pmax);
+    smem = max_smem(n_col_tiles);
   }
   if (smem > pl->smem_optin)
-    return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; use column tiles / smaller crop",
-                smem, pl->smem_optin);
+    return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
 
   SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * b->n_images, cudaMemcpyHostToDevice, stream));
   KParams kp = dbg ? *dbg : KParams{};
@@ -432,15 +413,10 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
-  kp.tiles_per_image = ntiles * n_col_tiles;
-  kp.n_items = kp.tiles_per_image * b->n_images;
-  kp.max_tw = kp.tile_cols;
-  kp.max_th = tile_rows;
-  kp.rgb_pmax = rgb_pmax;
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr);
-  dim3 grid(imin(kp.n_items, pl->num_sms));      // persistent: one CTA per SM
-  fn<<<grid, pipeline_threads(K), smem, stream>>>(kp);
+  dim3 grid(ntiles * n_col_tiles, b->n_images);
+  fn<<<grid, kThreads, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
   return SMOL_OK;
