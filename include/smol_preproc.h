@@ -108,7 +108,9 @@ typedef struct {
   int32_t cx0, cx1, cy0, cy1;   /* chroma footprint incl. upsample neighbours    */
   int32_t bx0[3], bx1[3], by0[3], by1[3];  /* ROI block ranges per component   */
   int64_t roi_blocks;           /* blocks under the footprint (sum over comps)  */
-  int64_t roi_coef_bytes;       /* algorithmic coefficient bytes of the image   */
+  int64_t roi_coef_bytes;       /* algorithmic coefficient bytes of the image:
+                                   roi_blocks x 128 (x 32 at scale 1/8: only the
+                                   DC sector of a dense-64 block is needed)     */
 } smol_geometry;
 
 /* Create a plan on the current CUDA device for batches of <= max_images.

@@ -193,12 +193,34 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     const int H = (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows));
     const int W = (int)__reduce_max_sync(0xffffffffu, (uint32_t)wcol);
     float m[8][8];
+#ifndef SMOL_IDCT_VARIANT
+#define SMOL_IDCT_VARIANT 2
+#endif
+#if SMOL_IDCT_VARIANT == 1        // W in {5, 8}, H in {6, 8}
     if (W <= 5) {
       if (H <= 6) idct_rows<5, 6>(raw, q, m); else idct_rows<5, 8>(raw, q, m);
     } else {
       if (H <= 6) idct_rows<8, 6>(raw, q, m); else idct_rows<8, 8>(raw, q, m);
     }
     if (H <= 6) idct_cols<6>(m, px); else idct_cols<8>(m, px);
+#elif SMOL_IDCT_VARIANT == 2      // H in {6, 8} only
+    (void)W;
+    if (H <= 6) { idct_rows<8, 6>(raw, q, m); idct_cols<6>(m, px); }
+    else { idct_rows<8, 8>(raw, q, m); idct_cols<8>(m, px); }
+#elif SMOL_IDCT_VARIANT == 3      // no pruning
+    (void)W; (void)H;
+    idct_rows<8, 8>(raw, q, m);
+    idct_cols<8>(m, px);
+#else                             // W in {4, 6, 8}, H in {4, 6, 8}
+    if (W <= 4) {
+      if (H <= 4) idct_rows<4, 4>(raw, q, m); else if (H <= 6) idct_rows<4, 6>(raw, q, m); else idct_rows<4, 8>(raw, q, m);
+    } else if (W <= 6) {
+      if (H <= 4) idct_rows<6, 4>(raw, q, m); else if (H <= 6) idct_rows<6, 6>(raw, q, m); else idct_rows<6, 8>(raw, q, m);
+    } else {
+      if (H <= 4) idct_rows<8, 4>(raw, q, m); else if (H <= 6) idct_rows<8, 6>(raw, q, m); else idct_rows<8, 8>(raw, q, m);
+    }
+    if (H <= 4) idct_cols<4>(m, px); else if (H <= 6) idct_cols<6>(m, px); else idct_cols<8>(m, px);
+#endif
   } else {
     // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7})
     float g[8][P];

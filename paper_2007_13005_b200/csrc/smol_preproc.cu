@@ -261,7 +261,9 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
     out->bx0[c] = L.bx0[c]; out->bx1[c] = L.bx1[c]; out->by0[c] = L.by0[c]; out->by1[c] = L.by1[c];
   }
   out->roi_blocks = tile_roi_blocks(L);
-  out->roi_coef_bytes = out->roi_blocks * 128;
+  // algorithmic coefficient bytes of the dense-64 layout: whole 128-B blocks,
+  // except at scale 1/8 where only the DC's 32-B sector is needed
+  out->roi_coef_bytes = out->roi_blocks * (params->scale_denom == 8 ? 32 : 128);
   return SMOL_OK;
 }
 
