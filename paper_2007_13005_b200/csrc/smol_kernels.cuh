@@ -131,18 +131,55 @@ __device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, ui
 // whole warp), inputs u < W.  Level shift and rounding offset (+128 + 1/2,
 // reading R3) ride on the DC term: t(0, .) = 1 exactly, so adding it to
 // D(0,0) adds it to every output sample.
+// Packed FP32x2 (FFMA2/FADD2, sm_100): two independent IEEE fp32 operations
+// per instruction, bitwise identical to the scalar ones.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// 8-point IDCT of two rows at once (lane .x = row v, .y = row v+1); same
+// operation order as idct8 (exact DC / u=4 paths preserved).
+template <int W>
+__device__ __forceinline__ void idct8x2(const float2 (&d)[8], float2 (&o)[8]) {
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    float2 e = d[0];
+    if (W > 4) e = (x == 0 || x == 3) ? __fadd2_rn(e, d[4]) : __ffma2_rn(d[4], f2(-1.f), e);
+    if (W > 2) e = __ffma2_rn(d[2], f2(basis_t(2, x)), e);
+    if (W > 6) e = __ffma2_rn(d[6], f2(basis_t(6, x)), e);
+    float2 od = f2(0.f);
+    if (W > 1) od = __fmul2_rn(d[1], f2(basis_t(1, x)));
+    if (W > 3) od = __ffma2_rn(d[3], f2(basis_t(3, x)), od);
+    if (W > 5) od = __ffma2_rn(d[5], f2(basis_t(5, x)), od);
+    if (W > 7) od = __ffma2_rn(d[7], f2(basis_t(7, x)), od);
+    if (W > 1) { o[x] = __fadd2_rn(e, od); o[7 - x] = __ffma2_rn(od, f2(-1.f), e); }
+    else { o[x] = e; o[7 - x] = e; }
+  }
+}
+
+// Full-scale block, row pass: rows v < HR (rows >= HR are all-zero in the
+// whole warp), inputs u < W, two rows per packed instruction.  Level shift
+// and rounding offset (+128 + 1/2, reading R3) ride on the DC term:
+// t(0, .) = 1 exactly, so adding it to D(0,0) adds it to every sample.
 template <int W, int HR>
 __device__ __forceinline__ void idct_rows(const int4 (&raw)[8], const float* q, float (&m)[8][8]) {
 #pragma unroll
-  for (int v = 0; v < HR; ++v) {
-    float d[8];
-    unpack_row(raw[v], d);
-    const float4 q0 = *reinterpret_cast<const float4*>(q + v * 8);
-    const float4 q1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
-    d[0] *= q0.x; d[1] *= q0.y; d[2] *= q0.z; d[3] *= q0.w;
-    d[4] *= q1.x; d[5] *= q1.y; d[6] *= q1.z; d[7] *= q1.w;
-    if (v == 0) d[0] += 128.5f;
-    idct8<W>(d, m[v]);
+  for (int v = 0; v < HR; v += 2) {
+    float a[8], b[8];
+    unpack_row(raw[v], a);
+    unpack_row(raw[v + 1], b);
+    const float4 qa0 = *reinterpret_cast<const float4*>(q + v * 8);
+    const float4 qa1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
+    const float4 qb0 = *reinterpret_cast<const float4*>(q + v * 8 + 8);
+    const float4 qb1 = *reinterpret_cast<const float4*>(q + v * 8 + 12);
+    float2 d[8];
+    d[0] = make_float2(a[0] * qa0.x, b[0] * qb0.x); d[1] = make_float2(a[1] * qa0.y, b[1] * qb0.y);
+    d[2] = make_float2(a[2] * qa0.z, b[2] * qb0.z); d[3] = make_float2(a[3] * qa0.w, b[3] * qb0.w);
+    d[4] = make_float2(a[4] * qa1.x, b[4] * qb1.x); d[5] = make_float2(a[5] * qa1.y, b[5] * qb1.y);
+    d[6] = make_float2(a[6] * qa1.z, b[6] * qb1.z); d[7] = make_float2(a[7] * qa1.w, b[7] * qb1.w);
+    if (v == 0) d[0].x += 128.5f;
+    float2 o[8];
+    idct8x2<W>(d, o);
+#pragma unroll
+    for (int x = 0; x < 8; ++x) { m[v][x] = o[x].x; m[v + 1][x] = o[x].y; }
   }
 }
 
@@ -273,6 +310,23 @@ __device__ __forceinline__ uint32_t colour(int Y, int cb16, int cr16) {
   return R | ((uint32_t)G << 8) | (B << 16);
 }
 
+// Two pixels at once: the same IEEE fp32 operations as colour(), packed
+// (FADD2/FFMA2), so results are bitwise identical.
+__device__ __forceinline__ uint2 colour2(int Y0, int Y1, int cb0, int cb1, int cr0, int cr1) {
+  const float2 yf = make_float2((float)Y0, (float)Y1);
+  const float2 tr = __ffma2_rn(make_float2((float)cr0, (float)cr1), make_float2(c_basis.kR, c_basis.kR),
+                               __fadd2_rn(yf, make_float2(c_basis.cR, c_basis.cR)));
+  const float2 tb = __ffma2_rn(make_float2((float)cb0, (float)cb1), make_float2(c_basis.kB, c_basis.kB),
+                               __fadd2_rn(yf, make_float2(c_basis.cB, c_basis.cB)));
+  const uint32_t u0 = 543917632u - 43017u * (uint32_t)cb0 - 89267u * (uint32_t)cr0;
+  const uint32_t u1 = 543917632u - 43017u * (uint32_t)cb1 - 89267u * (uint32_t)cr1;
+  const uint32_t G0 = (uint32_t)min(max(Y0 + (int)(u0 / 2000000u) - 136, 0), 255);
+  const uint32_t G1 = (uint32_t)min(max(Y1 + (int)(u1 / 2000000u) - 136, 0), 255);
+  // R | G<<8 | B<<16 via byte permutes
+  return make_uint2(__byte_perm(__byte_perm(floor_u8(tr.x), G0, 0x0040), floor_u8(tb.x), 0x5410),
+                    __byte_perm(__byte_perm(floor_u8(tr.y), G1, 0x0040), floor_u8(tb.y), 0x5410));
+}
+
 __device__ __forceinline__ int ldu8(const uint8_t* p) { return *p; }
 
 struct KParams {
@@ -280,6 +334,7 @@ struct KParams {
   const uint16_t* qtables;
   void* out;
   int OW, OH, tile_rows, tile_cols, n_col_tiles;
+  uint32_t magic;                  // 0x4B000000: bit pattern of 2^23 (byte -> float trick)
   float na[3], nb[3];              // y = x * na + nb = (x/255 - mean)/std
   int16_t* dbg_pl[3];              // debug planes (DEBUG instantiation only)
   int16_t* dbg_rgb;
@@ -525,12 +580,13 @@ smol_fused_kernel(const KParams kp) {
         const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
         const int slot = (2 * j) & (kRgbRing - 1);
         uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
-        const uint4 top = make_uint4(colour(y0 & 255, cbq[0], crq[0]), colour((y0 >> 8) & 255, cbq[1], crq[1]),
-                                     colour((y0 >> 16) & 255, cbq[2], crq[2]), colour(y0 >> 24, cbq[3], crq[3]));
+        const uint2 t01 = colour2(y0 & 255, (y0 >> 8) & 255, cbq[0], cbq[1], crq[0], crq[1]);
+        const uint2 t23 = colour2((y0 >> 16) & 255, y0 >> 24, cbq[2], cbq[3], crq[2], crq[3]);
+        const uint2 b01 = colour2(y1 & 255, (y1 >> 8) & 255, cbq[4], cbq[5], crq[4], crq[5]);
+        const uint2 b23 = colour2((y1 >> 16) & 255, y1 >> 24, cbq[6], cbq[7], crq[6], crq[7]);
+        const uint4 top = make_uint4(t01.x, t01.y, t23.x, t23.y);
         *reinterpret_cast<uint4*>(r0p) = top;
-        *reinterpret_cast<uint4*>(r0p + rgb_p) =
-            make_uint4(colour(y1 & 255, cbq[4], crq[4]), colour((y1 >> 8) & 255, cbq[5], crq[5]),
-                       colour((y1 >> 16) & 255, cbq[6], crq[6]), colour(y1 >> 24, cbq[7], crq[7]));
+        *reinterpret_cast<uint4*>(r0p + rgb_p) = make_uint4(b01.x, b01.y, b23.x, b23.y);
         if (slot == 0) *reinterpret_cast<uint4*>(r0p + kRgbRing * rgb_p) = top;   // guard row
       }
     }
@@ -564,8 +620,9 @@ smol_fused_kernel(const KParams kp) {
     // ---- bilinear + normalize + NCHW store, 4 output pixels per task -----
     {
       const int ntasko = (done - done_prev) * nq4;
-      const float na0 = kp.na[0], na1 = kp.na[1], na2 = kp.na[2];
-      const float nb0 = kp.nb[0], nb1 = kp.nb[1], nb2 = kp.nb[2];
+      const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
+      const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
+      const uint32_t magic = kp.magic;     // 0x4B000000 (2^23), kept in a register
       for (;;) {
         int chunk = 0;
         if (lane == 0) chunk = atomicAdd(&ctr[1], 32);
@@ -582,24 +639,32 @@ smol_fused_kernel(const KParams kp) {
         float y[3][4];
         const int4 txa = *reinterpret_cast<const int4*>(xt + ox);      // taps of ox, ox+1
         const int4 txb = *reinterpret_cast<const int4*>(xt + ox + 2);  // taps of ox+2, ox+3 (padded)
+        const float2 wy2 = f2(wy);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int2 tx = e == 0 ? make_int2(txa.x, txa.y) : e == 1 ? make_int2(txa.z, txa.w)
-                        : e == 2 ? make_int2(txb.x, txb.y) : make_int2(txb.z, txb.w);
-          const float wx = __int_as_float(tx.y);
-          const uint32_t* a = row0 + tx.x;
-          const uint32_t p00 = a[0], p01 = a[1], p10 = a[rgb_p], p11 = a[rgb_p + 1];
+        for (int e = 0; e < 4; e += 2) {
+          // two output pixels per packed FP32x2 instruction; bytes become
+          // 2^23 + b floats by one PRMT (exact), the bias cancels in b - a
+          const int2 t0 = e == 0 ? make_int2(txa.x, txa.y) : make_int2(txb.x, txb.y);
+          const int2 t1 = e == 0 ? make_int2(txa.z, txa.w) : make_int2(txb.z, txb.w);
+          const float2 wx = make_float2(__int_as_float(t0.y), __int_as_float(t1.y));
+          const uint32_t* a0 = row0 + t0.x;
+          const uint32_t* a1 = row0 + t1.x;
+          const uint32_t p00 = a0[0], p01 = a0[1], p10 = a0[rgb_p], p11 = a0[rgb_p + 1];
+          const uint32_t q00 = a1[0], q01 = a1[1], q10 = a1[rgb_p], q11 = a1[rgb_p + 1];
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            const float fa = byte_f(p00, ch), fb = byte_f(p01, ch);
-            const float fc = byte_f(p10, ch), fd = byte_f(p11, ch);
-            const float tp = fmaf(wx, fb - fa, fa);
-            const float bt = fmaf(wx, fd - fc, fc);
-            y[ch][e] = fmaf(wy, bt - tp, tp);
+            const int sel = 0x7540 + ch;
+            const float2 fa = make_float2(__uint_as_float(__byte_perm(p00, magic, sel)), __uint_as_float(__byte_perm(q00, magic, sel)));
+            const float2 fb = make_float2(__uint_as_float(__byte_perm(p01, magic, sel)), __uint_as_float(__byte_perm(q01, magic, sel)));
+            const float2 fc = make_float2(__uint_as_float(__byte_perm(p10, magic, sel)), __uint_as_float(__byte_perm(q10, magic, sel)));
+            const float2 fd = make_float2(__uint_as_float(__byte_perm(p11, magic, sel)), __uint_as_float(__byte_perm(q11, magic, sel)));
+            const float2 tp = __ffma2_rn(wx, __ffma2_rn(fa, f2(-1.f), fb), __fadd2_rn(fa, f2(-8388608.f)));
+            const float2 bt = __ffma2_rn(wx, __ffma2_rn(fc, f2(-1.f), fd), __fadd2_rn(fc, f2(-8388608.f)));
+            const float2 v = __ffma2_rn(wy2, __ffma2_rn(tp, f2(-1.f), bt), tp);
+            const float2 yn = __ffma2_rn(v, ch == 0 ? na0 : ch == 1 ? na1 : na2, ch == 0 ? nb0 : ch == 1 ? nb1 : nb2);
+            y[ch][e] = yn.x;
+            y[ch][e + 1] = yn.y;
           }
-          y[0][e] = fmaf(y[0][e], na0, nb0);
-          y[1][e] = fmaf(y[1][e], na1, nb1);
-          y[2][e] = fmaf(y[2][e], na2, nb2);
         }
         const size_t o = ((size_t)n * 3 * kp.OH + (oy0 + r)) * kp.OW + (ox0 + ox);
         if (vec4 && ox + 4 <= ntw) {

@@ -413,6 +413,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   kp.qtables = b->qtables;
   kp.out = out;
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;
+  kp.magic = 0x4B000000u;
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
