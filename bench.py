@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--tile-rows", type=int, default=0)
+    ap.add_argument("--layout", default="dense", choices=["dense", "packed"],
+                    help="coefficient block layout (packed: only the coefficients the scale uses)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -205,7 +207,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     cfg = synth.CONFIGS[args.config]
-    params = smol.params_from_config(cfg, tile_rows=args.tile_rows)
+    params = smol.params_from_config(cfg, tile_rows=args.tile_rows, layout=args.layout)
     # weak scaling: a global batch of cfg.n images per GPU, partitioned into
     # contiguous ROI-balanced ranges (one per rank); no data-path collective
     from paper_2007_13005_b200 import shard
@@ -214,9 +216,9 @@ def main():
     imgs = all_imgs[lo:hi]
     nloc = len(imgs)
     plan = smol.Plan(params, max(nloc, 1))
-    arena_bytes = sum(im.nbytes() for im in imgs)
+    arena_bytes = smol.batch_for(params, imgs[:1], qt).coef_bytes * len(imgs)
     reps = args.replicas or max(2, int(np.ceil(1.5 * L2_BYTES / max(arena_bytes, 1))) + 1)
-    batches = [smol.CoefBatch(imgs, qt) for _ in range(reps)]
+    batches = [smol.batch_for(params, imgs, qt) for _ in range(reps)]
     out = plan.new_output(nloc)
     stream = torch.cuda.Stream()
 
@@ -261,7 +263,7 @@ def main():
     launch_ms = statistics.median(a.elapsed_time(b) for a, b in evs)
 
     # ---- end to end: pinned host coefficients through smol_preproc_run_host --
-    host_batches = [smol.CoefBatch(imgs, qt, location="pinned") for _ in range(2)]
+    host_batches = [smol.batch_for(params, imgs, qt, location="pinned") for _ in range(2)]
     res_host = torch.empty((1,) + tuple(out.shape[1:]), dtype=out.dtype, pin_memory=True)
     for k in range(3):
         plan.run(host_batches[k % 2], out=out, stream=stream)
@@ -292,7 +294,7 @@ def main():
                        "alg_bytes_per_image": alg_bytes_img,
                        "roi_coef_bytes_per_image": g["roi_coef_bytes"],
                        "coef_stats": synth.coef_stats(imgs[:min(len(imgs), 64)]),
-                       "tile_rows": plan.params.tile_rows},
+                       "tile_rows": plan.params.tile_rows, "coef_layout": args.layout},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                          "kernel": "smol_fused_kernel", "launch_ms": launch_ms,

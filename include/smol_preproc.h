@@ -54,7 +54,14 @@ typedef enum {
 
 typedef enum { SMOL_OUT_F32_NCHW = 0, SMOL_OUT_F16_NCHW = 1 } smol_out_dtype;
 typedef enum { SMOL_RESIZE_SHORT_SIDE = 0, SMOL_RESIZE_EXACT = 1 } smol_resize_mode;
-typedef enum { SMOL_LAYOUT_DENSE64 = 0 } smol_coef_layout;
+/* Coefficient block layout (per component plane, block-raster rows):
+ *  DENSE64: 64 int16 per block, natural order (libjpeg JBLOCK).
+ *  PACKED : only the coefficients the plan's scale uses (reading R1: the
+ *           box-averaged basis of the others is exactly zero), row-major over
+ *           the index set, padded to 8 bytes per block:
+ *             1/1: = DENSE64;  1/2: u,v in {0,1,2,3,5,6,7} -> 52 int16 (104 B);
+ *             1/4: u,v in {0,1,3,5,7} -> 28 int16 (56 B);  1/8: DC -> 1 int16 (2 B). */
+typedef enum { SMOL_LAYOUT_DENSE64 = 0, SMOL_LAYOUT_PACKED = 1 } smol_coef_layout;
 
 /* Plan parameters (fixed for the plan's lifetime). */
 typedef struct {
@@ -77,12 +84,13 @@ typedef struct {
   int32_t subsampling;             /* 420 (anything else: SMOL_ERR_UNSUPPORTED)      */
   int32_t qtable[3];               /* Y, Cb, Cr index into batch qtables             */
   const int16_t* coef[3];          /* DEVICE (or pinned HOST for run_host):
-                                      [blocks_h][blocks_w][64] int16, natural
-                                      (row-major v*8+u) order, absolute DC;
+                                      [blocks_h][blocks_w][E] int16 blocks of the
+                                      plan's layout (E = 64 for DENSE64: natural
+                                      row-major v*8+u order), absolute DC;
                                       16-byte aligned                               */
   int32_t blocks_w[3], blocks_h[3];/* >= ceil(W/8), ceil(H/8) luma;
                                       >= ceil(W/16), ceil(H/16) chroma              */
-  int32_t row_stride_bytes[3];     /* >= blocks_w*128, multiple of 16                 */
+  int32_t row_stride_bytes[3];     /* >= blocks_w*2*E, multiple of 16                 */
   int32_t roi_left, roi_top;       /* optional ROI: crop window origin in resized
                                       coordinates (window = crop_w x crop_h);
                                       -1,-1 = centre crop                            */

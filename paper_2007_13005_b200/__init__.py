@@ -17,7 +17,9 @@ import numpy as np
 
 from ._native import (BatchDesc, Geometry, ImageDesc, Params, SmolError, build, check, lib,
                       SMOL_OUT_F16_NCHW, SMOL_OUT_F32_NCHW, SMOL_RESIZE_EXACT,
-                      SMOL_RESIZE_SHORT_SIDE, SMOL_LAYOUT_DENSE64, EXPORTS, LIB_PATH)
+                      SMOL_RESIZE_SHORT_SIDE, SMOL_LAYOUT_DENSE64, SMOL_LAYOUT_PACKED, EXPORTS,
+                      LIB_PATH)
+from .layout import block_elems, pack_plane
 
 __all__ = ["make_params", "params_from_config", "geometry", "CoefBatch", "Plan", "SmolError",
            "build", "lib", "EXPORTS", "LIB_PATH"]
@@ -29,7 +31,7 @@ IMAGENET_STD = (0.229, 0.224, 0.225)
 def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: int = 256,
                 resize_w: int = 0, resize_h: int = 0, crop_w: int = 0, crop_h: int = 0,
                 mean=IMAGENET_MEAN, std=IMAGENET_STD, out_dtype: str = "f32",
-                tile_rows: int = 0) -> Params:
+                tile_rows: int = 0, layout: str = "dense") -> Params:
     p = Params()
     p.scale_denom = scale_denom
     p.resize_mode = SMOL_RESIZE_SHORT_SIDE if resize_mode == "short" else SMOL_RESIZE_EXACT
@@ -38,9 +40,15 @@ def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: 
     p.mean = (ctypes.c_float * 3)(*mean)
     p.std = (ctypes.c_float * 3)(*std)
     p.out_dtype = SMOL_OUT_F16_NCHW if out_dtype == "f16" else SMOL_OUT_F32_NCHW
-    p.layout = SMOL_LAYOUT_DENSE64
+    p.layout = SMOL_LAYOUT_PACKED if layout == "packed" else SMOL_LAYOUT_DENSE64
     p.tile_rows = tile_rows
     return p
+
+
+def batch_for(params: Params, images, qtables, **kw) -> "CoefBatch":
+    """CoefBatch in the layout the plan's params expect."""
+    return CoefBatch(images, qtables, layout="packed" if params.layout == SMOL_LAYOUT_PACKED else "dense",
+                     scale_denom=params.scale_denom, **kw)
 
 
 def params_from_config(cfg, **kw) -> Params:
@@ -52,13 +60,13 @@ def params_from_config(cfg, **kw) -> Params:
     return make_params(**args)
 
 
-def _desc_for(width, height, blocks_w, blocks_h, qidx=(0, 1, 1), roi=None) -> ImageDesc:
+def _desc_for(width, height, blocks_w, blocks_h, qidx=(0, 1, 1), roi=None, strides=None) -> ImageDesc:
     d = ImageDesc()
     d.width, d.height, d.subsampling = width, height, 420
     d.qtable = (ctypes.c_int32 * 3)(*qidx)
     for c in range(3):
         d.blocks_w[c], d.blocks_h[c] = blocks_w[c], blocks_h[c]
-        d.row_stride_bytes[c] = blocks_w[c] * 128
+        d.row_stride_bytes[c] = blocks_w[c] * 128 if strides is None else strides[c]
     d.roi_left, d.roi_top = roi if roi is not None else (-1, -1)
     return d
 
@@ -78,24 +86,35 @@ class CoefBatch:
     images: sequence of objects with .width, .height, .coef (3 int16 arrays
     [bh][bw][64]) and .qidx; qtables: [nq][64] uint16.  location: "device"
     (HBM, for smol_preproc_run) or "pinned" (page-locked host memory, for the
-    end-to-end smol_preproc_run_host path).
+    end-to-end smol_preproc_run_host path).  layout/scale_denom select the
+    plan's coefficient layout: "packed" keeps only the coefficients the scale
+    uses (layout.pack_plane; what a host entropy decoder would emit).
     """
 
     def __init__(self, images: Sequence, qtables: np.ndarray, location: str = "device",
-                 device: Optional[int] = None, rois: Optional[Sequence] = None):
+                 device: Optional[int] = None, rois: Optional[Sequence] = None,
+                 layout: str = "dense", scale_denom: int = 1):
         import torch
         self.n = len(images)
-        sizes = [[int(c.size) for c in im.coef] for im in images]
+        k = scale_denom if layout == "packed" else 1
+        planes = []
+        cache = {}
+        for im in images:
+            key = id(im)
+            if key not in cache:
+                cache[key] = [pack_plane(np.ascontiguousarray(c, dtype=np.int16), k) for c in im.coef]
+            planes.append(cache[key])
+        sizes = [[int(p.size) for p in ps] for ps in planes]
         total = int(sum(sum(s) for s in sizes))
         host = np.empty(max(total, 8), np.int16)
         offs = []
         o = 0
-        for im, s in zip(images, sizes):
+        for ps, s in zip(planes, sizes):
             oo = []
             for ci in range(3):
-                host[o:o + s[ci]] = np.ascontiguousarray(im.coef[ci], dtype=np.int16).ravel()
+                host[o:o + s[ci]] = ps[ci].ravel()
                 oo.append(o)
-                o += s[ci]                      # every plane is a multiple of 64 elements
+                o += s[ci]                      # every plane row is a multiple of 16 bytes
             offs.append(oo)
         qt = np.ascontiguousarray(qtables, dtype=np.uint16).view(np.int16)
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -114,7 +133,8 @@ class CoefBatch:
         for i, (im, oo) in enumerate(zip(images, offs)):
             roi = rois[i] if rois is not None else None
             d = _desc_for(im.width, im.height, [c.shape[1] for c in im.coef],
-                          [c.shape[0] for c in im.coef], tuple(im.qidx), roi)
+                          [c.shape[0] for c in im.coef], tuple(im.qidx), roi,
+                          strides=[2 * p.shape[1] for p in planes[i]])
             for ci in range(3):
                 d.coef[ci] = base + 2 * oo[ci]
             self.descs[i] = d

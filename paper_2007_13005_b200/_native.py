@@ -23,7 +23,7 @@ SMOL_OK, SMOL_ERR_INVALID, SMOL_ERR_UNSUPPORTED, SMOL_ERR_CUDA, SMOL_ERR_NOMEM, 
 STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "UNSUPPORTED", 3: "CUDA", 4: "NOMEM", 5: "CAPACITY"}
 SMOL_OUT_F32_NCHW, SMOL_OUT_F16_NCHW = 0, 1
 SMOL_RESIZE_SHORT_SIDE, SMOL_RESIZE_EXACT = 0, 1
-SMOL_LAYOUT_DENSE64 = 0
+SMOL_LAYOUT_DENSE64, SMOL_LAYOUT_PACKED = 0, 1
 
 # every symbol include/smol_preproc.h declares (checked by tests/test_abi.py)
 EXPORTS = ["smol_preproc_plan", "smol_preproc_run", "smol_preproc_run_host", "smol_preproc_destroy",

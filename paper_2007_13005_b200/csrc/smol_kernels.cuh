@@ -203,11 +203,31 @@ __device__ __forceinline__ void idct_cols(const float (&m)[8][8], uint32_t (&px)
   }
 }
 
+// Coefficient-block layouts (smol_preproc.h smol_coef_layout).  DENSE64:
+// 64 int16 per block, natural order.  PACKED: only the coefficients whose
+// box-averaged basis a_k(u, .) is not identically zero at scale 1/K (reading
+// R1), row-major over the index set, padded to 8 bytes:
+//   K=2: u,v in {0,1,2,3,5,6,7}  49 -> 52 int16 (104 B)
+//   K=4: u,v in {0,1,3,5,7}      25 -> 28 int16 ( 56 B)
+//   K=8: DC only                  1 int16      (  2 B)
+template <int K, bool PACKED>
+struct BlockFmt {
+  static constexpr int kElems = !PACKED ? 64 : (K == 1 ? 64 : K == 2 ? 52 : K == 4 ? 28 : 1);
+};
+__host__ __device__ constexpr int packed_set(int K, int i) {   // i-th index of the K's set
+  return K == 2 ? (i < 4 ? i : i + 1) : K == 4 ? (i == 0 ? 0 : 2 * i - 1) : i;
+}
+__host__ __device__ constexpr int packed_n(int K) { return K == 2 ? 7 : K == 4 ? 5 : K == 8 ? 1 : 8; }
+
+__device__ __forceinline__ float half_of(const uint32_t (&w)[16], int e) {
+  return (e & 1) ? (float)((int)w[e >> 1] >> 16) : (float)(int16_t)(w[e >> 1] & 0xffff);
+}
+
 // Decode one block at scale 1/K: px[y] holds the P samples of output row y
 // (little-endian bytes, 2 words per row at K = 1).  `act` = this lane has a
 // block; every lane of the warp must call it (warp reductions pick the
-// nonzero row/column extents).
-template <int K>
+// nonzero row extent).
+template <int K, bool PACKED>
 __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const float* q,
                                              uint32_t (&px)[8][2]) {
   constexpr int P = 8 / K;
@@ -219,57 +239,45 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     for (int v = 0; v < 8; ++v)
       raw[v] = act ? __ldg(reinterpret_cast<const int4*>(src) + v) : make_int4(0, 0, 0, 0);
     uint32_t rows = 0;
-    int4 acc = make_int4(0, 0, 0, 0);
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      rows |= ((raw[v].x | raw[v].y | raw[v].z | raw[v].w) != 0) << v;
-      acc.x |= raw[v].x; acc.y |= raw[v].y; acc.z |= raw[v].z; acc.w |= raw[v].w;
-    }
-    const int wcol = acc.w ? ((acc.w >> 16) ? 8 : 7) : acc.z ? ((acc.z >> 16) ? 6 : 5)
-                   : acc.y ? ((acc.y >> 16) ? 4 : 3) : ((acc.x >> 16) ? 2 : 1);
+    for (int v = 0; v < 8; ++v) rows |= ((raw[v].x | raw[v].y | raw[v].z | raw[v].w) != 0) << v;
+    // prune by the warp's highest nonzero coefficient row (one code variant
+    // per extent: more variants cost more in I-cache misses than they save)
     const int H = (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows));
-    const int W = (int)__reduce_max_sync(0xffffffffu, (uint32_t)wcol);
     float m[8][8];
-#ifndef SMOL_IDCT_VARIANT
-#define SMOL_IDCT_VARIANT 2
-#endif
-#if SMOL_IDCT_VARIANT == 1        // W in {5, 8}, H in {6, 8}
-    if (W <= 5) {
-      if (H <= 6) idct_rows<5, 6>(raw, q, m); else idct_rows<5, 8>(raw, q, m);
-    } else {
-      if (H <= 6) idct_rows<8, 6>(raw, q, m); else idct_rows<8, 8>(raw, q, m);
-    }
-    if (H <= 6) idct_cols<6>(m, px); else idct_cols<8>(m, px);
-#elif SMOL_IDCT_VARIANT == 2      // H in {6, 8} only
-    (void)W;
     if (H <= 6) { idct_rows<8, 6>(raw, q, m); idct_cols<6>(m, px); }
     else { idct_rows<8, 8>(raw, q, m); idct_cols<8>(m, px); }
-#elif SMOL_IDCT_VARIANT == 3      // no pruning
-    (void)W; (void)H;
-    idct_rows<8, 8>(raw, q, m);
-    idct_cols<8>(m, px);
-#else                             // W in {4, 6, 8}, H in {4, 6, 8}
-    if (W <= 4) {
-      if (H <= 4) idct_rows<4, 4>(raw, q, m); else if (H <= 6) idct_rows<4, 6>(raw, q, m); else idct_rows<4, 8>(raw, q, m);
-    } else if (W <= 6) {
-      if (H <= 4) idct_rows<6, 4>(raw, q, m); else if (H <= 6) idct_rows<6, 6>(raw, q, m); else idct_rows<6, 8>(raw, q, m);
-    } else {
-      if (H <= 4) idct_rows<8, 4>(raw, q, m); else if (H <= 6) idct_rows<8, 6>(raw, q, m); else idct_rows<8, 8>(raw, q, m);
-    }
-    if (H <= 4) idct_cols<4>(m, px); else if (H <= 6) idct_cols<6>(m, px); else idct_cols<8>(m, px);
-#endif
   } else {
-    // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7})
+    // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7}):
+    // rows/columns outside the index set have an exactly-zero basis.
+    constexpr int NS = packed_n(K);
     float g[8][P];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      if ((K == 2 && v == 4) || (K == 4 && (v == 2 || v == 4 || v == 6))) {
+    for (int v = 0; v < 8; ++v)
 #pragma unroll
-        for (int j = 0; j < P; ++j) g[v][j] = 0.f;
-        continue;
+      for (int j = 0; j < P; ++j) g[v][j] = 0.f;
+    uint32_t w[16];
+    if constexpr (PACKED) {
+      constexpr int NW = BlockFmt<K, true>::kElems / 4;   // 8-byte words
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        const int2 t = act ? __ldg(reinterpret_cast<const int2*>(src) + i) : make_int2(0, 0);
+        w[2 * i] = (uint32_t)t.x;
+        w[2 * i + 1] = (uint32_t)t.y;
       }
+    }
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      const int v = packed_set(K, i);
       float d[8];
-      unpack_row(act ? __ldg(reinterpret_cast<const int4*>(src) + v) : make_int4(0, 0, 0, 0), d);
+      if constexpr (PACKED) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[u] = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < NS; ++jj) d[packed_set(K, jj)] = half_of(w, i * NS + jj);
+      } else {
+        unpack_row(act ? __ldg(reinterpret_cast<const int4*>(src) + v) : make_int4(0, 0, 0, 0), d);
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u) d[u] *= q[v * 8 + u];
       if (v == 0) d[0] += 128.5f;           // level shift + rounding offset (DC weight is exactly 1)
@@ -367,7 +375,7 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[2], int e) {
   return (w[e >> 2] >> (8 * (e & 3))) & 255u;
 }
 
-template <int K, bool F16, bool DEBUG>
+template <int K, bool F16, bool DEBUG, bool PACKED>
 __global__ void __launch_bounds__(kThreads, SMOL_MIN_BLOCKS)
 smol_fused_kernel(const KParams kp) {
   constexpr int P = 8 / K;                 // decoded samples per block side
@@ -448,9 +456,10 @@ smol_fused_kernel(const KParams kp) {
         bcol = tt - brow * nbxc;
         brow += cb0;
       }
-      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * 64;
+      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] +
+                           (size_t)(L.bx0[c] + bcol) * BlockFmt<K, PACKED>::kElems;
       uint32_t px[8][2];
-      decode_block<K>(act, src, qf + c * 64, px);
+      decode_block<K, PACKED>(act, src, qf + c * 64, px);
       if (!act) continue;
       if (c == 0) {
         uint8_t* d = yring + bcol * P;
@@ -524,9 +533,11 @@ smol_fused_kernel(const KParams kp) {
       for (int k = tid; k < ny + 2 * nc; k += 32) {
         int c = 0, brow = yb0 + k;
         if (k >= ny) { c = 1 + (k - ny >= nc); brow = cb0 + (k - ny) - (c - 1) * nc; }
-        const int16_t* p = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)L.bx0[c] * 64;
-        const uint32_t bytes = (uint32_t)(L.bx1[c] - L.bx0[c] + 1) * 128u;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+        // 16-B aligned segment [bx0 * S, (bx1 + 1) * S) of the (16-B padded) block row
+        constexpr int SB = BlockFmt<K, PACKED>::kElems * 2;
+        const uint32_t lo = ((uint32_t)L.bx0[c] * SB) & ~15u, hi = ((uint32_t)(L.bx1[c] + 1) * SB + 15u) & ~15u;
+        const char* p = reinterpret_cast<const char*>(im.coef[c] + (size_t)brow * im.stride[c]) + lo;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(hi - lo) : "memory");
       }
     }
 

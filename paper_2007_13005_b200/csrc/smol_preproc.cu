@@ -115,11 +115,17 @@ int32_t validate_params(const smol_preproc_params* p) {
   }
   if (p->out_dtype != SMOL_OUT_F32_NCHW && p->out_dtype != SMOL_OUT_F16_NCHW)
     return fail(SMOL_ERR_INVALID, "params.out_dtype=%d", p->out_dtype);
-  if (p->layout != SMOL_LAYOUT_DENSE64)
-    return fail(SMOL_ERR_UNSUPPORTED, "params.layout=%d (only DENSE64)", p->layout);
+  if (p->layout != SMOL_LAYOUT_DENSE64 && p->layout != SMOL_LAYOUT_PACKED)
+    return fail(SMOL_ERR_INVALID, "params.layout=%d", p->layout);
   if (p->tile_rows < 0 || p->tile_rows > 4096)
     return fail(SMOL_ERR_INVALID, "params.tile_rows=%d", p->tile_rows);
   return SMOL_OK;
+}
+
+// int16 elements per coefficient block of a layout at scale 1/K (smol_kernels.cuh BlockFmt)
+int block_elems(int K, int layout) {
+  if (layout != SMOL_LAYOUT_PACKED || K == 1) return 64;
+  return K == 2 ? 52 : K == 4 ? 28 : 1;
 }
 
 // Per-image geometry (readings R4, R7, R11); fills the device descriptor's
@@ -176,9 +182,10 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
     if (d->blocks_w[c] < need_w[c] || d->blocks_h[c] < need_h[c])
       return fail(SMOL_ERR_INVALID, "image %d: blocks_w[%d]=%d / blocks_h[%d]=%d < required %d / %d", idx, c,
                   d->blocks_w[c], c, d->blocks_h[c], need_w[c], need_h[c]);
-    if (d->row_stride_bytes[c] < d->blocks_w[c] * 128 || d->row_stride_bytes[c] % 16)
+    const int bb = 2 * block_elems(p->scale_denom, p->layout);
+    if (d->row_stride_bytes[c] < d->blocks_w[c] * bb || d->row_stride_bytes[c] % 16)
       return fail(SMOL_ERR_INVALID, "image %d: row_stride_bytes[%d]=%d (need >= %d, multiple of 16)", idx, c,
-                  d->row_stride_bytes[c], d->blocks_w[c] * 128);
+                  d->row_stride_bytes[c], d->blocks_w[c] * bb);
     if (d->qtable[c] < 0 || d->qtable[c] >= n_qtables)
       return fail(SMOL_ERR_INVALID, "image %d: qtable[%d]=%d not in [0,%d)", idx, c, d->qtable[c], n_qtables);
     g.coef[c] = d->coef[c];
@@ -200,18 +207,19 @@ int auto_tile_rows(int OH, int n_images) {
 
 using KernelFn = void (*)(const KParams);
 
-template <int K>
+template <int K, bool PK>
 KernelFn pick_kernel(bool f16, bool dbg) {
-  if (dbg) return f16 ? smol_fused_kernel<K, true, true> : smol_fused_kernel<K, false, true>;
-  return f16 ? smol_fused_kernel<K, true, false> : smol_fused_kernel<K, false, false>;
+  if (dbg) return f16 ? smol_fused_kernel<K, true, true, PK> : smol_fused_kernel<K, false, true, PK>;
+  return f16 ? smol_fused_kernel<K, true, false, PK> : smol_fused_kernel<K, false, false, PK>;
 }
 
-KernelFn select_kernel(int K, bool f16, bool dbg) {
+// scale 1 has no packed variant: the packed layout of scale 1 is DENSE64
+KernelFn select_kernel(int K, bool f16, bool dbg, bool packed) {
   switch (K) {
-    case 1: return pick_kernel<1>(f16, dbg);
-    case 2: return pick_kernel<2>(f16, dbg);
-    case 4: return pick_kernel<4>(f16, dbg);
-    default: return pick_kernel<8>(f16, dbg);
+    case 1: return pick_kernel<1, false>(f16, dbg);
+    case 2: return packed ? pick_kernel<2, true>(f16, dbg) : pick_kernel<2, false>(f16, dbg);
+    case 4: return packed ? pick_kernel<4, true>(f16, dbg) : pick_kernel<4, false>(f16, dbg);
+    default: return packed ? pick_kernel<8, true>(f16, dbg) : pick_kernel<8, false>(f16, dbg);
   }
 }
 
@@ -261,9 +269,10 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
     out->bx0[c] = L.bx0[c]; out->bx1[c] = L.bx1[c]; out->by0[c] = L.by0[c]; out->by1[c] = L.by1[c];
   }
   out->roi_blocks = tile_roi_blocks(L);
-  // algorithmic coefficient bytes of the dense-64 layout: whole 128-B blocks,
-  // except at scale 1/8 where only the DC's 32-B sector is needed
-  out->roi_coef_bytes = out->roi_blocks * (params->scale_denom == 8 ? 32 : 128);
+  // algorithmic coefficient bytes: whole blocks of the layout, except dense-64
+  // at scale 1/8 where only the DC's 32-B sector is needed
+  const int bb = 2 * block_elems(params->scale_denom, params->layout);
+  out->roi_coef_bytes = out->roi_blocks * ((params->scale_denom == 8 && params->layout == SMOL_LAYOUT_DENSE64) ? 32 : bb);
   return SMOL_OK;
 }
 
@@ -302,7 +311,7 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     int limit = pl->smem_optin;
     for (int dbg = 0; dbg < 2 && e == cudaSuccess; ++dbg) {
       cudaFuncAttributes fa;
-      KernelFn fn = select_kernel(params->scale_denom, f16, dbg);
+      KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED);
       e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) break;
       const int dyn = pl->smem_optin - (int)fa.sharedSizeBytes;
@@ -417,7 +426,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
-  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr);
+  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr,
+                              pl->p.layout == SMOL_LAYOUT_PACKED);
   dim3 grid(ntiles * n_col_tiles, b->n_images);
   fn<<<grid, kThreads, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());

@@ -299,3 +299,46 @@ def _sample_check(name, n_sample, quality=75):
 @pytest.mark.parametrize("name,n_sample", [("c2", 8), ("c3a", 8), ("c3b", 8), ("c4", 64), ("c5", 3)])
 def test_full_size_sampled(name, n_sample):
     _sample_check(name, n_sample)
+
+
+@pytest.mark.parametrize("name", ["c3a", "c3b", "c4", "c5", "c2"])
+def test_packed_layout_equals_dense(name):
+    cfg = synth.CONFIGS[name]
+    n = {"c4": 16, "c5": 2}.get(name, 4)
+    imgs, qt = synth.distinct_images(cfg, n_distinct=n)
+    pd, po = _cfg_params(cfg)
+    pp = smol.params_from_config(cfg, layout="packed")
+    a = smol.Plan(pd, n).run(smol.batch_for(pd, imgs, qt))
+    b = smol.Plan(pp, n).run(smol.batch_for(pp, imgs, qt))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b), name
+
+
+@pytest.mark.parametrize("name", ["c3a", "c3b", "c4"])
+def test_packed_layout_parity_and_poison(name):
+    cfg = synth.CONFIGS[name]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=3)
+    pp = smol.params_from_config(cfg, layout="packed")
+    po = oracle.params_from_config(cfg)
+    plan = smol.Plan(pp, 3)
+    clean = plan.run(smol.batch_for(pp, imgs, qt)).clone()
+    torch.cuda.synchronize()
+    for i, im in enumerate(imgs):
+        ref = oracle.run_image(po, im, qt).astype(np.float64)
+        err = np.abs(clean[i].float().cpu().numpy() - ref)
+        aff = helpers.affected_outputs(po, im, qt)
+        assert err[~aff].max(initial=0) <= TOL[cfg.out_dtype]
+    poisoned = []
+    for im in imgs:
+        g = smol.geometry(pp, im.width, im.height)
+        coef = []
+        for ci in range(3):
+            c = im.coef[ci].copy()
+            keep = np.zeros(c.shape[:2], bool)
+            keep[g["by0"][ci]:g["by1"][ci] + 1, g["bx0"][ci]:g["bx1"][ci] + 1] = True
+            c[~keep] = 32767
+            coef.append(c)
+        poisoned.append(synth.CoefImage(im.width, im.height, coef))
+    dirty = plan.run(smol.batch_for(pp, poisoned, qt))
+    torch.cuda.synchronize()
+    assert torch.equal(clean, dirty)
