@@ -219,7 +219,8 @@ __host__ __device__ constexpr int packed_set(int K, int i) {   // i-th index of 
 }
 __host__ __device__ constexpr int packed_n(int K) { return K == 2 ? 7 : K == 4 ? 5 : K == 8 ? 1 : 8; }
 
-__device__ __forceinline__ float half_of(const uint32_t (&w)[16], int e) {
+template <int NWORDS>
+__device__ __forceinline__ float half_of(const uint32_t (&w)[NWORDS], int e) {
   return (e & 1) ? (float)((int)w[e >> 1] >> 16) : (float)(int16_t)(w[e >> 1] & 0xffff);
 }
 
@@ -256,9 +257,9 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     for (int v = 0; v < 8; ++v)
 #pragma unroll
       for (int j = 0; j < P; ++j) g[v][j] = 0.f;
-    uint32_t w[16];
+    constexpr int NW = PACKED ? BlockFmt<K, true>::kElems / 4 : 1;   // 8-byte words
+    uint32_t w[2 * NW];
     if constexpr (PACKED) {
-      constexpr int NW = BlockFmt<K, true>::kElems / 4;   // 8-byte words
 #pragma unroll
       for (int i = 0; i < NW; ++i) {
         const int2 t = act ? __ldg(reinterpret_cast<const int2*>(src) + i) : make_int2(0, 0);
