@@ -132,9 +132,13 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
 int32_t smol_preproc_run(smol_preproc_plan_t* plan, const smol_batch_desc* batch,
                          void* out, void* stream);
 
-/* Same as smol_preproc_run, but coefficient pointers (and qtables) may be
- * pinned HOST memory: the fused kernel reads only the ROI blocks across PCIe
- * (end-to-end path; no separate staging copy).  out: DEVICE. */
+/* Same as smol_preproc_run, but coefficient pointers may be pinned HOST
+ * memory (qtables stay DEVICE).  Only the ROI block rows cross PCIe: a gather
+ * kernel on the plan's internal copy stream stages them into plan-owned device
+ * memory (double-buffered: the next call's transfer overlaps this call's fused
+ * kernel), then the fused kernel runs on `stream`.  The staging buffers are
+ * allocated on first use and grown when a larger batch arrives (the only
+ * allocation in any run call).  out: DEVICE. */
 int32_t smol_preproc_run_host(smol_preproc_plan_t* plan, const smol_batch_desc* batch,
                               void* out, void* stream);
 

@@ -225,6 +225,33 @@ KernelFn select_kernel(int K, bool f16, bool dbg, bool packed) {
 
 }  // namespace
 
+// One image's ROI block rows to gather: per component, rows [by0, by1] x
+// blocks [bx0, bx1] of the (pinned host) plane -> a compact device copy.
+struct GatherDesc {
+  const int16_t* src[3];     // host plane (device-addressable pinned memory)
+  int16_t* dst[3];           // staging
+  int32_t src_stride[3];     // int16 elements per source block row
+  int32_t dst_stride[3];     // int16 elements per staged row (16-B multiple)
+  int32_t by0[3], rows[3];   // first ROI block row, ROI block rows
+  int32_t col0[3], ncol[3];  // first ROI element in a row (bx0 * E), elements per row
+};
+
+// High-MLP copy of the ROI block rows (8-byte chunks; one CTA per image):
+// PCIe reads stay in flight from every thread instead of only from the
+// fused kernel's IDCT threads.
+__global__ void __launch_bounds__(256) smol_gather_kernel(const GatherDesc* gd) {
+  const GatherDesc g = gd[blockIdx.x];
+  for (int c = 0; c < 3; ++c) {
+    const int nq = g.ncol[c] >> 2;                       // 8-byte chunks per row
+    const int total = nq * g.rows[c];
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int r = t / nq, q = t - r * nq;
+      const int2 v = __ldcs(reinterpret_cast<const int2*>(g.src[c] + (size_t)(g.by0[c] + r) * g.src_stride[c] + g.col0[c]) + q);
+      reinterpret_cast<int2*>(g.dst[c] + (size_t)r * g.dst_stride[c])[q] = v;
+    }
+  }
+}
+
 struct smol_preproc_plan {
   smol_preproc_params p;
   int max_images = 0;
@@ -237,6 +264,15 @@ struct smol_preproc_plan {
   cudaEvent_t ev[kRing] = {};
   int ring = 0;
   float na[3], nb[3];
+  // end-to-end (run_host) staging: ROI block rows gathered from pinned host
+  // memory into device memory on a copy stream, double-buffered
+  cudaStream_t copy_stream = nullptr;
+  int16_t* stage[2] = {nullptr, nullptr};
+  size_t stage_cap[2] = {0, 0};            // int16 elements
+  GatherDesc* d_gather = nullptr;          // [2][max_images]
+  GatherDesc* h_gather = nullptr;          // pinned [2][max_images]
+  cudaEvent_t stage_free[2] = {}, stage_ready[2] = {};
+  int stage_slot = 0;
 };
 
 extern "C" {
@@ -304,6 +340,13 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   for (int i = 0; i < kRing && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&pl->stage_free[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->stage_ready[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_gather, sizeof(GatherDesc) * (size_t)max_images * 2);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_gather, sizeof(GatherDesc) * (size_t)max_images * 2);
   if (e == cudaSuccess) {
     // opt every instantiation of this plan's (scale, dtype) in to the largest
     // dynamic smem the device allows next to the kernel's static smem
@@ -333,6 +376,14 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (!pl) return;
   for (int i = 0; i < kRing; ++i)
     if (pl->ev[i]) { cudaEventSynchronize(pl->ev[i]); cudaEventDestroy(pl->ev[i]); }
+  for (int i = 0; i < 2; ++i) {
+    if (pl->stage_free[i]) { cudaEventSynchronize(pl->stage_free[i]); cudaEventDestroy(pl->stage_free[i]); }
+    if (pl->stage_ready[i]) cudaEventDestroy(pl->stage_ready[i]);
+    if (pl->stage[i]) cudaFree(pl->stage[i]);
+  }
+  if (pl->d_gather) cudaFree(pl->d_gather);
+  if (pl->h_gather) cudaFreeHost(pl->h_gather);
+  if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->d_desc) cudaFree(pl->d_desc);
   if (pl->h_desc) cudaFreeHost(pl->h_desc);
   delete pl;
@@ -353,7 +404,7 @@ int32_t smol_preproc_launches_per_run(const smol_preproc_plan_t* pl) {
 namespace {
 
 int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream_v,
-                 const KParams* dbg) {
+                 const KParams* dbg, bool staged = false) {
   g_last_error.clear();
   if (!pl) return fail(SMOL_ERR_INVALID, "plan is NULL");
   if (!b) return fail(SMOL_ERR_INVALID, "batch is NULL");
@@ -416,6 +467,62 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   if (smem > pl->smem_optin)
     return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
 
+  if (staged) {
+    // End-to-end path: gather each image's ROI block rows (the whole output's
+    // tap footprint) from pinned host memory into a compact device staging
+    // buffer on the plan's copy stream, then point the descriptors at it.
+    const int sl = pl->stage_slot;
+    pl->stage_slot ^= 1;
+    GatherDesc* hg = pl->h_gather + (size_t)sl * pl->max_images;
+    GatherDesc* dg = pl->d_gather + (size_t)sl * pl->max_images;
+    SMOL_CUDA(cudaEventSynchronize(pl->stage_free[sl]));     // host side: hg reusable
+    const int E = block_elems(K, pl->p.layout);
+    size_t need = 0;
+    for (int i = 0; i < b->n_images; ++i) {
+      TileLayout L;
+      tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L);
+      GatherDesc& g = hg[i];
+      for (int c = 0; c < 3; ++c) {
+        const int ncol = (L.bx1[c] - L.bx0[c] + 1) * E;
+        g.src[c] = h[i].coef[c];
+        g.src_stride[c] = h[i].stride[c];
+        g.by0[c] = L.by0[c];
+        g.rows[c] = L.by1[c] - L.by0[c] + 1;
+        g.col0[c] = L.bx0[c] * E;
+        g.ncol[c] = ncol;
+        // leading pad so the kernel's virtual row base (row - col0) is 16-B
+        // aligned, as for an original plane (its L2 bulk prefetch needs it)
+        const int pad = (L.bx0[c] * E) & 7;
+        g.dst_stride[c] = (pad + ncol + 7) & ~7;             // 16-B rows
+        g.dst[c] = reinterpret_cast<int16_t*>(need + pad);    // offset; rebased below
+        need += (size_t)g.dst_stride[c] * g.rows[c];
+      }
+    }
+    if (need > pl->stage_cap[sl]) {                           // grow once (amortised)
+      SMOL_CUDA(cudaStreamSynchronize(pl->copy_stream));
+      if (pl->stage[sl]) SMOL_CUDA(cudaFree(pl->stage[sl]));
+      pl->stage[sl] = nullptr;
+      SMOL_CUDA(cudaMalloc(&pl->stage[sl], need * 2 + 256));
+      pl->stage_cap[sl] = need;
+    }
+    int16_t* base = pl->stage[sl];
+    for (int i = 0; i < b->n_images; ++i)
+      for (int c = 0; c < 3; ++c) {
+        GatherDesc& g = hg[i];
+        g.dst[c] = base + reinterpret_cast<size_t>(g.dst[c]);
+        // descriptor of the staged plane: same absolute block indexing
+        h[i].coef[c] = g.dst[c] - (ptrdiff_t)g.by0[c] * g.dst_stride[c] - g.col0[c];
+        h[i].stride[c] = g.dst_stride[c];
+      }
+    SMOL_CUDA(cudaStreamWaitEvent(pl->copy_stream, pl->stage_free[sl], 0));   // previous user done
+    SMOL_CUDA(cudaMemcpyAsync(dg, hg, sizeof(GatherDesc) * b->n_images, cudaMemcpyHostToDevice,
+                              pl->copy_stream));
+    smol_gather_kernel<<<b->n_images, 256, 0, pl->copy_stream>>>(dg);
+    SMOL_CUDA(cudaGetLastError());
+    SMOL_CUDA(cudaEventRecord(pl->stage_ready[sl], pl->copy_stream));
+    SMOL_CUDA(cudaStreamWaitEvent(stream, pl->stage_ready[sl], 0));
+  }
+
   SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * b->n_images, cudaMemcpyHostToDevice, stream));
   KParams kp = dbg ? *dbg : KParams{};
   kp.imgs = d;
@@ -432,6 +539,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   fn<<<grid, kThreads, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
+  if (staged) SMOL_CUDA(cudaEventRecord(pl->stage_free[pl->stage_slot ^ 1], stream));
   return SMOL_OK;
 }
 
@@ -444,8 +552,10 @@ int32_t smol_preproc_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void
 }
 
 int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream) {
-  // Pinned host coefficient memory is device-addressable under UVA: the
-  // fused kernel reads only the ROI blocks across PCIe.
+  // Pinned host coefficient memory is device-addressable under UVA.  Only the
+  // ROI block rows cross PCIe: a gather kernel on the plan's copy stream
+  // stages them (double-buffered, so batch k+1's transfer overlaps batch k's
+  // fused kernel), then the fused kernel runs on `stream`.
   // Probe image 0's planes (a batch normally comes from one pinned arena).
   if (b && b->images && b->n_images > 0) {
     for (int c = 0; c < 3; ++c) {
@@ -458,7 +568,7 @@ int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b,
       }
     }
   }
-  return run_impl(pl, b, out, stream, nullptr);
+  return run_impl(pl, b, out, stream, nullptr, /*staged=*/true);
 }
 
 int32_t smol_debug_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, int16_t* y_dbg,

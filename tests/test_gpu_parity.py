@@ -342,3 +342,18 @@ def test_packed_layout_parity_and_poison(name):
     dirty = plan.run(smol.batch_for(pp, poisoned, qt))
     torch.cuda.synchronize()
     assert torch.equal(clean, dirty)
+
+
+@pytest.mark.parametrize("name,layout", [("c2", "dense"), ("c3b", "packed"), ("c4", "packed"), ("c3a", "packed")])
+def test_run_host_staged_equals_device(name, layout):
+    cfg = synth.CONFIGS[name]
+    n = 8
+    imgs, qt = synth.distinct_images(cfg, n_distinct=n)
+    ps = smol.params_from_config(cfg, layout=layout)
+    plan = smol.Plan(ps, n)
+    a = plan.run(smol.batch_for(ps, imgs, qt)).clone()
+    hb = [smol.batch_for(ps, imgs, qt, location="pinned") for _ in range(2)]
+    outs = [plan.run(hb[k % 2]) for k in range(5)]          # back-to-back: exercises the double buffer
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(a, o), name
