@@ -242,12 +242,17 @@ struct GatherDesc {
 __global__ void __launch_bounds__(256) smol_gather_kernel(const GatherDesc* gd) {
   const GatherDesc g = gd[blockIdx.x];
   for (int c = 0; c < 3; ++c) {
-    const int nq = g.ncol[c] >> 2;                       // 8-byte chunks per row
+    // 8-byte chunks covering [col0, col0 + ncol) rounded out to 4 elements;
+    // source and staged rows share their alignment mod 16 B (see run_impl)
+    const int a0 = g.col0[c] & ~3;
+    const int nq = ((g.col0[c] + g.ncol[c] + 3) >> 2) - (a0 >> 2);
     const int total = nq * g.rows[c];
+    const int16_t* src = g.src[c] + (size_t)g.by0[c] * g.src_stride[c] + a0;
+    int16_t* dst = g.dst[c] - (g.col0[c] & 3);
     for (int t = threadIdx.x; t < total; t += blockDim.x) {
       const int r = t / nq, q = t - r * nq;
-      const int2 v = __ldcs(reinterpret_cast<const int2*>(g.src[c] + (size_t)(g.by0[c] + r) * g.src_stride[c] + g.col0[c]) + q);
-      reinterpret_cast<int2*>(g.dst[c] + (size_t)r * g.dst_stride[c])[q] = v;
+      const int2 v = __ldcs(reinterpret_cast<const int2*>(src + (size_t)r * g.src_stride[c]) + q);
+      reinterpret_cast<int2*>(dst + (size_t)r * g.dst_stride[c])[q] = v;
     }
   }
 }
