@@ -79,6 +79,11 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc is not None:
+            # a timed region shorter than the sampling period still gets the
+            # sample that closes it (clocks decay over >100 ms after work ends)
+            t0 = time.time()
+            while len(self.lines) <= self.start and time.time() - t0 < 0.2 and self.proc.poll() is None:
+                time.sleep(0.005)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)

@@ -64,6 +64,10 @@ constexpr int kYP = 512;
 constexpr int kCP = 256;
 constexpr int kCPad = 8;
 constexpr int kCSlots = 18;
+constexpr int kOffY = 0;                                   // Y ring
+constexpr int kOffC = kOffY + kYRing * kYP;                // Cb ring, then Cr ring
+constexpr int kOffQ = kOffC + 2 * kCSlots * kCP;           // dequant tables (3 x 64 float)
+constexpr int kOffRgb = kOffQ + 3 * 64 * 4;                // RGB ring (size depends on the tile)
 
 struct TileLayout {
   int oy0, oy1, ox0, ox1;          // output tile
@@ -110,12 +114,15 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.nsteps = ((imax(L.ly1, 2 * L.cy1) - L.r0) / kStepRows) + 1;
   L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= kYP) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= kCP);
   int off = 0;
-  L.off_q = off;   off += 3 * 64 * 4;                         // dequant tables (float)
-  L.off_xt = off;  off += align16((ox1 - ox0 + 3) * 8);       // x taps: {4 x0, w}
+  // fixed-size regions first, at compile-time offsets (kOff*), so the hot
+  // loops address them as immediates instead of keeping base pointers live
+  L.off_y = kOffY;
+  L.off_c = kOffC;
+  L.off_q = kOffQ;
+  L.off_rgb = kOffRgb;
+  off = kOffRgb + align16(L.rgb_p * 4 * (kRgbRing + 1));
+  L.off_xt = off;  off += ((ox1 - ox0 + 4) >> 1) * 16;       // x taps per pixel pair: {4 x0 a, 4 x0 b, w a, w b}
   L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {y0 | y1<<16, w}
-  L.off_y = off;   off += kYRing * kYP;
-  L.off_c = off;   off += 2 * kCSlots * kCP;
-  L.off_rgb = off; off += align16(L.rgb_p * 4 * (kRgbRing + 1));
   L.total = off;
 }
 

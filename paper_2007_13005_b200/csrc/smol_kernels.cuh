@@ -21,6 +21,23 @@
 
 #include "smol_geom.cuh"
 
+// Code-generation options (kept switchable for A/B measurement).
+#ifndef SMOL_OPT_COLSTATIC
+#define SMOL_OPT_COLSTATIC 1
+#endif
+#ifndef SMOL_OPT_ATOM
+#define SMOL_OPT_ATOM 0
+#endif
+#ifndef SMOL_OPT_COLFFMA2
+#define SMOL_OPT_COLFFMA2 0
+#endif
+#ifndef SMOL_OUT_PER_GRAB
+#define SMOL_OUT_PER_GRAB 1      // output tasks per lane per work-counter grab
+#endif
+#ifndef SMOL_OPT_YMAGIC
+#define SMOL_OPT_YMAGIC 1
+#endif
+
 namespace smol {
 
 // Basis constants, computed on the host in double from their definitions
@@ -36,6 +53,7 @@ struct Basis {
   float a2[2][8];
   float a4[8];
   float kR, kB, cR, cB;
+  float2 tp[4][4];   // column pass pairs: tp[k][y] = (t[2k][y], t[2k+1][y])
 };
 
 __constant__ Basis c_basis;
@@ -183,6 +201,55 @@ __device__ __forceinline__ void idct_rows(const int4 (&raw)[8], const float* q, 
   }
 }
 
+// Row pass with the pairs kept: M[k][x] = (m[2k][x], m[2k+1][x]).
+template <int W, int HR>
+__device__ __forceinline__ void idct_rows2(const int4 (&raw)[8], const float* q, float2 (&M)[4][8]) {
+#pragma unroll
+  for (int v = 0; v < HR; v += 2) {
+    float a[8], b[8];
+    unpack_row(raw[v], a);
+    unpack_row(raw[v + 1], b);
+    const float4 qa0 = *reinterpret_cast<const float4*>(q + v * 8);
+    const float4 qa1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
+    const float4 qb0 = *reinterpret_cast<const float4*>(q + v * 8 + 8);
+    const float4 qb1 = *reinterpret_cast<const float4*>(q + v * 8 + 12);
+    float2 d[8];
+    d[0] = make_float2(a[0] * qa0.x, b[0] * qb0.x); d[1] = make_float2(a[1] * qa0.y, b[1] * qb0.y);
+    d[2] = make_float2(a[2] * qa0.z, b[2] * qb0.z); d[3] = make_float2(a[3] * qa0.w, b[3] * qb0.w);
+    d[4] = make_float2(a[4] * qa1.x, b[4] * qb1.x); d[5] = make_float2(a[5] * qa1.y, b[5] * qb1.y);
+    d[6] = make_float2(a[6] * qa1.z, b[6] * qb1.z); d[7] = make_float2(a[7] * qa1.w, b[7] * qb1.w);
+    if (v == 0) d[0].x += 128.5f;
+    idct8x2<W>(d, M[v >> 1]);
+  }
+}
+
+// Column pass on the row pairs: lane .x accumulates the even-v terms and
+// lane .y the odd-v terms of f[y] = sum_v m[v] t(v, y); the mirror output is
+// f[7-y] = even - odd (t(v, 7-y) = (-1)^v t(v, y)).  The chain starts from
+// m[0] * t(0, y) = m[0] exactly, so DC-only inputs stay exact (reading R3).
+template <int H>
+__device__ __forceinline__ void idct_cols2(const float2 (&M)[4][8], uint32_t (&px)[8][2]) {
+#pragma unroll
+  for (int x = 0; x < 8; ++x) {
+    float f[8];
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      float2 acc = __fmul2_rn(M[0][x], c_basis.tp[0][y]);
+#pragma unroll
+      for (int k = 1; k < H / 2; ++k) acc = __ffma2_rn(M[k][x], c_basis.tp[k][y], acc);
+      f[y] = acc.x + acc.y;
+      f[7 - y] = acc.x - acc.y;
+    }
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const uint32_t b = floor_u8(f[y]);
+      uint32_t& w = px[y][x >> 2];
+      if ((x & 3) == 0) w = b;
+      else w = __byte_perm(w, b, (x & 3) == 1 ? 0x3240 : (x & 3) == 2 ? 0x3410 : 0x4210);
+    }
+  }
+}
+
 template <int H>
 __device__ __forceinline__ void idct_cols(const float (&m)[8][8], uint32_t (&px)[8][2]) {
   // column x's bytes are merged into the row words as they are produced
@@ -245,9 +312,15 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     // prune by the warp's highest nonzero coefficient row (one code variant
     // per extent: more variants cost more in I-cache misses than they save)
     const int H = (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows));
+#if SMOL_OPT_COLFFMA2
+    float2 M[4][8];
+    if (H <= 6) { idct_rows2<8, 6>(raw, q, M); idct_cols2<6>(M, px); }
+    else { idct_rows2<8, 8>(raw, q, M); idct_cols2<8>(M, px); }
+#else
     float m[8][8];
     if (H <= 6) { idct_rows<8, 6>(raw, q, m); idct_cols<6>(m, px); }
     else { idct_rows<8, 8>(raw, q, m); idct_cols<8>(m, px); }
+#endif
   } else {
     // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7}):
     // rows/columns outside the index set have an exactly-zero basis.
@@ -319,6 +392,24 @@ __device__ __forceinline__ uint32_t colour(int Y, int cb16, int cr16) {
   return R | ((uint32_t)G << 8) | (B << 16);
 }
 
+// Two pixels from 2^23-biased luma floats (one PRMT per sample builds the
+// bits 0x4B0000YY = 2^23 + Y; subtracting 2^23 is exact), so no I2F is
+// needed for Y; G uses the biased bits directly (the bias cancels in the
+// IADD3).  Same IEEE fp32 operations as colour() otherwise.
+__device__ __forceinline__ uint2 colour2m(uint32_t m0, uint32_t m1, int cb0, int cb1, int cr0, int cr1) {
+  const float2 yf = __fadd2_rn(make_float2(__uint_as_float(m0), __uint_as_float(m1)), f2(-8388608.f));
+  const float2 tr = __ffma2_rn(make_float2((float)cr0, (float)cr1), make_float2(c_basis.kR, c_basis.kR),
+                               __fadd2_rn(yf, make_float2(c_basis.cR, c_basis.cR)));
+  const float2 tb = __ffma2_rn(make_float2((float)cb0, (float)cb1), make_float2(c_basis.kB, c_basis.kB),
+                               __fadd2_rn(yf, make_float2(c_basis.cB, c_basis.cB)));
+  const uint32_t u0 = 543917632u - 43017u * (uint32_t)cb0 - 89267u * (uint32_t)cr0;
+  const uint32_t u1 = 543917632u - 43017u * (uint32_t)cb1 - 89267u * (uint32_t)cr1;
+  const uint32_t G0 = (uint32_t)min(max((int)(m0 + u0 / 2000000u - (0x4B000000u + 136u)), 0), 255);
+  const uint32_t G1 = (uint32_t)min(max((int)(m1 + u1 / 2000000u - (0x4B000000u + 136u)), 0), 255);
+  return make_uint2(__byte_perm(__byte_perm(floor_u8(tr.x), G0, 0x0040), floor_u8(tb.x), 0x5410),
+                    __byte_perm(__byte_perm(floor_u8(tr.y), G1, 0x0040), floor_u8(tb.y), 0x5410));
+}
+
 // Two pixels at once: the same IEEE fp32 operations as colour(), packed
 // (FADD2/FFMA2), so results are bitwise identical.
 __device__ __forceinline__ uint2 colour2(int Y0, int Y1, int cb0, int cb1, int cr0, int cr1) {
@@ -372,8 +463,28 @@ __device__ __forceinline__ void put_row(uint8_t* d, const uint32_t (&w)[2]) {
   else *d = (uint8_t)w[0];
 }
 
+__device__ __forceinline__ uint32_t lds_u32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
 __device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[2], int e) {
-  return (w[e >> 2] >> (8 * (e & 3))) & 255u;
+  return ((e < 4 ? w[0] : w[1]) >> (8 * (e & 3))) & 255u;   // select: no dynamic register indexing
+}
+
+// Dynamic work distribution: lane 0 takes the next 32 tasks from a shared
+// counter and broadcasts the base.  With SMOL_OPT_ATOM the atomic is issued as
+// one predicated ATOMS (the compiler otherwise emits its warp-aggregation
+// sequence around atomicAdd).
+__device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
+  int chunk = 0;
+#if SMOL_OPT_ATOM
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(ctr);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, 0;\n\t"
+      "@p atom.shared.add.u32 %0, [%2], %3;\n\t}"
+      : "+r"(chunk) : "r"(lane), "r"(a), "r"(n) : "memory");
+#else
+  if (lane == 0) chunk = atomicAdd(ctr, n);
+#endif
+  return __shfl_sync(0xffffffffu, chunk, 0);
 }
 
 template <int K, bool F16, bool DEBUG, bool PACKED>
@@ -397,25 +508,30 @@ smol_fused_kernel(const KParams kp) {
     ctr[1] = 0;
   }
   __syncthreads();
-  float* qf = reinterpret_cast<float*>(smem + L.off_q);
+  float* qf = reinterpret_cast<float*>(smem + kOffQ);
   int2* xt = reinterpret_cast<int2*>(smem + L.off_xt);
   int2* yt = reinterpret_cast<int2*>(smem + L.off_yt);
-  uint8_t* yring = smem + L.off_y;
-  uint8_t* cring = smem + L.off_c;
-  uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + L.off_rgb);
+  uint8_t* yring = smem + kOffY;
+  uint8_t* cring = smem + kOffC;
+  uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + kOffRgb);
   constexpr int kCStride = kCSlots * kCP;  // Cr ring follows the Cb ring
   const int ntw = ox1 - ox0, nth = oy1 - oy0;
   const int rgb_p = L.rgb_p;
+  const int pitch4 = rgb_p * 4;             // RGB ring row pitch in bytes
 
   // ---- prologue: dequant tables (Q/8, exact) and bilinear taps ----------
   // Taps use exact-integer coordinates (R9).  Where the upper tap is clamped
   // (i1 == i0) its weight is zeroed so the kernel may always read i0 + 1.
   for (int i = tid; i < 3 * 64; i += kThreads)
     qf[i] = (float)kp.qtables[im.qidx[i >> 6] * 64 + (i & 63)] * 0.125f;
+  // x taps per output-pixel pair: {byte offset of x0 (a), (b), w (a), w (b)},
+  // so a pair's weights load into an adjacent register pair for FFMA2
   for (int i = tid; i < ntw + 3; i += kThreads) {
     int i0, i1; float w;
     src_tap(im.left + ox0 + min(i, ntw - 1), im.Wd, im.Wr, i0, i1, w);
-    xt[i] = make_int2(i0 - L.rgb_x0, __float_as_int(i1 == i0 ? 0.f : w));
+    int* e = reinterpret_cast<int*>(xt) + (i >> 1) * 4 + (i & 1);
+    e[0] = (i0 - L.rgb_x0) * 4;
+    e[2] = __float_as_int(i1 == i0 ? 0.f : w);
   }
   for (int i = tid; i < nth; i += kThreads) {
     int i0, i1; float w;
@@ -551,13 +667,17 @@ smol_fused_kernel(const KParams kp) {
       const int j0 = (ready_prev + 1) >> 1;
       const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
       const int ntaskc = nq * ntask4;
+#if SMOL_OPT_COLSTATIC
+      // colour tasks all cost the same and nothing else runs in this phase:
+      // a static round-robin needs no work counter
+      for (int t = tid; t < ntaskc; t += kThreads) {
+#else
       for (;;) {
-        int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(&ctr[0], 32);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        const int chunk = grab_chunk(&ctr[0], lane);
         if (chunk >= ntaskc) break;
         const int t = chunk + lane;
         if (t >= ntaskc) continue;
+#endif
         const int rr = (int)fdiv((uint32_t)t, fd_t4);
         const int p = t - rr * ntask4;
         const int j = j0 + rr;                               // chroma row of the quads
@@ -592,10 +712,18 @@ smol_fused_kernel(const KParams kp) {
         const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
         const int slot = (2 * j) & (kRgbRing - 1);
         uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
+#if SMOL_OPT_YMAGIC
+        const uint32_t mg = 0x4B000000u;
+        const uint2 t01 = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x7541), cbq[0], cbq[1], crq[0], crq[1]);
+        const uint2 t23 = colour2m(__byte_perm(y0, mg, 0x7542), __byte_perm(y0, mg, 0x7543), cbq[2], cbq[3], crq[2], crq[3]);
+        const uint2 b01 = colour2m(__byte_perm(y1, mg, 0x7540), __byte_perm(y1, mg, 0x7541), cbq[4], cbq[5], crq[4], crq[5]);
+        const uint2 b23 = colour2m(__byte_perm(y1, mg, 0x7542), __byte_perm(y1, mg, 0x7543), cbq[6], cbq[7], crq[6], crq[7]);
+#else
         const uint2 t01 = colour2(y0 & 255, (y0 >> 8) & 255, cbq[0], cbq[1], crq[0], crq[1]);
         const uint2 t23 = colour2((y0 >> 16) & 255, y0 >> 24, cbq[2], cbq[3], crq[2], crq[3]);
         const uint2 b01 = colour2(y1 & 255, (y1 >> 8) & 255, cbq[4], cbq[5], crq[4], crq[5]);
         const uint2 b23 = colour2((y1 >> 16) & 255, y1 >> 24, cbq[6], cbq[7], crq[6], crq[7]);
+#endif
         const uint4 top = make_uint4(t01.x, t01.y, t23.x, t23.y);
         *reinterpret_cast<uint4*>(r0p) = top;
         *reinterpret_cast<uint4*>(r0p + rgb_p) = make_uint4(b01.x, b01.y, b23.x, b23.y);
@@ -636,33 +764,34 @@ smol_fused_kernel(const KParams kp) {
       const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
       const uint32_t magic = kp.magic;     // 0x4B000000 (2^23), kept in a register
       for (;;) {
-        int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(&ctr[1], 32);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        const int chunk = grab_chunk(&ctr[1], lane, 32 * SMOL_OUT_PER_GRAB);
         if (chunk >= ntasko) break;
-        const int t = chunk + lane;
-        if (t >= ntasko) continue;
+#pragma unroll 1
+       for (int h = 0; h < SMOL_OUT_PER_GRAB; ++h) {
+        const int t = chunk + 32 * h + lane;
+        if (t >= ntasko) break;
         const int rr = (int)fdiv((uint32_t)t, fd_q4);
         const int r = done_prev + rr;
         const int ox = 4 * (t - rr * nq4);
         const int2 ty = yt[r];
         const float wy = __int_as_float(ty.y);
-        const uint32_t* row0 = rgb + ((ty.x & 0xffff) & (kRgbRing - 1)) * rgb_p;
+        const uint8_t* row0 = reinterpret_cast<const uint8_t*>(rgb) + ((ty.x & 0xffff) & (kRgbRing - 1)) * pitch4;
+        const uint8_t* row1 = row0 + pitch4;
         float y[3][4];
-        const int4 txa = *reinterpret_cast<const int4*>(xt + ox);      // taps of ox, ox+1
-        const int4 txb = *reinterpret_cast<const int4*>(xt + ox + 2);  // taps of ox+2, ox+3 (padded)
+        const int4* xt4 = reinterpret_cast<const int4*>(xt);
+        const int4 txa = xt4[ox >> 1];          // taps of ox, ox+1
+        const int4 txb = xt4[(ox >> 1) + 1];    // taps of ox+2, ox+3 (padded)
         const float2 wy2 = f2(wy);
 #pragma unroll
         for (int e = 0; e < 4; e += 2) {
           // two output pixels per packed FP32x2 instruction; bytes become
           // 2^23 + b floats by one PRMT (exact), the bias cancels in b - a
-          const int2 t0 = e == 0 ? make_int2(txa.x, txa.y) : make_int2(txb.x, txb.y);
-          const int2 t1 = e == 0 ? make_int2(txa.z, txa.w) : make_int2(txb.z, txb.w);
-          const float2 wx = make_float2(__int_as_float(t0.y), __int_as_float(t1.y));
-          const uint32_t* a0 = row0 + t0.x;
-          const uint32_t* a1 = row0 + t1.x;
-          const uint32_t p00 = a0[0], p01 = a0[1], p10 = a0[rgb_p], p11 = a0[rgb_p + 1];
-          const uint32_t q00 = a1[0], q01 = a1[1], q10 = a1[rgb_p], q11 = a1[rgb_p + 1];
+          const int4 tx = e == 0 ? txa : txb;
+          const float2 wx = make_float2(__int_as_float(tx.z), __int_as_float(tx.w));
+          const uint32_t p00 = lds_u32(row0 + tx.x), p01 = lds_u32(row0 + tx.x + 4);
+          const uint32_t p10 = lds_u32(row1 + tx.x), p11 = lds_u32(row1 + tx.x + 4);
+          const uint32_t q00 = lds_u32(row0 + tx.y), q01 = lds_u32(row0 + tx.y + 4);
+          const uint32_t q10 = lds_u32(row1 + tx.y), q11 = lds_u32(row1 + tx.y + 4);
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
             const int sel = 0x7540 + ch;
@@ -705,6 +834,7 @@ smol_fused_kernel(const KParams kp) {
             }
           }
         }
+       }
       }
     }
     __syncthreads();
