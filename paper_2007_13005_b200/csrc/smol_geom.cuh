@@ -13,12 +13,17 @@
 
 namespace smol {
 
-constexpr int kThreads = 256;             // threads per CTA (8 warps)
-constexpr int kWarps = kThreads / 32;
+// Threads per CTA: the kernel is instantiated for 256 (3 CTAs per SM) and
+// 192 (4 CTAs per SM, used when the tile's shared memory allows 4); both
+// keep 24 warps per SM at <= 80 registers per thread.
+constexpr int kThreadsWide = 256, kThreadsNarrow = 192;
 constexpr int kStepRows = 16;             // decoded luma rows per rolling step (one MCU row at scale 1)
 constexpr int kYRing = 32;                // luma rows kept in smem (two steps)
 constexpr int kCRing = 16;                // chroma rows kept per component (two steps)
-constexpr int kRgbRing = 32;              // RGB rows kept
+// RGB rows kept: output(s) reads rows [ready_{s-1}, ready_s + 1] after
+// colour(s) wrote (ready_{s-1}, ready_s] (+ one garbage row at the footprint
+// ends); ready_s - ready_{s-1} <= 18, so 20 rows never alias a live row.
+constexpr int kRgbRing = 20;
 
 SMOL_HD int ceil_div(int a, int b) { return (a + b - 1) / b; }
 SMOL_HD int imin(int a, int b) { return a < b ? a : b; }
@@ -59,15 +64,16 @@ SMOL_HD int align16(int x) { return (x + 15) & ~15; }
 //          (r & 15) + 1, slot 0 mirrors slot 16 and slot 17 mirrors slot 1, so
 //          rows j-1, j, j+1 are always at constant stride; column
 //          c - xbase[c] + kCPad (image-edge columns replicated into the pad)
-//   RGB : kRgbRing + 1 slots (slot 32 mirrors slot 0) x rgb_p u32
-constexpr int kYP = 512;
-constexpr int kCP = 256;
+//   RGB : kRgbRing + 1 slots (row r in slot r mod kRgbRing; the last slot mirrors slot 0) x rgb_p u32
+// Ring pitches come in two compile-time configurations (kernel template
+// parameter YP, chroma pitch YP/2): wide (512) and narrow (384, fits 4 CTAs
+// per SM for footprints up to ~370 decoded columns).
+constexpr int kYPWide = 512, kYPNarrow = 384;
 constexpr int kCPad = 8;
 constexpr int kCSlots = 18;
-constexpr int kOffY = 0;                                   // Y ring
-constexpr int kOffC = kOffY + kYRing * kYP;                // Cb ring, then Cr ring
-constexpr int kOffQ = kOffC + 2 * kCSlots * kCP;           // dequant tables (3 x 64 float)
-constexpr int kOffRgb = kOffQ + 3 * 64 * 4;                // RGB ring (size depends on the tile)
+__host__ __device__ constexpr int off_c(int yp) { return kYRing * yp; }                  // Cb ring, then Cr ring (Y ring at 0)
+__host__ __device__ constexpr int off_q(int yp) { return off_c(yp) + 2 * kCSlots * (yp / 2); }   // dequant tables (3 x 64 float)
+__host__ __device__ constexpr int off_rgb(int yp) { return off_q(yp) + 3 * 64 * 4; }     // RGB ring (size depends on the tile)
 
 struct TileLayout {
   int oy0, oy1, ox0, ox1;          // output tile
@@ -79,10 +85,11 @@ struct TileLayout {
   int r0, nsteps;                  // first rolling-step row (16-aligned) and step count
   int fits;                        // footprint fits the fixed ring pitches
   // byte offsets in dynamic shared memory
-  int off_q, off_xt, off_yt, off_y, off_c, off_rgb, total;
+  int off_q, off_xt, off_yt, off_st, off_y, off_c, off_rgb, total;
 };
 
-SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, int ox1, TileLayout& L) {
+SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, int ox1, TileLayout& L,
+                         int yp = kYPWide) {
   const int P = 8 / K;
   int a, b; float w;
   L.oy0 = oy0; L.oy1 = oy1; L.ox0 = ox0; L.ox1 = ox1;
@@ -112,17 +119,18 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.r0 = L.ly0 & ~(kStepRows - 1);
   // the last step must cover luma row ly1 and chroma row cy1 (luma 2 cy1)
   L.nsteps = ((imax(L.ly1, 2 * L.cy1) - L.r0) / kStepRows) + 1;
-  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= kYP) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= kCP);
+  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= yp) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= yp / 2);
   int off = 0;
   // fixed-size regions first, at compile-time offsets (kOff*), so the hot
   // loops address them as immediates instead of keeping base pointers live
-  L.off_y = kOffY;
-  L.off_c = kOffC;
-  L.off_q = kOffQ;
-  L.off_rgb = kOffRgb;
-  off = kOffRgb + align16(L.rgb_p * 4 * (kRgbRing + 1));
+  L.off_y = 0;
+  L.off_c = off_c(yp);
+  L.off_q = off_q(yp);
+  L.off_rgb = off_rgb(yp);
+  off = off_rgb(yp) + align16(L.rgb_p * 4 * (kRgbRing + 1));
   L.off_xt = off;  off += ((ox1 - ox0 + 4) >> 1) * 16;       // x taps per pixel pair: {4 x0 a, 4 x0 b, w a, w b}
   L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {y0 | y1<<16, w}
+  L.off_st = off;  off += align16(L.nsteps * 8);              // per-step {ready, done}
   L.total = off;
 }
 

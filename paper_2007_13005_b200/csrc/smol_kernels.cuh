@@ -451,9 +451,6 @@ __device__ __forceinline__ float byte_f(uint32_t x, int b) {
 }
 
 
-#ifndef SMOL_MIN_BLOCKS
-#define SMOL_MIN_BLOCKS 3
-#endif
 
 template <int P>
 __device__ __forceinline__ void put_row(uint8_t* d, const uint32_t (&w)[2]) {
@@ -462,6 +459,10 @@ __device__ __forceinline__ void put_row(uint8_t* d, const uint32_t (&w)[2]) {
   else if constexpr (P == 2) *reinterpret_cast<uint16_t*>(d) = (uint16_t)w[0];
   else *d = (uint8_t)w[0];
 }
+
+// RGB ring slot of decoded row r >= 0 (kRgbRing is even, so an even row's
+// odd neighbour never wraps)
+__device__ __forceinline__ int rgb_slot(int r) { return (int)((uint32_t)r % (uint32_t)kRgbRing); }
 
 __device__ __forceinline__ uint32_t lds_u32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
 
@@ -487,8 +488,8 @@ __device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
   return __shfl_sync(0xffffffffu, chunk, 0);
 }
 
-template <int K, bool F16, bool DEBUG, bool PACKED>
-__global__ void __launch_bounds__(kThreads, SMOL_MIN_BLOCKS)
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
+__global__ void __launch_bounds__(kThreads, 768 / kThreads)
 smol_fused_kernel(const KParams kp) {
   constexpr int P = 8 / K;                 // decoded samples per block side
   extern __shared__ __align__(16) uint8_t smem[];
@@ -503,17 +504,18 @@ smol_fused_kernel(const KParams kp) {
   __shared__ int ctr[2];                   // dynamic work counters (colour, output)
   if (tid == 0) {
     im = kp.imgs[n];
-    tile_layout(im, K, oy0, oy1, ox0, ox1, L);
+    tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP);
     ctr[0] = 0;
     ctr[1] = 0;
   }
   __syncthreads();
-  float* qf = reinterpret_cast<float*>(smem + kOffQ);
+  constexpr int kCP = kYP / 2;              // chroma ring pitch
+  float* qf = reinterpret_cast<float*>(smem + off_q(kYP));
   int2* xt = reinterpret_cast<int2*>(smem + L.off_xt);
   int2* yt = reinterpret_cast<int2*>(smem + L.off_yt);
-  uint8_t* yring = smem + kOffY;
-  uint8_t* cring = smem + kOffC;
-  uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + kOffRgb);
+  uint8_t* yring = smem;
+  uint8_t* cring = smem + off_c(kYP);
+  uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + off_rgb(kYP));
   constexpr int kCStride = kCSlots * kCP;  // Cr ring follows the Cb ring
   const int ntw = ox1 - ox0, nth = oy1 - oy0;
   const int rgb_p = L.rgb_p;
@@ -573,8 +575,7 @@ smol_fused_kernel(const KParams kp) {
         bcol = tt - brow * nbxc;
         brow += cb0;
       }
-      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] +
-                           (size_t)(L.bx0[c] + bcol) * BlockFmt<K, PACKED>::kElems;
+      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * BlockFmt<K, PACKED>::kElems;
       uint32_t px[8][2];
       decode_block<K, PACKED>(act, src, qf + c * 64, px);
       if (!act) continue;
@@ -607,13 +608,27 @@ smol_fused_kernel(const KParams kp) {
     }
   };
 
+  // per-step schedule, computed once: ready_s = last RGB row available after
+  // step s (monotone), done_s = output rows whose lower tap row is <= ready_s
+  // (taps are monotone: binary search)
+  int2* st = reinterpret_cast<int2*>(smem + L.off_st);
+  for (int s = tid; s < L.nsteps; s += kThreads) {
+    const int ready = max(L.ly0 - 1, ready_after(L, im.Hc, s));
+    int lo = 0, hi = nth;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)((uint32_t)yt[mid].x >> 16) <= ready) lo = mid + 1; else hi = mid;
+    }
+    st[s] = make_int2(ready, lo);
+  }
   int ready_prev = L.ly0 - 1;
   int done_prev = 0;                       // output rows of the tile finished
   idct_step(0);
   __syncthreads();
 
   for (int s = 0; s < L.nsteps; ++s) {
-    const int ready = max(ready_prev, ready_after(L, im.Hc, s));
+    const int2 sts = st[s];
+    const int ready = sts.x;
     if (tid == 0) ctr[1] = 0;
 
     if constexpr (DEBUG) {
@@ -641,13 +656,13 @@ smol_fused_kernel(const KParams kp) {
     // ---- prefetch step s+1's ROI block rows into L2 (TMA bulk prefetch) --
     // one contiguous segment per (component, block row); the IDCT of step
     // s+1 (next phase) then hits L2 instead of waiting on HBM.
-    if (s + 1 < L.nsteps && tid < 32) {
+    if (s + 1 < L.nsteps && tid >= kThreads - 32) {
       const int R = L.r0 + kStepRows * (s + 1);
       const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
       const int cb0 = max(L.by0[1], (R >> 1) / P);
       const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
       const int ny = max(0, yb1 - yb0 + 1), nc = max(0, cb1 - cb0 + 1);
-      for (int k = tid; k < ny + 2 * nc; k += 32) {
+      for (int k = lane; k < ny + 2 * nc; k += 32) {
         int c = 0, brow = yb0 + k;
         if (k >= ny) { c = 1 + (k - ny >= nc); brow = cb0 + (k - ny) - (c - 1) * nc; }
         // 16-B aligned segment [bx0 * S, (bx1 + 1) * S) of the (16-B padded) block row
@@ -710,7 +725,7 @@ smol_fused_kernel(const KParams kp) {
         const uint8_t* yr = yring + ((2 * j) & (kYRing - 1)) * kYP + (2 * i - L.xbase[0]);
         const uint32_t y0 = *reinterpret_cast<const uint32_t*>(yr);
         const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
-        const int slot = (2 * j) & (kRgbRing - 1);
+        const int slot = rgb_slot(2 * j);
         uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
 #if SMOL_OPT_YMAGIC
         const uint32_t mg = 0x4B000000u;
@@ -737,22 +752,13 @@ smol_fused_kernel(const KParams kp) {
       int16_t* dst = kp.dbg_rgb + n * kp.dbg_stride_rgb;
       for (int y = ready_prev + 1; y <= ready; ++y)
         for (int x = L.lx0 + tid; x <= L.lx1; x += kThreads) {
-          const uint32_t v = rgb[(y & (kRgbRing - 1)) * rgb_p + (x - L.rgb_x0)];
+          const uint32_t v = rgb[rgb_slot(y) * rgb_p + (x - L.rgb_x0)];
           const size_t o = ((size_t)y * im.Wd + x) * 3;
           dst[o] = v & 255; dst[o + 1] = (v >> 8) & 255; dst[o + 2] = (v >> 16) & 255;
         }
     }
 
-    // rows whose lower tap row is ready (taps are monotone): binary search
-    int done;
-    {
-      int lo = done_prev, hi = nth;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if ((int)((uint32_t)yt[mid].x >> 16) <= ready) lo = mid + 1; else hi = mid;
-      }
-      done = lo;
-    }
+    const int done = sts.y;
 
     // ---- next step's IDCT (writes only Y/chroma rings: no reader now) ----
     if (s + 1 < L.nsteps) idct_step(s + 1);
@@ -775,7 +781,7 @@ smol_fused_kernel(const KParams kp) {
         const int ox = 4 * (t - rr * nq4);
         const int2 ty = yt[r];
         const float wy = __int_as_float(ty.y);
-        const uint8_t* row0 = reinterpret_cast<const uint8_t*>(rgb) + ((ty.x & 0xffff) & (kRgbRing - 1)) * pitch4;
+        const uint8_t* row0 = reinterpret_cast<const uint8_t*>(rgb) + rgb_slot(ty.x & 0xffff) * pitch4;
         const uint8_t* row1 = row0 + pitch4;
         float y[3][4];
         const int4* xt4 = reinterpret_cast<const int4*>(xt);

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <new>
 #include <string>
@@ -209,21 +210,37 @@ int auto_tile_rows(int OH, int n_images) {
 
 using KernelFn = void (*)(const KParams);
 
-template <int K, bool PK>
+// Kernel configurations: wide = 256 threads, 512-B Y ring pitch (3 CTAs per
+// SM); narrow = 192 threads, 384-B pitch (4 CTAs per SM when the tile's smem
+// allows).  Both run 24 warps per SM at <= 80 registers.
+template <int NT> struct Cfg { static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : kYPWide; };
+
+template <int K, bool PK, int NT>
 KernelFn pick_kernel(bool f16, bool dbg) {
-  if (dbg) return f16 ? smol_fused_kernel<K, true, true, PK> : smol_fused_kernel<K, false, true, PK>;
-  return f16 ? smol_fused_kernel<K, true, false, PK> : smol_fused_kernel<K, false, false, PK>;
+  constexpr int YP = Cfg<NT>::yp;
+  if (dbg) return f16 ? smol_fused_kernel<K, true, true, PK, NT, YP> : smol_fused_kernel<K, false, true, PK, NT, YP>;
+  return f16 ? smol_fused_kernel<K, true, false, PK, NT, YP> : smol_fused_kernel<K, false, false, PK, NT, YP>;
+}
+
+template <int NT>
+KernelFn select_kernel_nt(int K, bool f16, bool dbg, bool packed) {
+  switch (K) {
+    case 1: return pick_kernel<1, false, NT>(f16, dbg);
+    case 2: return packed ? pick_kernel<2, true, NT>(f16, dbg) : pick_kernel<2, false, NT>(f16, dbg);
+    case 4: return packed ? pick_kernel<4, true, NT>(f16, dbg) : pick_kernel<4, false, NT>(f16, dbg);
+    default: return packed ? pick_kernel<8, true, NT>(f16, dbg) : pick_kernel<8, false, NT>(f16, dbg);
+  }
 }
 
 // scale 1 has no packed variant: the packed layout of scale 1 is DENSE64
-KernelFn select_kernel(int K, bool f16, bool dbg, bool packed) {
-  switch (K) {
-    case 1: return pick_kernel<1, false>(f16, dbg);
-    case 2: return packed ? pick_kernel<2, true>(f16, dbg) : pick_kernel<2, false>(f16, dbg);
-    case 4: return packed ? pick_kernel<4, true>(f16, dbg) : pick_kernel<4, false>(f16, dbg);
-    default: return packed ? pick_kernel<8, true>(f16, dbg) : pick_kernel<8, false>(f16, dbg);
-  }
+KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt) {
+  return nt == kThreadsNarrow ? select_kernel_nt<kThreadsNarrow>(K, f16, dbg, packed)
+                              : select_kernel_nt<kThreadsWide>(K, f16, dbg, packed);
 }
+
+// Largest dynamic smem per CTA that keeps `ctas` CTAs resident per SM:
+// 228 KB per SM less a 1 KB reservation per CTA, less static smem (< 512 B).
+constexpr int smem_budget(int ctas) { return (228 * 1024 - ctas * 1024) / ctas - 512; }
 
 }  // namespace
 
@@ -266,6 +283,8 @@ struct smol_preproc_plan {
   int OW = 0, OH = 0;          // 0 when the output size is image dependent (never: validated)
   int tile_rows = 0;               // 0 = automatic per batch size
   int smem_optin = 0;
+  int min_col_tiles = 1;                  // SMOL_COL_TILES=k forces >= k column tiles (A/B)
+  int nt_mode = 0;                        // SMOL_THREADS=192|256 forces the CTA size (A/B)
   DevImage* d_desc = nullptr;  // [kRing][max_images]
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
   cudaEvent_t ev[kRing] = {};
@@ -339,6 +358,8 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (params->crop_w > 0) { pl->OW = params->crop_w; pl->OH = params->crop_h; }
   else { pl->OW = params->resize_w; pl->OH = params->resize_h; }
   pl->tile_rows = params->tile_rows;
+  if (const char* e = std::getenv("SMOL_COL_TILES")) pl->min_col_tiles = std::atoi(e);
+  if (const char* e = std::getenv("SMOL_THREADS")) pl->nt_mode = std::atoi(e);
   for (int c = 0; c < 3; ++c) {
     pl->na[c] = (float)(1.0 / (255.0 * (double)params->std[c]));
     pl->nb[c] = (float)(-(double)params->mean[c] / (double)params->std[c]);
@@ -359,9 +380,10 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     // dynamic smem the device allows next to the kernel's static smem
     const bool f16 = params->out_dtype == SMOL_OUT_F16_NCHW;
     int limit = pl->smem_optin;
-    for (int dbg = 0; dbg < 2 && e == cudaSuccess; ++dbg) {
+    for (int v = 0; v < 4 && e == cudaSuccess; ++v) {
+      const int dbg = v & 1, nt = v < 2 ? kThreadsWide : kThreadsNarrow;
       cudaFuncAttributes fa;
-      KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED);
+      KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED, nt);
       e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) break;
       const int dyn = pl->smem_optin - (int)fa.sharedSizeBytes;
@@ -444,7 +466,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   // shared memory of the largest tile over the batch's distinct geometries
   // (a tile whose footprint exceeds the fixed ring pitches reports INT_MAX/2)
   auto cols_of = [&](int n_col_tiles) { return (ceil_div(pl->OW, n_col_tiles) + 3) & ~3; };  // multiple of 4
-  auto max_smem = [&](int n_col_tiles) {
+  auto max_smem = [&](int n_col_tiles, int yp) {
     const int tile_cols = cols_of(n_col_tiles);
     n_col_tiles = ceil_div(pl->OW, tile_cols);
     int m = 0;
@@ -457,23 +479,33 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
         for (int u = 0; u < n_col_tiles; ++u) {
           TileLayout L;
           tile_layout(h[i], K, t * tile_rows, imin(pl->OH, (t + 1) * tile_rows), u * tile_cols,
-                      imin(pl->OW, (u + 1) * tile_cols), L);
+                      imin(pl->OW, (u + 1) * tile_cols), L, yp);
           m = imax(m, L.fits ? L.total : (1 << 30));
         }
       prev_w = di->width; prev_h = di->height; prev_l = di->roi_left; prev_t = di->roi_top;
     }
     return m;
   };
-  // column tiles only when a full-width tile would not leave 2 CTAs per SM
+  // Narrow configuration (192 threads, 384-B ring pitch) when full-width
+  // tiles fit it with 4 CTAs per SM; otherwise wide (256 threads, 512-B
+  // pitch), adding column tiles only when a tile would not leave 2 CTAs/SM.
   int n_col_tiles = 1;
-  int smem = max_smem(1);
-  while (smem > pl->smem_optin / 2 && n_col_tiles < 64 && 8 * n_col_tiles <= pl->OW) {
-    n_col_tiles *= 2;
-    smem = max_smem(n_col_tiles);
+  int nt = kThreadsNarrow;
+  int smem = max_smem(1, kYPNarrow);
+  if (smem > smem_budget(4) || pl->nt_mode == kThreadsWide || pl->min_col_tiles > 1) {
+    nt = kThreadsWide;
+    smem = max_smem(1, kYPWide);
+    while (smem > pl->smem_optin / 2 && n_col_tiles < 64 && 8 * n_col_tiles <= pl->OW) {
+      n_col_tiles *= 2;
+      smem = max_smem(n_col_tiles, kYPWide);
+    }
+    if (pl->min_col_tiles > n_col_tiles && 8 * pl->min_col_tiles <= pl->OW) {   // A/B override
+      n_col_tiles = pl->min_col_tiles;
+      smem = max_smem(n_col_tiles, kYPWide);
+    }
   }
   if (smem > pl->smem_optin)
     return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
-
   if (staged) {
     // End-to-end path: gather each image's ROI block rows (the whole output's
     // tap footprint) from pinned host memory into a compact device staging
@@ -541,9 +573,9 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr,
-                              pl->p.layout == SMOL_LAYOUT_PACKED);
+                              pl->p.layout == SMOL_LAYOUT_PACKED, nt);
   dim3 grid(ntiles * n_col_tiles, b->n_images);
-  fn<<<grid, kThreads, smem, stream>>>(kp);
+  fn<<<grid, nt, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
   if (staged) SMOL_CUDA(cudaEventRecord(pl->stage_free[pl->stage_slot ^ 1], stream));
