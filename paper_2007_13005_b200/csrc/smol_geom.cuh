@@ -128,7 +128,7 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.off_q = off_q(yp);
   L.off_rgb = off_rgb(yp);
   off = off_rgb(yp) + align16(L.rgb_p * 4 * (kRgbRing + 1));
-  L.off_xt = off;  off += ((ox1 - ox0 + 4) >> 1) * 16;       // x taps per pixel pair: {4 x0 a, 4 x0 b, w a, w b}
+  L.off_xt = off;  off += ((ox1 - ox0 + 3) >> 2) * 32;       // x taps per pixel pair: {4 x0 a, 4 x0 b, w a, w b}
   L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {y0 | y1<<16, w}
   L.off_st = off;  off += align16(L.nsteps * 8);              // per-step {ready, done}
   L.total = off;

@@ -526,12 +526,15 @@ smol_fused_kernel(const KParams kp) {
   // (i1 == i0) its weight is zeroed so the kernel may always read i0 + 1.
   for (int i = tid; i < 3 * 64; i += kThreads)
     qf[i] = (float)kp.qtables[im.qidx[i >> 6] * 64 + (i & 63)] * 0.125f;
-  // x taps per output-pixel pair: {byte offset of x0 (a), (b), w (a), w (b)},
-  // so a pair's weights load into an adjacent register pair for FFMA2
-  for (int i = tid; i < ntw + 3; i += kThreads) {
+  // x taps per output-pixel pair {byte offset of x0 (a), (b), w (a), w (b)},
+  // so a pair's weights load into an adjacent register pair for FFMA2.
+  // Output task q (pixels 4q .. 4q+3) reads pair A at [q] and pair B at
+  // [nq4 + q]: consecutive lanes read consecutive 16-B entries.
+  const int nq4 = (ntw + 3) >> 2;
+  for (int i = tid; i < 4 * nq4; i += kThreads) {
     int i0, i1; float w;
     src_tap(im.left + ox0 + min(i, ntw - 1), im.Wd, im.Wr, i0, i1, w);
-    int* e = reinterpret_cast<int*>(xt) + (i >> 1) * 4 + (i & 1);
+    int* e = reinterpret_cast<int*>(xt) + (((i >> 1) & 1) * nq4 + (i >> 2)) * 4 + (i & 1);
     e[0] = (i0 - L.rgb_x0) * 4;
     e[2] = __float_as_int(i1 == i0 ? 0.f : w);
   }
@@ -544,7 +547,6 @@ smol_fused_kernel(const KParams kp) {
   const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
   const int ntask4 = L.rgb_w >> 2;          // 4-column colour tasks per quad row
   const FastDiv fd_t4 = make_fastdiv(ntask4);
-  const int nq4 = (ntw + 3) >> 2;
   const FastDiv fd_q4 = make_fastdiv(nq4);
   const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0);
   const size_t plane_sz = (size_t)kp.OH * kp.OW;
@@ -785,8 +787,8 @@ smol_fused_kernel(const KParams kp) {
         const uint8_t* row1 = row0 + pitch4;
         float y[3][4];
         const int4* xt4 = reinterpret_cast<const int4*>(xt);
-        const int4 txa = xt4[ox >> 1];          // taps of ox, ox+1
-        const int4 txb = xt4[(ox >> 1) + 1];    // taps of ox+2, ox+3 (padded)
+        const int4 txa = xt4[ox >> 2];          // taps of ox, ox+1
+        const int4 txb = xt4[nq4 + (ox >> 2)];  // taps of ox+2, ox+3 (padded)
         const float2 wy2 = f2(wy);
 #pragma unroll
         for (int e = 0; e < 4; e += 2) {
