@@ -37,6 +37,17 @@ UNIT = "images/s"
 L2_BYTES = 126 * 2 ** 20
 
 
+def _traffic(cfg_name: str, layout: str):
+    """ncu DRAM bytes per launch of the fused kernel for this workload, from
+    the committed capture summary (profiles/traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(f"{cfg_name}/{layout}")
+        return None if t is None else float(t["read"] + t["write"])
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -305,7 +316,7 @@ def main():
                        "coef_stats": synth.coef_stats(imgs[:min(len(imgs), 64)]),
                        "tile_rows": plan.params.tile_rows, "coef_layout": args.layout},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": _traffic(cfg.name, args.layout), "peak_source": peak_src,
                          "kernel": "smol_fused_kernel", "launch_ms": launch_ms,
                          "alg_bytes_per_launch": alg_bytes_launch},
             "e2e": {"value": e2e_value, "unit": UNIT,
