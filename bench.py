@@ -183,6 +183,77 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _eq4(args, plan, batches, reps, out, stream, nloc, t_pre):
+    """Eq. 4 beside the measurement: T_exec of ResNet-50
+    on this GPU (torchvision architecture, random init: no weights offline;
+    fp16, channels_last, CUDA graph, the same batch), the measured pipelined
+    throughput (preprocessing of batch k+1 on one stream overlapping the DNN
+    on batch k on another, double-buffered), and the predictions of min()
+    (Eq. 4), sum and exec-only with their errors."""
+    import torch
+    import torchvision
+    from paper_2007_13005_b200 import throughput as tpm
+    torch.backends.cudnn.benchmark = True
+    model = torchvision.models.resnet50(weights=None).cuda().eval().half().to(memory_format=torch.channels_last)
+    bufs = [out, torch.empty_like(out)]
+    xs = [torch.empty(out.shape, device="cuda", dtype=torch.half).to(memory_format=torch.channels_last)
+          for _ in range(2)]
+    side = torch.cuda.Stream()
+    graphs = []
+    with torch.inference_mode():
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                model(xs[0].copy_(bufs[0]))
+        torch.cuda.current_stream().wait_stream(side)
+        for i in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                model(xs[i].copy_(bufs[i]))        # dtype/layout conversion is part of the DNN step
+            graphs.append(g)
+    torch.cuda.synchronize()
+    k_exec = 20
+    dnn = torch.cuda.Stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(dnn):
+        for k in range(3):
+            graphs[k % 2].replay()
+        e0.record(dnn)
+        for k in range(k_exec):
+            graphs[k % 2].replay()
+        e1.record(dnn)
+    torch.cuda.synchronize()
+    t_exec = nloc * k_exec / (e0.elapsed_time(e1) / 1e3)
+    # pipelined: preprocessing (stream `stream`) -> DNN (stream `dnn`), two buffers
+    k_pipe = 20
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    for f in free:
+        f.record(dnn)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    p0.record(stream)
+    for k in range(k_pipe):
+        b = k % 2
+        stream.wait_event(free[b])
+        plan.run(batches[k % reps], out=bufs[b], stream=stream)
+        ready[b].record(stream)
+        dnn.wait_event(ready[b])
+        with torch.cuda.stream(dnn):
+            graphs[b].replay()
+        free[b].record(dnn)
+    stream.wait_stream(dnn)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    t_pipe = nloc * k_pipe / (p0.elapsed_time(p1) / 1e3)
+    return {"t_preproc": t_pre, "t_exec": t_exec, "pipelined_measured": t_pipe,
+            "dnn": f"ResNet-50 (torchvision architecture, random init), fp16 channels_last, CUDA graph, "
+                   f"batch {nloc}, incl. the NCHW->fp16 channels_last conversion of the preprocessed batch",
+            "models": tpm.model_errors(t_pipe, t_pre, [t_exec]),
+            "note": "Eq. 4 min() assumes the two stages run on disjoint resources (the paper's CPU "
+                    "preprocessing + GPU DNN); here both share one B200, where the sum model applies"}
+
+
 def _workload_name(cfg):
     out = "x".join(str(v) for v in (3,) + cfg.out_hw)
     return (f"{cfg.name}: {cfg.n} x {cfg.width}x{cfg.height} 4:2:0 JPEG coefficients (q{cfg.quality}), "
@@ -204,6 +275,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--tile-rows", type=int, default=0)
+    ap.add_argument("--eq4", action="store_true",
+                    help="also measure ResNet-50 on this GPU and pipelined preprocessing+DNN (Eq. 4 report)")
     ap.add_argument("--layout", default="dense", choices=["dense", "packed"],
                     help="coefficient block layout (packed: only the coefficients the scale uses)")
     args = ap.parse_args()
@@ -330,6 +403,11 @@ def main():
         c = clk.summary()
         if c:
             line["clocks"] = c
+        if args.eq4 and world == 1:
+            try:
+                line["eq4"] = _eq4(args, plan, batches, reps, out, stream, nloc, value)
+            except Exception as e:  # noqa: BLE001
+                line["eq4"] = {"error": repr(e)}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = _cpu_baseline(cfg, imgs[:64], qt, args.cpu_budget, 16 * cfg.n)

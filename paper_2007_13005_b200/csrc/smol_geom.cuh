@@ -13,10 +13,12 @@
 
 namespace smol {
 
-// Threads per CTA: the kernel is instantiated for 256 (3 CTAs per SM) and
-// 192 (4 CTAs per SM, used when the tile's shared memory allows 4); both
-// keep 24 warps per SM at <= 80 registers per thread.
-constexpr int kThreadsWide = 256, kThreadsNarrow = 192;
+// Threads per CTA: the kernel is instantiated for 256 (3 CTAs per SM), 192
+// (4 CTAs per SM, used when the tile's shared memory allows 4) and 128 (6
+// CTAs per SM, small footprints: thumbnails, reduced-scale decodes, where a
+// CTA's serial prologue/barrier latency dominates and more CTAs per SM hide
+// it); all keep 24 warps per SM at <= 80 registers per thread.
+constexpr int kThreadsWide = 256, kThreadsNarrow = 192, kThreadsTiny = 128;
 constexpr int kStepRows = 16;             // decoded luma rows per rolling step (one MCU row at scale 1)
 constexpr int kYRing = 32;                // luma rows kept in smem (two steps)
 constexpr int kCRing = 16;                // chroma rows kept per component (two steps)
@@ -48,10 +50,18 @@ struct __align__(16) DevImage {
 SMOL_HD void src_tap(int d, int in, int out, int& i0, int& i1, float& w) {
   long long num = (long long)(2 * d + 1) * in - out;
   if (num < 0) num = 0;
-  long long den = 2LL * out;
-  long long q = num / den;
-  i0 = (int)q;
-  w = (float)(num - q * den) / (float)den;   // both exact in fp32 (< 2^24)
+  const long long den = 2LL * out;
+  if (num < (1LL << 32)) {
+    // 32-bit unsigned division (the common case; the 64-bit one is a long
+    // software routine on the GPU)
+    const uint32_t n32 = (uint32_t)num, d32 = (uint32_t)den, q32 = n32 / d32;
+    i0 = (int)q32;
+    w = (float)(n32 - q32 * d32) / (float)d32;   // both exact in fp32 (< 2^24)
+  } else {
+    const long long q = num / den;
+    i0 = (int)q;
+    w = (float)(num - q * den) / (float)den;
+  }
   if (i0 > in - 1) i0 = in - 1;
   i1 = imin(i0 + 1, in - 1);
 }
@@ -66,9 +76,16 @@ SMOL_HD int align16(int x) { return (x + 15) & ~15; }
 //          c - xbase[c] + kCPad (image-edge columns replicated into the pad)
 //   RGB : kRgbRing + 1 slots (row r in slot r mod kRgbRing; the last slot mirrors slot 0) x rgb_p u32
 // Ring pitches come in two compile-time configurations (kernel template
-// parameter YP, chroma pitch YP/2): wide (512) and narrow (384, fits 4 CTAs
-// per SM for footprints up to ~370 decoded columns).
-constexpr int kYPWide = 512, kYPNarrow = 384;
+// parameter YP, chroma pitch YP/2): wide (512), narrow (384, fits 4 CTAs
+// per SM for footprints up to ~370 decoded columns) and tiny (128, footprints
+// up to ~110 decoded columns).
+constexpr int kYPWide = 512, kYPNarrow = 384, kYPTiny = 128;
+// RGB ring pitch (u32): yp - kRgbPitchPad, which is 4 (mod 32) so that rows
+// r and r+1 start in different shared-memory banks
+#ifndef SMOL_RGB_PITCH_PAD
+#define SMOL_RGB_PITCH_PAD 28
+#endif
+__host__ __device__ constexpr int rgb_pitch(int yp) { return yp - SMOL_RGB_PITCH_PAD; }
 constexpr int kCPad = 8;
 constexpr int kCSlots = 18;
 __host__ __device__ constexpr int off_c(int yp) { return kYRing * yp; }                  // Cb ring, then Cr ring (Y ring at 0)
@@ -81,7 +98,7 @@ struct TileLayout {
   int cy0, cy1, cx0, cx1;          // chroma footprint incl. triangle neighbours (R2)
   int by0[3], by1[3], bx0[3], bx1[3];   // ROI block ranges per component
   int xbase[3];                    // decoded column of ring column 0 (= bx0 * P)
-  int rgb_x0, rgb_w, rgb_p;        // RGB ring: first column, width, pitch (u32; multiples of 4)
+  int rgb_x0, rgb_w, rgb_p;        // RGB ring: first column, width, pitch (u32; rgb_pitch(yp), compile-time in the kernel)
   int r0, nsteps;                  // first rolling-step row (16-aligned) and step count
   int fits;                        // footprint fits the fixed ring pitches
   // byte offsets in dynamic shared memory
@@ -115,11 +132,12 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   for (int c = 0; c < 3; ++c) L.xbase[c] = L.bx0[c] * P;
   L.rgb_x0 = L.lx0 & ~3;
   L.rgb_w = ((L.lx1 | 3) - L.rgb_x0 + 1);
-  L.rgb_p = L.rgb_w + 4;
+  L.rgb_p = rgb_pitch(yp);         // fixed pitch (u32): row r+1 is an immediate offset from row r
   L.r0 = L.ly0 & ~(kStepRows - 1);
   // the last step must cover luma row ly1 and chroma row cy1 (luma 2 cy1)
   L.nsteps = ((imax(L.ly1, 2 * L.cy1) - L.r0) / kStepRows) + 1;
-  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= yp) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= yp / 2);
+  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= yp) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= yp / 2) &&
+           (L.rgb_w + 4 <= L.rgb_p);
   int off = 0;
   // fixed-size regions first, at compile-time offsets (kOff*), so the hot
   // loops address them as immediates instead of keeping base pointers live
@@ -129,7 +147,7 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.off_rgb = off_rgb(yp);
   off = off_rgb(yp) + align16(L.rgb_p * 4 * (kRgbRing + 1));
   L.off_xt = off;  off += ((ox1 - ox0 + 3) >> 2) * 32;       // x taps per pixel pair: {4 x0 a, 4 x0 b, w a, w b}
-  L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {y0 | y1<<16, w}
+  L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {ring byte offset of row y0 | y1<<16, w}
   L.off_st = off;  off += align16(L.nsteps * 8);              // per-step {ready, done}
   L.total = off;
 }

@@ -18,6 +18,7 @@
 #pragma once
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <type_traits>
 
 #include "smol_geom.cuh"
 
@@ -53,6 +54,7 @@ struct Basis {
   float a2[2][8];
   float a4[8];
   float kR, kB, cR, cB;
+  uint32_t gK1, gCb, gCr;          // G = Y + (gK1 + gCb cb16 + gCr cr16) / 2e6 - 136 (mod 2^32; see colour())
   float2 tp[4][4];   // column pass pairs: tp[k][y] = (t[2k][y], t[2k+1][y])
 };
 
@@ -402,8 +404,10 @@ __device__ __forceinline__ uint2 colour2m(uint32_t m0, uint32_t m1, int cb0, int
                                __fadd2_rn(yf, make_float2(c_basis.cR, c_basis.cR)));
   const float2 tb = __ffma2_rn(make_float2((float)cb0, (float)cb1), make_float2(c_basis.kB, c_basis.kB),
                                __fadd2_rn(yf, make_float2(c_basis.cB, c_basis.cB)));
-  const uint32_t u0 = 543917632u - 43017u * (uint32_t)cb0 - 89267u * (uint32_t)cr0;
-  const uint32_t u1 = 543917632u - 43017u * (uint32_t)cb1 - 89267u * (uint32_t)cr1;
+  // constants from the constant bank (IMAD c[][] operand): as immediates the
+  // compiler re-materialises them with a MOV per use under register pressure
+  const uint32_t u0 = c_basis.gK1 + c_basis.gCb * (uint32_t)cb0 + c_basis.gCr * (uint32_t)cr0;
+  const uint32_t u1 = c_basis.gK1 + c_basis.gCb * (uint32_t)cb1 + c_basis.gCr * (uint32_t)cr1;
   const uint32_t G0 = (uint32_t)min(max((int)(m0 + u0 / 2000000u - (0x4B000000u + 136u)), 0), 255);
   const uint32_t G1 = (uint32_t)min(max((int)(m1 + u1 / 2000000u - (0x4B000000u + 136u)), 0), 255);
   return make_uint2(__byte_perm(__byte_perm(floor_u8(tr.x), G0, 0x0040), floor_u8(tb.x), 0x5410),
@@ -518,8 +522,8 @@ smol_fused_kernel(const KParams kp) {
   uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + off_rgb(kYP));
   constexpr int kCStride = kCSlots * kCP;  // Cr ring follows the Cb ring
   const int ntw = ox1 - ox0, nth = oy1 - oy0;
-  const int rgb_p = L.rgb_p;
-  const int pitch4 = rgb_p * 4;             // RGB ring row pitch in bytes
+  constexpr int rgb_p = rgb_pitch(kYP);     // RGB ring row pitch (u32), = L.rgb_p
+  constexpr int pitch4 = rgb_p * 4;         // in bytes
 
   // ---- prologue: dequant tables (Q/8, exact) and bilinear taps ----------
   // Taps use exact-integer coordinates (R9).  Where the upper tap is clamped
@@ -538,10 +542,12 @@ smol_fused_kernel(const KParams kp) {
     e[0] = (i0 - L.rgb_x0) * 4;
     e[2] = __float_as_int(i1 == i0 ? 0.f : w);
   }
+  // y taps per output row: {byte offset of RGB ring row i0 | i1 << 16, w}
+  // (row i0 + 1 is at +pitch4: the ring's guard slot mirrors slot 0)
   for (int i = tid; i < nth; i += kThreads) {
     int i0, i1; float w;
     src_tap(im.top + oy0 + i, im.Hd, im.Hr, i0, i1, w);
-    yt[i] = make_int2(i0 | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
+    yt[i] = make_int2((rgb_slot(i0) * pitch4) | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
   }
   const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
   const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
@@ -549,7 +555,9 @@ smol_fused_kernel(const KParams kp) {
   const FastDiv fd_t4 = make_fastdiv(ntask4);
   const FastDiv fd_q4 = make_fastdiv(nq4);
   const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0);
-  const size_t plane_sz = (size_t)kp.OH * kp.OW;
+  const uint32_t plane_sz = (uint32_t)kp.OH * kp.OW;   // < 2^31 elements (host-checked)
+  using OutT = typename std::conditional<F16, __half, float>::type;
+  OutT* const outb = reinterpret_cast<OutT*>(kp.out) + ((size_t)n * 3 * kp.OH + oy0) * kp.OW + ox0;
   __syncthreads();
 
   // ---- IDCT of one rolling step's ROI blocks (static: thread per block) --
@@ -561,6 +569,9 @@ smol_fused_kernel(const KParams kp) {
     const int ny = max(0, yb1 - yb0 + 1) * nbx0;
     const int nc = max(0, cb1 - cb0 + 1) * nbxc;
     const int ntask = ny + 2 * nc;
+    // scale 1/8: one DC load per block; unrolled so several loads are in
+    // flight per thread
+#pragma unroll(K == 8 ? 4 : 1)
     for (int base = tid & ~31; base < ntask; base += kThreads) {
       const int t = base + lane;
       const bool act = t < ntask;
@@ -658,7 +669,9 @@ smol_fused_kernel(const KParams kp) {
     // ---- prefetch step s+1's ROI block rows into L2 (TMA bulk prefetch) --
     // one contiguous segment per (component, block row); the IDCT of step
     // s+1 (next phase) then hits L2 instead of waiting on HBM.
-    if (s + 1 < L.nsteps && tid >= kThreads - 32) {
+    // (not for dense blocks at scale 1/8: only the DC's 32-B sector is read
+    // there, and a row prefetch would pull all 128 B of every block)
+    if ((K != 8 || PACKED) && s + 1 < L.nsteps && tid >= kThreads - 32) {
       const int R = L.r0 + kStepRows * (s + 1);
       const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
       const int cb0 = max(L.by0[1], (R >> 1) / P);
@@ -783,7 +796,7 @@ smol_fused_kernel(const KParams kp) {
         const int ox = 4 * (t - rr * nq4);
         const int2 ty = yt[r];
         const float wy = __int_as_float(ty.y);
-        const uint8_t* row0 = reinterpret_cast<const uint8_t*>(rgb) + rgb_slot(ty.x & 0xffff) * pitch4;
+        const uint8_t* row0 = reinterpret_cast<const uint8_t*>(rgb) + (ty.x & 0xffff);
         const uint8_t* row1 = row0 + pitch4;
         float y[3][4];
         const int4* xt4 = reinterpret_cast<const int4*>(xt);
@@ -815,7 +828,7 @@ smol_fused_kernel(const KParams kp) {
             y[ch][e + 1] = yn.y;
           }
         }
-        const size_t o = ((size_t)n * 3 * kp.OH + (oy0 + r)) * kp.OW + (ox0 + ox);
+        OutT* const ot = outb + (uint32_t)(r * kp.OW + ox);
         if (vec4 && ox + 4 <= ntw) {
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
@@ -825,9 +838,9 @@ smol_fused_kernel(const KParams kp) {
               uint2 v;
               v.x = *reinterpret_cast<const uint32_t*>(&h0);
               v.y = *reinterpret_cast<const uint32_t*>(&h1);
-              __stcs(reinterpret_cast<uint2*>(reinterpret_cast<__half*>(kp.out) + o + ch * plane_sz), v);
+              __stcs(reinterpret_cast<uint2*>(ot + ch * plane_sz), v);
             } else {
-              __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(kp.out) + o + ch * plane_sz),
+              __stcs(reinterpret_cast<float4*>(ot + ch * plane_sz),
                      make_float4(y[ch][0], y[ch][1], y[ch][2], y[ch][3]));
             }
           }
@@ -837,8 +850,8 @@ smol_fused_kernel(const KParams kp) {
             if (ox + e >= ntw) break;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-              if constexpr (F16) reinterpret_cast<__half*>(kp.out)[o + e + ch * plane_sz] = __float2half_rn(y[ch][e]);
-              else reinterpret_cast<float*>(kp.out)[o + e + ch * plane_sz] = y[ch][e];
+              if constexpr (F16) ot[e + ch * plane_sz] = __float2half_rn(y[ch][e]);
+              else ot[e + ch * plane_sz] = y[ch][e];
             }
           }
         }

@@ -76,6 +76,9 @@ void init_basis(Basis& b) {
   b.kB = (float)(1.772 / 16.0);
   b.cR = (float)(0.5 - 2048.0 * 1.402 / 16.0);
   b.cB = (float)(0.5 - 2048.0 * 1.772 / 16.0 + 1.0 / 8192.0);
+  b.gK1 = 543917632u;
+  b.gCb = (uint32_t)-43017;
+  b.gCr = (uint32_t)-89267;
 }
 
 std::mutex g_basis_mu;
@@ -213,7 +216,9 @@ using KernelFn = void (*)(const KParams);
 // Kernel configurations: wide = 256 threads, 512-B Y ring pitch (3 CTAs per
 // SM); narrow = 192 threads, 384-B pitch (4 CTAs per SM when the tile's smem
 // allows).  Both run 24 warps per SM at <= 80 registers.
-template <int NT> struct Cfg { static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : kYPWide; };
+template <int NT> struct Cfg {
+  static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
+};
 
 template <int K, bool PK, int NT>
 KernelFn pick_kernel(bool f16, bool dbg) {
@@ -235,6 +240,7 @@ KernelFn select_kernel_nt(int K, bool f16, bool dbg, bool packed) {
 // scale 1 has no packed variant: the packed layout of scale 1 is DENSE64
 KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt) {
   return nt == kThreadsNarrow ? select_kernel_nt<kThreadsNarrow>(K, f16, dbg, packed)
+       : nt == kThreadsTiny   ? select_kernel_nt<kThreadsTiny>(K, f16, dbg, packed)
                               : select_kernel_nt<kThreadsWide>(K, f16, dbg, packed);
 }
 
@@ -350,6 +356,12 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   SMOL_CUDA(cudaGetDevice(&dev));
   rc = ensure_basis(dev);
   if (rc) return rc;
+  {
+    const long long ow = params->crop_w > 0 ? params->crop_w : params->resize_w;
+    const long long oh = params->crop_w > 0 ? params->crop_h : params->resize_h;
+    if (ow > 65535 || oh > 65535 || 3 * ow * oh >= (1LL << 31))
+      return fail(SMOL_ERR_INVALID, "output %lldx%lld too large (3*H*W must be < 2^31 elements)", ow, oh);
+  }
   smol_preproc_plan_t* pl = new (std::nothrow) smol_preproc_plan_t();
   if (!pl) return fail(SMOL_ERR_NOMEM, "plan allocation");
   pl->p = *params;
@@ -380,8 +392,8 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     // dynamic smem the device allows next to the kernel's static smem
     const bool f16 = params->out_dtype == SMOL_OUT_F16_NCHW;
     int limit = pl->smem_optin;
-    for (int v = 0; v < 4 && e == cudaSuccess; ++v) {
-      const int dbg = v & 1, nt = v < 2 ? kThreadsWide : kThreadsNarrow;
+    for (int v = 0; v < 6 && e == cudaSuccess; ++v) {
+      const int dbg = v & 1, nt = v < 2 ? kThreadsWide : v < 4 ? kThreadsNarrow : kThreadsTiny;
       cudaFuncAttributes fa;
       KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED, nt);
       e = cudaFuncGetAttributes(&fa, fn);
@@ -490,8 +502,12 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   // tiles fit it with 4 CTAs per SM; otherwise wide (256 threads, 512-B
   // pitch), adding column tiles only when a tile would not leave 2 CTAs/SM.
   int n_col_tiles = 1;
-  int nt = kThreadsNarrow;
-  int smem = max_smem(1, kYPNarrow);
+  int nt = kThreadsTiny;
+  int smem = max_smem(1, kYPTiny);
+  if (smem > smem_budget(6) || (pl->nt_mode != 0 && pl->nt_mode != kThreadsTiny) || pl->min_col_tiles > 1) {
+    nt = kThreadsNarrow;
+    smem = max_smem(1, kYPNarrow);
+  }
   if (smem > smem_budget(4) || pl->nt_mode == kThreadsWide || pl->min_col_tiles > 1) {
     nt = kThreadsWide;
     smem = max_smem(1, kYPWide);
