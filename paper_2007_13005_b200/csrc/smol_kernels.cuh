@@ -35,11 +35,19 @@
 #ifndef SMOL_OUT_PER_GRAB
 #define SMOL_OUT_PER_GRAB 1      // output tasks per lane per work-counter grab
 #endif
+#ifndef SMOL_OUT_UNROLL
+#define SMOL_OUT_UNROLL 1        // output tasks of one grab interleaved by the compiler
+#endif
+#ifndef SMOL_COL_UNROLL
+#define SMOL_COL_UNROLL 1
+#endif
 #ifndef SMOL_OPT_YMAGIC
 #define SMOL_OPT_YMAGIC 1
 #endif
 
 namespace smol {
+
+constexpr int kOutUnroll = SMOL_OUT_UNROLL, kColUnroll = SMOL_COL_UNROLL;   // (#pragma unroll does not expand macros)
 
 // Basis constants, computed on the host in double from their definitions
 // (smol_preproc.cu: init_basis) and uploaded once per device.
@@ -700,6 +708,7 @@ smol_fused_kernel(const KParams kp) {
 #if SMOL_OPT_COLSTATIC
       // colour tasks all cost the same and nothing else runs in this phase:
       // a static round-robin needs no work counter
+#pragma unroll(kColUnroll)
       for (int t = tid; t < ntaskc; t += kThreads) {
 #else
       for (;;) {
@@ -787,10 +796,18 @@ smol_fused_kernel(const KParams kp) {
       for (;;) {
         const int chunk = grab_chunk(&ctr[1], lane, 32 * SMOL_OUT_PER_GRAB);
         if (chunk >= ntasko) break;
-#pragma unroll 1
+#pragma unroll(kOutUnroll)
        for (int h = 0; h < SMOL_OUT_PER_GRAB; ++h) {
-        const int t = chunk + 32 * h + lane;
-        if (t >= ntasko) break;
+        const int t0 = chunk + 32 * h + lane;
+#if SMOL_OUT_UNROLL > 1
+        // predicated (no break) so the compiler can interleave unrolled tasks
+        const bool live = t0 < ntasko;
+        const int t = live ? t0 : ntasko - 1;
+#else
+        if (t0 >= ntasko) break;
+        const bool live = true;
+        const int t = t0;
+#endif
         const int rr = (int)fdiv((uint32_t)t, fd_q4);
         const int r = done_prev + rr;
         const int ox = 4 * (t - rr * nq4);
@@ -829,7 +846,8 @@ smol_fused_kernel(const KParams kp) {
           }
         }
         OutT* const ot = outb + (uint32_t)(r * kp.OW + ox);
-        if (vec4 && ox + 4 <= ntw) {
+        if (!live) {
+        } else if (vec4 && ox + 4 <= ntw) {
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
             if constexpr (F16) {

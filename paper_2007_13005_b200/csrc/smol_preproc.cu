@@ -202,20 +202,28 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
   return SMOL_OK;
 }
 
-// Tiles per image: enough CTAs for ~6 resident per SM across the batch
-// (148 SMs; hardware scheduling balances the tail), each tile at least 8
-// output rows.
-int auto_tile_rows(int OH, int n_images) {
-  const int want = ceil_div(148 * 6, n_images > 0 ? n_images : 1);
-  const int ntiles = imax(1, imin(want, ceil_div(OH, 8)));
-  return ceil_div(OH, ntiles);
+// Tiles per image t: every extra row tile re-decodes the MCU rows its
+// footprint shares with a neighbour (~10 % more decode work per tile), while
+// n*t CTAs run in ceil(n*t / slots) waves of the resident CTA slots.  Pick the
+// t in 1..8 minimising  waves(t) / t * (1 + 0.1 (t - 1))  (relative time).
+// Measured (profiles/r01c_tile_sweep.md): c2 t=2, c3a t=2, c3b t=3, c5 t=2,
+// c4 t=1 are each the fastest of the heights swept.
+int auto_tile_rows(int OH, int n_images, int slots) {
+  const int n = n_images > 0 ? n_images : 1;
+  int best_t = 1;
+  double best = 1e30;
+  for (int t = 1; t <= imin(8, ceil_div(OH, 8)); ++t) {
+    const long long waves = ((long long)n * t + slots - 1) / slots;
+    const double cost = (double)waves / t * (1.0 + 0.1 * (t - 1));
+    if (cost < best - 1e-9) { best = cost; best_t = t; }
+  }
+  return ceil_div(OH, best_t);
 }
 
 using KernelFn = void (*)(const KParams);
 
-// Kernel configurations: wide = 256 threads, 512-B Y ring pitch (3 CTAs per
-// SM); narrow = 192 threads, 384-B pitch (4 CTAs per SM when the tile's smem
-// allows).  Both run 24 warps per SM at <= 80 registers.
+int Cfg_yp(int nt) { return nt == kThreadsNarrow ? kYPNarrow : nt == kThreadsTiny ? kYPTiny : kYPWide; }
+
 template <int NT> struct Cfg {
   static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
 };
@@ -289,6 +297,7 @@ struct smol_preproc_plan {
   int OW = 0, OH = 0;          // 0 when the output size is image dependent (never: validated)
   int tile_rows = 0;               // 0 = automatic per batch size
   int smem_optin = 0;
+  int num_sms = 148;
   int min_col_tiles = 1;                  // SMOL_COL_TILES=k forces >= k column tiles (A/B)
   int nt_mode = 0;                        // SMOL_THREADS=192|256 forces the CTA size (A/B)
   DevImage* d_desc = nullptr;  // [kRing][max_images]
@@ -377,6 +386,7 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     pl->nb[c] = (float)(-(double)params->mean[c] / (double)params->std[c]);
   }
   cudaError_t e = cudaDeviceGetAttribute(&pl->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   for (int i = 0; i < kRing && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
@@ -468,8 +478,10 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   DevImage* d = pl->d_desc + (size_t)slot * pl->max_images;
 
   // validate + build descriptors; shared memory = max over distinct geometries
-  const int tile_rows = pl->tile_rows > 0 ? imin(pl->tile_rows, pl->OH) : auto_tile_rows(pl->OH, b->n_images);
-  const int ntiles = ceil_div(pl->OH, tile_rows);
+  // provisional tile height (4 CTAs per SM); final once the CTA size is known
+  const bool auto_rows = pl->tile_rows <= 0;
+  int tile_rows = auto_rows ? auto_tile_rows(pl->OH, b->n_images, pl->num_sms * 4) : imin(pl->tile_rows, pl->OH);
+  int ntiles = ceil_div(pl->OH, tile_rows);
   // validate every descriptor once
   for (int i = 0; i < b->n_images; ++i) {
     int32_t rc = validate_image(&pl->p, &b->images[i], i, b->n_qtables, h[i]);
@@ -518,6 +530,14 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
     if (pl->min_col_tiles > n_col_tiles && 8 * pl->min_col_tiles <= pl->OW) {   // A/B override
       n_col_tiles = pl->min_col_tiles;
       smem = max_smem(n_col_tiles, kYPWide);
+    }
+  }
+  if (auto_rows && n_col_tiles == 1) {
+    const int tr = auto_tile_rows(pl->OH, b->n_images, pl->num_sms * (768 / nt));
+    if (tr != tile_rows) {
+      tile_rows = tr;
+      ntiles = ceil_div(pl->OH, tile_rows);
+      smem = max_smem(1, Cfg_yp(nt));
     }
   }
   if (smem > pl->smem_optin)
