@@ -238,6 +238,27 @@ def test_tile_rows_invariance(tile_rows):
     assert torch.equal(ref, out)
 
 
+@pytest.mark.parametrize("name", ["c1", "c3b", "c4"])
+def test_cta_config_invariance(name, monkeypatch):
+    # the same batch through the tiny (128 threads), narrow (192) and wide
+    # (256) kernel configurations: bit-identical outputs, and the tiny one
+    # (chosen automatically for these footprints) matches the oracle
+    cfg = synth.CONFIGS[name]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=3)
+    ps, po = _cfg_params(cfg)
+    outs = {}
+    for nt in ("128", "192", "256"):
+        monkeypatch.setenv("SMOL_THREADS", nt)
+        plan = smol.Plan(ps, len(imgs))
+        outs[nt] = plan.run(smol.CoefBatch(imgs, qt))
+        torch.cuda.synchronize()
+        plan.close()
+    assert torch.equal(outs["128"], outs["192"])
+    assert torch.equal(outs["128"], outs["256"])
+    monkeypatch.delenv("SMOL_THREADS")
+    _check(cfg, imgs, qt, ps, po)
+
+
 def test_run_host_pinned_equals_device():
     cfg = synth.CONFIGS["c2"]
     imgs, qt = synth.distinct_images(cfg, n_distinct=4)
