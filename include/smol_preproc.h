@@ -142,6 +142,73 @@ int32_t smol_preproc_run(smol_preproc_plan_t* plan, const smol_batch_desc* batch
 int32_t smol_preproc_run_host(smol_preproc_plan_t* plan, const smol_batch_desc* batch,
                               void* out, void* stream);
 
+/* ---- Compact coefficient transport (§6.4
+ * Huffman decoding stays on the host, so what crosses PCIe is
+ * the entropy decoder's output; P:959-968 / P:1790-1796: pinned buffers
+ * allocated once and reused).  A Huffman decoder produces each block as a
+ * short list of nonzero coefficients; shipping 64 int16 per block instead
+ * makes PCIe the end-to-end bound.  A compact record holds, for one image and
+ * one plan, only the ROI blocks (the tap footprint of the whole output, the
+ * same ranges smol_debug_geometry reports) and, per block, only the nonzero
+ * coefficients among those the plan's scale uses (reading R1):
+ *
+ *   offset 0   header, 64 B: uint32 magic 0x31434D53 ("SMC1"), uint32 E
+ *              (elements per block of the plan's layout), uint32 n_values,
+ *              uint32 0, int32 bx0[3], by0[3], nbx[3], nby[3] (ROI block
+ *              ranges per component Y, Cb, Cr)
+ *   64         uint64 bitmap[nblocks]: per ROI block (component-major, then
+ *              block-raster), bit e set <=> element e of the layout block is
+ *              nonzero
+ *   ..         uint32 row_start[nrows]: per ROI block row (component-major),
+ *              index of the row's first value in values[]
+ *   align 16   int16 values[n_values]: the nonzero elements, in block order
+ *              and ascending element index within a block
+ *   +2, align 16  (end: >= 2 zero bytes after the values; record size is a
+ *              multiple of 16)
+ *
+ * Everything outside the ROI and every element the scale does not use
+ * (reading R1: u or v = 4 at 1/2, u or v in {2,4,6} at 1/4, AC at 1/8;
+ * PACKED padding) is dropped, which leaves the output bit-identical to
+ * smol_preproc_run on the dense planes. */
+typedef struct {
+  int32_t width, height;           /* SOF size in pixels, > 0                        */
+  int32_t subsampling;             /* 420                                            */
+  int32_t qtable[3];               /* Y, Cb, Cr index into batch qtables             */
+  int32_t roi_left, roi_top;       /* as smol_image_desc (-1,-1 = centre crop)       */
+  int64_t offset;                  /* byte offset of the image's record in `arena`,
+                                      multiple of 16                                 */
+} smol_compact_image;
+
+typedef struct {
+  int32_t n_images;                /* 0 is allowed (no-op)                           */
+  const smol_compact_image* images;/* HOST array of n_images                          */
+  const void* arena;               /* records: pinned HOST (cudaMallocHost /
+                                      cudaHostRegister) or DEVICE memory, 16-B aligned */
+  int64_t arena_bytes;             /* every record lies inside [0, arena_bytes)      */
+  const uint16_t* qtables;         /* DEVICE [n_qtables][64] natural order           */
+  int32_t n_qtables;               /* 1..4                                            */
+} smol_compact_batch;
+
+/* Host only (no CUDA call): encode one image into a compact record for plans
+ * with `params`.  image->coef[] are HOST planes in the params' layout (the
+ * smol_image_desc rules apply; 16-B alignment is not required here).  With
+ * dst == NULL only *written = record size is returned; otherwise the record is
+ * written to dst (capacity bytes; SMOL_ERR_CAPACITY if too small) and
+ * *written = its size. */
+int32_t smol_compact_encode(const smol_preproc_params* params, const smol_image_desc* image,
+                            void* dst, int64_t capacity, int64_t* written);
+
+/* End-to-end run from compact records.  The byte range of the arena the batch
+ * uses is copied host->device in one DMA on the plan's copy stream (skipped
+ * when the arena is DEVICE memory); then, on `stream`, an expand kernel
+ * rebuilds the ROI blocks of the plan's layout in plan-owned staging and the
+ * fused kernel runs (double-buffered: the next call's DMA overlaps this
+ * call's expand + fused kernel).  Each record's header must match the ROI ranges
+ * the plan computes for its image (SMOL_ERR_INVALID otherwise).  Staging is
+ * allocated on first use and grown for a larger batch.  out: DEVICE. */
+int32_t smol_preproc_run_compact(smol_preproc_plan_t* plan, const smol_compact_batch* batch,
+                                 void* out, void* stream);
+
 void smol_preproc_destroy(smol_preproc_plan_t* plan);
 
 /* Output tensor shape (C=3, OH, OW) of the plan. */

@@ -15,13 +15,15 @@ from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._native import (BatchDesc, Geometry, ImageDesc, Params, SmolError, build, check, lib,
+from ._native import (BatchDesc, CompactBatchDesc, CompactImage, Geometry, ImageDesc, Params,
+                      SmolError, build, check, lib,
                       SMOL_OUT_F16_NCHW, SMOL_OUT_F32_NCHW, SMOL_RESIZE_EXACT,
                       SMOL_RESIZE_SHORT_SIDE, SMOL_LAYOUT_DENSE64, SMOL_LAYOUT_PACKED, EXPORTS,
                       LIB_PATH)
 from .layout import block_elems, pack_plane
 
-__all__ = ["make_params", "params_from_config", "geometry", "CoefBatch", "Plan", "SmolError",
+__all__ = ["make_params", "params_from_config", "geometry", "CoefBatch", "CompactBatch",
+           "compact_encode", "Plan", "SmolError",
            "build", "lib", "EXPORTS", "LIB_PATH"]
 
 IMAGENET_MEAN = (0.485, 0.456, 0.406)
@@ -145,6 +147,81 @@ class CoefBatch:
         self.desc.n_qtables = int(qtables.shape[0])
 
 
+def compact_encode(params: Params, im, roi=None) -> np.ndarray:
+    """One image's compact record (smol_compact_encode, host only) as uint8.
+
+    im: object with .width, .height, .coef (3 int16 [bh][bw][64]) and .qidx;
+    the planes are first put in the params' layout (what the host entropy
+    decoder holds), then the C encoder keeps the ROI blocks' nonzero used
+    coefficients (include/smol_preproc.h "Compact coefficient transport")."""
+    k = params.scale_denom if params.layout == SMOL_LAYOUT_PACKED else 1
+    planes = [pack_plane(np.ascontiguousarray(c, dtype=np.int16), k) for c in im.coef]
+    d = _desc_for(im.width, im.height, [c.shape[1] for c in im.coef], [c.shape[0] for c in im.coef],
+                  tuple(im.qidx), roi, strides=[2 * p.shape[1] for p in planes])
+    for ci in range(3):
+        d.coef[ci] = planes[ci].ctypes.data
+    n = ctypes.c_int64()
+    check(lib().smol_compact_encode(ctypes.byref(params), ctypes.byref(d), None, 0, ctypes.byref(n)))
+    rec = np.zeros(n.value, np.uint8)
+    check(lib().smol_compact_encode(ctypes.byref(params), ctypes.byref(d), rec.ctypes.data, n.value,
+                                    ctypes.byref(n)))
+    return rec
+
+
+class CompactBatch:
+    """N images as compact records (the end-to-end transport, SURVEY §8(f)
+    N1) in one arena: location "pinned" (page-locked host memory, copied by
+    smol_preproc_run_compact in one DMA) or "device".  Records are encoded
+    for `params` (layout, scale and crop fix the ROI and element set)."""
+
+    def __init__(self, params: Params, images: Sequence, qtables: np.ndarray, location: str = "pinned",
+                 device: Optional[int] = None, rois: Optional[Sequence] = None):
+        import torch
+        self.n = len(images)
+        cache = {}
+        recs = []
+        for i, im in enumerate(images):
+            roi = rois[i] if rois is not None else None
+            key = (id(im), roi)
+            if key not in cache:
+                cache[key] = compact_encode(params, im, roi)
+            recs.append(cache[key])
+        offs, o = [], 0
+        for r in recs:
+            offs.append(o)
+            o += r.size                           # records are multiples of 16 bytes
+        host = np.zeros(max(o, 16), np.uint8)
+        for r, oo in zip(recs, offs):
+            host[oo:oo + r.size] = r
+        qt = np.ascontiguousarray(qtables, dtype=np.uint16).view(np.int16)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        if location == "pinned":
+            self.arena = torch.from_numpy(host).pin_memory()
+        elif location == "device":
+            self.arena = torch.from_numpy(host).to(dev)
+        else:
+            raise ValueError(location)
+        self.location = location
+        self.qtables = torch.from_numpy(qt.copy()).to(dev)
+        self.arena_bytes = int(o)
+        self.images = (CompactImage * max(self.n, 1))()
+        for i, (im, oo) in enumerate(zip(images, offs)):
+            ci = CompactImage()
+            ci.width, ci.height, ci.subsampling = im.width, im.height, 420
+            ci.qtable = (ctypes.c_int32 * 3)(*tuple(im.qidx))
+            roi = rois[i] if rois is not None else None
+            ci.roi_left, ci.roi_top = roi if roi is not None else (-1, -1)
+            ci.offset = oo
+            self.images[i] = ci
+        self.desc = CompactBatchDesc()
+        self.desc.n_images = self.n
+        self.desc.images = ctypes.cast(self.images, ctypes.POINTER(CompactImage))
+        self.desc.arena = self.arena.data_ptr()
+        self.desc.arena_bytes = max(self.arena_bytes, 16)
+        self.desc.qtables = self.qtables.data_ptr()
+        self.desc.n_qtables = int(qtables.shape[0])
+
+
 class Plan:
     """smol_preproc_plan on the current CUDA device."""
 
@@ -175,9 +252,13 @@ class Plan:
         s = torch.cuda.current_stream() if stream is None else stream
         return s.cuda_stream
 
-    def run(self, batch: CoefBatch, out=None, stream=None):
+    def run(self, batch, out=None, stream=None):
         if out is None:
             out = self.new_output(batch.n)
+        if isinstance(batch, CompactBatch):
+            check(lib().smol_preproc_run_compact(self._h, ctypes.byref(batch.desc), out.data_ptr(),
+                                                 self._stream(stream)))
+            return out
         fn = lib().smol_preproc_run_host if batch.location == "pinned" else lib().smol_preproc_run
         check(fn(self._h, ctypes.byref(batch.desc), out.data_ptr(), self._stream(stream)))
         return out

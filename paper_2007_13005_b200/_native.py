@@ -14,7 +14,7 @@ _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libsmol_preproc.so")
 HEADER = os.path.join(_ROOT, "include", "smol_preproc.h")
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in
-           ("smol_preproc.cu", "smol_kernels.cuh", "smol_geom.cuh")]
+           ("smol_preproc.cu", "smol_kernels.cuh", "smol_geom.cuh", "smol_compact.cuh")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
@@ -28,7 +28,8 @@ SMOL_LAYOUT_DENSE64, SMOL_LAYOUT_PACKED = 0, 1
 # every symbol include/smol_preproc.h declares (checked by tests/test_abi.py)
 EXPORTS = ["smol_preproc_plan", "smol_preproc_run", "smol_preproc_run_host", "smol_preproc_destroy",
            "smol_preproc_output_shape", "smol_preproc_launches_per_run", "smol_debug_geometry",
-           "smol_debug_run", "smol_last_error", "smol_abi_version"]
+           "smol_debug_run", "smol_last_error", "smol_abi_version", "smol_compact_encode",
+           "smol_preproc_run_compact"]
 
 
 class Params(ctypes.Structure):
@@ -46,6 +47,19 @@ class ImageDesc(ctypes.Structure):
                 ("coef", ctypes.c_void_p * 3), ("blocks_w", ctypes.c_int32 * 3),
                 ("blocks_h", ctypes.c_int32 * 3), ("row_stride_bytes", ctypes.c_int32 * 3),
                 ("roi_left", ctypes.c_int32), ("roi_top", ctypes.c_int32)]
+
+
+class CompactImage(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("subsampling", ctypes.c_int32), ("qtable", ctypes.c_int32 * 3),
+                ("roi_left", ctypes.c_int32), ("roi_top", ctypes.c_int32),
+                ("offset", ctypes.c_int64)]
+
+
+class CompactBatchDesc(ctypes.Structure):
+    _fields_ = [("n_images", ctypes.c_int32), ("images", ctypes.POINTER(CompactImage)),
+                ("arena", ctypes.c_void_p), ("arena_bytes", ctypes.c_int64),
+                ("qtables", ctypes.c_void_p), ("n_qtables", ctypes.c_int32)]
 
 
 class BatchDesc(ctypes.Structure):
@@ -117,6 +131,8 @@ def lib():
         L.smol_last_error.argtypes = []
         L.smol_last_error.restype = ctypes.c_char_p
         L.smol_abi_version.argtypes = []
+        L.smol_compact_encode.argtypes = [P(Params), P(ImageDesc), vp, ctypes.c_int64, P(ctypes.c_int64)]
+        L.smol_preproc_run_compact.argtypes = [vp, P(CompactBatchDesc), vp, vp]
         for name in EXPORTS:
             f = getattr(L, name)
             if f.restype is ctypes.c_int:           # ctypes default

@@ -500,17 +500,14 @@ __device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
   return __shfl_sync(0xffffffffu, chunk, 0);
 }
 
+// One output tile (image n, output rows [oy0, oy1), columns [ox0, ox1)) of
+// the fused path.
 template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
-__global__ void __launch_bounds__(kThreads, 768 / kThreads)
-smol_fused_kernel(const KParams kp) {
+__device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const int oy0, const int oy1,
+                                       const int ox0, const int ox1) {
   constexpr int P = 8 / K;                 // decoded samples per block side
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
-  const int n = blockIdx.y;
-  const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
-  const int oy0 = trow * kp.tile_rows, oy1 = min(kp.OH, oy0 + kp.tile_rows);
-  const int ox0 = tcol * kp.tile_cols, ox1 = min(kp.OW, ox0 + kp.tile_cols);
-
   __shared__ DevImage im;
   __shared__ TileLayout L;
   __shared__ int ctr[2];                   // dynamic work counters (colour, output)
@@ -880,6 +877,16 @@ smol_fused_kernel(const KParams kp) {
     ready_prev = ready;
     done_prev = done;
   }
+}
+
+// The fused kernel: one (image, row band, column band) tile per CTA.
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
+__global__ void __launch_bounds__(kThreads, 768 / kThreads)
+smol_fused_kernel(const __grid_constant__ KParams kp) {
+  const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
+  const int oy0 = trow * kp.tile_rows, ox0 = tcol * kp.tile_cols;
+  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP>(kp, blockIdx.y, oy0, min(kp.OH, oy0 + kp.tile_rows), ox0,
+                                                   min(kp.OW, ox0 + kp.tile_cols));
 }
 
 }  // namespace smol

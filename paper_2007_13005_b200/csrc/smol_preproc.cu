@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <algorithm>
+#include <climits>
 #include <mutex>
 #include <new>
 #include <string>
@@ -17,6 +19,7 @@
 #include "smol_preproc.h"
 #include "smol_geom.cuh"
 #include "smol_kernels.cuh"
+#include "smol_compact.cuh"
 
 using namespace smol;
 
@@ -175,7 +178,7 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
 }
 
 int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, int idx, int n_qtables,
-                       DevImage& g) {
+                       DevImage& g, bool need_align = true) {
   int32_t rc = image_geometry(p, d, idx, g);
   if (rc) return rc;
   const int need_w[3] = {ceil_div(d->width, 8), ceil_div(d->width, 16), ceil_div(d->width, 16)};
@@ -183,7 +186,7 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
   static const char* names[3] = {"Y", "Cb", "Cr"};
   for (int c = 0; c < 3; ++c) {
     if (!d->coef[c]) return fail(SMOL_ERR_INVALID, "image %d: coef[%d] (%s) is NULL", idx, c, names[c]);
-    if (reinterpret_cast<uintptr_t>(d->coef[c]) % 16)
+    if (need_align && reinterpret_cast<uintptr_t>(d->coef[c]) % 16)
       return fail(SMOL_ERR_INVALID, "image %d: coef[%d] not 16-byte aligned", idx, c);
     if (d->blocks_w[c] < need_w[c] || d->blocks_h[c] < need_h[c])
       return fail(SMOL_ERR_INVALID, "image %d: blocks_w[%d]=%d / blocks_h[%d]=%d < required %d / %d", idx, c,
@@ -309,9 +312,15 @@ struct smol_preproc_plan {
   // memory into device memory on a copy stream, double-buffered
   cudaStream_t copy_stream = nullptr;
   int16_t* stage[2] = {nullptr, nullptr};
-  size_t stage_cap[2] = {0, 0};            // int16 elements
+  size_t stage_cap[2] = {0, 0};            // bytes
   GatherDesc* d_gather = nullptr;          // [2][max_images]
   GatherDesc* h_gather = nullptr;          // pinned [2][max_images]
+  // compact transport (run_compact): device copy of the records, expand descriptors
+  uint8_t* cbuf[2] = {nullptr, nullptr};
+  size_t cbuf_cap[2] = {0, 0};
+  ExpandDesc* d_expand = nullptr;          // [2][max_images]
+  ExpandDesc* h_expand = nullptr;          // pinned [2][max_images]
+  std::vector<TileLayout> layouts;         // host scratch (whole-output footprints)
   cudaEvent_t stage_free[2] = {}, stage_ready[2] = {};
   int stage_slot = 0;
 };
@@ -397,6 +406,9 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   }
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_gather, sizeof(GatherDesc) * (size_t)max_images * 2);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_gather, sizeof(GatherDesc) * (size_t)max_images * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
+  if (e == cudaSuccess) pl->layouts.reserve(max_images);
   if (e == cudaSuccess) {
     // opt every instantiation of this plan's (scale, dtype) in to the largest
     // dynamic smem the device allows next to the kernel's static smem
@@ -431,7 +443,10 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
     if (pl->stage_free[i]) { cudaEventSynchronize(pl->stage_free[i]); cudaEventDestroy(pl->stage_free[i]); }
     if (pl->stage_ready[i]) cudaEventDestroy(pl->stage_ready[i]);
     if (pl->stage[i]) cudaFree(pl->stage[i]);
+    if (pl->cbuf[i]) cudaFree(pl->cbuf[i]);
   }
+  if (pl->d_expand) cudaFree(pl->d_expand);
+  if (pl->h_expand) cudaFreeHost(pl->h_expand);
   if (pl->d_gather) cudaFree(pl->d_gather);
   if (pl->h_gather) cudaFreeHost(pl->h_gather);
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
@@ -454,21 +469,74 @@ int32_t smol_preproc_launches_per_run(const smol_preproc_plan_t* pl) {
 
 namespace {
 
-int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream_v,
-                 const KParams* dbg, bool staged = false) {
+// Where the coefficient blocks come from.
+enum class Src { kDevice, kGather, kCompact };
+
+// Validate a compact image descriptor into its device descriptor (coefficient
+// pointers are set by the staging step).
+int32_t validate_compact_image(const smol_preproc_params* p, const smol_compact_image* ci, int idx,
+                               int n_qtables, DevImage& g) {
+  smol_image_desc d{};
+  d.width = ci->width; d.height = ci->height; d.subsampling = ci->subsampling;
+  d.roi_left = ci->roi_left; d.roi_top = ci->roi_top;
+  int32_t rc = image_geometry(p, &d, idx, g);
+  if (rc) return rc;
+  if (ci->offset < 0 || ci->offset % 16)
+    return fail(SMOL_ERR_INVALID, "image %d: record offset %lld not a non-negative multiple of 16", idx,
+                (long long)ci->offset);
+  for (int c = 0; c < 3; ++c) {
+    if (ci->qtable[c] < 0 || ci->qtable[c] >= n_qtables)
+      return fail(SMOL_ERR_INVALID, "image %d: qtable[%d]=%d not in [0,%d)", idx, c, ci->qtable[c], n_qtables);
+    g.qidx[c] = ci->qtable[c];
+    g.nbw[c] = ceil_div(ci->width, c ? 16 : 8);
+    g.coef[c] = nullptr;
+    g.stride[c] = 0;
+  }
+  return SMOL_OK;
+}
+
+// Staged-plane layout of one image's ROI block rows (whole-output footprint):
+// per component rows [by0, by1] x elements [bx0 E, (bx1 + 1) E), each row
+// padded to 16 B with a leading pad so the kernel's virtual row base
+// (row - col0) is 16-B aligned, as for an original plane (its L2 bulk
+// prefetch needs it).  Returns the staged int16 elements; offsets in dst_off.
+size_t stage_layout(const TileLayout& L, int E, int32_t (&dst_stride)[3], size_t (&dst_off)[3], size_t need) {
+  for (int c = 0; c < 3; ++c) {
+    const int ncol = (L.bx1[c] - L.bx0[c] + 1) * E;
+    const int pad = (L.bx0[c] * E) & 7;
+    dst_stride[c] = (pad + ncol + 7) & ~7;
+    dst_off[c] = need + pad;
+    need += (size_t)dst_stride[c] * (L.by1[c] - L.by0[c] + 1);
+  }
+  return need;
+}
+
+int32_t grow(void** buf, size_t* cap, size_t need, cudaStream_t s) {
+  if (need <= *cap) return SMOL_OK;
+  SMOL_CUDA(cudaStreamSynchronize(s));
+  if (*buf) SMOL_CUDA(cudaFree(*buf));
+  *buf = nullptr;
+  *cap = 0;
+  SMOL_CUDA(cudaMalloc(buf, need + 256));
+  *cap = need;
+  return SMOL_OK;
+}
+
+int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, const uint16_t* qtables,
+                 int n_qtables, void* out, void* stream_v, const KParams* dbg, Src src,
+                 const smol_compact_batch* cb = nullptr) {
   g_last_error.clear();
-  if (!pl) return fail(SMOL_ERR_INVALID, "plan is NULL");
-  if (!b) return fail(SMOL_ERR_INVALID, "batch is NULL");
-  if (b->n_images < 0) return fail(SMOL_ERR_INVALID, "n_images=%d < 0", b->n_images);
-  if (b->n_images == 0) return SMOL_OK;
-  if (b->n_images > pl->max_images)
-    return fail(SMOL_ERR_CAPACITY, "n_images=%d > plan capacity %d", b->n_images, pl->max_images);
-  if (!b->images) return fail(SMOL_ERR_INVALID, "batch.images is NULL");
-  if (!b->qtables || b->n_qtables < 1 || b->n_qtables > 4)
-    return fail(SMOL_ERR_INVALID, "batch.qtables NULL or n_qtables=%d not in [1,4]", b->n_qtables);
+  if (n_images < 0) return fail(SMOL_ERR_INVALID, "n_images=%d < 0", n_images);
+  if (n_images == 0) return SMOL_OK;
+  if (n_images > pl->max_images)
+    return fail(SMOL_ERR_CAPACITY, "n_images=%d > plan capacity %d", n_images, pl->max_images);
+  if (!images) return fail(SMOL_ERR_INVALID, "batch.images is NULL");
+  if (!qtables || n_qtables < 1 || n_qtables > 4)
+    return fail(SMOL_ERR_INVALID, "batch.qtables NULL or n_qtables=%d not in [1,4]", n_qtables);
   if (!out) return fail(SMOL_ERR_INVALID, "out is NULL");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_v);
   const int K = pl->p.scale_denom;
+  const bool packed = pl->p.layout == SMOL_LAYOUT_PACKED;
 
   // ring slot: wait until the run that last used it has consumed its descriptors
   const int slot = pl->ring;
@@ -477,14 +545,15 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   DevImage* h = pl->h_desc + (size_t)slot * pl->max_images;
   DevImage* d = pl->d_desc + (size_t)slot * pl->max_images;
 
-  // validate + build descriptors; shared memory = max over distinct geometries
   // provisional tile height (4 CTAs per SM); final once the CTA size is known
   const bool auto_rows = pl->tile_rows <= 0;
-  int tile_rows = auto_rows ? auto_tile_rows(pl->OH, b->n_images, pl->num_sms * 4) : imin(pl->tile_rows, pl->OH);
+  int tile_rows = auto_rows ? auto_tile_rows(pl->OH, n_images, pl->num_sms * 4) : imin(pl->tile_rows, pl->OH);
   int ntiles = ceil_div(pl->OH, tile_rows);
   // validate every descriptor once
-  for (int i = 0; i < b->n_images; ++i) {
-    int32_t rc = validate_image(&pl->p, &b->images[i], i, b->n_qtables, h[i]);
+  for (int i = 0; i < n_images; ++i) {
+    int32_t rc = src == Src::kCompact
+        ? validate_compact_image(&pl->p, &static_cast<const smol_compact_image*>(images)[i], i, n_qtables, h[i])
+        : validate_image(&pl->p, &static_cast<const smol_image_desc*>(images)[i], i, n_qtables, h[i]);
     if (rc) return rc;
   }
   // shared memory of the largest tile over the batch's distinct geometries
@@ -494,25 +563,27 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
     const int tile_cols = cols_of(n_col_tiles);
     n_col_tiles = ceil_div(pl->OW, tile_cols);
     int m = 0;
-    int prev_w = -1, prev_h = -1, prev_l = -2, prev_t = -2;
-    for (int i = 0; i < b->n_images; ++i) {
-      const smol_image_desc* di = &b->images[i];
-      if (di->width == prev_w && di->height == prev_h && di->roi_left == prev_l && di->roi_top == prev_t)
+    const DevImage* prev = nullptr;
+    for (int i = 0; i < n_images; ++i) {
+      const DevImage& g = h[i];
+      if (prev && g.Wd == prev->Wd && g.Hd == prev->Hd && g.left == prev->left && g.top == prev->top &&
+          g.nbw[0] == prev->nbw[0] && g.nbw[1] == prev->nbw[1])
         continue;
       for (int t = 0; t < ntiles; ++t)
         for (int u = 0; u < n_col_tiles; ++u) {
           TileLayout L;
-          tile_layout(h[i], K, t * tile_rows, imin(pl->OH, (t + 1) * tile_rows), u * tile_cols,
+          tile_layout(g, K, t * tile_rows, imin(pl->OH, (t + 1) * tile_rows), u * tile_cols,
                       imin(pl->OW, (u + 1) * tile_cols), L, yp);
           m = imax(m, L.fits ? L.total : (1 << 30));
         }
-      prev_w = di->width; prev_h = di->height; prev_l = di->roi_left; prev_t = di->roi_top;
+      prev = &g;
     }
     return m;
   };
-  // Narrow configuration (192 threads, 384-B ring pitch) when full-width
-  // tiles fit it with 4 CTAs per SM; otherwise wide (256 threads, 512-B
-  // pitch), adding column tiles only when a tile would not leave 2 CTAs/SM.
+  // Tiny configuration (128 threads, 128-B rings, 6 CTAs/SM) for small
+  // footprints, narrow (192 threads, 384-B ring pitch) when full-width tiles
+  // fit it with 4 CTAs per SM; otherwise wide (256 threads, 512-B pitch),
+  // adding column tiles only when a tile would not leave 2 CTAs/SM.
   int n_col_tiles = 1;
   int nt = kThreadsTiny;
   int smem = max_smem(1, kYPTiny);
@@ -533,7 +604,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
     }
   }
   if (auto_rows && n_col_tiles == 1) {
-    const int tr = auto_tile_rows(pl->OH, b->n_images, pl->num_sms * (768 / nt));
+    const int tr = auto_tile_rows(pl->OH, n_images, pl->num_sms * (768 / nt));
     if (tr != tile_rows) {
       tile_rows = tr;
       ntiles = ceil_div(pl->OH, tile_rows);
@@ -542,80 +613,201 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
   }
   if (smem > pl->smem_optin)
     return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
-  if (staged) {
-    // End-to-end path: gather each image's ROI block rows (the whole output's
-    // tap footprint) from pinned host memory into a compact device staging
-    // buffer on the plan's copy stream, then point the descriptors at it.
+
+  if (src != Src::kDevice) {
+    // Staged paths: each image's ROI block rows (the whole output's tap
+    // footprint) are rebuilt in a plan-owned device buffer on the plan's copy
+    // stream -- gathered from pinned host planes (kGather) or expanded from
+    // compact records (kCompact) -- then the descriptors point at it.
     const int sl = pl->stage_slot;
     pl->stage_slot ^= 1;
+    SMOL_CUDA(cudaEventSynchronize(pl->stage_free[sl]));     // host side: descriptor slot reusable
+    const int E = block_elems(K, pl->p.layout);
     GatherDesc* hg = pl->h_gather + (size_t)sl * pl->max_images;
     GatherDesc* dg = pl->d_gather + (size_t)sl * pl->max_images;
-    SMOL_CUDA(cudaEventSynchronize(pl->stage_free[sl]));     // host side: hg reusable
-    const int E = block_elems(K, pl->p.layout);
+    ExpandDesc* he = pl->h_expand + (size_t)sl * pl->max_images;
+    ExpandDesc* de = pl->d_expand + (size_t)sl * pl->max_images;
     size_t need = 0;
-    for (int i = 0; i < b->n_images; ++i) {
-      TileLayout L;
+    size_t offs[3];
+    int32_t strides[3];
+    std::vector<TileLayout>& Ls = pl->layouts;
+    Ls.resize(n_images);
+    for (int i = 0; i < n_images; ++i) {
+      TileLayout& L = Ls[i];
       tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L);
-      GatherDesc& g = hg[i];
+      need = stage_layout(L, E, strides, offs, need);
       for (int c = 0; c < 3; ++c) {
-        const int ncol = (L.bx1[c] - L.bx0[c] + 1) * E;
-        g.src[c] = h[i].coef[c];
-        g.src_stride[c] = h[i].stride[c];
-        g.by0[c] = L.by0[c];
-        g.rows[c] = L.by1[c] - L.by0[c] + 1;
-        g.col0[c] = L.bx0[c] * E;
-        g.ncol[c] = ncol;
-        // leading pad so the kernel's virtual row base (row - col0) is 16-B
-        // aligned, as for an original plane (its L2 bulk prefetch needs it)
-        const int pad = (L.bx0[c] * E) & 7;
-        g.dst_stride[c] = (pad + ncol + 7) & ~7;             // 16-B rows
-        g.dst[c] = reinterpret_cast<int16_t*>(need + pad);    // offset; rebased below
-        need += (size_t)g.dst_stride[c] * g.rows[c];
+        if (src == Src::kGather) {
+          GatherDesc& g = hg[i];
+          g.src[c] = h[i].coef[c];
+          g.src_stride[c] = h[i].stride[c];
+          g.by0[c] = L.by0[c];
+          g.rows[c] = L.by1[c] - L.by0[c] + 1;
+          g.col0[c] = L.bx0[c] * E;
+          g.ncol[c] = (L.bx1[c] - L.bx0[c] + 1) * E;
+          g.dst_stride[c] = strides[c];
+          g.dst[c] = reinterpret_cast<int16_t*>(offs[c]);          // offset; rebased below
+        } else {
+          ExpandDesc& e = he[i];
+          e.dst[c] = reinterpret_cast<int16_t*>(offs[c]);
+          e.dst_stride[c] = strides[c];
+          e.nbx[c] = L.bx1[c] - L.bx0[c] + 1;
+          e.nby[c] = L.by1[c] - L.by0[c] + 1;
+          e.E = E;
+        }
+        h[i].stride[c] = strides[c];
       }
     }
-    if (need > pl->stage_cap[sl]) {                           // grow once (amortised)
-      SMOL_CUDA(cudaStreamSynchronize(pl->copy_stream));
-      if (pl->stage[sl]) SMOL_CUDA(cudaFree(pl->stage[sl]));
-      pl->stage[sl] = nullptr;
-      SMOL_CUDA(cudaMalloc(&pl->stage[sl], need * 2 + 256));
-      pl->stage_cap[sl] = need;
-    }
+    void* sbuf = pl->stage[sl];
+    int32_t rc = grow(&sbuf, &pl->stage_cap[sl], need * 2, pl->copy_stream);
+    pl->stage[sl] = static_cast<int16_t*>(sbuf);
+    if (rc) return rc;
     int16_t* base = pl->stage[sl];
-    for (int i = 0; i < b->n_images; ++i)
+    for (int i = 0; i < n_images; ++i) {
+      const TileLayout& L = Ls[i];
       for (int c = 0; c < 3; ++c) {
-        GatherDesc& g = hg[i];
-        g.dst[c] = base + reinterpret_cast<size_t>(g.dst[c]);
+        int16_t** dp = src == Src::kGather ? &hg[i].dst[c] : &he[i].dst[c];
+        *dp = base + reinterpret_cast<size_t>(*dp);
         // descriptor of the staged plane: same absolute block indexing
-        h[i].coef[c] = g.dst[c] - (ptrdiff_t)g.by0[c] * g.dst_stride[c] - g.col0[c];
-        h[i].stride[c] = g.dst_stride[c];
+        h[i].coef[c] = *dp - (ptrdiff_t)L.by0[c] * h[i].stride[c] - (ptrdiff_t)L.bx0[c] * E;
       }
+    }
+    // Every host->device copy of a staged run goes on the copy stream, small
+    // descriptors first: an H2D copy on `stream` would queue in the copy
+    // engine behind the next batch's bulk transfer and serialise the pipeline.
     SMOL_CUDA(cudaStreamWaitEvent(pl->copy_stream, pl->stage_free[sl], 0));   // previous user done
-    SMOL_CUDA(cudaMemcpyAsync(dg, hg, sizeof(GatherDesc) * b->n_images, cudaMemcpyHostToDevice,
-                              pl->copy_stream));
-    smol_gather_kernel<<<b->n_images, 256, 0, pl->copy_stream>>>(dg);
-    SMOL_CUDA(cudaGetLastError());
+    if (src == Src::kGather) {
+      SMOL_CUDA(cudaMemcpyAsync(dg, hg, sizeof(GatherDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      smol_gather_kernel<<<n_images, 256, 0, pl->copy_stream>>>(dg);
+      SMOL_CUDA(cudaGetLastError());
+    } else {
+      // records: bounds (and, for host arenas, header) checks, then one DMA of
+      // the batch's byte range
+      const smol_compact_image* ci = static_cast<const smol_compact_image*>(images);
+      cudaPointerAttributes pa;
+      if (cudaPointerGetAttributes(&pa, cb->arena) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SMOL_ERR_INVALID, "compact arena is neither host nor device memory");
+      }
+      const bool on_device = pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged;
+      const uint8_t* arena = static_cast<const uint8_t*>(cb->arena);
+      int64_t lo = INT64_MAX, hi = 0;
+      for (int i = 0; i < n_images; ++i) {
+        const ExpandDesc& e = he[i];
+        int64_t nblocks = 0, nrows = 0;
+        for (int c = 0; c < 3; ++c) { nblocks += (int64_t)e.nbx[c] * e.nby[c]; nrows += e.nby[c]; }
+        int64_t bytes = compact_values_off(nblocks, nrows);
+        if (ci[i].offset + bytes > cb->arena_bytes)
+          return fail(SMOL_ERR_INVALID, "image %d: record at %lld (>= %lld B) outside arena of %lld B", i,
+                      (long long)ci[i].offset, (long long)bytes, (long long)cb->arena_bytes);
+        if (!on_device) {
+          CompactHeader hd;
+          memcpy(&hd, arena + ci[i].offset, sizeof(hd));
+          bool ok = hd.magic == kCompactMagic && (int)hd.E == E;
+          for (int c = 0; c < 3 && ok; ++c)
+            ok = hd.bx0[c] == Ls[i].bx0[c] && hd.by0[c] == Ls[i].by0[c] && hd.nbx[c] == e.nbx[c] &&
+                 hd.nby[c] == e.nby[c];
+          if (!ok)
+            return fail(SMOL_ERR_INVALID, "image %d: compact record header does not match this plan's "
+                        "layout/ROI (bad magic, E or block ranges)", i);
+          bytes = compact_record_bytes(nblocks, nrows, hd.n_values);
+          if (ci[i].offset + bytes > cb->arena_bytes)
+            return fail(SMOL_ERR_INVALID, "image %d: record (%lld B) overruns the arena", i, (long long)bytes);
+        }
+        lo = std::min<int64_t>(lo, ci[i].offset);
+        hi = std::max<int64_t>(hi, ci[i].offset + bytes);
+      }
+      const uint8_t* rec_base = arena;
+      if (on_device) {
+        lo = 0;
+      } else {
+        void* cbuf = pl->cbuf[sl];
+        rc = grow(&cbuf, &pl->cbuf_cap[sl], (size_t)(hi - lo), pl->copy_stream);
+        pl->cbuf[sl] = static_cast<uint8_t*>(cbuf);
+        if (rc) return rc;
+        rec_base = pl->cbuf[sl];
+      }
+      for (int i = 0; i < n_images; ++i) he[i].rec = rec_base + (ci[i].offset - lo);
+      SMOL_CUDA(cudaMemcpyAsync(de, he, sizeof(ExpandDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (!on_device)
+        SMOL_CUDA(cudaMemcpyAsync(pl->cbuf[sl], arena + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice,
+                                  pl->copy_stream));
+    }
     SMOL_CUDA(cudaEventRecord(pl->stage_ready[sl], pl->copy_stream));
     SMOL_CUDA(cudaStreamWaitEvent(stream, pl->stage_ready[sl], 0));
+    if (src == Src::kCompact) {
+      // expand on the compute stream: the copy stream carries only copies,
+      // so batch k+1's transfer overlaps batch k's expand + fused kernel
+      smol_expand_kernel<<<n_images, kExpandWarps * 32, 0, stream>>>(de);
+      SMOL_CUDA(cudaGetLastError());
+    }
   }
 
-  SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * b->n_images, cudaMemcpyHostToDevice, stream));
+  if (src == Src::kDevice)
+    SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, stream));
   KParams kp = dbg ? *dbg : KParams{};
   kp.imgs = d;
-  kp.qtables = b->qtables;
+  kp.qtables = qtables;
   kp.out = out;
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;
   kp.magic = 0x4B000000u;
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
-  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr,
-                              pl->p.layout == SMOL_LAYOUT_PACKED, nt);
-  dim3 grid(ntiles * n_col_tiles, b->n_images);
+  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt);
+  dim3 grid(ntiles * n_col_tiles, n_images);
   fn<<<grid, nt, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
-  if (staged) SMOL_CUDA(cudaEventRecord(pl->stage_free[pl->stage_slot ^ 1], stream));
+  if (src != Src::kDevice) SMOL_CUDA(cudaEventRecord(pl->stage_free[pl->stage_slot ^ 1], stream));
   return SMOL_OK;
+}
+
+int32_t run_batch(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream,
+                  const KParams* dbg, Src src) {
+  g_last_error.clear();
+  if (!pl) return fail(SMOL_ERR_INVALID, "plan is NULL");
+  if (!b) return fail(SMOL_ERR_INVALID, "batch is NULL");
+  return run_impl(pl, b->n_images, b->images, b->qtables, b->n_qtables, out, stream, dbg, src);
+}
+
+// Compact record of one image (format: include/smol_preproc.h).  Pass 1
+// (dst == NULL) counts, pass 2 writes.
+int64_t compact_encode_pass(const smol_image_desc* d, const TileLayout& L, int E, uint64_t mask,
+                            uint8_t* dst, uint32_t* n_values_out) {
+  int64_t nblocks = 0, nrows = 0;
+  for (int c = 0; c < 3; ++c) {
+    nblocks += (int64_t)(L.bx1[c] - L.bx0[c] + 1) * (L.by1[c] - L.by0[c] + 1);
+    nrows += L.by1[c] - L.by0[c] + 1;
+  }
+  uint64_t* bm = dst ? reinterpret_cast<uint64_t*>(dst + kCompactHeader) : nullptr;
+  uint32_t* rs = dst ? reinterpret_cast<uint32_t*>(dst + compact_rowstart_off(nblocks)) : nullptr;
+  int16_t* vals = dst ? reinterpret_cast<int16_t*>(dst + compact_values_off(nblocks, nrows)) : nullptr;
+  uint32_t nv = 0;
+  int64_t bi = 0, ri = 0;
+  for (int c = 0; c < 3; ++c) {
+    const int stride = d->row_stride_bytes[c] / 2;
+    for (int by = L.by0[c]; by <= L.by1[c]; ++by) {
+      if (rs) rs[ri] = nv;
+      ++ri;
+      for (int bx = L.bx0[c]; bx <= L.bx1[c]; ++bx) {
+        const int16_t* blk = d->coef[c] + (size_t)by * stride + (size_t)bx * E;
+        uint64_t m = 0;
+        for (int e = 0; e < E; ++e)
+          if (((mask >> e) & 1) && blk[e] != 0) {
+            m |= 1ull << e;
+            if (vals) vals[nv] = blk[e];
+            ++nv;
+          }
+        if (bm) bm[bi] = m;
+        ++bi;
+      }
+    }
+  }
+  *n_values_out = nv;
+  return compact_record_bytes(nblocks, nrows, nv);
 }
 
 }  // namespace
@@ -623,7 +815,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, v
 extern "C" {
 
 int32_t smol_preproc_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream) {
-  return run_impl(pl, b, out, stream, nullptr);
+  return run_batch(pl, b, out, stream, nullptr, Src::kDevice);
 }
 
 int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream) {
@@ -643,7 +835,52 @@ int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b,
       }
     }
   }
-  return run_impl(pl, b, out, stream, nullptr, /*staged=*/true);
+  return run_batch(pl, b, out, stream, nullptr, Src::kGather);
+}
+
+int32_t smol_preproc_run_compact(smol_preproc_plan_t* pl, const smol_compact_batch* b, void* out, void* stream) {
+  g_last_error.clear();
+  if (!pl) return fail(SMOL_ERR_INVALID, "plan is NULL");
+  if (!b) return fail(SMOL_ERR_INVALID, "batch is NULL");
+  if (b->n_images > 0 && (!b->arena || reinterpret_cast<uintptr_t>(b->arena) % 16 || b->arena_bytes <= 0))
+    return fail(SMOL_ERR_INVALID, "compact arena NULL, not 16-byte aligned or empty");
+  return run_impl(pl, b->n_images, b->images, b->qtables, b->n_qtables, out, stream, nullptr, Src::kCompact, b);
+}
+
+int32_t smol_compact_encode(const smol_preproc_params* p, const smol_image_desc* d, void* dst, int64_t capacity,
+                            int64_t* written) {
+  g_last_error.clear();
+  int32_t rc = validate_params(p);
+  if (rc) return rc;
+  if (!d || !written) return fail(SMOL_ERR_INVALID, "image/written is NULL");
+  DevImage g{};
+  rc = validate_image(p, d, 0, 4, g, /*need_align=*/false);
+  if (rc) return rc;
+  const int OW = p->crop_w > 0 ? p->crop_w : g.Wr, OH = p->crop_w > 0 ? p->crop_h : g.Hr;
+  TileLayout L;
+  tile_layout(g, p->scale_denom, 0, OH, 0, OW, L);
+  const int E = block_elems(p->scale_denom, p->layout);
+  const uint64_t mask = used_mask(p->scale_denom, p->layout == SMOL_LAYOUT_PACKED);
+  uint32_t nv = 0;
+  const int64_t bytes = compact_encode_pass(d, L, E, mask, nullptr, &nv);
+  *written = bytes;
+  if (!dst) return SMOL_OK;
+  if (capacity < bytes)
+    return fail(SMOL_ERR_CAPACITY, "compact record needs %lld B > capacity %lld", (long long)bytes,
+                (long long)capacity);
+  uint8_t* o = static_cast<uint8_t*>(dst);
+  memset(o, 0, (size_t)bytes);
+  CompactHeader hd{};
+  hd.magic = kCompactMagic;
+  hd.E = (uint32_t)E;
+  hd.n_values = nv;
+  for (int c = 0; c < 3; ++c) {
+    hd.bx0[c] = L.bx0[c]; hd.by0[c] = L.by0[c];
+    hd.nbx[c] = L.bx1[c] - L.bx0[c] + 1; hd.nby[c] = L.by1[c] - L.by0[c] + 1;
+  }
+  memcpy(o, &hd, sizeof(hd));
+  compact_encode_pass(d, L, E, mask, o, &nv);
+  return SMOL_OK;
 }
 
 int32_t smol_debug_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, int16_t* y_dbg,
@@ -653,7 +890,7 @@ int32_t smol_debug_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* 
   KParams kp{};
   kp.dbg_pl[0] = y_dbg; kp.dbg_pl[1] = cb_dbg; kp.dbg_pl[2] = cr_dbg; kp.dbg_rgb = rgb_dbg;
   kp.dbg_stride_y = sy; kp.dbg_stride_c = sc; kp.dbg_stride_rgb = srgb;
-  return run_impl(pl, b, out, stream, &kp);
+  return run_batch(pl, b, out, stream, &kp, Src::kDevice);
 }
 
 }  // extern "C"

@@ -1,0 +1,187 @@
+"""Compact coefficient transport (include/smol_preproc.h).
+
+CPU: the C encoder (smol_compact_encode, host only) against an independent
+Python reader of the record format written from the header's description:
+the record must hold exactly the ROI blocks smol_debug_geometry reports and,
+per block, exactly the nonzero coefficients the scale uses (reading R1), so
+decoding it gives back the input on the used set and zero elsewhere.
+
+GPU: smol_preproc_run_compact must be bit-identical to smol_preproc_run on the
+dense device planes (the compact path only changes transport), and within
+the north_star tolerance of the oracle."""
+import struct
+
+import numpy as np
+import pytest
+
+import paper_2007_13005_b200 as smol
+import synth
+from paper_2007_13005_b200 import layout as lay
+
+MAGIC = 0x31434D53
+
+
+def read_record(rec: np.ndarray):
+    """Parse one record -> (E, ranges, {(c, by, bx): int16[E] block})."""
+    b = rec.tobytes()
+    magic, E, nval, zero = struct.unpack_from("<4I", b, 0)
+    assert magic == MAGIC and zero == 0
+    f = struct.unpack_from("<12i", b, 16)
+    bx0, by0, nbx, nby = f[0:3], f[3:6], f[6:9], f[9:12]
+    nblocks = sum(nbx[c] * nby[c] for c in range(3))
+    nrows = sum(nby)
+    bm = np.frombuffer(b, np.uint64, nblocks, 64)
+    rs = np.frombuffer(b, np.uint32, nrows, 64 + 8 * nblocks)
+    voff = -(-(64 + 8 * nblocks + 4 * nrows) // 16) * 16
+    vals = np.frombuffer(b, np.int16, nval, voff)
+    assert len(b) == -(-(voff + 2 * nval + 2) // 16) * 16
+    blocks = {}
+    k = bi = ri = 0
+    for c in range(3):
+        for r in range(nby[c]):
+            assert rs[ri] == k               # row starts index the value array
+            ri += 1
+            for x in range(nbx[c]):
+                m = int(bm[bi]); bi += 1
+                blk = np.zeros(E, np.int16)
+                for e in range(E):
+                    if (m >> e) & 1:
+                        blk[e] = vals[k]; k += 1
+                assert m >> E == 0
+                blocks[(c, by0[c] + r, bx0[c] + x)] = blk
+    assert k == nval
+    return E, (bx0, by0, nbx, nby), blocks
+
+
+def used_elements(k: int, packed: bool):
+    """Element indices of a stored block that scale 1/k uses (reading R1),
+    from the layout's index sets (not from the C mask)."""
+    idx = lay.index_set(k)
+    return list(range(len(idx))) if (packed and k > 1) else idx
+
+
+@pytest.mark.parametrize("name,layout,quality", [("c1", "dense", 75), ("c2", "dense", 75), ("c2", "dense", 95),
+                                                 ("c3a", "dense", 75), ("c3a", "packed", 75),
+                                                 ("c3b", "packed", 95), ("c4", "packed", 75),
+                                                 ("c4", "dense", 75)])
+def test_encoder_roundtrip_against_python_reader(name, layout, quality):
+    cfg = synth.CONFIGS[name]
+    imgs, _ = synth.distinct_images(cfg, n_distinct=2, quality=quality)
+    p = smol.params_from_config(cfg, layout=layout)
+    k = cfg.scale_denom
+    packed = layout == "packed"
+    used = used_elements(k, packed)
+    for im in imgs:
+        rec = smol.compact_encode(p, im)
+        assert rec.size % 16 == 0
+        E, (bx0, by0, nbx, nby), blocks = read_record(rec)
+        assert E == lay.block_elems(k, packed)
+        g = smol.geometry(p, im.width, im.height)
+        for c in range(3):
+            assert (bx0[c], by0[c]) == (g["bx0"][c], g["by0"][c])
+            assert (bx0[c] + nbx[c] - 1, by0[c] + nby[c] - 1) == (g["bx1"][c], g["by1"][c])
+        assert len(blocks) == g["roi_blocks"]
+        stored = [lay.pack_plane(np.asarray(cc, np.int16), k if packed else 1) for cc in im.coef]
+        for (c, by, bx), blk in blocks.items():
+            src = stored[c][by, bx * E:(bx + 1) * E]
+            want = np.zeros(E, np.int16)
+            want[used] = src[used]
+            np.testing.assert_array_equal(blk, want, err_msg=f"{name} comp {c} block ({by},{bx})")
+
+
+def test_encoder_size_query_capacity_and_compression():
+    cfg = synth.CONFIGS["c2"]
+    imgs, _ = synth.distinct_images(cfg, n_distinct=2)
+    p = smol.params_from_config(cfg)
+    im = imgs[0]
+    rec = smol.compact_encode(p, im)
+    planes = [lay.pack_plane(np.asarray(c, np.int16), 1) for c in im.coef]
+    d = smol._desc_for(im.width, im.height, [c.shape[1] for c in im.coef], [c.shape[0] for c in im.coef],
+                       tuple(im.qidx), None, strides=[2 * q.shape[1] for q in planes])
+    import ctypes
+    for ci in range(3):
+        d.coef[ci] = planes[ci].ctypes.data
+    n = ctypes.c_int64()
+    smol.check(smol.lib().smol_compact_encode(ctypes.byref(p), ctypes.byref(d), None, 0, ctypes.byref(n)))
+    assert n.value == rec.size
+    small = np.zeros(rec.size - 16, np.uint8)
+    rc = smol.lib().smol_compact_encode(ctypes.byref(p), ctypes.byref(d), small.ctypes.data, small.size,
+                                        ctypes.byref(n))
+    assert rc == 5                                    # SMOL_ERR_CAPACITY
+    # natural q75 coefficients: far fewer bytes than the dense ROI blocks
+    g = smol.geometry(p, im.width, im.height)
+    assert rec.size < 0.25 * g["roi_coef_bytes"], (rec.size, g["roi_coef_bytes"])
+    # an all-zero image: header + bitmaps + row starts only
+    z = synth.CoefImage(im.width, im.height, [np.zeros_like(c) for c in im.coef])
+    _, _, blocks = read_record(smol.compact_encode(p, z))
+    assert all(not b.any() for b in blocks.values())
+
+
+def test_encoder_explicit_roi_and_errors():
+    cfg = synth.CONFIGS["c2"]
+    imgs, _ = synth.distinct_images(cfg, n_distinct=1)
+    p = smol.params_from_config(cfg)
+    im = imgs[0]
+    g = smol.geometry(p, im.width, im.height, roi=(0, 0))
+    _, (bx0, by0, nbx, nby), _ = read_record(smol.compact_encode(p, im, roi=(0, 0)))
+    assert (bx0[0], by0[0]) == (g["bx0"][0], g["by0"][0]) == (0, 0)
+    with pytest.raises(smol.SmolError) as e:
+        smol.compact_encode(p, im, roi=(500, 0))       # outside the resized image
+    assert e.value.status == 1
+
+
+# ------------------------------------------------------------------ GPU ----
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,layout", [("c1", "dense"), ("c2", "dense"), ("c3a", "packed"), ("c3a", "dense"),
+                                         ("c3b", "packed"), ("c4", "packed"), ("c4", "dense"), ("c5", "packed")])
+def test_run_compact_equals_device(name, layout):
+    import torch
+    cfg = synth.CONFIGS[name]
+    n = {"c5": 2, "c4": 16}.get(name, 6)
+    imgs, qt = synth.distinct_images(cfg, n_distinct=n)
+    ps = smol.params_from_config(cfg, layout=layout)
+    plan = smol.Plan(ps, n)
+    a = plan.run(smol.batch_for(ps, imgs, qt)).clone()
+    cbs = [smol.CompactBatch(ps, imgs, qt, location="pinned") for _ in range(2)]
+    outs = [plan.run(cbs[k % 2]).clone() for k in range(5)]       # back-to-back: double buffer
+    outs.append(plan.run(smol.CompactBatch(ps, imgs, qt, location="device")))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(a, o), name
+    plan.close()
+
+
+@pytest.mark.gpu
+def test_run_compact_stress_rois_and_hetero_sizes():
+    import torch
+    import oracle
+    rng = np.random.default_rng(2007)
+    cfg = synth.CONFIGS["c2"]
+    qt = synth.quant_tables(95)
+    imgs = [synth.make_image(rng, int(w), int(h), qt, mode=m)
+            for (w, h), m in zip(synth.random_sizes(rng, 6, 40, 400), ["natural", "stress"] * 3)]
+    ps = smol.params_from_config(cfg, resize_short=64, crop_w=48, crop_h=40)
+    plan = smol.Plan(ps, len(imgs))
+    rois = [None] * len(imgs)
+    rois[1] = (0, 0)
+    a = plan.run(smol.CoefBatch(imgs, qt, rois=[r if r else (-1, -1) for r in rois])).clone()
+    b = plan.run(smol.CompactBatch(ps, imgs, qt, rois=[r if r else (-1, -1) for r in rois]))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+def test_run_compact_rejects_foreign_records():
+    cfg = synth.CONFIGS["c3a"]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=2)
+    pd = smol.params_from_config(cfg)
+    pp = smol.params_from_config(cfg, layout="packed")
+    plan = smol.Plan(pp, 2)
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(smol.CompactBatch(pd, imgs, qt))       # encoded for the dense layout
+    assert e.value.status == 1 and "image 0" in str(e.value)
+    cb = smol.CompactBatch(pp, imgs, qt)
+    cb.desc.arena_bytes = 64
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(cb)
+    assert e.value.status == 1
