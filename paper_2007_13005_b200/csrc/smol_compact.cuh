@@ -59,40 +59,53 @@ struct ExpandDesc {
 #if defined(__CUDACC__)
 constexpr int kExpandWarps = 8;
 constexpr int kExpandChunkVals = 32 * 64 + 8;  // values of one 32-block chunk (worst case) + alignment slack
+// per-lane block buffers are padded by 8 bytes (lane stride 2E + 8 bytes) so
+// the lanes' zeroing/scatter stores do not all land in one shared-memory bank
+constexpr int kExpandLanePad = 4;               // int16 elements
+constexpr int kExpandBlkBuf = 32 * (64 + kExpandLanePad);
+// dynamic shared memory per CTA: per warp a 32-block output buffer + the chunk's values
+constexpr int kExpandSmem = kExpandWarps * (kExpandBlkBuf * 2 + kExpandChunkVals * 2);
+constexpr int kExpandSplit = 4;                 // CTAs per image (block rows interleaved)
 
-// One CTA per image; a warp expands one ROI block row at a time, 32 blocks
-// per chunk: each lane reads one bitmap, a warp scan of the popcounts gives
-// each block's first value; the chunk's values (contiguous in the record) are
-// copied to the warp's shared-memory buffer with independent coalesced loads
-// (so the dependent per-block gathers below hit shared memory, not HBM
-// latency); then the warp writes the chunk's blocks one after another: lane
-// l produces elements 2l, 2l+1 (one coalesced 32-bit store per lane, a 128-B
-// block per warp instruction at E = 64).  E = 1 (DC plane): lane per block.
+// kExpandSplit CTAs per image (block rows interleaved); a warp expands one ROI
+// block row at a time, 32 blocks (one per lane) per chunk:
+//   1. each lane reads its block's bitmap; a warp scan of the popcounts gives
+//      each block's first value;
+//   2. the chunk's values (contiguous in the record) are copied to shared
+//      memory with independent coalesced loads;
+//   3. each lane zeroes its block in a shared buffer and scatters its nonzero
+//      values into it (one iteration per set bit);
+//   4. the chunk's 32 blocks are contiguous in the staged row: the warp copies
+//      the buffer out with coalesced 8-byte stores.
+// E = 1 (DC plane): lane per block, direct store.
 __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const ExpandDesc* eds) {
-  __shared__ int16_t sv[kExpandWarps][kExpandChunkVals];
-  const ExpandDesc e = eds[blockIdx.x];
+  extern __shared__ __align__(16) uint8_t esm[];
+  const ExpandDesc e = eds[blockIdx.x / kExpandSplit];
+  const int part = blockIdx.x % kExpandSplit;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int16_t* buf = sv[warp];
-  int blk_base[3], row_base[3];
-  int nblocks = 0, nrows = 0;
-  for (int c = 0; c < 3; ++c) {
-    blk_base[c] = nblocks; row_base[c] = nrows;
-    nblocks += e.nbx[c] * e.nby[c];
-    nrows += e.nby[c];
-  }
+  int16_t* blk = reinterpret_cast<int16_t*>(esm) + warp * kExpandBlkBuf;
+  int16_t* buf = reinterpret_cast<int16_t*>(esm + kExpandWarps * kExpandBlkBuf * 2) + warp * kExpandChunkVals;
+  const int E = e.E;
+  const uint32_t fd_wpb = make_fastdiv((uint32_t)(E / 4 > 0 ? E / 4 : 1)).m;
+  // component bases without dynamically indexed arrays (no local memory)
+  const int nb0 = e.nbx[0] * e.nby[0], nb1 = e.nbx[1] * e.nby[1], nb2 = e.nbx[2] * e.nby[2];
+  const int r1 = e.nby[0], r2 = e.nby[0] + e.nby[1], nrows = r2 + e.nby[2];
+  const int nblocks = nb0 + nb1 + nb2;
   const uint64_t* bm_all = reinterpret_cast<const uint64_t*>(e.rec + kCompactHeader);
   const uint32_t* rowst = reinterpret_cast<const uint32_t*>(e.rec + compact_rowstart_off(nblocks));
   const int16_t* vals = reinterpret_cast<const int16_t*>(e.rec + compact_values_off(nblocks, nrows));
-  for (int gr = warp; gr < nrows; gr += kExpandWarps) {
-    const int c = gr >= row_base[2] ? 2 : gr >= row_base[1] ? 1 : 0;
-    const int r = gr - row_base[c];
-    const int nbx = e.nbx[c];
-    const uint64_t* bm = bm_all + blk_base[c] + (int64_t)r * nbx;
-    int16_t* drow = e.dst[c] + (int64_t)r * e.dst_stride[c];
+  for (int gr = part * kExpandWarps + warp; gr < nrows; gr += kExpandWarps * kExpandSplit) {
+    const int c = gr >= r2 ? 2 : gr >= r1 ? 1 : 0;
+    const int r = gr - (c == 2 ? r2 : c == 1 ? r1 : 0);
+    const int nbx = c == 2 ? e.nbx[2] : c == 1 ? e.nbx[1] : e.nbx[0];
+    const uint64_t* bm = bm_all + (c == 2 ? nb0 + nb1 : c == 1 ? nb0 : 0) + (int64_t)r * nbx;
+    int16_t* const dst_c = c == 2 ? e.dst[2] : c == 1 ? e.dst[1] : e.dst[0];
+    const int stride_c = c == 2 ? e.dst_stride[2] : c == 1 ? e.dst_stride[1] : e.dst_stride[0];
+    int16_t* drow = dst_c + (int64_t)r * stride_c;
     uint32_t vbase = __ldg(rowst + gr);
     for (int ch = 0; ch < nbx; ch += 32) {
       const int b = ch + lane;
-      const uint64_t m = b < nbx ? __ldg(bm + b) : 0ull;
+      uint64_t m = b < nbx ? __ldg(bm + b) : 0ull;
       const int cnt = __popcll(m);
       int inc = cnt;
 #pragma unroll
@@ -100,32 +113,39 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
         const int t = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += t;
       }
-      const int first = inc - cnt;                       // relative to the chunk
       const int total = __shfl_sync(0xffffffffu, inc, 31);
-      // stage the chunk's values: 32-bit loads from the 4-B aligned start
+      // 2. stage the chunk's values (32-bit loads from the 4-B aligned start)
       const int16_t* src = vals + vbase;
       const int mis = (int)(reinterpret_cast<uintptr_t>(src) & 3) >> 1;     // 0 or 1 element
       const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src - mis);
       const int nw = (total + mis + 1) >> 1;
       uint32_t* b32 = reinterpret_cast<uint32_t*>(buf);
       for (int w = lane; w < nw; w += 32) b32[w] = __ldg(s32 + w);
-      __syncwarp();
-      const int16_t* cv = buf + mis;
       const int nb = min(32, nbx - ch);
-      if (e.E == 1) {
-        if (b < nbx) drow[b] = m ? cv[first] : (int16_t)0;
+      if (E == 1) {
+        __syncwarp();
+        if (b < nbx) drow[b] = m ? buf[mis + inc - cnt] : (int16_t)0;
       } else {
-        const int e0 = 2 * lane;
-        for (int j = 0; j < nb; ++j) {
-          const uint64_t mj = __shfl_sync(0xffffffffu, m, j);
-          const int fj = __shfl_sync(0xffffffffu, first, j);
-          if (e0 < e.E) {
-            const int k = fj + __popcll(mj & ((1ull << e0) - 1ull));
-            const uint32_t b0 = (uint32_t)(mj >> e0) & 1u, b1 = (uint32_t)(mj >> (e0 + 1)) & 1u;
-            const uint32_t v0 = b0 ? (uint16_t)cv[k] : 0u;
-            const uint32_t v1 = b1 ? (uint16_t)cv[k + b0] : 0u;
-            *reinterpret_cast<uint32_t*>(drow + (int64_t)(ch + j) * e.E + e0) = v0 | (v1 << 16);
-          }
+        // 3. zero + scatter this lane's block (E*2 bytes, a multiple of 8)
+        const int ls = E + kExpandLanePad;                 // lane stride (elements)
+        int16_t* mine = blk + lane * ls;
+        uint2* m8 = reinterpret_cast<uint2*>(mine);
+        for (int q = 0; q < E / 4; ++q) m8[q] = make_uint2(0u, 0u);
+        __syncwarp();                                       // staged values visible
+        int k = mis + inc - cnt;
+        while (m) {
+          const int el = __ffsll((long long)m) - 1;
+          m &= m - 1;
+          mine[el] = buf[k++];
+        }
+        __syncwarp();
+        // 4. copy the nb blocks out (contiguous in the staged row): 8-byte
+        // word w of the chunk is word w % wpb of block w / wpb
+        const int wpb = E / 4;                              // 8-byte words per block
+        uint2* to8 = reinterpret_cast<uint2*>(drow + (int64_t)ch * E);
+        for (int w = lane; w < nb * wpb; w += 32) {
+          const int bb = (int)__umulhi((uint32_t)w, fd_wpb);   // w / wpb (w < 2^16)
+          to8[w] = reinterpret_cast<const uint2*>(blk + bb * ls)[w - bb * wpb];
         }
       }
       __syncwarp();

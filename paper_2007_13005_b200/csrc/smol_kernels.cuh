@@ -32,11 +32,15 @@
 #ifndef SMOL_OPT_COLFFMA2
 #define SMOL_OPT_COLFFMA2 0
 #endif
+// Output-phase scheduling (measured, profiles/r01h_output_schedule.md): at
+// scale 1 the output tasks share the phase with the next step's IDCT and are
+// grabbed dynamically, two per lane per grab, interleaved by the compiler; at
+// scales 1/2..1/8 that IDCT is small and a static stride wins.
 #ifndef SMOL_OUT_PER_GRAB
-#define SMOL_OUT_PER_GRAB 1      // output tasks per lane per work-counter grab
+#define SMOL_OUT_PER_GRAB 2      // scale 1: output tasks per lane per work-counter grab
 #endif
-#ifndef SMOL_OUT_UNROLL
-#define SMOL_OUT_UNROLL 1        // output tasks of one grab interleaved by the compiler
+#ifndef SMOL_OUT_STATIC
+#define SMOL_OUT_STATIC 2        // 0: dynamic everywhere; 1: static everywhere; 2: static at scales 1/2..1/8
 #endif
 #ifndef SMOL_COL_UNROLL
 #define SMOL_COL_UNROLL 1
@@ -47,7 +51,7 @@
 
 namespace smol {
 
-constexpr int kOutUnroll = SMOL_OUT_UNROLL, kColUnroll = SMOL_COL_UNROLL;   // (#pragma unroll does not expand macros)
+constexpr int kColUnroll = SMOL_COL_UNROLL;   // (#pragma unroll does not expand macros)
 
 // Basis constants, computed on the host in double from their definitions
 // (smol_preproc.cu: init_basis) and uploaded once per device.
@@ -790,21 +794,21 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
       const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
       const uint32_t magic = kp.magic;     // 0x4B000000 (2^23), kept in a register
-      for (;;) {
-        const int chunk = grab_chunk(&ctr[1], lane, 32 * SMOL_OUT_PER_GRAB);
+      // dynamic warp-chunk grabbing balances output tasks against the IDCT of
+      // step s+1 running in the same phase; SMOL_OUT_STATIC (1: always, 2:
+      // reduced scales only, where that IDCT is small) strides statically
+      constexpr bool kOutStatic = SMOL_OUT_STATIC == 1 || (SMOL_OUT_STATIC == 2 && K != 1);
+      constexpr int kPer = kOutStatic ? 1 : SMOL_OUT_PER_GRAB;   // tasks per lane per grab (unrolled)
+      for (int chunk = kOutStatic ? (tid >> 5) * 32 : 0;; chunk += kThreads * kPer) {
+        if constexpr (!kOutStatic) chunk = grab_chunk(&ctr[1], lane, 32 * kPer);
         if (chunk >= ntasko) break;
-#pragma unroll(kOutUnroll)
-       for (int h = 0; h < SMOL_OUT_PER_GRAB; ++h) {
+#pragma unroll
+       for (int h = 0; h < kPer; ++h) {
         const int t0 = chunk + 32 * h + lane;
-#if SMOL_OUT_UNROLL > 1
-        // predicated (no break) so the compiler can interleave unrolled tasks
+        // (predicated, no break, so the compiler can interleave unrolled tasks)
         const bool live = t0 < ntasko;
+        if (kPer == 1 && !live) break;
         const int t = live ? t0 : ntasko - 1;
-#else
-        if (t0 >= ntasko) break;
-        const bool live = true;
-        const int t = t0;
-#endif
         const int rr = (int)fdiv((uint32_t)t, fd_q4);
         const int r = done_prev + rr;
         const int ox = 4 * (t - rr * nq4);

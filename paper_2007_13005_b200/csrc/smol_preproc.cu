@@ -177,9 +177,26 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
   return SMOL_OK;
 }
 
+// Same geometry as the previous image of the batch (its size fields can be
+// reused: batches are mostly runs of equal-size images).
+inline bool same_geometry(const smol_image_desc* a, const smol_image_desc* b) {
+  return a->width == b->width && a->height == b->height && a->subsampling == b->subsampling &&
+         a->roi_left == b->roi_left && a->roi_top == b->roi_top;
+}
+inline void copy_geometry(const DevImage& from, DevImage& g) {
+  g.Wd = from.Wd; g.Hd = from.Hd; g.Wc = from.Wc; g.Hc = from.Hc;
+  g.Wr = from.Wr; g.Hr = from.Hr; g.left = from.left; g.top = from.top;
+}
+inline bool same_layout_inputs(const DevImage& a, const DevImage& b) {
+  return a.Wd == b.Wd && a.Hd == b.Hd && a.Wc == b.Wc && a.Hc == b.Hc && a.Wr == b.Wr && a.Hr == b.Hr &&
+         a.left == b.left && a.top == b.top && a.nbw[0] == b.nbw[0] && a.nbw[1] == b.nbw[1];
+}
+
 int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, int idx, int n_qtables,
-                       DevImage& g, bool need_align = true) {
-  int32_t rc = image_geometry(p, d, idx, g);
+                       DevImage& g, bool need_align = true, const DevImage* geom = nullptr) {
+  int32_t rc = SMOL_OK;
+  if (geom) copy_geometry(*geom, g);
+  else rc = image_geometry(p, d, idx, g);
   if (rc) return rc;
   const int need_w[3] = {ceil_div(d->width, 8), ceil_div(d->width, 16), ceil_div(d->width, 16)};
   const int need_h[3] = {ceil_div(d->height, 8), ceil_div(d->height, 16), ceil_div(d->height, 16)};
@@ -409,6 +426,8 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
   if (e == cudaSuccess) pl->layouts.reserve(max_images);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(smol_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kExpandSmem);
   if (e == cudaSuccess) {
     // opt every instantiation of this plan's (scale, dtype) in to the largest
     // dynamic smem the device allows next to the kernel's static smem
@@ -475,12 +494,16 @@ enum class Src { kDevice, kGather, kCompact };
 // Validate a compact image descriptor into its device descriptor (coefficient
 // pointers are set by the staging step).
 int32_t validate_compact_image(const smol_preproc_params* p, const smol_compact_image* ci, int idx,
-                               int n_qtables, DevImage& g) {
-  smol_image_desc d{};
-  d.width = ci->width; d.height = ci->height; d.subsampling = ci->subsampling;
-  d.roi_left = ci->roi_left; d.roi_top = ci->roi_top;
-  int32_t rc = image_geometry(p, &d, idx, g);
-  if (rc) return rc;
+                               int n_qtables, DevImage& g, const DevImage* geom = nullptr) {
+  if (geom) {
+    copy_geometry(*geom, g);
+  } else {
+    smol_image_desc d{};
+    d.width = ci->width; d.height = ci->height; d.subsampling = ci->subsampling;
+    d.roi_left = ci->roi_left; d.roi_top = ci->roi_top;
+    int32_t rc = image_geometry(p, &d, idx, g);
+    if (rc) return rc;
+  }
   if (ci->offset < 0 || ci->offset % 16)
     return fail(SMOL_ERR_INVALID, "image %d: record offset %lld not a non-negative multiple of 16", idx,
                 (long long)ci->offset);
@@ -551,9 +574,18 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   int ntiles = ceil_div(pl->OH, tile_rows);
   // validate every descriptor once
   for (int i = 0; i < n_images; ++i) {
-    int32_t rc = src == Src::kCompact
-        ? validate_compact_image(&pl->p, &static_cast<const smol_compact_image*>(images)[i], i, n_qtables, h[i])
-        : validate_image(&pl->p, &static_cast<const smol_image_desc*>(images)[i], i, n_qtables, h[i]);
+    int32_t rc;
+    if (src == Src::kCompact) {
+      const smol_compact_image* ci = static_cast<const smol_compact_image*>(images);
+      const bool same = i > 0 && ci[i].width == ci[i - 1].width && ci[i].height == ci[i - 1].height &&
+                        ci[i].subsampling == ci[i - 1].subsampling && ci[i].roi_left == ci[i - 1].roi_left &&
+                        ci[i].roi_top == ci[i - 1].roi_top;
+      rc = validate_compact_image(&pl->p, &ci[i], i, n_qtables, h[i], same ? &h[i - 1] : nullptr);
+    } else {
+      const smol_image_desc* di = static_cast<const smol_image_desc*>(images);
+      const bool same = i > 0 && same_geometry(&di[i], &di[i - 1]);
+      rc = validate_image(&pl->p, &di[i], i, n_qtables, h[i], true, same ? &h[i - 1] : nullptr);
+    }
     if (rc) return rc;
   }
   // shared memory of the largest tile over the batch's distinct geometries
@@ -634,7 +666,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     Ls.resize(n_images);
     for (int i = 0; i < n_images; ++i) {
       TileLayout& L = Ls[i];
-      tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L);
+      if (i > 0 && same_layout_inputs(h[i], h[i - 1])) L = Ls[i - 1];
+      else tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L);
       need = stage_layout(L, E, strides, offs, need);
       for (int c = 0; c < 3; ++c) {
         if (src == Src::kGather) {
@@ -740,7 +773,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     if (src == Src::kCompact) {
       // expand on the compute stream: the copy stream carries only copies,
       // so batch k+1's transfer overlaps batch k's expand + fused kernel
-      smol_expand_kernel<<<n_images, kExpandWarps * 32, 0, stream>>>(de);
+      smol_expand_kernel<<<n_images * kExpandSplit, kExpandWarps * 32, kExpandSmem, stream>>>(de);
       SMOL_CUDA(cudaGetLastError());
     }
   }
