@@ -271,7 +271,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="smol", choices=["smol", "reference"])
     ap.add_argument("--replicas", type=int, default=0, help="rotating input replicas (0 = auto: > L2)")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--tile-rows", type=int, default=0)
@@ -365,7 +365,7 @@ def main():
     res_host = torch.empty((1,) + tuple(out.shape[1:]), dtype=out.dtype, pin_memory=True)
 
     def e2e_time(host_batches):
-        for k in range(3):
+        for k in range(6):
             plan.run(host_batches[k % 2], out=out, stream=stream)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

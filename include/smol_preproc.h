@@ -152,18 +152,19 @@ int32_t smol_preproc_run_host(smol_preproc_plan_t* plan, const smol_batch_desc* 
  * same ranges smol_debug_geometry reports) and, per block, only the nonzero
  * coefficients among those the plan's scale uses (reading R1):
  *
- *   offset 0   header, 64 B: uint32 magic 0x31434D53 ("SMC1"), uint32 E
- *              (elements per block of the plan's layout), uint32 n_values,
- *              uint32 0, int32 bx0[3], by0[3], nbx[3], nby[3] (ROI block
- *              ranges per component Y, Cb, Cr)
- *   64         uint64 bitmap[nblocks]: per ROI block (component-major, then
- *              block-raster), bit e set <=> element e of the layout block is
- *              nonzero
- *   ..         uint32 row_start[nrows]: per ROI block row (component-major),
- *              index of the row's first value in values[]
- *   align 16   int16 values[n_values]: the nonzero elements, in block order
- *              and ascending element index within a block
- *   +2, align 16  (end: >= 2 zero bytes after the values; record size is a
+ *   offset 0   header, 64 B: uint32 magic 0x32434D53 ("SMC2"), uint32 E
+ *              (elements per block of the plan's layout), uint32 n_units
+ *              (u16 units of the entry stream), uint32 0, int32 bx0[3], by0[3],
+ *              nbx[3], nby[3] (ROI block ranges per component Y, Cb, Cr)
+ *   64         uint8 len[nblocks]: per ROI block (component-major, then
+ *              block-raster), the units of its entries (<= 128)
+ *   align 4    uint32 row_start[nrows]: per ROI block row (component-major),
+ *              index of the row's first unit in the entry stream
+ *   align 16   uint16 entry stream: per block, one entry per nonzero element
+ *              in ascending element index e: the unit e | v << 6 when
+ *              -511 <= v <= 511 (v as 10-bit two's complement), else the
+ *              escape e | (-512 << 6) followed by v as int16
+ *   +2, align 16  (end: >= 2 zero bytes after the stream; record size is a
  *              multiple of 16)
  *
  * Everything outside the ROI and every element the scale does not use

@@ -9,11 +9,11 @@
 
 namespace smol {
 
-constexpr uint32_t kCompactMagic = 0x31434D53u;   // "SMC1"
+constexpr uint32_t kCompactMagic = 0x32434D53u;   // "SMC2"
 constexpr int kCompactHeader = 64;
 
 struct CompactHeader {            // the 64-byte record header
-  uint32_t magic, E, n_values, zero;
+  uint32_t magic, E, n_units, zero;      // n_units: u16 units of the entry stream
   int32_t bx0[3], by0[3], nbx[3], nby[3];
 };
 static_assert(sizeof(CompactHeader) == kCompactHeader, "compact header is 64 bytes");
@@ -36,15 +36,22 @@ inline uint64_t used_mask(int K, bool packed) {
   return m;
 }
 
-// Record section offsets (bytes) for `nblocks` ROI blocks in `nrows` block rows.
-SMOL_HD int64_t compact_rowstart_off(int64_t nblocks) { return kCompactHeader + 8 * nblocks; }
-SMOL_HD int64_t compact_values_off(int64_t nblocks, int64_t nrows) {
+// Entry of one nonzero coefficient: u16 = pos | v << 6 (pos = element index
+// in the stored block, v = value as 10-bit two's complement) for
+// -511 <= v <= 511; otherwise the escape pos | (-512 << 6) followed by the
+// int16 value in the next unit.
+constexpr int kEscape = -512;
+
+// Record section offsets (bytes) for `nblocks` ROI blocks in `nrows` block
+// rows: u8 block lengths (units) at 64, u32 row starts (4-B aligned), entry
+// stream (16-B aligned; at least 2 zero bytes follow it, so a 32-bit load of
+// the last unit stays inside the record).
+SMOL_HD int64_t compact_rowstart_off(int64_t nblocks) { return (kCompactHeader + nblocks + 3) & ~3LL; }
+SMOL_HD int64_t compact_entries_off(int64_t nblocks, int64_t nrows) {
   return (compact_rowstart_off(nblocks) + 4 * nrows + 15) & ~15LL;
 }
-// (at least 2 zero bytes follow the values, so a 32-bit load of the last value
-// stays inside the record)
-SMOL_HD int64_t compact_record_bytes(int64_t nblocks, int64_t nrows, int64_t nvalues) {
-  return (compact_values_off(nblocks, nrows) + 2 * nvalues + 2 + 15) & ~15LL;
+SMOL_HD int64_t compact_record_bytes(int64_t nblocks, int64_t nrows, int64_t nunits) {
+  return (compact_entries_off(nblocks, nrows) + 2 * nunits + 2 + 15) & ~15LL;
 }
 
 // One image to expand: record (device) -> staged ROI rows of the plan's layout.
@@ -57,24 +64,24 @@ struct ExpandDesc {
 };
 
 #if defined(__CUDACC__)
-constexpr int kExpandWarps = 8;
-constexpr int kExpandChunkVals = 32 * 64 + 8;  // values of one 32-block chunk (worst case) + alignment slack
+constexpr int kExpandWarps = 4;
+constexpr int kExpandChunkVals = 32 * 128 + 8; // entry units of one 32-block chunk (worst case: all escaped) + slack
 // per-lane block buffers are padded by 8 bytes (lane stride 2E + 8 bytes) so
 // the lanes' zeroing/scatter stores do not all land in one shared-memory bank
 constexpr int kExpandLanePad = 4;               // int16 elements
 constexpr int kExpandBlkBuf = 32 * (64 + kExpandLanePad);
 // dynamic shared memory per CTA: per warp a 32-block output buffer + the chunk's values
 constexpr int kExpandSmem = kExpandWarps * (kExpandBlkBuf * 2 + kExpandChunkVals * 2);
-constexpr int kExpandSplit = 4;                 // CTAs per image (block rows interleaved)
+constexpr int kExpandSplit = 8;                 // CTAs per image (block rows interleaved)
 
 // kExpandSplit CTAs per image (block rows interleaved); a warp expands one ROI
 // block row at a time, 32 blocks (one per lane) per chunk:
-//   1. each lane reads its block's bitmap; a warp scan of the popcounts gives
-//      each block's first value;
-//   2. the chunk's values (contiguous in the record) are copied to shared
+//   1. each lane reads its block's entry length; a warp scan gives each
+//      block's first entry;
+//   2. the chunk's entries (contiguous in the record) are copied to shared
 //      memory with independent coalesced loads;
-//   3. each lane zeroes its block in a shared buffer and scatters its nonzero
-//      values into it (one iteration per set bit);
+//   3. each lane zeroes its block in a shared buffer and scatters its entries
+//      into it;
 //   4. the chunk's 32 blocks are contiguous in the staged row: the warp copies
 //      the buffer out with coalesced 8-byte stores.
 // E = 1 (DC plane): lane per block, direct store.
@@ -91,22 +98,21 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
   const int nb0 = e.nbx[0] * e.nby[0], nb1 = e.nbx[1] * e.nby[1], nb2 = e.nbx[2] * e.nby[2];
   const int r1 = e.nby[0], r2 = e.nby[0] + e.nby[1], nrows = r2 + e.nby[2];
   const int nblocks = nb0 + nb1 + nb2;
-  const uint64_t* bm_all = reinterpret_cast<const uint64_t*>(e.rec + kCompactHeader);
+  const uint8_t* len_all = e.rec + kCompactHeader;
   const uint32_t* rowst = reinterpret_cast<const uint32_t*>(e.rec + compact_rowstart_off(nblocks));
-  const int16_t* vals = reinterpret_cast<const int16_t*>(e.rec + compact_values_off(nblocks, nrows));
+  const uint16_t* units = reinterpret_cast<const uint16_t*>(e.rec + compact_entries_off(nblocks, nrows));
   for (int gr = part * kExpandWarps + warp; gr < nrows; gr += kExpandWarps * kExpandSplit) {
     const int c = gr >= r2 ? 2 : gr >= r1 ? 1 : 0;
     const int r = gr - (c == 2 ? r2 : c == 1 ? r1 : 0);
     const int nbx = c == 2 ? e.nbx[2] : c == 1 ? e.nbx[1] : e.nbx[0];
-    const uint64_t* bm = bm_all + (c == 2 ? nb0 + nb1 : c == 1 ? nb0 : 0) + (int64_t)r * nbx;
+    const uint8_t* lens = len_all + (c == 2 ? nb0 + nb1 : c == 1 ? nb0 : 0) + (int64_t)r * nbx;
     int16_t* const dst_c = c == 2 ? e.dst[2] : c == 1 ? e.dst[1] : e.dst[0];
     const int stride_c = c == 2 ? e.dst_stride[2] : c == 1 ? e.dst_stride[1] : e.dst_stride[0];
     int16_t* drow = dst_c + (int64_t)r * stride_c;
     uint32_t vbase = __ldg(rowst + gr);
     for (int ch = 0; ch < nbx; ch += 32) {
       const int b = ch + lane;
-      uint64_t m = b < nbx ? __ldg(bm + b) : 0ull;
-      const int cnt = __popcll(m);
+      const int cnt = b < nbx ? (int)__ldg(lens + b) : 0;   // units of this block's entries
       int inc = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -114,29 +120,37 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
         if (lane >= o) inc += t;
       }
       const int total = __shfl_sync(0xffffffffu, inc, 31);
-      // 2. stage the chunk's values (32-bit loads from the 4-B aligned start)
-      const int16_t* src = vals + vbase;
-      const int mis = (int)(reinterpret_cast<uintptr_t>(src) & 3) >> 1;     // 0 or 1 element
+      // 2. stage the chunk's entry units (32-bit loads from the 4-B aligned start)
+      const uint16_t* src = units + vbase;
+      const int mis = (int)(reinterpret_cast<uintptr_t>(src) & 3) >> 1;     // 0 or 1 unit
       const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src - mis);
       const int nw = (total + mis + 1) >> 1;
       uint32_t* b32 = reinterpret_cast<uint32_t*>(buf);
       for (int w = lane; w < nw; w += 32) b32[w] = __ldg(s32 + w);
       const int nb = min(32, nbx - ch);
+      const uint16_t* ub = reinterpret_cast<const uint16_t*>(buf) + mis + (inc - cnt);
       if (E == 1) {
         __syncwarp();
-        if (b < nbx) drow[b] = m ? buf[mis + inc - cnt] : (int16_t)0;
+        if (b < nbx) {
+          int16_t v = 0;
+          if (cnt) {
+            v = (int16_t)ub[0] >> 6;
+            if (v == kEscape) v = (int16_t)ub[1];
+          }
+          drow[b] = v;
+        }
       } else {
         // 3. zero + scatter this lane's block (E*2 bytes, a multiple of 8)
         const int ls = E + kExpandLanePad;                 // lane stride (elements)
         int16_t* mine = blk + lane * ls;
         uint2* m8 = reinterpret_cast<uint2*>(mine);
         for (int q = 0; q < E / 4; ++q) m8[q] = make_uint2(0u, 0u);
-        __syncwarp();                                       // staged values visible
-        int k = mis + inc - cnt;
-        while (m) {
-          const int el = __ffsll((long long)m) - 1;
-          m &= m - 1;
-          mine[el] = buf[k++];
+        __syncwarp();                                       // staged entries visible
+        for (int j = 0; j < cnt; ++j) {
+          const uint16_t u = ub[j];
+          int16_t v = (int16_t)u >> 6;
+          if (v == kEscape) v = (int16_t)ub[++j];
+          mine[u & 63] = v;
         }
         __syncwarp();
         // 4. copy the nb blocks out (contiguous in the staged row): 8-byte

@@ -730,7 +730,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
         const ExpandDesc& e = he[i];
         int64_t nblocks = 0, nrows = 0;
         for (int c = 0; c < 3; ++c) { nblocks += (int64_t)e.nbx[c] * e.nby[c]; nrows += e.nby[c]; }
-        int64_t bytes = compact_values_off(nblocks, nrows);
+        int64_t bytes = compact_entries_off(nblocks, nrows);
         if (ci[i].offset + bytes > cb->arena_bytes)
           return fail(SMOL_ERR_INVALID, "image %d: record at %lld (>= %lld B) outside arena of %lld B", i,
                       (long long)ci[i].offset, (long long)bytes, (long long)cb->arena_bytes);
@@ -744,7 +744,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
           if (!ok)
             return fail(SMOL_ERR_INVALID, "image %d: compact record header does not match this plan's "
                         "layout/ROI (bad magic, E or block ranges)", i);
-          bytes = compact_record_bytes(nblocks, nrows, hd.n_values);
+          bytes = compact_record_bytes(nblocks, nrows, hd.n_units);
           if (ci[i].offset + bytes > cb->arena_bytes)
             return fail(SMOL_ERR_INVALID, "image %d: record (%lld B) overruns the arena", i, (long long)bytes);
         }
@@ -809,38 +809,43 @@ int32_t run_batch(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, 
 // Compact record of one image (format: include/smol_preproc.h).  Pass 1
 // (dst == NULL) counts, pass 2 writes.
 int64_t compact_encode_pass(const smol_image_desc* d, const TileLayout& L, int E, uint64_t mask,
-                            uint8_t* dst, uint32_t* n_values_out) {
+                            uint8_t* dst, uint32_t* n_units_out) {
   int64_t nblocks = 0, nrows = 0;
   for (int c = 0; c < 3; ++c) {
     nblocks += (int64_t)(L.bx1[c] - L.bx0[c] + 1) * (L.by1[c] - L.by0[c] + 1);
     nrows += L.by1[c] - L.by0[c] + 1;
   }
-  uint64_t* bm = dst ? reinterpret_cast<uint64_t*>(dst + kCompactHeader) : nullptr;
+  uint8_t* lens = dst ? dst + kCompactHeader : nullptr;
   uint32_t* rs = dst ? reinterpret_cast<uint32_t*>(dst + compact_rowstart_off(nblocks)) : nullptr;
-  int16_t* vals = dst ? reinterpret_cast<int16_t*>(dst + compact_values_off(nblocks, nrows)) : nullptr;
-  uint32_t nv = 0;
+  uint16_t* units = dst ? reinterpret_cast<uint16_t*>(dst + compact_entries_off(nblocks, nrows)) : nullptr;
+  uint32_t nu = 0;
   int64_t bi = 0, ri = 0;
   for (int c = 0; c < 3; ++c) {
     const int stride = d->row_stride_bytes[c] / 2;
     for (int by = L.by0[c]; by <= L.by1[c]; ++by) {
-      if (rs) rs[ri] = nv;
+      if (rs) rs[ri] = nu;
       ++ri;
       for (int bx = L.bx0[c]; bx <= L.bx1[c]; ++bx) {
         const int16_t* blk = d->coef[c] + (size_t)by * stride + (size_t)bx * E;
-        uint64_t m = 0;
-        for (int e = 0; e < E; ++e)
-          if (((mask >> e) & 1) && blk[e] != 0) {
-            m |= 1ull << e;
-            if (vals) vals[nv] = blk[e];
-            ++nv;
+        const uint32_t first = nu;
+        for (int e = 0; e < E; ++e) {
+          const int v = blk[e];
+          if (!((mask >> e) & 1) || v == 0) continue;
+          if (v >= -511 && v <= 511) {
+            if (units) units[nu] = (uint16_t)(e | (v << 6));
+            nu += 1;
+          } else {
+            if (units) { units[nu] = (uint16_t)(e | (kEscape << 6)); units[nu + 1] = (uint16_t)(int16_t)v; }
+            nu += 2;
           }
-        if (bm) bm[bi] = m;
+        }
+        if (lens) lens[bi] = (uint8_t)(nu - first);          // <= 2 * 64
         ++bi;
       }
     }
   }
-  *n_values_out = nv;
-  return compact_record_bytes(nblocks, nrows, nv);
+  *n_units_out = nu;
+  return compact_record_bytes(nblocks, nrows, nu);
 }
 
 }  // namespace
@@ -906,7 +911,7 @@ int32_t smol_compact_encode(const smol_preproc_params* p, const smol_image_desc*
   CompactHeader hd{};
   hd.magic = kCompactMagic;
   hd.E = (uint32_t)E;
-  hd.n_values = nv;
+  hd.n_units = nv;
   for (int c = 0; c < 3; ++c) {
     hd.bx0[c] = L.bx0[c]; hd.by0[c] = L.by0[c];
     hd.nbx[c] = L.bx1[c] - L.bx0[c] + 1; hd.nby[c] = L.by1[c] - L.by0[c] + 1;

@@ -18,38 +18,46 @@ import paper_2007_13005_b200 as smol
 import synth
 from paper_2007_13005_b200 import layout as lay
 
-MAGIC = 0x31434D53
+MAGIC = 0x32434D53
 
 
 def read_record(rec: np.ndarray):
-    """Parse one record -> (E, ranges, {(c, by, bx): int16[E] block})."""
+    """Parse one record (format: include/smol_preproc.h) ->
+    (E, ranges, {(c, by, bx): int16[E] block})."""
     b = rec.tobytes()
-    magic, E, nval, zero = struct.unpack_from("<4I", b, 0)
+    magic, E, nunits, zero = struct.unpack_from("<4I", b, 0)
     assert magic == MAGIC and zero == 0
     f = struct.unpack_from("<12i", b, 16)
     bx0, by0, nbx, nby = f[0:3], f[3:6], f[6:9], f[9:12]
     nblocks = sum(nbx[c] * nby[c] for c in range(3))
     nrows = sum(nby)
-    bm = np.frombuffer(b, np.uint64, nblocks, 64)
-    rs = np.frombuffer(b, np.uint32, nrows, 64 + 8 * nblocks)
-    voff = -(-(64 + 8 * nblocks + 4 * nrows) // 16) * 16
-    vals = np.frombuffer(b, np.int16, nval, voff)
-    assert len(b) == -(-(voff + 2 * nval + 2) // 16) * 16
+    lens = np.frombuffer(b, np.uint8, nblocks, 64)
+    rso = -(-(64 + nblocks) // 4) * 4
+    rs = np.frombuffer(b, np.uint32, nrows, rso)
+    uoff = -(-(rso + 4 * nrows) // 16) * 16
+    units = np.frombuffer(b, np.uint16, nunits, uoff)
+    assert len(b) == -(-(uoff + 2 * nunits + 2) // 16) * 16
     blocks = {}
     k = bi = ri = 0
     for c in range(3):
         for r in range(nby[c]):
-            assert rs[ri] == k               # row starts index the value array
+            assert rs[ri] == k               # row starts index the entry stream
             ri += 1
             for x in range(nbx[c]):
-                m = int(bm[bi]); bi += 1
+                end = k + int(lens[bi]); bi += 1
                 blk = np.zeros(E, np.int16)
-                for e in range(E):
-                    if (m >> e) & 1:
-                        blk[e] = vals[k]; k += 1
-                assert m >> E == 0
+                last = -1
+                while k < end:
+                    u = int(units[k]); k += 1
+                    pos, v = u & 63, (u >> 6) - (1024 if u >> 15 else 0)
+                    if v == -512:
+                        v = int(np.int16(units[k])); k += 1
+                        assert not -511 <= v <= 511      # escapes only for large values
+                    assert v != 0 and pos > last and pos < E
+                    last = pos
+                    blk[pos] = v
                 blocks[(c, by0[c] + r, bx0[c] + x)] = blk
-    assert k == nval
+    assert k == nunits
     return E, (bx0, by0, nbx, nby), blocks
 
 
@@ -87,6 +95,22 @@ def test_encoder_roundtrip_against_python_reader(name, layout, quality):
             want = np.zeros(E, np.int16)
             want[used] = src[used]
             np.testing.assert_array_equal(blk, want, err_msg=f"{name} comp {c} block ({by},{bx})")
+
+
+def test_encoder_roundtrip_stress_escapes():
+    """Dense uniform coefficients with small quantisers: many |v| > 511 (escape
+    entries) and odd sizes."""
+    rng = np.random.default_rng(13005)
+    qt = synth.quant_tables(95)
+    p = smol.params_from_config(synth.CONFIGS["c2"], resize_short=64, crop_w=48, crop_h=40)
+    n_esc = 0
+    for (w, h) in [(97, 61), (200, 333), (64, 64)]:
+        im = synth.make_image(rng, w, h, qt, mode="stress")
+        E, _, blocks = read_record(smol.compact_encode(p, im))
+        for (c, by, bx), blk in blocks.items():
+            np.testing.assert_array_equal(blk, np.asarray(im.coef[c][by, bx], np.int16))
+            n_esc += int((np.abs(blk.astype(np.int32)) > 511).sum())
+    assert n_esc > 100
 
 
 def test_encoder_size_query_capacity_and_compression():
