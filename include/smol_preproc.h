@@ -81,7 +81,10 @@ typedef struct {
 /* One entropy-decoded 4:2:0 image. */
 typedef struct {
   int32_t width, height;           /* SOF size in pixels, > 0                        */
-  int32_t subsampling;             /* 420 (anything else: SMOL_ERR_UNSUPPORTED)      */
+  int32_t subsampling;             /* 420, or 400 = grayscale (one component, T.81
+                                      Nf = 1: coef[1..2], their blocks/strides and
+                                      qtable[1..2] are ignored; R = G = B = Y);
+                                      anything else: SMOL_ERR_UNSUPPORTED            */
   int32_t qtable[3];               /* Y, Cb, Cr index into batch qtables             */
   const int16_t* coef[3];          /* DEVICE (or pinned HOST for run_host):
                                       [blocks_h][blocks_w][E] int16 blocks of the
@@ -173,7 +176,8 @@ int32_t smol_preproc_run_host(smol_preproc_plan_t* plan, const smol_batch_desc* 
  * smol_preproc_run on the dense planes. */
 typedef struct {
   int32_t width, height;           /* SOF size in pixels, > 0                        */
-  int32_t subsampling;             /* 420                                            */
+  int32_t subsampling;             /* 420 or 400 (grayscale: the record has no
+                                      chroma rows)                                   */
   int32_t qtable[3];               /* Y, Cb, Cr index into batch qtables             */
   int32_t roi_left, roi_top;       /* as smol_image_desc (-1,-1 = centre crop)       */
   int64_t offset;                  /* byte offset of the image's record in `arena`,

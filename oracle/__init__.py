@@ -189,6 +189,9 @@ def _image(im, qtables: np.ndarray, keep: list) -> _Image:
     c = _Image()
     c.width, c.height = im.width, im.height
     for ci in range(3):
+        if ci >= len(im.coef):               # grayscale: one component
+            c.comp[ci] = _Plane()
+            continue
         coef = np.ascontiguousarray(im.coef[ci], dtype=np.int16)
         q = np.ascontiguousarray(qtables[im.qidx[ci]], dtype=np.uint16)
         keep += [coef, q]
@@ -223,11 +226,12 @@ def run_batch(p: _Params, imgs: Sequence, qtables: np.ndarray, threads: int = 1,
 
 
 def decode_image_planes(p: _Params, im, qtables: np.ndarray, with_v: bool = False):
-    """Decoded u8 Y, Cb, Cr planes (and optional unrounded v) at p's scale."""
+    """Decoded u8 Y, Cb, Cr planes (Y only for a grayscale image) and optional
+    unrounded v at p's scale."""
     g = geometry(p, im.width, im.height)
     k = p.scale_denom
     out = []
-    for ci in range(3):
+    for ci in range(len(im.coef)):
         w, h = (g.Wd, g.Hd) if ci == 0 else (g.Wc, g.Hc)
         v, u8 = decode_plane(im.coef[ci], qtables[im.qidx[ci]], k, w, h)
         out.append((v, u8) if with_v else u8)

@@ -290,9 +290,16 @@ int oracle_run_image(const oracle_params* p, const oracle_image* im, int32_t lef
   rc = 10;
   if (Y && Cb && Cr && rgb) {
     rc = oracle_decode_plane(&im->comp[0], p->scale_denom, g.Wd, g.Hd, NULL, Y);
-    if (!rc) rc = oracle_decode_plane(&im->comp[1], p->scale_denom, g.Wc, g.Hc, NULL, Cb);
-    if (!rc) rc = oracle_decode_plane(&im->comp[2], p->scale_denom, g.Wc, g.Hc, NULL, Cr);
-    if (!rc) rc = oracle_upsample_color(Y, g.Wd, g.Hd, Cb, Cr, g.Wc, g.Hc, NULL, rgb);
+    if (im->comp[1].coef == NULL) {
+      /* grayscale (one component, T.81 A.1.1 Nf = 1): the JFIF colour space
+       * is Y only, i.e. R = G = B = Y (R6 with Cb = Cr = 128) */
+      for (int32_t i = 0; !rc && i < g.Wd * g.Hd; ++i)
+        rgb[3 * i] = rgb[3 * i + 1] = rgb[3 * i + 2] = Y[i];
+    } else {
+      if (!rc) rc = oracle_decode_plane(&im->comp[1], p->scale_denom, g.Wc, g.Hc, NULL, Cb);
+      if (!rc) rc = oracle_decode_plane(&im->comp[2], p->scale_denom, g.Wc, g.Hc, NULL, Cr);
+      if (!rc) rc = oracle_upsample_color(Y, g.Wd, g.Hd, Cb, Cr, g.Wc, g.Hc, NULL, rgb);
+    }
     if (!rc) rc = oracle_resize_crop_normalize(rgb, g.Wd, g.Hd, g.Wr, g.Hr, g.left, g.top,
                                                g.OW, g.OH, p->mean, p->std, p->out_f16, out, NULL);
   }

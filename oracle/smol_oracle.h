@@ -41,7 +41,8 @@ typedef struct {
 
 typedef struct {
   int32_t width, height;      /* SOF size in pixels */
-  oracle_plane comp[3];       /* Y, Cb, Cr (4:2:0) */
+  oracle_plane comp[3];       /* Y, Cb, Cr (4:2:0); comp[1].coef == NULL: grayscale
+                                 (one component; R = G = B = Y) */
 } oracle_image;
 
 typedef struct {

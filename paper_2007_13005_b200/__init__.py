@@ -63,20 +63,24 @@ def params_from_config(cfg, **kw) -> Params:
 
 
 def _desc_for(width, height, blocks_w, blocks_h, qidx=(0, 1, 1), roi=None, strides=None) -> ImageDesc:
+    """Descriptor of a 4:2:0 image (3 planes) or a grayscale one (1 plane:
+    subsampling 400, chroma fields zero)."""
     d = ImageDesc()
-    d.width, d.height, d.subsampling = width, height, 420
-    d.qtable = (ctypes.c_int32 * 3)(*qidx)
-    for c in range(3):
+    gray = len(blocks_w) == 1
+    d.width, d.height, d.subsampling = width, height, 400 if gray else 420
+    d.qtable = (ctypes.c_int32 * 3)(*(tuple(qidx) + (0, 0, 0))[:3])
+    for c in range(len(blocks_w)):
         d.blocks_w[c], d.blocks_h[c] = blocks_w[c], blocks_h[c]
         d.row_stride_bytes[c] = blocks_w[c] * 128 if strides is None else strides[c]
     d.roi_left, d.roi_top = roi if roi is not None else (-1, -1)
     return d
 
 
-def geometry(params: Params, width: int, height: int, roi=None) -> dict:
+def geometry(params: Params, width: int, height: int, roi=None, gray: bool = False) -> dict:
     """Host-only geometry of one image (smol_debug_geometry)."""
-    d = _desc_for(width, height, [(width + 7) // 8, (width + 15) // 16, (width + 15) // 16],
-                  [(height + 7) // 8, (height + 15) // 16, (height + 15) // 16], roi=roi)
+    n = 1 if gray else 3
+    d = _desc_for(width, height, [(width + 7) // 8, (width + 15) // 16, (width + 15) // 16][:n],
+                  [(height + 7) // 8, (height + 15) // 16, (height + 15) // 16][:n], roi=roi)
     g = Geometry()
     check(lib().smol_debug_geometry(ctypes.byref(params), ctypes.byref(d), ctypes.byref(g)))
     return g.as_dict()
@@ -113,7 +117,7 @@ class CoefBatch:
         o = 0
         for ps, s in zip(planes, sizes):
             oo = []
-            for ci in range(3):
+            for ci in range(len(ps)):
                 host[o:o + s[ci]] = ps[ci].ravel()
                 oo.append(o)
                 o += s[ci]                      # every plane row is a multiple of 16 bytes
@@ -137,7 +141,7 @@ class CoefBatch:
             d = _desc_for(im.width, im.height, [c.shape[1] for c in im.coef],
                           [c.shape[0] for c in im.coef], tuple(im.qidx), roi,
                           strides=[2 * p.shape[1] for p in planes[i]])
-            for ci in range(3):
+            for ci in range(len(im.coef)):
                 d.coef[ci] = base + 2 * oo[ci]
             self.descs[i] = d
         self.desc = BatchDesc()
@@ -158,7 +162,7 @@ def compact_encode(params: Params, im, roi=None) -> np.ndarray:
     planes = [pack_plane(np.ascontiguousarray(c, dtype=np.int16), k) for c in im.coef]
     d = _desc_for(im.width, im.height, [c.shape[1] for c in im.coef], [c.shape[0] for c in im.coef],
                   tuple(im.qidx), roi, strides=[2 * p.shape[1] for p in planes])
-    for ci in range(3):
+    for ci in range(len(planes)):
         d.coef[ci] = planes[ci].ctypes.data
     n = ctypes.c_int64()
     check(lib().smol_compact_encode(ctypes.byref(params), ctypes.byref(d), None, 0, ctypes.byref(n)))
@@ -207,8 +211,9 @@ class CompactBatch:
         self.images = (CompactImage * max(self.n, 1))()
         for i, (im, oo) in enumerate(zip(images, offs)):
             ci = CompactImage()
-            ci.width, ci.height, ci.subsampling = im.width, im.height, 420
-            ci.qtable = (ctypes.c_int32 * 3)(*tuple(im.qidx))
+            ci.width, ci.height = im.width, im.height
+            ci.subsampling = 400 if len(im.coef) == 1 else 420
+            ci.qtable = (ctypes.c_int32 * 3)(*(tuple(im.qidx) + (0, 0, 0))[:3])
             roi = rois[i] if rois is not None else None
             ci.roi_left, ci.roi_top = roi if roi is not None else (-1, -1)
             ci.offset = oo

@@ -41,6 +41,7 @@ struct __align__(16) DevImage {
   int32_t Wc, Hc;           // decoded chroma size
   int32_t Wr, Hr;           // resized size
   int32_t left, top;        // crop origin in resized coordinates
+  int32_t gray;             // 1: one component (subsampling 400): no chroma blocks, Cb = Cr = 128
 };
 
 // Reading R9: the half-pixel bilinear source index of destination index d
@@ -129,6 +130,10 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
     L.by0[c] = L.cy0 / P; L.by1[c] = L.cy1 / P;
     L.bx0[c] = L.cx0 / P; L.bx1[c] = L.cx1 / P;
   }
+  // grayscale: no chroma block rows (the kernel fills the chroma rings with
+  // 128, the neutral value, so colour conversion gives R = G = B = Y)
+  if (im.gray)
+    for (int c = 1; c < 3; ++c) L.by1[c] = L.by0[c] - 1;
   for (int c = 0; c < 3; ++c) L.xbase[c] = L.bx0[c] * P;
   L.rgb_x0 = L.lx0 & ~3;
   L.rgb_w = ((L.lx1 | 3) - L.rgb_x0 + 1);

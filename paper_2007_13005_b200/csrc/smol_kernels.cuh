@@ -558,6 +558,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     src_tap(im.top + oy0 + i, im.Hd, im.Hr, i0, i1, w);
     yt[i] = make_int2((rgb_slot(i0) * pitch4) | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
   }
+  if (im.gray)       // grayscale: neutral chroma everywhere in the rings (read only by colour)
+    for (int i = tid; i < 2 * kCStride / 4; i += kThreads) reinterpret_cast<uint32_t*>(cring)[i] = 0x80808080u;
   const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
   const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
   const int ntask4 = L.rgb_w >> 2;          // 4-column colour tasks per quad row

@@ -145,8 +145,9 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
     return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d must be > 0", idx, d->width, d->height);
   if (d->width > 65535 || d->height > 65535)
     return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d > 65535 (JPEG limit)", idx, d->width, d->height);
-  if (d->subsampling != 420)
-    return fail(SMOL_ERR_UNSUPPORTED, "image %d: subsampling=%d (only 420)", idx, d->subsampling);
+  if (d->subsampling != 420 && d->subsampling != 400)
+    return fail(SMOL_ERR_UNSUPPORTED, "image %d: subsampling=%d (420 or 400 only)", idx, d->subsampling);
+  g.gray = d->subsampling == 400;
   g.Wd = ceil_div(d->width, k);
   g.Hd = ceil_div(d->height, k);
   g.Wc = ceil_div(d->width, 2 * k);
@@ -186,10 +187,12 @@ inline bool same_geometry(const smol_image_desc* a, const smol_image_desc* b) {
 inline void copy_geometry(const DevImage& from, DevImage& g) {
   g.Wd = from.Wd; g.Hd = from.Hd; g.Wc = from.Wc; g.Hc = from.Hc;
   g.Wr = from.Wr; g.Hr = from.Hr; g.left = from.left; g.top = from.top;
+  g.gray = from.gray;
 }
 inline bool same_layout_inputs(const DevImage& a, const DevImage& b) {
   return a.Wd == b.Wd && a.Hd == b.Hd && a.Wc == b.Wc && a.Hc == b.Hc && a.Wr == b.Wr && a.Hr == b.Hr &&
-         a.left == b.left && a.top == b.top && a.nbw[0] == b.nbw[0] && a.nbw[1] == b.nbw[1];
+         a.left == b.left && a.top == b.top && a.nbw[0] == b.nbw[0] && a.nbw[1] == b.nbw[1] &&
+         a.gray == b.gray;
 }
 
 int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, int idx, int n_qtables,
@@ -202,6 +205,11 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
   const int need_h[3] = {ceil_div(d->height, 8), ceil_div(d->height, 16), ceil_div(d->height, 16)};
   static const char* names[3] = {"Y", "Cb", "Cr"};
   for (int c = 0; c < 3; ++c) {
+    g.nbw[c] = need_w[c];
+    if (c > 0 && g.gray) {             // grayscale: chroma fields are ignored
+      g.coef[c] = nullptr; g.stride[c] = 0; g.qidx[c] = 0;
+      continue;
+    }
     if (!d->coef[c]) return fail(SMOL_ERR_INVALID, "image %d: coef[%d] (%s) is NULL", idx, c, names[c]);
     if (need_align && reinterpret_cast<uintptr_t>(d->coef[c]) % 16)
       return fail(SMOL_ERR_INVALID, "image %d: coef[%d] not 16-byte aligned", idx, c);
@@ -508,9 +516,12 @@ int32_t validate_compact_image(const smol_preproc_params* p, const smol_compact_
     return fail(SMOL_ERR_INVALID, "image %d: record offset %lld not a non-negative multiple of 16", idx,
                 (long long)ci->offset);
   for (int c = 0; c < 3; ++c) {
-    if (ci->qtable[c] < 0 || ci->qtable[c] >= n_qtables)
-      return fail(SMOL_ERR_INVALID, "image %d: qtable[%d]=%d not in [0,%d)", idx, c, ci->qtable[c], n_qtables);
-    g.qidx[c] = ci->qtable[c];
+    g.qidx[c] = 0;
+    if (!(c > 0 && g.gray)) {
+      if (ci->qtable[c] < 0 || ci->qtable[c] >= n_qtables)
+        return fail(SMOL_ERR_INVALID, "image %d: qtable[%d]=%d not in [0,%d)", idx, c, ci->qtable[c], n_qtables);
+      g.qidx[c] = ci->qtable[c];
+    }
     g.nbw[c] = ceil_div(ci->width, c ? 16 : 8);
     g.coef[c] = nullptr;
     g.stride[c] = 0;
@@ -863,7 +874,7 @@ int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b,
   // fused kernel), then the fused kernel runs on `stream`.
   // Probe image 0's planes (a batch normally comes from one pinned arena).
   if (b && b->images && b->n_images > 0) {
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < (b->images[0].subsampling == 400 ? 1 : 3); ++c) {
       cudaPointerAttributes a;
       if (cudaPointerGetAttributes(&a, b->images[0].coef[c]) != cudaSuccess ||
           (a.type != cudaMemoryTypeHost && a.type != cudaMemoryTypeDevice &&

@@ -75,11 +75,16 @@ def quant_tables(quality: int) -> np.ndarray:
 
 @dataclasses.dataclass
 class CoefImage:
-    """One entropy-decoded 4:2:0 JPEG: 3 coefficient planes [bh][bw][64] int16."""
+    """One entropy-decoded JPEG: 3 coefficient planes [bh][bw][64] int16
+    (4:2:0 Y, Cb, Cr) or 1 (grayscale Y)."""
     width: int
     height: int
-    coef: List[np.ndarray]                 # Y, Cb, Cr
-    qidx: Tuple[int, int, int] = (0, 1, 1)
+    coef: List[np.ndarray]                 # Y, Cb, Cr  (or Y only)
+    qidx: Tuple[int, ...] = (0, 1, 1)
+
+    @property
+    def gray(self) -> bool:
+        return len(self.coef) == 1
 
     @property
     def blocks_w(self):
@@ -226,6 +231,15 @@ def encode_420(rgb: np.ndarray, qtables: np.ndarray) -> CoefImage:
     return CoefImage(w, h, coef)
 
 
+def encode_gray(rgb: np.ndarray, qtables: np.ndarray) -> CoefImage:
+    """Encoder stand-in for a grayscale JPEG: JFIF luma of the RGB field, one
+    component, 8x8 MCUs (T.81 A.2.2: non-interleaved single component)."""
+    h, w, _ = rgb.shape
+    Y = _rgb_to_ycbcr(rgb)[..., 0]
+    Y = _pad_edge(Y, 8 * -(-h // 8), 8 * -(-w // 8))
+    return CoefImage(w, h, [_fdct_quantize(Y, qtables[0])], (0,))
+
+
 def stress_image(rng: np.random.Generator, width: int, height: int,
                  qtables: np.ndarray, limit: int = 2047) -> CoefImage:
     """Dense uniform coefficients with dequantized |D| <= limit, plus 5% DC-only
@@ -252,6 +266,8 @@ def make_image(rng: np.random.Generator, width: int, height: int, qtables: np.nd
         return encode_420(natural_rgb(rng, width, height), qtables)
     if mode == "stress":
         return stress_image(rng, width, height, qtables)
+    if mode == "gray":
+        return encode_gray(natural_rgb(rng, width, height), qtables)
     raise ValueError(mode)
 
 

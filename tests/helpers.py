@@ -50,7 +50,7 @@ def make_tie_free(im, qt, k: int, max_iter: int = 50):
     P = 8 // k
     coef = [c.copy() for c in im.coef]
     rng = np.random.default_rng(12345)
-    for ci in range(3):
+    for ci in range(len(coef)):
         q = qt[im.qidx[ci]]
         bh, bw = coef[ci].shape[:2]
         for _ in range(max_iter):
@@ -91,9 +91,11 @@ def affected_outputs(po, im, qt, roi=None):
     g = oracle.geometry(po, im.width, im.height)
     left, top = (g.left, g.top) if roi is None else roi
     bands = [b for (_, _, b) in oracle_planes(po, im, qt)]
-    c16, _ = oracle.upsample_color(np.zeros((g.Hd, g.Wd), np.uint8),
-                                   bands[1].astype(np.uint8), bands[2].astype(np.uint8))
-    pix = bands[0] | (c16[..., 0] > 0) | (c16[..., 1] > 0)
+    pix = bands[0]
+    if len(bands) == 3:
+        c16, _ = oracle.upsample_color(np.zeros((g.Hd, g.Wd), np.uint8),
+                                       bands[1].astype(np.uint8), bands[2].astype(np.uint8))
+        pix = pix | (c16[..., 0] > 0) | (c16[..., 1] > 0)
     y0, y1 = _taps(g.OH, top, g.Hd, g.Hr)
     x0, x1 = _taps(g.OW, left, g.Wd, g.Wr)
     return (pix[y0][:, x0] | pix[y0][:, x1] | pix[y1][:, x0] | pix[y1][:, x1])

@@ -110,3 +110,36 @@ def test_batch_permutation_and_threads(oracle_mod):
     perm = [3, 0, 4, 1, 2]
     b = oracle_mod.run_batch(p, [imgs[i] for i in perm], qt, threads=3)
     assert np.array_equal(a[perm], b)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_grayscale_equals_neutral_chroma(oracle_mod, k):
+    """Grayscale (one component): R = G = B = Y.  Pinned against the 4:2:0
+    path on the same luma with all-zero chroma coefficients (Cb = Cr = 128
+    after the level shift), whose colour conversion is the gray axis (R6,
+    pinned separately): the two code paths must agree exactly."""
+    rng = np.random.default_rng(400 + k)
+    qt = synth.quant_tables(75)
+    for (w, h) in [(64, 48), (97, 61), (33, 17)]:
+        g = synth.make_image(rng, w, h, qt, mode="gray")
+        assert g.gray and g.coef[0].shape[:2] == (-(-h // 8), -(-w // 8))
+        z = [np.zeros((-(-h // 16), -(-w // 16), 64), np.int16) for _ in range(2)]
+        c420 = synth.CoefImage(w, h, [g.coef[0]] + z, (0, 1, 1))
+        p = oracle_mod.make_params(scale_denom=k, resize_mode="exact", resize_w=40, resize_h=24)
+        a = oracle_mod.run_image(p, g, qt)
+        b = oracle_mod.run_image(p, c420, qt)
+        np.testing.assert_array_equal(a, b)
+
+
+def test_grayscale_constant_closed_form(oracle_mod):
+    """A DC-only gray image of level c gives (c/255 - mean)/std per channel."""
+    qt = np.ones((2, 64), np.uint16)
+    for dc, c in [(36, 133), (-36, 124), (0, 128), (1016, 255)]:
+        coef = np.zeros((3, 4, 64), np.int16)
+        coef[..., 0] = dc
+        im = synth.CoefImage(30, 20, [coef], (0,))
+        p = oracle_mod.make_params(resize_mode="exact", resize_w=16, resize_h=8)
+        out = oracle_mod.run_image(p, im, qt).astype(np.float64)
+        for ch in range(3):
+            want = (c / 255 - synth.IMAGENET_MEAN[ch]) / synth.IMAGENET_STD[ch]
+            np.testing.assert_allclose(out[ch], np.float32(want), rtol=0, atol=1e-6)
