@@ -450,6 +450,7 @@ struct KParams {
   const uint16_t* qtables;
   void* out;
   int OW, OH, tile_rows, tile_cols, n_col_tiles;
+  const int4* cta_map;             // non-null: 1-D grid, CTA -> {image, oy0, oy1, 0}
   uint32_t magic;                  // 0x4B000000: bit pattern of 2^23 (byte -> float trick)
   float na[3], nb[3];              // y = x * na + nb = (x/255 - mean)/std
   int16_t* dbg_pl[3];              // debug planes (DEBUG instantiation only)
@@ -889,10 +890,17 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
 template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
 __global__ void __launch_bounds__(kThreads, 768 / kThreads)
 smol_fused_kernel(const __grid_constant__ KParams kp) {
-  const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
-  const int oy0 = trow * kp.tile_rows, ox0 = tcol * kp.tile_cols;
-  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP>(kp, blockIdx.y, oy0, min(kp.OH, oy0 + kp.tile_rows), ox0,
-                                                   min(kp.OW, ox0 + kp.tile_cols));
+  int n, oy0, oy1, ox0, ox1;
+  if (kp.cta_map) {            // 1-D grid: per-CTA {image, oy0, oy1} (full-width tiles)
+    const int4 m = kp.cta_map[blockIdx.x];
+    n = m.x; oy0 = m.y; oy1 = m.z; ox0 = 0; ox1 = kp.OW;
+  } else {
+    const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
+    n = blockIdx.y;
+    oy0 = trow * kp.tile_rows; oy1 = min(kp.OH, oy0 + kp.tile_rows);
+    ox0 = tcol * kp.tile_cols; ox1 = min(kp.OW, ox0 + kp.tile_cols);
+  }
+  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP>(kp, n, oy0, oy1, ox0, ox1);
 }
 
 }  // namespace smol

@@ -329,6 +329,10 @@ struct smol_preproc_plan {
   int min_col_tiles = 1;                  // SMOL_COL_TILES=k forces >= k column tiles (A/B)
   int nt_mode = 0;                        // SMOL_THREADS=192|256 forces the CTA size (A/B)
   DevImage* d_desc = nullptr;  // [kRing][max_images]
+  int4* d_map = nullptr;       // [kRing][map_cap] balanced CTA map (see run_impl)
+  int4* h_map = nullptr;       // pinned
+  int map_cap = 0;
+  int cta_map_mode = 1;        // SMOL_CTA_MAP=0 disables the balanced map (A/B)
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
   cudaEvent_t ev[kRing] = {};
   int ring = 0;
@@ -415,6 +419,7 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   pl->tile_rows = params->tile_rows;
   if (const char* e = std::getenv("SMOL_COL_TILES")) pl->min_col_tiles = std::atoi(e);
   if (const char* e = std::getenv("SMOL_THREADS")) pl->nt_mode = std::atoi(e);
+  if (const char* e = std::getenv("SMOL_CTA_MAP")) pl->cta_map_mode = std::atoi(e);
   for (int c = 0; c < 3; ++c) {
     pl->na[c] = (float)(1.0 / (255.0 * (double)params->std[c]));
     pl->nb[c] = (float)(-(double)params->mean[c] / (double)params->std[c]);
@@ -434,6 +439,11 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
   if (e == cudaSuccess) pl->layouts.reserve(max_images);
+  if (e == cudaSuccess) {
+    pl->map_cap = pl->num_sms * 8;
+    e = cudaMalloc(&pl->d_map, sizeof(int4) * (size_t)pl->map_cap * kRing);
+    if (e == cudaSuccess) e = cudaMallocHost(&pl->h_map, sizeof(int4) * (size_t)pl->map_cap * kRing);
+  }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(smol_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kExpandSmem);
   if (e == cudaSuccess) {
@@ -478,6 +488,8 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (pl->h_gather) cudaFreeHost(pl->h_gather);
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->d_desc) cudaFree(pl->d_desc);
+  if (pl->d_map) cudaFree(pl->d_map);
+  if (pl->h_map) cudaFreeHost(pl->h_map);
   if (pl->h_desc) cudaFreeHost(pl->h_desc);
   delete pl;
 }
@@ -654,6 +666,30 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       smem = max_smem(1, Cfg_yp(nt));
     }
   }
+  // Balanced CTA map: when the automatic tiling leaves one partial wave
+  // (n * t CTAs < resident slots S), give S - n t images one more (shorter)
+  // tile so every slot is busy, and launch the taller tiles first.  The time
+  // is set by the SMs holding the most work; with 512 tiles of 112 rows on
+  // 592 slots (c2) those hold 4 tiles while others hold 3.
+  int map_n = 0;
+  int4* hm = pl->h_map + (size_t)slot * pl->map_cap;
+  int4* dm = pl->d_map + (size_t)slot * pl->map_cap;
+  // (scale 1 only: at 1/2..1/8 a tile spans few 16-row rolling steps and the
+  // extra tiles' halos cost more than the idle slots, measured r01m)
+  if (pl->cta_map_mode && auto_rows && n_col_tiles == 1 && K == 1) {
+    const int S = pl->num_sms * (768 / nt);
+    const long long base = (long long)n_images * ntiles;
+    if (base < S && S <= pl->map_cap && ntiles + 1 <= pl->OH / 8) {
+      const int extra = (int)std::min<long long>(S - base, n_images);   // images with ntiles + 1 tiles
+      for (int pass = 0; pass < 2; ++pass)          // taller tiles (ntiles per image) first
+        for (int i = pass == 0 ? extra : 0; i < (pass == 0 ? n_images : extra); ++i) {
+          const int t = ntiles + (i < extra ? 1 : 0);
+          for (int j = 0; j < t; ++j)
+            hm[map_n++] = make_int4(i, (int)((long long)j * pl->OH / t), (int)((long long)(j + 1) * pl->OH / t), 0);
+        }
+      smem += 64;      // tile positions differ from the uniform grid's: one step of slack
+    }
+  }
   if (smem > pl->smem_optin)
     return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
 
@@ -779,6 +815,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
         SMOL_CUDA(cudaMemcpyAsync(pl->cbuf[sl], arena + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice,
                                   pl->copy_stream));
     }
+    if (map_n)
+      SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaEventRecord(pl->stage_ready[sl], pl->copy_stream));
     SMOL_CUDA(cudaStreamWaitEvent(stream, pl->stage_ready[sl], 0));
     if (src == Src::kCompact) {
@@ -791,6 +829,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
 
   if (src == Src::kDevice)
     SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, stream));
+  if (map_n && src == Src::kDevice)
+    SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, stream));
   KParams kp = dbg ? *dbg : KParams{};
   kp.imgs = d;
   kp.qtables = qtables;
@@ -801,7 +841,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt);
-  dim3 grid(ntiles * n_col_tiles, n_images);
+  kp.cta_map = map_n ? dm : nullptr;
+  dim3 grid = map_n ? dim3(map_n, 1) : dim3(ntiles * n_col_tiles, n_images);
   fn<<<grid, nt, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));

@@ -378,3 +378,25 @@ def test_run_host_staged_equals_device(name, layout):
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(a, o), name
+
+
+@pytest.mark.parametrize("n", [4, 16, 256])
+def test_balanced_cta_map_invariance(n, monkeypatch):
+    """The balanced CTA map (extra, shorter tiles for some images when the tile
+    grid leaves resident slots idle) changes only the tiling: outputs must be
+    bit-identical to the uniform tile grid."""
+    cfg = synth.CONFIGS["c2"]
+    imgs, qt = synth.batch_images(cfg, n=n, n_distinct=min(n, 8))
+    ps, po = _cfg_params(cfg)
+    outs = {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("SMOL_CTA_MAP", m)
+        plan = smol.Plan(ps, n)
+        outs[m] = plan.run(smol.CoefBatch(imgs, qt)).clone()
+        torch.cuda.synchronize()
+        plan.close()
+    assert torch.equal(outs["0"], outs["1"])
+    ref = oracle.run_image(po, imgs[0], qt).astype(np.float64)
+    err = np.abs(outs["1"][0].float().cpu().numpy() - ref).max(axis=0)
+    aff = helpers.affected_outputs(po, imgs[0], qt)
+    assert err[~aff].max(initial=0) <= TOL[cfg.out_dtype]
