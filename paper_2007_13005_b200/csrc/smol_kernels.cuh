@@ -886,9 +886,19 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   }
 }
 
+// Resident CTAs per SM the kernel is register-budgeted for: 24 warps at <= 80
+// registers, except the tiny configuration at scales 1/2 and 1/4, whose IDCT
+// fits 64 registers without spills: 8 CTAs (32 warps) per SM there for the
+// latency-bound small footprints (c3b +5 %).  At 1/8 (DC only) the same
+// change measured -11 % on c4 (profiles/r01p_occupancy.md), so it keeps 6.
+template <int K>
+__host__ __device__ constexpr int kCtasPerSm(int threads) {
+  return ((K == 2 || K == 4) && threads == kThreadsTiny) ? 8 : 768 / threads;
+}
+
 // The fused kernel: one (image, row band, column band) tile per CTA.
 template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
-__global__ void __launch_bounds__(kThreads, 768 / kThreads)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm<K>(kThreads))
 smol_fused_kernel(const __grid_constant__ KParams kp) {
   int n, oy0, oy1, ox0, ox1;
   if (kp.cta_map) {            // 1-D grid: per-CTA {image, oy0, oy1} (full-width tiles)

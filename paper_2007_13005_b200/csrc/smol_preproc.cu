@@ -658,8 +658,15 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       smem = max_smem(n_col_tiles, kYPWide);
     }
   }
+  // resident CTAs per SM of the chosen kernel at this shared-memory size
+  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt);
+  int occ = 768 / nt;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    occ = 768 / nt;
+  }
   if (auto_rows && n_col_tiles == 1) {
-    const int tr = auto_tile_rows(pl->OH, n_images, pl->num_sms * (768 / nt));
+    const int tr = auto_tile_rows(pl->OH, n_images, pl->num_sms * occ);
     if (tr != tile_rows) {
       tile_rows = tr;
       ntiles = ceil_div(pl->OH, tile_rows);
@@ -677,7 +684,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // (scale 1 only: at 1/2..1/8 a tile spans few 16-row rolling steps and the
   // extra tiles' halos cost more than the idle slots, measured r01m)
   if (pl->cta_map_mode && auto_rows && n_col_tiles == 1 && K == 1) {
-    const int S = pl->num_sms * (768 / nt);
+    const int S = pl->num_sms * occ;
     const long long base = (long long)n_images * ntiles;
     if (base < S && S <= pl->map_cap && ntiles + 1 <= pl->OH / 8) {
       const int extra = (int)std::min<long long>(S - base, n_images);   // images with ntiles + 1 tiles
@@ -840,7 +847,6 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
-  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt);
   kp.cta_map = map_n ? dm : nullptr;
   dim3 grid = map_n ? dim3(map_n, 1) : dim3(ntiles * n_col_tiles, n_images);
   fn<<<grid, nt, smem, stream>>>(kp);
