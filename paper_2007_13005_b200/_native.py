@@ -14,7 +14,7 @@ _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libsmol_preproc.so")
 HEADER = os.path.join(_ROOT, "include", "smol_preproc.h")
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in
-           ("smol_preproc.cu", "smol_kernels.cuh", "smol_geom.cuh", "smol_compact.cuh")]
+           ("smol_preproc.cu", "smol_kernels.cuh", "smol_geom.cuh", "smol_compact.cuh", "smol_thumb.cuh")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 

@@ -1,0 +1,161 @@
+// smol_thumb.cuh -- warp-per-image kernel for 1/8-scale decodes of small
+// images (thumbnails; BASELINE c4: 161x161 -> 1/8 -> 64x64, batch 4096).
+//
+// At scale 1/8 a block decodes to one sample: its DC (reading R1), so a
+// 161x161 image is a 21x21 luma + 11x11 chroma picture and the work is the
+// 64x64x3 output.  The tiled kernel spends most of such a CTA's life in
+// barrier-separated phases with global-latency round trips between them;
+// here one warp owns one image end to end (no CTA barriers, only __syncwarp),
+// many images per SM are in flight, and the kernel is bound by the output
+// stores.  Same arithmetic as the tiled kernel for every u8 step (DC round,
+// 4:2:0 triangle upsample, exact colour) and the same packed fp32 bilinear +
+// normalize, so its outputs are bit-identical to the tiled kernel's.
+#pragma once
+#include "smol_kernels.cuh"
+
+namespace smol {
+
+constexpr int kThumbWarps = 4;                 // images in flight per CTA
+constexpr int kThumbMaxFoot = 32;              // decoded luma footprint limit (px per side)
+constexpr int kThumbMaxOut = 128;              // output width / height limit
+constexpr int kThumbCP = kThumbMaxFoot / 2 + 2;   // chroma footprint pitch
+struct ThumbWarpSmem {
+  uint32_t rgb[kThumbMaxFoot * kThumbMaxFoot];  // RGBx of the luma footprint
+  uint8_t y[kThumbMaxFoot * kThumbMaxFoot];
+  uint8_t c[2][kThumbCP * kThumbCP];
+  int2 xt[kThumbMaxOut];                         // per output column: {x0 - lx0 | (x1 - lx0) << 16, w}
+  int2 yt[kThumbMaxOut];                         // per output row:    {y0 - ly0 | (y1 - ly0) << 16, w}
+  TileLayout L;
+};
+constexpr int kThumbSmem = kThumbWarps * (int)sizeof(ThumbWarpSmem);
+
+template <bool F16, bool PACKED>
+__global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __grid_constant__ KParams kp,
+                                                                      int n_images) {
+  extern __shared__ __align__(16) uint8_t tsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ThumbWarpSmem& S = reinterpret_cast<ThumbWarpSmem*>(tsm)[warp];
+  constexpr int E = PACKED ? 1 : 64;            // DC at element 0 of a stored block
+  using OutT = typename std::conditional<F16, __half, float>::type;
+  const int OW = kp.OW, OH = kp.OH;
+  const uint32_t plane = (uint32_t)OW * OH;
+  for (int n = blockIdx.x * kThumbWarps + warp; n < n_images; n += gridDim.x * kThumbWarps) {
+    const DevImage im = kp.imgs[n];
+    if (lane == 0) tile_layout(im, 8, 0, OH, 0, OW, S.L, kYPTiny);
+    __syncwarp();
+    const int lx0 = S.L.lx0, ly0 = S.L.ly0, fw = S.L.lx1 - lx0 + 1, fh = S.L.ly1 - ly0 + 1;
+    const int cx0 = S.L.cx0, cy0 = S.L.cy0, cw = S.L.cx1 - cx0 + 1, ch = S.L.cy1 - cy0 + 1;
+    // taps (reading R9: exact integers); a clamped upper tap gets weight 0
+    for (int i = lane; i < OW; i += 32) {
+      int i0, i1; float w;
+      src_tap(im.left + i, im.Wd, im.Wr, i0, i1, w);
+      S.xt[i] = make_int2((i0 - lx0) | ((i1 - lx0) << 16), __float_as_int(i1 == i0 ? 0.f : w));
+    }
+    for (int i = lane; i < OH; i += 32) {
+      int i0, i1; float w;
+      src_tap(im.top + i, im.Hd, im.Hr, i0, i1, w);
+      S.yt[i] = make_int2((i0 - ly0) | ((i1 - ly0) << 16), __float_as_int(i1 == i0 ? 0.f : w));
+    }
+    // 1/8 decode (reading R1/R3): u8 = clamp(floor(DC * Q0 / 8 + 128 + 1/2))
+    const float qy = (float)kp.qtables[im.qidx[0] * 64] * 0.125f;
+    for (int p = lane; p < fw * fh; p += 32) {
+      const int r = p / fw, x = p - r * fw;
+      const int16_t dc = __ldg(im.coef[0] + (size_t)(ly0 + r) * im.stride[0] + (size_t)(lx0 + x) * E);
+      S.y[r * kThumbMaxFoot + x] = (uint8_t)round_u8((float)dc * qy);
+    }
+    for (int cc = 0; cc < 2; ++cc) {
+      const float qc = (float)kp.qtables[im.qidx[1 + cc] * 64] * 0.125f;
+      for (int p = lane; p < cw * ch; p += 32) {
+        const int r = p / cw, x = p - r * cw;
+        uint8_t v = 128;                          // grayscale: neutral chroma (reading R14)
+        if (!im.gray) {
+          const int16_t dc = __ldg(im.coef[1 + cc] + (size_t)(cy0 + r) * im.stride[1 + cc] + (size_t)(cx0 + x) * E);
+          v = (uint8_t)round_u8((float)dc * qc);
+        }
+        S.c[cc][r * kThumbCP + x] = v;
+      }
+    }
+    __syncwarp();
+    // 4:2:0 centred triangle upsample (reading R2, neighbours clamped to the
+    // valid chroma size) + exact JFIF colour (R6)
+    for (int p = lane; p < fw * fh; p += 32) {
+      const int r = p / fw, x = p - r * fw;
+      const int X = lx0 + x, Yr = ly0 + r;
+      const int i = X >> 1, j = Yr >> 1;
+      const int in = min(max((X & 1) ? i + 1 : i - 1, 0), im.Wc - 1);
+      const int jn = min(max((Yr & 1) ? j + 1 : j - 1, 0), im.Hc - 1);
+      const int a = (j - cy0) * kThumbCP, b = (jn - cy0) * kThumbCP;
+      const int ci = i - cx0, cn = in - cx0;
+      const int cb = 9 * S.c[0][a + ci] + 3 * S.c[0][a + cn] + 3 * S.c[0][b + ci] + S.c[0][b + cn];
+      const int cr = 9 * S.c[1][a + ci] + 3 * S.c[1][a + cn] + 3 * S.c[1][b + ci] + S.c[1][b + cn];
+      S.rgb[r * kThumbMaxFoot + x] = colour(S.y[r * kThumbMaxFoot + x], cb, cr);
+    }
+    __syncwarp();
+    // bilinear (reading R8) + normalize, 4 consecutive output pixels per lane,
+    // two pixels per packed FP32x2 instruction; u8 -> float by one PRMT into
+    // the 2^23 magic (the bias cancels in b - a) -- the tiled kernel's
+    // formulation, so the outputs are bit-identical to it
+    OutT* const outn = reinterpret_cast<OutT*>(kp.out) + (size_t)n * 3 * plane;
+    const int nq = (OW + 3) >> 2;
+    const uint32_t magic = kp.magic;
+    const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
+    const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
+    for (int t = lane; t < nq * OH; t += 32) {
+      const int oy = t / nq, ox = 4 * (t - oy * nq);
+      const int2 ty = S.yt[oy];
+      const float2 wy2 = f2(__int_as_float(ty.y));
+      const uint32_t* r0 = S.rgb + (ty.x & 0xffff) * kThumbMaxFoot;
+      const uint32_t* r1 = S.rgb + (ty.x >> 16) * kThumbMaxFoot;
+      float v[3][4];
+#pragma unroll
+      for (int e = 0; e < 4; e += 2) {
+        const int2 ta = S.xt[min(ox + e, OW - 1)], tb = S.xt[min(ox + e + 1, OW - 1)];
+        const float2 wx = make_float2(__int_as_float(ta.y), __int_as_float(tb.y));
+        const uint32_t p00 = r0[ta.x & 0xffff], p01 = r0[ta.x >> 16], p10 = r1[ta.x & 0xffff], p11 = r1[ta.x >> 16];
+        const uint32_t q00 = r0[tb.x & 0xffff], q01 = r0[tb.x >> 16], q10 = r1[tb.x & 0xffff], q11 = r1[tb.x >> 16];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int sel = 0x7540 + c;
+          const float2 fa = make_float2(__uint_as_float(__byte_perm(p00, magic, sel)), __uint_as_float(__byte_perm(q00, magic, sel)));
+          const float2 fb = make_float2(__uint_as_float(__byte_perm(p01, magic, sel)), __uint_as_float(__byte_perm(q01, magic, sel)));
+          const float2 fc = make_float2(__uint_as_float(__byte_perm(p10, magic, sel)), __uint_as_float(__byte_perm(q10, magic, sel)));
+          const float2 fd = make_float2(__uint_as_float(__byte_perm(p11, magic, sel)), __uint_as_float(__byte_perm(q11, magic, sel)));
+          const float2 tp = __ffma2_rn(wx, __ffma2_rn(fa, f2(-1.f), fb), __fadd2_rn(fa, f2(-8388608.f)));
+          const float2 bt = __ffma2_rn(wx, __ffma2_rn(fc, f2(-1.f), fd), __fadd2_rn(fc, f2(-8388608.f)));
+          const float2 vv = __ffma2_rn(wy2, __ffma2_rn(tp, f2(-1.f), bt), tp);
+          const float2 yn = __ffma2_rn(vv, c == 0 ? na0 : c == 1 ? na1 : na2, c == 0 ? nb0 : c == 1 ? nb1 : nb2);
+          v[c][e] = yn.x;
+          v[c][e + 1] = yn.y;
+        }
+      }
+      OutT* const o = outn + (uint32_t)oy * OW + ox;
+      if ((OW & 3) == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if constexpr (F16) {
+            const __half2 h0 = __floats2half2_rn(v[c][0], v[c][1]), h1 = __floats2half2_rn(v[c][2], v[c][3]);
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t*>(&h0);
+            u.y = *reinterpret_cast<const uint32_t*>(&h1);
+            __stcs(reinterpret_cast<uint2*>(o + c * plane), u);
+          } else {
+            __stcs(reinterpret_cast<float4*>(o + c * plane), make_float4(v[c][0], v[c][1], v[c][2], v[c][3]));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (ox + e >= OW) break;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if constexpr (F16) o[e + c * plane] = __float2half_rn(v[c][e]);
+            else o[e + c * plane] = v[c][e];
+          }
+        }
+      }
+    }
+    __syncwarp();                                 // smem reused by the warp's next image
+  }
+}
+
+}  // namespace smol

@@ -400,3 +400,35 @@ def test_balanced_cta_map_invariance(n, monkeypatch):
     err = np.abs(outs["1"][0].float().cpu().numpy() - ref).max(axis=0)
     aff = helpers.affected_outputs(po, imgs[0], qt)
     assert err[~aff].max(initial=0) <= TOL[cfg.out_dtype]
+
+
+@pytest.mark.parametrize("layout,out_dtype", [("packed", "f32"), ("dense", "f32"), ("packed", "f16")])
+def test_thumb_kernel_matches_tiled_kernel_and_oracle(layout, out_dtype, monkeypatch):
+    """Scale 1/8 small images go to the warp-per-image kernel (smol_thumb.cuh),
+    which runs the tiled kernel's arithmetic step for step: outputs must be
+    bit-identical to the tiled kernel and within the north_star tolerance of
+    the oracle.  Mixed gray/colour, odd sizes and stress coefficients."""
+    cfg = synth.CONFIGS["c4"]
+    rng = np.random.default_rng(8)
+    qt = synth.quant_tables(75)
+    imgs, _ = synth.distinct_images(cfg, n_distinct=6)
+    imgs += [synth.make_image(rng, 161, 161, qt, mode="gray"), synth.make_image(rng, 150, 97, qt),
+             synth.make_image(rng, 255, 199, qt, mode="stress")]
+    ps = smol.params_from_config(cfg, layout=layout, out_dtype=out_dtype)
+    po = oracle.params_from_config(cfg)
+    po.out_f16 = 1 if out_dtype == "f16" else 0
+    outs = {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("SMOL_THUMB", m)
+        plan = smol.Plan(ps, len(imgs))
+        outs[m] = plan.run(smol.batch_for(ps, imgs, qt)).float().cpu().numpy()
+        plan.close()
+    tol = 2e-3 if out_dtype == "f16" else 1e-4
+    assert np.array_equal(outs["0"], outs["1"])
+    widen = 2.0 / (255 * min(synth.IMAGENET_STD))
+    for i, im in enumerate(imgs):
+        ref = oracle.run_image(po, im, qt).astype(np.float64)
+        err = np.abs(outs["1"][i] - ref).max(axis=0)
+        aff = helpers.affected_outputs(po, im, qt)
+        assert err[~aff].max(initial=0) <= tol, (i, err[~aff].max())
+        assert err.max() <= tol + widen
