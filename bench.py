@@ -417,7 +417,8 @@ def main():
                        "tile_rows": plan.params.tile_rows, "coef_layout": args.layout},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(cfg.name, args.layout), "peak_source": peak_src,
-                         "kernel": "smol_fused_kernel", "launch_ms": launch_ms,
+                         "kernel": ("smol_thumb_kernel" if cfg.scale_denom == 8 and args.layout == "packed"
+                                    else "smol_fused_kernel"), "launch_ms": launch_ms,
                          "alg_bytes_per_launch": alg_bytes_launch},
             "e2e": e2e,
             "gpu_launches": args.steps * plan.launches_per_run(),
