@@ -6,15 +6,15 @@
 // Each CTA walks its tile's decoded-row footprint in 16-row steps (one MCU
 // row at scale 1) with rolling shared-memory windows, so every coefficient
 // block under the footprint is read and transformed once per tile:
-//   step s:  IDCT   the ROI blocks of luma rows [R, R+16) and chroma rows
-//                   [R/2, R/2+8) (thread per block; warp-uniform pruning of
-//                   all-zero high rows/columns) -> u8 Y / Cb / Cr rings
-//            sync
-//            colour RGB rows (ready_{s-1}, ready_s]: 4:2:0 triangle upsample
-//                   of an even/odd luma pair + exact JFIF -> packed RGBx ring
-//            sync
-//            output every output row whose lower tap row is ready: bilinear
-//                   + FMA normalize, 2 pixels per thread, NCHW stores
+//   IDCT(0)                                                          sync
+//   step s:  L2 bulk prefetch of step s+1's ROI block rows
+//            colour RGB rows (ready_{s-1}, ready_s]: 2x4-pixel tasks, 4:2:0
+//                   triangle upsample + exact JFIF -> packed RGBx ring   sync
+//            IDCT(s+1): thread per block, warp-uniform pruning of all-zero
+//                   high rows -> u8 Y / Cb / Cr rings
+//            + output of every output row whose lower tap row is ready:
+//                   bilinear + FMA normalize, 4 pixels per task, NCHW
+//                   streaming stores                                    sync
 #pragma once
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -22,16 +22,6 @@
 
 #include "smol_geom.cuh"
 
-// Code-generation options (kept switchable for A/B measurement).
-#ifndef SMOL_OPT_COLSTATIC
-#define SMOL_OPT_COLSTATIC 1
-#endif
-#ifndef SMOL_OPT_ATOM
-#define SMOL_OPT_ATOM 0
-#endif
-#ifndef SMOL_OPT_COLFFMA2
-#define SMOL_OPT_COLFFMA2 0
-#endif
 // Output-phase scheduling (measured, profiles/r01h_output_schedule.md): at
 // scale 1 the output tasks share the phase with the next step's IDCT and are
 // grabbed dynamically, two per lane per grab, interleaved by the compiler; at
@@ -42,16 +32,9 @@
 #ifndef SMOL_OUT_STATIC
 #define SMOL_OUT_STATIC 2        // 0: dynamic everywhere; 1: static everywhere; 2: static at scales 1/2..1/8
 #endif
-#ifndef SMOL_COL_UNROLL
-#define SMOL_COL_UNROLL 1
-#endif
-#ifndef SMOL_OPT_YMAGIC
-#define SMOL_OPT_YMAGIC 1
-#endif
 
 namespace smol {
 
-constexpr int kColUnroll = SMOL_COL_UNROLL;   // (#pragma unroll does not expand macros)
 
 // Basis constants, computed on the host in double from their definitions
 // (smol_preproc.cu: init_basis) and uploaded once per device.
@@ -215,55 +198,6 @@ __device__ __forceinline__ void idct_rows(const int4 (&raw)[8], const float* q, 
   }
 }
 
-// Row pass with the pairs kept: M[k][x] = (m[2k][x], m[2k+1][x]).
-template <int W, int HR>
-__device__ __forceinline__ void idct_rows2(const int4 (&raw)[8], const float* q, float2 (&M)[4][8]) {
-#pragma unroll
-  for (int v = 0; v < HR; v += 2) {
-    float a[8], b[8];
-    unpack_row(raw[v], a);
-    unpack_row(raw[v + 1], b);
-    const float4 qa0 = *reinterpret_cast<const float4*>(q + v * 8);
-    const float4 qa1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
-    const float4 qb0 = *reinterpret_cast<const float4*>(q + v * 8 + 8);
-    const float4 qb1 = *reinterpret_cast<const float4*>(q + v * 8 + 12);
-    float2 d[8];
-    d[0] = make_float2(a[0] * qa0.x, b[0] * qb0.x); d[1] = make_float2(a[1] * qa0.y, b[1] * qb0.y);
-    d[2] = make_float2(a[2] * qa0.z, b[2] * qb0.z); d[3] = make_float2(a[3] * qa0.w, b[3] * qb0.w);
-    d[4] = make_float2(a[4] * qa1.x, b[4] * qb1.x); d[5] = make_float2(a[5] * qa1.y, b[5] * qb1.y);
-    d[6] = make_float2(a[6] * qa1.z, b[6] * qb1.z); d[7] = make_float2(a[7] * qa1.w, b[7] * qb1.w);
-    if (v == 0) d[0].x += 128.5f;
-    idct8x2<W>(d, M[v >> 1]);
-  }
-}
-
-// Column pass on the row pairs: lane .x accumulates the even-v terms and
-// lane .y the odd-v terms of f[y] = sum_v m[v] t(v, y); the mirror output is
-// f[7-y] = even - odd (t(v, 7-y) = (-1)^v t(v, y)).  The chain starts from
-// m[0] * t(0, y) = m[0] exactly, so DC-only inputs stay exact (reading R3).
-template <int H>
-__device__ __forceinline__ void idct_cols2(const float2 (&M)[4][8], uint32_t (&px)[8][2]) {
-#pragma unroll
-  for (int x = 0; x < 8; ++x) {
-    float f[8];
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      float2 acc = __fmul2_rn(M[0][x], c_basis.tp[0][y]);
-#pragma unroll
-      for (int k = 1; k < H / 2; ++k) acc = __ffma2_rn(M[k][x], c_basis.tp[k][y], acc);
-      f[y] = acc.x + acc.y;
-      f[7 - y] = acc.x - acc.y;
-    }
-#pragma unroll
-    for (int y = 0; y < 8; ++y) {
-      const uint32_t b = floor_u8(f[y]);
-      uint32_t& w = px[y][x >> 2];
-      if ((x & 3) == 0) w = b;
-      else w = __byte_perm(w, b, (x & 3) == 1 ? 0x3240 : (x & 3) == 2 ? 0x3410 : 0x4210);
-    }
-  }
-}
-
 template <int H>
 __device__ __forceinline__ void idct_cols(const float (&m)[8][8], uint32_t (&px)[8][2]) {
   // column x's bytes are merged into the row words as they are produced
@@ -326,15 +260,10 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     // prune by the warp's highest nonzero coefficient row (one code variant
     // per extent: more variants cost more in I-cache misses than they save)
     const int H = (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows));
-#if SMOL_OPT_COLFFMA2
-    float2 M[4][8];
-    if (H <= 6) { idct_rows2<8, 6>(raw, q, M); idct_cols2<6>(M, px); }
-    else { idct_rows2<8, 8>(raw, q, M); idct_cols2<8>(M, px); }
-#else
+    // (a column pass on FFMA2 row pairs was measured no faster)
     float m[8][8];
     if (H <= 6) { idct_rows<8, 6>(raw, q, m); idct_cols<6>(m, px); }
     else { idct_rows<8, 8>(raw, q, m); idct_cols<8>(m, px); }
-#endif
   } else {
     // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7}):
     // rows/columns outside the index set have an exactly-zero basis.
@@ -426,23 +355,6 @@ __device__ __forceinline__ uint2 colour2m(uint32_t m0, uint32_t m1, int cb0, int
                     __byte_perm(__byte_perm(floor_u8(tr.y), G1, 0x0040), floor_u8(tb.y), 0x5410));
 }
 
-// Two pixels at once: the same IEEE fp32 operations as colour(), packed
-// (FADD2/FFMA2), so results are bitwise identical.
-__device__ __forceinline__ uint2 colour2(int Y0, int Y1, int cb0, int cb1, int cr0, int cr1) {
-  const float2 yf = make_float2((float)Y0, (float)Y1);
-  const float2 tr = __ffma2_rn(make_float2((float)cr0, (float)cr1), make_float2(c_basis.kR, c_basis.kR),
-                               __fadd2_rn(yf, make_float2(c_basis.cR, c_basis.cR)));
-  const float2 tb = __ffma2_rn(make_float2((float)cb0, (float)cb1), make_float2(c_basis.kB, c_basis.kB),
-                               __fadd2_rn(yf, make_float2(c_basis.cB, c_basis.cB)));
-  const uint32_t u0 = 543917632u - 43017u * (uint32_t)cb0 - 89267u * (uint32_t)cr0;
-  const uint32_t u1 = 543917632u - 43017u * (uint32_t)cb1 - 89267u * (uint32_t)cr1;
-  const uint32_t G0 = (uint32_t)min(max(Y0 + (int)(u0 / 2000000u) - 136, 0), 255);
-  const uint32_t G1 = (uint32_t)min(max(Y1 + (int)(u1 / 2000000u) - 136, 0), 255);
-  // R | G<<8 | B<<16 via byte permutes
-  return make_uint2(__byte_perm(__byte_perm(floor_u8(tr.x), G0, 0x0040), floor_u8(tb.x), 0x5410),
-                    __byte_perm(__byte_perm(floor_u8(tr.y), G1, 0x0040), floor_u8(tb.y), 0x5410));
-}
-
 __device__ __forceinline__ int ldu8(const uint8_t* p) { return *p; }
 
 struct KParams {
@@ -487,26 +399,14 @@ __device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[2], int e) {
   return ((e < 4 ? w[0] : w[1]) >> (8 * (e & 3))) & 255u;   // select: no dynamic register indexing
 }
 
-// Dynamic work distribution: lane 0 takes the next 32 tasks from a shared
-// counter and broadcasts the base.  With SMOL_OPT_ATOM the atomic is issued as
-// one predicated ATOMS (the compiler otherwise emits its warp-aggregation
-// sequence around atomicAdd).
+// Dynamic work distribution: lane 0 takes the next n tasks from a shared
+// counter and broadcasts the base.
 __device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
   int chunk = 0;
-#if SMOL_OPT_ATOM
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(ctr);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, 0;\n\t"
-      "@p atom.shared.add.u32 %0, [%2], %3;\n\t}"
-      : "+r"(chunk) : "r"(lane), "r"(a), "r"(n) : "memory");
-#else
   if (lane == 0) chunk = atomicAdd(ctr, n);
-#endif
   return __shfl_sync(0xffffffffu, chunk, 0);
 }
 
-// One output tile (image n, output rows [oy0, oy1), columns [ox0, ox1)) of
-// the fused path.
 template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
 __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const int oy0, const int oy1,
                                        const int ox0, const int ox1) {
@@ -515,11 +415,10 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   const int tid = threadIdx.x, lane = tid & 31;
   __shared__ DevImage im;
   __shared__ TileLayout L;
-  __shared__ int ctr[2];                   // dynamic work counters (colour, output)
+  __shared__ int ctr[2];                   // dynamic work counter of the output phase (ctr[1])
   if (tid == 0) {
     im = kp.imgs[n];
     tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP);
-    ctr[0] = 0;
     ctr[1] = 0;
   }
   __syncthreads();
@@ -709,18 +608,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       const int j0 = (ready_prev + 1) >> 1;
       const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
       const int ntaskc = nq * ntask4;
-#if SMOL_OPT_COLSTATIC
       // colour tasks all cost the same and nothing else runs in this phase:
       // a static round-robin needs no work counter
-#pragma unroll(kColUnroll)
       for (int t = tid; t < ntaskc; t += kThreads) {
-#else
-      for (;;) {
-        const int chunk = grab_chunk(&ctr[0], lane);
-        if (chunk >= ntaskc) break;
-        const int t = chunk + lane;
-        if (t >= ntaskc) continue;
-#endif
         const int rr = (int)fdiv((uint32_t)t, fd_t4);
         const int p = t - rr * ntask4;
         const int j = j0 + rr;                               // chroma row of the quads
@@ -755,18 +645,11 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
         const int slot = rgb_slot(2 * j);
         uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
-#if SMOL_OPT_YMAGIC
         const uint32_t mg = 0x4B000000u;
         const uint2 t01 = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x7541), cbq[0], cbq[1], crq[0], crq[1]);
         const uint2 t23 = colour2m(__byte_perm(y0, mg, 0x7542), __byte_perm(y0, mg, 0x7543), cbq[2], cbq[3], crq[2], crq[3]);
         const uint2 b01 = colour2m(__byte_perm(y1, mg, 0x7540), __byte_perm(y1, mg, 0x7541), cbq[4], cbq[5], crq[4], crq[5]);
         const uint2 b23 = colour2m(__byte_perm(y1, mg, 0x7542), __byte_perm(y1, mg, 0x7543), cbq[6], cbq[7], crq[6], crq[7]);
-#else
-        const uint2 t01 = colour2(y0 & 255, (y0 >> 8) & 255, cbq[0], cbq[1], crq[0], crq[1]);
-        const uint2 t23 = colour2((y0 >> 16) & 255, y0 >> 24, cbq[2], cbq[3], crq[2], crq[3]);
-        const uint2 b01 = colour2(y1 & 255, (y1 >> 8) & 255, cbq[4], cbq[5], crq[4], crq[5]);
-        const uint2 b23 = colour2((y1 >> 16) & 255, y1 >> 24, cbq[6], cbq[7], crq[6], crq[7]);
-#endif
         const uint4 top = make_uint4(t01.x, t01.y, t23.x, t23.y);
         *reinterpret_cast<uint4*>(r0p) = top;
         *reinterpret_cast<uint4*>(r0p + rgb_p) = make_uint4(b01.x, b01.y, b23.x, b23.y);
@@ -774,7 +657,6 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       }
     }
     __syncthreads();
-    if (tid == 0) ctr[0] = 0;
 
     if constexpr (DEBUG) {
       int16_t* dst = kp.dbg_rgb + n * kp.dbg_stride_rgb;
