@@ -432,3 +432,25 @@ def test_thumb_kernel_matches_tiled_kernel_and_oracle(layout, out_dtype, monkeyp
         aff = helpers.affected_outputs(po, im, qt)
         assert err[~aff].max(initial=0) <= tol, (i, err[~aff].max())
         assert err.max() <= tol + widen
+
+
+@pytest.mark.parametrize("w,h,k,out_wh", [(1920, 1080, 1, (640, 360)), (3000, 2000, 2, (448, 300)),
+                                           (4000, 3000, 8, (250, 188))])
+def test_large_footprints_column_tiles(w, h, k, out_wh):
+    """Decoded footprints wider than the widest shared-memory ring (512 px):
+    the plan splits tiles into column bands; parity with the oracle (maximum
+    sizes of the path: 1080p at full scale, 12 MP at 1/8)."""
+    rng = np.random.default_rng(w + k)
+    qt = synth.quant_tables(75)
+    imgs = [synth.make_image(rng, w, h, qt)]
+    cfg = synth.Config("big", 1, w, h, k, "exact", resize_w=out_wh[0], resize_h=out_wh[1])
+    ps, po = _cfg_params(cfg)
+    plan = smol.Plan(ps, 1)
+    out = plan.run(smol.CoefBatch(imgs, qt))
+    torch.cuda.synchronize()
+    ref = oracle.run_image(po, imgs[0], qt).astype(np.float64)
+    err = np.abs(out[0].float().cpu().numpy() - ref).max(axis=0)
+    aff = helpers.affected_outputs(po, imgs[0], qt)        # reading R3 tie band
+    assert err[~aff].max(initial=0) <= TOL[cfg.out_dtype], err[~aff].max()
+    assert err.max() <= TOL[cfg.out_dtype] + 2.0 / (255 * min(synth.IMAGENET_STD))
+    plan.close()
