@@ -209,8 +209,12 @@ int32_t smol_compact_encode(const smol_preproc_params* params, const smol_image_
  * rebuilds the ROI blocks of the plan's layout in plan-owned staging and the
  * fused kernel runs (double-buffered: the next call's DMA overlaps this
  * call's expand + fused kernel).  Each record's header must match the ROI ranges
- * the plan computes for its image (SMOL_ERR_INVALID otherwise).  Staging is
- * allocated on first use and grown for a larger batch.  out: DEVICE. */
+ * the plan computes for its image and lie inside the arena: checked on the
+ * host (SMOL_ERR_INVALID) when the arena is host memory; a DEVICE arena is
+ * not read by the host, so only its record offsets are checked and the
+ * records are trusted to come from smol_compact_encode with this plan's
+ * params.  Staging is allocated on first use and grown for a larger batch.
+ * out: DEVICE. */
 int32_t smol_preproc_run_compact(smol_preproc_plan_t* plan, const smol_compact_batch* batch,
                                  void* out, void* stream);
 
