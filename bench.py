@@ -48,6 +48,17 @@ def _traffic(cfg_name: str, layout: str):
         return None
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -139,7 +150,7 @@ def _cpu_baseline(cfg, imgs, qt, budget_s: float, max_images: int):
     with ThreadPoolExecutor(cores) as ex:
         list(ex.map(lambda im: oracle.run_image(po, im, qt), sample))
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
             "sample": f"{n} {cfg.name} images ({cfg.width}x{cfg.height}, cycling the batch), "
                       f"thread pool of {cores} over images, {dt:.1f} s wall",
             "seconds": dt}
@@ -178,6 +189,7 @@ def run_reference(args, rank, world):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": _workload_name(cfg), "sample_per_step": n},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "cpu_model": _cpu_model(),
                              "sample": f"{n} images of {cfg.name} per step, thread pool of {cores}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
