@@ -209,3 +209,44 @@ def test_run_compact_rejects_foreign_records():
     with pytest.raises(smol.SmolError) as e:
         plan.run(cb)
     assert e.value.status == 1
+
+
+def test_encoder_roundtrip_int16_extremes():
+    """Full int16 range (the ABI accepts any coefficient): the escape
+    boundaries -512/-511/511/512 and -32768/32767 survive the record."""
+    rng = np.random.default_rng(2)
+    w, h = 48, 40
+    special = np.array([-32768, 32767, -512, -511, 511, 512, -1, 1, 0, 0, 0, 0], np.int16)
+    coef = []
+    for (bh, bw) in [(5, 6), (3, 3), (3, 3)]:
+        c = rng.choice(special, size=(bh, bw, 64)).astype(np.int16)
+        c[0, 0] = rng.integers(-32768, 32768, size=64, dtype=np.int64).astype(np.int16)
+        coef.append(c)
+    im = synth.CoefImage(w, h, coef)
+    p = smol.make_params(scale_denom=1, resize_mode="exact", resize_w=w, resize_h=h)
+    E, _, blocks = read_record(smol.compact_encode(p, im))
+    g = smol.geometry(p, w, h)
+    assert len(blocks) == g["roi_blocks"]
+    for (c, by, bx), blk in blocks.items():
+        np.testing.assert_array_equal(blk, coef[c][by, bx])
+
+
+@pytest.mark.gpu
+def test_run_compact_int16_extremes_equal_dense():
+    import torch
+    rng = np.random.default_rng(3)
+    special = np.array([-32768, 32767, -512, -511, 511, 512, -1, 1, 0, 0, 0, 0], np.int16)
+    imgs = []
+    for (w, h) in [(48, 40), (130, 77)]:
+        shapes = [(-(-h // 8), -(-w // 8)), (-(-h // 16), -(-w // 16)), (-(-h // 16), -(-w // 16))]
+        imgs.append(synth.CoefImage(w, h, [rng.choice(special, size=s + (64,)).astype(np.int16) for s in shapes]))
+    qt = synth.quant_tables(50)
+    for k in (1, 2, 4):
+        p = smol.params_from_config(synth.CONFIGS["c1"], scale_denom=k, resize_w=24, resize_h=16)
+        plan = smol.Plan(p, len(imgs))
+        a = plan.run(smol.batch_for(p, imgs, qt)).clone()
+        b = plan.run(smol.CompactBatch(p, imgs, qt))
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), k
+        assert torch.isfinite(a).all()
+        plan.close()
