@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     __syncwarp();
     const int lx0 = S.L.lx0, ly0 = S.L.ly0, fw = S.L.lx1 - lx0 + 1, fh = S.L.ly1 - ly0 + 1;
     const int cx0 = S.L.cx0, cy0 = S.L.cy0, cw = S.L.cx1 - cx0 + 1, ch = S.L.cy1 - cy0 + 1;
+    // magic-number divisions by the runtime widths (all operands < 2^16)
+    const FastDiv fd_fw = make_fastdiv(fw), fd_cw = make_fastdiv(cw), fd_nq = make_fastdiv((OW + 3) >> 2);
     // taps (reading R9: exact integers); a clamped upper tap gets weight 0
     for (int i = lane; i < OW; i += 32) {
       int i0, i1; float w;
@@ -59,14 +61,14 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     // 1/8 decode (reading R1/R3): u8 = clamp(floor(DC * Q0 / 8 + 128 + 1/2))
     const float qy = (float)kp.qtables[im.qidx[0] * 64] * 0.125f;
     for (int p = lane; p < fw * fh; p += 32) {
-      const int r = p / fw, x = p - r * fw;
+      const int r = (int)fdiv((uint32_t)p, fd_fw), x = p - r * fw;
       const int16_t dc = __ldg(im.coef[0] + (size_t)(ly0 + r) * im.stride[0] + (size_t)(lx0 + x) * E);
       S.y[r * kThumbMaxFoot + x] = (uint8_t)round_u8((float)dc * qy);
     }
     for (int cc = 0; cc < 2; ++cc) {
       const float qc = (float)kp.qtables[im.qidx[1 + cc] * 64] * 0.125f;
       for (int p = lane; p < cw * ch; p += 32) {
-        const int r = p / cw, x = p - r * cw;
+        const int r = (int)fdiv((uint32_t)p, fd_cw), x = p - r * cw;
         uint8_t v = 128;                          // grayscale: neutral chroma (reading R14)
         if (!im.gray) {
           const int16_t dc = __ldg(im.coef[1 + cc] + (size_t)(cy0 + r) * im.stride[1 + cc] + (size_t)(cx0 + x) * E);
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     // 4:2:0 centred triangle upsample (reading R2, neighbours clamped to the
     // valid chroma size) + exact JFIF colour (R6)
     for (int p = lane; p < fw * fh; p += 32) {
-      const int r = p / fw, x = p - r * fw;
+      const int r = (int)fdiv((uint32_t)p, fd_fw), x = p - r * fw;
       const int X = lx0 + x, Yr = ly0 + r;
       const int i = X >> 1, j = Yr >> 1;
       const int in = min(max((X & 1) ? i + 1 : i - 1, 0), im.Wc - 1);
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
     const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
     for (int t = lane; t < nq * OH; t += 32) {
-      const int oy = t / nq, ox = 4 * (t - oy * nq);
+      const int oy = (int)fdiv((uint32_t)t, fd_nq), ox = 4 * (t - oy * nq);
       const int2 ty = S.yt[oy];
       const float2 wy2 = f2(__int_as_float(ty.y));
       const uint32_t* r0 = S.rgb + (ty.x & 0xffff) * kThumbMaxFoot;
