@@ -20,10 +20,10 @@ constexpr int kThumbMaxFoot = 32;              // decoded luma footprint limit (
 constexpr int kThumbMaxOut = 128;              // output width / height limit
 constexpr int kThumbCP = kThumbMaxFoot / 2 + 2;   // chroma footprint pitch
 struct ThumbWarpSmem {
-  uint32_t rgb[kThumbMaxFoot * kThumbMaxFoot];  // RGBx of the luma footprint
+  uint32_t rgb[kThumbMaxFoot * kThumbMaxFoot + 1];  // RGBx of the luma footprint (+1: x0 + 1 read at the end)
   uint8_t y[kThumbMaxFoot * kThumbMaxFoot];
   uint8_t c[2][kThumbCP * kThumbCP];
-  int2 xt[kThumbMaxOut];                         // per output column: {x0 - lx0 | (x1 - lx0) << 16, w}
+  int4 xp[kThumbMaxOut / 2];                     // per output column pair: {4 x0 (a), 4 x0 (b), w (a), w (b)}
   int2 yt[kThumbMaxOut];                         // per output row:    {y0 - ly0 | (y1 - ly0) << 16, w}
   TileLayout L;
 };
@@ -48,10 +48,15 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     // magic-number divisions by the runtime widths (all operands < 2^16)
     const FastDiv fd_fw = make_fastdiv(fw), fd_cw = make_fastdiv(cw), fd_nq = make_fastdiv((OW + 3) >> 2);
     // taps (reading R9: exact integers); a clamped upper tap gets weight 0
-    for (int i = lane; i < OW; i += 32) {
-      int i0, i1; float w;
-      src_tap(im.left + i, im.Wd, im.Wr, i0, i1, w);
-      S.xt[i] = make_int2((i0 - lx0) | ((i1 - lx0) << 16), __float_as_int(i1 == i0 ? 0.f : w));
+    // column taps per output pair, byte offsets of x0 in an RGB row; the
+    // kernel always reads x0 + 1 (a clamped upper tap has weight 0, and the
+    // byte -> float trick keeps even stale words finite)
+    for (int q = lane; q < (OW + 1) >> 1; q += 32) {
+      int a0, a1, b0, b1; float wa, wb;
+      src_tap(im.left + 2 * q, im.Wd, im.Wr, a0, a1, wa);
+      src_tap(im.left + min(2 * q + 1, OW - 1), im.Wd, im.Wr, b0, b1, wb);
+      S.xp[q] = make_int4(4 * (a0 - lx0), 4 * (b0 - lx0), __float_as_int(a1 == a0 ? 0.f : wa),
+                          __float_as_int(b1 == b0 ? 0.f : wb));
     }
     for (int i = lane; i < OH; i += 32) {
       int i0, i1; float w;
@@ -111,10 +116,14 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
       float v[3][4];
 #pragma unroll
       for (int e = 0; e < 4; e += 2) {
-        const int2 ta = S.xt[min(ox + e, OW - 1)], tb = S.xt[min(ox + e + 1, OW - 1)];
-        const float2 wx = make_float2(__int_as_float(ta.y), __int_as_float(tb.y));
-        const uint32_t p00 = r0[ta.x & 0xffff], p01 = r0[ta.x >> 16], p10 = r1[ta.x & 0xffff], p11 = r1[ta.x >> 16];
-        const uint32_t q00 = r0[tb.x & 0xffff], q01 = r0[tb.x >> 16], q10 = r1[tb.x & 0xffff], q11 = r1[tb.x >> 16];
+        const int4 tx = S.xp[min((ox + e) >> 1, ((OW + 1) >> 1) - 1)];
+        const float2 wx = make_float2(__int_as_float(tx.z), __int_as_float(tx.w));
+        const uint8_t* a0 = reinterpret_cast<const uint8_t*>(r0) + tx.x;
+        const uint8_t* a1 = reinterpret_cast<const uint8_t*>(r1) + tx.x;
+        const uint8_t* b0 = reinterpret_cast<const uint8_t*>(r0) + tx.y;
+        const uint8_t* b1 = reinterpret_cast<const uint8_t*>(r1) + tx.y;
+        const uint32_t p00 = lds_u32(a0), p01 = lds_u32(a0 + 4), p10 = lds_u32(a1), p11 = lds_u32(a1 + 4);
+        const uint32_t q00 = lds_u32(b0), q01 = lds_u32(b0 + 4), q10 = lds_u32(b1), q11 = lds_u32(b1 + 4);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const int sel = 0x7540 + c;
