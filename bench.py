@@ -7,17 +7,30 @@ store) for every image of the batch, in one fused kernel launch.  Default
 workload: BASELINE.json configs[1] = c2, 256 ImageNet-shaped 500x375 4:2:0
 images, full-scale decode, short side 256, centre crop 224, fp32 NCHW.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl smol|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                  [--impl smol|reference] [--scaling weak|strong]
+                  [--configs c1,c3a,c3b,c4,c5|none] [--no-eq4]
 
-N > 1: launched by torchrun, one process per GPU; every rank processes its
-own batch (images are independent; no data-path collective: weak scaling).
-Timing: CUDA events on the launching stream, barrier + synchronize on both
-sides, max over ranks.  Prints one JSON line (rank 0).
+N > 1: launched by torchrun, one process per GPU.  Images are independent
+units: every rank runs its own contiguous, ROI-balanced range
+of the batch; there is no data-path collective and no NCCL communicator --
+the ranks meet only in a gloo (host) barrier around the timed region and in
+the max-over-ranks reduction of their device times.  Timing: CUDA events on
+the launching stream, barrier + synchronize on both sides, max over ranks.
+Rank 0 prints one JSON line.
+
+Besides the headline config, the default run times the other BASELINE.json
+configs (c1, c3a, c3b, c4, c5) under "configs" (value, launch time,
+SURVEY 8(d) algorithmic bytes and HBM fraction of each), measures the pinned
+host->device copy peak for the end-to-end roofline, reports the Eq. 4
+throughput model beside the measurement (ResNet-50 on the same GPU), and
+times the CPU oracle on a bounded sample (cpu_baseline).
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -35,6 +48,21 @@ import synth  # noqa: E402
 METRIC = "preprocessed images/sec"
 UNIT = "images/s"
 L2_BYTES = 126 * 2 ** 20
+# coefficient layout each config is benchmarked in: PACKED stores only the
+# coefficients the scale uses (what a host entropy decoder would hand over);
+# at scale 1 it is the dense-64 layout
+LAYOUT = {"c1": "dense", "c2": "dense", "c3a": "packed", "c3b": "packed", "c4": "packed", "c5": "packed"}
+# distinct synthetic images per config (replicated into distinct buffers)
+N_DISTINCT = {"c5": 16}
+# PAPER.md context numbers (another machine's: AWS g4dn.xlarge, one T4 + 4 vCPUs)
+PAPER_CONTEXT = {
+    "hardware": "AWS g4dn.xlarge: NVIDIA T4 GPU + 4 vCPU cores (PAPER.md P:384-392)",
+    "resnet50_tensorrt_img_s": 4513,
+    "resnet50_tensorrt_cite": "PAPER.md P:346-362 (Table: ResNet-50 on the T4, TensorRT 4,513 im/s)",
+    "preproc_vs_resnet50_exec": "preprocessing (libjpeg-turbo + OpenCV on the CPU cores) 7.1x lower "
+                                "throughput than ResNet-50 execution on the T4 (P:394-402)",
+    "smol_pipelined_low_res": "Smol preprocessing / DNN / pipelined: 5.9k / 4.2k / 3.6k im/s (P:1376-1380)",
+}
 
 
 def _traffic(cfg_name: str, layout: str):
@@ -134,6 +162,51 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+def _workload_name(cfg):
+    out = "x".join(str(v) for v in (3,) + cfg.out_hw)
+    return (f"{cfg.name}: {cfg.n} x {cfg.width}x{cfg.height} 4:2:0 JPEG coefficients (q{cfg.quality}), "
+            f"decode scale 1/{cfg.scale_denom}, "
+            + (f"resize short {cfg.resize_short}, crop {cfg.crop_w}x{cfg.crop_h}" if cfg.resize_mode == "short"
+               else f"resize {cfg.resize_w}x{cfg.resize_h}")
+            + f" -> {cfg.out_dtype} NCHW {out}")
+
+
+def _config_key(cfg):
+    """The `config` object both arms print (identical for the same workload)."""
+    return {"workload": _workload_name(cfg)}
+
+
+# ----------------------------------------------------------- distributed ---
+class Group:
+    """Host-side process group of the N > 1 run: gloo only (no NCCL).  The
+    path has no data exchange; ranks only barrier around the timed region and
+    reduce their device times (max)."""
+
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        from paper_2007_13005_b200 import shard
+        return shard.max_over_ranks(v)
+
+    def close(self):
+        if self.dist:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+# --------------------------------------------------------------- oracle ---
 def _cpu_baseline(cfg, imgs, qt, budget_s: float, max_images: int):
     """The oracle as it stands, on this host's cores, over a bounded sample."""
     import oracle
@@ -156,9 +229,9 @@ def _cpu_baseline(cfg, imgs, qt, budget_s: float, max_images: int):
             "seconds": dt}
 
 
-def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle (this tier's reference arm)."""
-    if rank != 0:
+def run_reference(args, grp):
+    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    if grp.rank != 0:
         return
     cfg = synth.CONFIGS[args.config]
     imgs, qt = synth.distinct_images(cfg, n_distinct=min(cfg.n, 16))
@@ -185,9 +258,10 @@ def run_reference(args, rank, world):
     value = n * args.steps / dt
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": _workload_name(cfg), "sample_per_step": n},
+            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _config_key(cfg),
+            "workload_detail": {"sample_per_step": n,
+                                "note": "each step is a bounded sample of the workload's images"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "cpu_model": _cpu_model(),
                              "sample": f"{n} images of {cfg.name} per step, thread pool of {cores}"},
@@ -195,7 +269,8 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def _eq4(args, plan, batches, reps, out, stream, nloc, t_pre):
+# ---------------------------------------------------------------- Eq. 4 ---
+def _eq4(plan, batches, reps, out, stream, nloc, t_pre):
     """Eq. 4 beside the measurement: T_exec of ResNet-50
     on this GPU (torchvision architecture, random init: no weights offline;
     fp16, channels_last, CUDA graph, the same batch), the measured pipelined
@@ -263,16 +338,183 @@ def _eq4(args, plan, batches, reps, out, stream, nloc, t_pre):
                    f"batch {nloc}, incl. the NCHW->fp16 channels_last conversion of the preprocessed batch",
             "models": tpm.model_errors(t_pipe, t_pre, [t_exec]),
             "note": "Eq. 4 min() assumes the two stages run on disjoint resources (the paper's CPU "
-                    "preprocessing + GPU DNN); here both share one B200, where the sum model applies"}
+                    "preprocessing + GPU DNN); here both share one B200, where the sum model applies",
+            "paper_context": PAPER_CONTEXT}
 
 
-def _workload_name(cfg):
-    out = "x".join(str(v) for v in (3,) + cfg.out_hw)
-    return (f"{cfg.name}: {cfg.n} x {cfg.width}x{cfg.height} 4:2:0 JPEG coefficients (q{cfg.quality}), "
-            f"decode scale 1/{cfg.scale_denom}, "
-            + (f"resize short {cfg.resize_short}, crop {cfg.crop_w}x{cfg.crop_h}" if cfg.resize_mode == "short"
-               else f"resize {cfg.resize_w}x{cfg.resize_h}")
-            + f" -> {cfg.out_dtype} NCHW {out}")
+def _pcie_h2d_peak(nbytes: int = 256 << 20) -> dict:
+    """Pinned host -> device copy bandwidth (best of 5, CUDA events): the
+    roofline of the end-to-end path's transfer."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    best = 0.0
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        with torch.cuda.stream(s):
+            d.copy_(h, non_blocking=True)
+        b.record(s)
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+    return {"gbs": best, "bytes": nbytes, "how": "pinned host->device torch copy of 256 MiB, best of 6"}
+
+
+# ------------------------------------------------------------- workload ---
+class Workload:
+    """One config on this rank: its shard of the batch, plan, rotating
+    device replicas (inputs larger than L2), output, stream."""
+
+    def __init__(self, cfg, grp, scaling, batch=0, tile_rows=0, layout=None, replicas=0, n_distinct=None):
+        import torch
+        import paper_2007_13005_b200 as smol
+        from paper_2007_13005_b200 import shard
+        self.cfg = cfg
+        self.layout = layout or LAYOUT[cfg.name]
+        self.params = smol.params_from_config(cfg, tile_rows=tile_rows, layout=self.layout)
+        n_total = (batch or cfg.n) * (grp.world if scaling == "weak" else 1)
+        nd = n_distinct or N_DISTINCT.get(cfg.name)
+        self.all_imgs, self.qt = synth.batch_images(cfg, n=n_total, n_distinct=min(n_total, nd or 64))
+        lo, hi = shard.partition(shard.roi_weights(self.params, self.all_imgs), grp.world)[grp.rank]
+        self.imgs = self.all_imgs[lo:hi]            # this rank allocates only its own shard
+        self.n_total = n_total
+        self.nloc = len(self.imgs)
+        self.plan = smol.Plan(self.params, max(self.nloc, 1))
+        one = smol.batch_for(self.params, self.imgs[:1], self.qt)
+        self.arena_bytes = one.coef_bytes * max(self.nloc, 1)
+        self.reps = replicas or max(2, int(np.ceil(1.5 * L2_BYTES / max(self.arena_bytes, 1))) + 1)
+        self.batches = [smol.batch_for(self.params, self.imgs, self.qt) for _ in range(self.reps)]
+        self.out = self.plan.new_output(max(self.nloc, 1))[:self.nloc]
+        self.stream = torch.cuda.Stream()
+        g = smol.geometry(self.params, cfg.width, cfg.height)
+        self.geom = g
+        self.out_bytes = 3 * g["OH"] * g["OW"] * (2 if cfg.out_dtype == "f16" else 4)
+        # SURVEY 8(d): ROI coefficients the scale uses + the output tensor
+        self.alg_bytes_img = g["roi_coef_bytes"] + self.out_bytes
+        self.storage_bytes_img = g["storage_coef_bytes"] + self.out_bytes
+
+    def step(self, k, out=None):
+        if self.nloc:
+            self.plan.run(self.batches[k % self.reps], out=self.out if out is None else out, stream=self.stream)
+
+    def timed(self, grp, steps, warmup, clocks=None):
+        """Device time of `steps` back-to-back steps (CUDA events on the
+        launching stream; barrier + synchronize on both sides; max over ranks)."""
+        import torch
+        with torch.cuda.stream(self.stream):
+            for k in range(warmup):
+                self.step(k)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        grp.barrier()
+        torch.cuda.synchronize()
+        ctx = clocks if clocks is not None else _Null()
+        with ctx:
+            ev0.record(self.stream)
+            for k in range(steps):
+                self.step(k)
+            ev1.record(self.stream)
+            torch.cuda.synchronize()
+        grp.barrier()
+        return grp.max(ev0.elapsed_time(ev1))
+
+    def launch_ms(self, n=50):
+        """Median duration of one launch (events bracketing each run on its stream)."""
+        import torch
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for k, (a, b) in enumerate(evs):
+            a.record(self.stream)
+            self.step(k)
+            b.record(self.stream)
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+    def kernel_name(self):
+        return ("smol_thumb_kernel" if self.cfg.scale_denom == 8 and self.layout == "packed"
+                else "smol_fused_kernel")
+
+    def e2e(self, grp, steps):
+        """Same metric through the public end-to-end entry points, pinned host
+        inputs: smol_preproc_run_compact (compact records; one H2D DMA +
+        expand kernel + fused kernel) and smol_preproc_run_host (dense ROI
+        block rows gathered over PCIe); each step also reads one image's
+        output back to the host.  At scale 1/8 the packed DC plane is already
+        smaller than a compact record, so run_host is the e2e path there."""
+        import torch
+        import paper_2007_13005_b200 as smol
+        res_host = torch.empty((1,) + tuple(self.out.shape[1:]), dtype=self.out.dtype, pin_memory=True)
+
+        def e2e_time(host_batches):
+            for k in range(6):
+                self.plan.run(host_batches[k % 2], out=self.out, stream=self.stream)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            grp.barrier()
+            e0.record(self.stream)
+            for k in range(steps):
+                self.plan.run(host_batches[k % 2], out=self.out, stream=self.stream)
+                with torch.cuda.stream(self.stream):
+                    res_host.copy_(self.out[:1], non_blocking=True)
+            e1.record(self.stream)
+            torch.cuda.synchronize()
+            ms = grp.max(e0.elapsed_time(e1) / steps)
+            return self.n_total / (ms / 1e3), ms
+
+        d2h = int(res_host.numel() * res_host.element_size()) * grp.world
+        gather_value, gather_ms = e2e_time([smol.batch_for(self.params, self.imgs, self.qt, location="pinned")
+                                            for _ in range(2)])
+        gather_h2d = self.geom["storage_coef_bytes"] * self.n_total
+        if self.cfg.scale_denom == 8:
+            return {"value": gather_value, "unit": UNIT, "h2d_bytes_per_step": gather_h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": gather_ms,
+                    "path": "smol_preproc_run_host: ROI block rows of the packed DC plane gathered from pinned "
+                            "host memory; D2H of one image's output as the step's result read"}
+        # host entropy-decoder side: encoding a record (not timed in e2e; reported)
+        t0 = time.perf_counter()
+        nenc = min(len(self.imgs), 16)
+        for im in self.imgs[:nenc]:
+            smol.compact_encode(self.params, im)
+        enc_us = (time.perf_counter() - t0) / max(nenc, 1) * 1e6
+        cbs = [smol.CompactBatch(self.params, self.imgs, self.qt, location="pinned") for _ in range(2)]
+        compact_value, compact_ms = e2e_time(cbs)
+        compact_h2d = cbs[0].arena_bytes * grp.world
+        return {"value": compact_value, "unit": UNIT, "h2d_bytes_per_step": compact_h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": compact_ms,
+                "path": "smol_preproc_run_compact: compact records (ROI blocks, nonzero used coefficients) "
+                        "in pinned host memory -> one H2D DMA + expand kernel + fused kernel; D2H of one "
+                        "image's output as the step's result read",
+                "host_encode_us_per_image": enc_us,
+                "host_encode_note": "smol_compact_encode from dense host planes, one host thread (the host "
+                                    "entropy decoder's hand-off; outside the timed region)",
+                "run_host": {"value": gather_value, "h2d_bytes_per_step": gather_h2d, "ms_per_step": gather_ms,
+                             "path": "dense ROI block rows gathered from pinned host memory"}}
+
+    def close(self):
+        self.plan.close()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _config_entry(w: "Workload", grp, peak, min_ms=60.0):
+    """Timing of one extra config: enough steps for >= min_ms of device time."""
+    probe = w.timed(grp, 5, 3)
+    steps = int(min(3000, max(20, math.ceil(min_ms / max(probe / 5, 1e-3)))))
+    ms = w.timed(grp, steps, 3)
+    lm = w.launch_ms()
+    achieved = w.alg_bytes_img * w.nloc / (lm / 1e3) / 1e9
+    return {"workload": _workload_name(w.cfg), "layout": w.layout, "value": w.n_total * steps / (ms / 1e3),
+            "unit": UNIT, "steps": steps, "ms_per_step": ms / steps, "launch_ms": lm,
+            "alg_bytes_per_image": w.alg_bytes_img, "roi_coef_bytes_per_image": w.geom["roi_coef_bytes"],
+            "storage_bytes_per_image": w.storage_bytes_img, "achieved_gbs": achieved, "peak_gbs": peak,
+            "frac": achieved / peak, "kernel": w.kernel_name(), "traffic": _traffic(w.cfg.name, w.layout),
+            "batch_per_gpu": w.nloc}
 
 
 def main():
@@ -282,178 +524,107 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="smol", choices=["smol", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the config's N images per GPU; strong: the config's N split over the GPUs")
     ap.add_argument("--replicas", type=int, default=0, help="rotating input replicas (0 = auto: > L2)")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--tile-rows", type=int, default=0)
-    ap.add_argument("--eq4", action="store_true",
-                    help="also measure ResNet-50 on this GPU and pipelined preprocessing+DNN (Eq. 4 report)")
+    ap.add_argument("--no-eq4", action="store_true", help="skip the Eq. 4 report (ResNet-50 on this GPU)")
+    ap.add_argument("--eq4", action="store_true", help=argparse.SUPPRESS)   # (on by default)
+    ap.add_argument("--configs", default="c1,c3a,c3b,c4,c5",
+                    help="other configs timed after the headline one ('none' to skip)")
     ap.add_argument("--batch", type=int, default=0, help="images per GPU (0 = the config's N)")
-    ap.add_argument("--layout", default="dense", choices=["dense", "packed"],
-                    help="coefficient block layout (packed: only the coefficients the scale uses)")
+    ap.add_argument("--layout", default=None, choices=["dense", "packed"],
+                    help="coefficient block layout (default per config: dense at scale 1, packed otherwise)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-
+    grp = Group()
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, grp)
+        grp.close()
         return
 
     import torch
-    import paper_2007_13005_b200 as smol
-
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-
+    torch.cuda.set_device(grp.local_rank)
     cfg = synth.CONFIGS[args.config]
-    params = smol.params_from_config(cfg, tile_rows=args.tile_rows, layout=args.layout)
-    # weak scaling: a global batch of cfg.n images per GPU, partitioned into
-    # contiguous ROI-balanced ranges (one per rank); no data-path collective
-    from paper_2007_13005_b200 import shard
-    per_gpu = args.batch or cfg.n
-    all_imgs, qt = synth.batch_images(cfg, n=per_gpu * world)
-    lo, hi = shard.partition(shard.roi_weights(params, all_imgs), world)[rank]
-    imgs = all_imgs[lo:hi]
-    nloc = len(imgs)
-    plan = smol.Plan(params, max(nloc, 1))
-    arena_bytes = smol.batch_for(params, imgs[:1], qt).coef_bytes * len(imgs)
-    reps = args.replicas or max(2, int(np.ceil(1.5 * L2_BYTES / max(arena_bytes, 1))) + 1)
-    batches = [smol.batch_for(params, imgs, qt) for _ in range(reps)]
-    out = plan.new_output(nloc)
-    stream = torch.cuda.Stream()
+    w = Workload(cfg, grp, args.scaling, batch=args.batch, tile_rows=args.tile_rows, layout=args.layout,
+                 replicas=args.replicas)
 
-    # algorithmic bytes per image: ROI coefficients + output tensor
-    g = smol.geometry(params, cfg.width, cfg.height)
-    out_bytes = 3 * g["OH"] * g["OW"] * (2 if cfg.out_dtype == "f16" else 4)
-    alg_bytes_img = g["roi_coef_bytes"] + out_bytes
-    alg_bytes_launch = alg_bytes_img * nloc
+    # ---- timed region: K steps of the headline config ------------------------
+    clk = ClockSampler(grp.local_rank)
+    ms_max = w.timed(grp, args.steps, args.warmup, clocks=clk)
+    value = w.n_total * args.steps / (ms_max / 1e3)
+    launch_ms = w.launch_ms(min(max(args.steps, 20), 50))
+    e2e = w.e2e(grp, args.e2e_steps)
 
-    def step(k, o=out):
-        plan.run(batches[k % reps], out=o, stream=stream)
-
-    with torch.cuda.stream(stream):
-        for k in range(args.warmup):
-            step(k)
-    torch.cuda.synchronize()
-
-    # ---- timed region: K steps --------------------------------------------
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        ev0.record(stream)
-        for k in range(args.steps):
-            step(k)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms_max = shard.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
-    value = len(all_imgs) * args.steps / (ms_max / 1e3)
-
-    # ---- per-launch kernel duration (events bracket each launch) ------------
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(min(args.steps, 50))]
-    for k, (a, b) in enumerate(evs):
-        a.record(stream)
-        step(k)
-        b.record(stream)
-    torch.cuda.synchronize()
-    launch_ms = statistics.median(a.elapsed_time(b) for a, b in evs)
-
-    # ---- end to end: pinned host inputs -> device -> result read ------------
-    # Two public entry points: smol_preproc_run_compact (compact records, one
-    # DMA + expand kernel; the headline e2e) and smol_preproc_run_host (dense
-    # ROI block rows gathered over PCIe).  At scale 1/8 the packed DC plane is
-    # already smaller than a compact record, so run_host is the e2e path there.
-    res_host = torch.empty((1,) + tuple(out.shape[1:]), dtype=out.dtype, pin_memory=True)
-
-    def e2e_time(host_batches):
-        for k in range(6):
-            plan.run(host_batches[k % 2], out=out, stream=stream)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for k in range(args.e2e_steps):
-            plan.run(host_batches[k % 2], out=out, stream=stream)
-            with torch.cuda.stream(stream):
-                res_host.copy_(out[:1], non_blocking=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms = shard.max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, device="cuda")
-        return len(all_imgs) / (ms / 1e3)
-
-    gather_value = e2e_time([smol.batch_for(params, imgs, qt, location="pinned") for _ in range(2)])
-    gather_h2d = g["roi_coef_bytes"] * len(all_imgs)
-    use_compact = cfg.scale_denom != 8
-    if use_compact:
-        cbs = [smol.CompactBatch(params, imgs, qt, location="pinned") for _ in range(2)]
-        compact_value = e2e_time(cbs)
-        compact_h2d = cbs[0].arena_bytes * world
-    d2h = int(res_host.numel() * res_host.element_size()) * world
-    if use_compact:
-        e2e = {"value": compact_value, "unit": UNIT, "h2d_bytes_per_step": compact_h2d, "d2h_bytes_per_step": d2h,
-               "path": "smol_preproc_run_compact: compact records (ROI blocks, nonzero used coefficients) "
-                       "in pinned host memory -> one H2D DMA + expand kernel + fused kernel; D2H of one "
-                       "image's output as the step's result read",
-               "run_host": {"value": gather_value, "h2d_bytes_per_step": gather_h2d,
-                            "path": "dense ROI block rows gathered from pinned host memory"}}
-    else:
-        e2e = {"value": gather_value, "unit": UNIT, "h2d_bytes_per_step": gather_h2d, "d2h_bytes_per_step": d2h,
-               "path": "smol_preproc_run_host: ROI block rows of the packed DC plane gathered from pinned "
-                       "host memory; D2H of one image's output as the step's result read"}
-
-    if rank == 0:
-        peak, peak_src = _peaks()
-        achieved = alg_bytes_launch / (launch_ms / 1e3) / 1e9
+    peak, peak_src = _peaks()
+    line = None
+    if grp.rank == 0:
+        achieved = w.alg_bytes_img * w.nloc / (launch_ms / 1e3) / 1e9
+        pcie = _pcie_h2d_peak()
+        e2e["pcie_h2d_peak_gbs"] = pcie["gbs"]
+        e2e["pcie_achieved_gbs"] = e2e["h2d_bytes_per_step"] / grp.world / (e2e["ms_per_step"] / 1e3) / 1e9
+        e2e["pcie_frac"] = e2e["pcie_achieved_gbs"] / pcie["gbs"]
+        e2e["pcie_peak_how"] = pcie["how"]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": grp.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": cfg.out_dtype if False else "f32",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32" if cfg.out_dtype == "f32" else "f16",
             "data": "synthetic (seeded natural-image JPEG coefficients, synth/)",
-            "config": {"workload": _workload_name(cfg), "batch_per_gpu": nloc,
-                       "global_batch": len(all_imgs), "parallelism": f"image shards x{world}, no collective",
-                       "l2": f"inputs larger than L2: {reps} rotating replicas of the "
-                             f"{arena_bytes / 1e6:.0f} MB coefficient arena",
-                       "alg_bytes_per_image": alg_bytes_img,
-                       "roi_coef_bytes_per_image": g["roi_coef_bytes"],
-                       "coef_stats": synth.coef_stats(imgs[:min(len(imgs), 64)]),
-                       "tile_rows": plan.params.tile_rows, "coef_layout": args.layout},
+            "config": _config_key(cfg),
+            "workload_detail": {
+                "batch_per_gpu": w.nloc, "global_batch": w.n_total,
+                "parallelism": f"image shards x{grp.world} ({args.scaling} scaling), no collective, no NCCL",
+                "l2": f"inputs larger than L2: {w.reps} rotating replicas of the "
+                      f"{w.arena_bytes / 1e6:.0f} MB coefficient arena",
+                "alg_bytes_per_image": w.alg_bytes_img,
+                "roi_coef_bytes_per_image": w.geom["roi_coef_bytes"],
+                "storage_bytes_per_image": w.storage_bytes_img,
+                "coef_stats": synth.coef_stats(w.imgs[:min(w.nloc, 64)]),
+                "tile_rows": w.plan.params.tile_rows, "coef_layout": w.layout},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _traffic(cfg.name, args.layout), "peak_source": peak_src,
-                         "kernel": ("smol_thumb_kernel" if cfg.scale_denom == 8 and args.layout == "packed"
-                                    else "smol_fused_kernel"), "launch_ms": launch_ms,
-                         "alg_bytes_per_launch": alg_bytes_launch},
+                         "frac": achieved / peak, "traffic": _traffic(cfg.name, w.layout), "peak_source": peak_src,
+                         "kernel": w.kernel_name(), "launch_ms": launch_ms,
+                         "alg_bytes_per_launch": w.alg_bytes_img * w.nloc,
+                         "bytes_def": "SURVEY 8(d): ROI coefficients the scale uses (K_s x 2 B per ROI block) "
+                                      "+ output tensor, per image x images per launch"},
             "e2e": e2e,
-            "gpu_launches": args.steps * plan.launches_per_run(),
+            "gpu_launches": args.steps * w.plan.launches_per_run(),
         }
-        line["dtype"] = "f32" if cfg.out_dtype == "f32" else "f16"
         c = clk.summary()
         if c:
             line["clocks"] = c
-        if args.eq4 and world == 1:
+    # ---- Eq. 4 report (N = 1), the other configs, the CPU oracle ------------
+    if line is not None and grp.world == 1 and not args.no_eq4:
+        try:
+            line["eq4"] = _eq4(w.plan, w.batches, w.reps, w.out, w.stream, w.nloc, value)
+        except Exception as e:  # noqa: BLE001
+            line["eq4"] = {"error": repr(e)}
+    names = [] if args.configs in ("", "none") else [c for c in args.configs.split(",") if c != cfg.name]
+    if names:
+        entries = {}
+        for name in names:
+            wx = Workload(synth.CONFIGS[name], grp, args.scaling)
             try:
-                line["eq4"] = _eq4(args, plan, batches, reps, out, stream, nloc, value)
-            except Exception as e:  # noqa: BLE001
-                line["eq4"] = {"error": repr(e)}
-        if world == 1 and not args.no_cpu_baseline:
+                entries[name] = _config_entry(wx, grp, peak)
+            finally:
+                wx.close()
+                del wx
+                torch.cuda.empty_cache()
+        if line is not None:
+            line["configs"] = entries
+    if line is not None:
+        if grp.world == 1 and not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = _cpu_baseline(cfg, imgs[:64], qt, args.cpu_budget, 16 * cfg.n)
+                line["cpu_baseline"] = _cpu_baseline(cfg, w.imgs[:64], w.qt, args.cpu_budget, 16 * cfg.n)
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)
-    plan.close()
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    w.close()
+    grp.close()
 
 
 if __name__ == "__main__":

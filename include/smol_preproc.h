@@ -119,9 +119,13 @@ typedef struct {
   int32_t cx0, cx1, cy0, cy1;   /* chroma footprint incl. upsample neighbours    */
   int32_t bx0[3], bx1[3], by0[3], by1[3];  /* ROI block ranges per component   */
   int64_t roi_blocks;           /* blocks under the footprint (sum over comps)  */
-  int64_t roi_coef_bytes;       /* algorithmic coefficient bytes of the image:
-                                   roi_blocks x 128 (x 32 at scale 1/8: only the
-                                   DC sector of a dense-64 block is needed)     */
+  int64_t roi_coef_bytes;       /* algorithmic coefficient bytes of the image
+                                   (SURVEY 8(d)): roi_blocks x 2 B x the K_s
+                                   coefficients scale 1/k uses (64/49/25/1 at
+                                   k = 1/2/4/8, reading R1), in any layout     */
+  int64_t storage_coef_bytes;   /* bytes the plan's layout stores for those
+                                   blocks: 128 (DENSE64; 32 at k = 8, the DC's
+                                   sector) or 128/104/56/2 (PACKED)            */
 } smol_geometry;
 
 /* Create a plan on the current CUDA device for batches of <= max_images.

@@ -13,10 +13,13 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libsmol_preproc.so")
 HEADER = os.path.join(_ROOT, "include", "smol_preproc.h")
-SOURCES = [os.path.join(_PKG, "csrc", f) for f in
-           ("smol_preproc.cu", "smol_kernels.cuh", "smol_geom.cuh", "smol_compact.cuh", "smol_thumb.cuh")]
+_CSRC = os.path.join(_PKG, "csrc")
+# translation units (compiled in parallel, then linked) and the headers they include
+UNITS = ["smol_preproc.cu", "smol_inst_k1.cu", "smol_inst_k2.cu", "smol_inst_k4.cu", "smol_inst_k8.cu"]
+HEADERS = ["smol_kernels.cuh", "smol_geom.cuh", "smol_compact.cuh", "smol_thumb.cuh", "smol_launch.h"]
+SOURCES = [os.path.join(_CSRC, f) for f in UNITS + HEADERS]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-Xfatbin", "-compress-all"]
 
 # smol_status
 SMOL_OK, SMOL_ERR_INVALID, SMOL_ERR_UNSUPPORTED, SMOL_ERR_CUDA, SMOL_ERR_NOMEM, SMOL_ERR_CAPACITY = range(6)
@@ -72,7 +75,8 @@ class Geometry(ctypes.Structure):
                                                "OW", "OH", "lx0", "lx1", "ly0", "ly1",
                                                "cx0", "cx1", "cy0", "cy1")] +
                 [(n, ctypes.c_int32 * 3) for n in ("bx0", "bx1", "by0", "by1")] +
-                [("roi_blocks", ctypes.c_int64), ("roi_coef_bytes", ctypes.c_int64)])
+                [("roi_blocks", ctypes.c_int64), ("roi_coef_bytes", ctypes.c_int64),
+                 ("storage_coef_bytes", ctypes.c_int64)])
 
     def as_dict(self):
         d = {}
@@ -90,16 +94,34 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libsmol_preproc.so (in-tree)."""
+    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libsmol_preproc.so
+    (in-tree): every unit compiled to an object in parallel, then linked."""
     if not force and not _stale():
         return LIB_PATH
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(_PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(_ROOT, "include"), "-I", _CSRC]
+
+    def compile_unit(u):
+        obj = os.path.join(objdir, u.replace(".cu", f".{os.getpid()}.o"))
+        cmd = ["nvcc", *NVCC_FLAGS, *inc, "-c", "-o", obj, os.path.join(_CSRC, u)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{r.stderr}")
+        return obj, r.stderr
+
+    with ThreadPoolExecutor(len(UNITS)) as ex:
+        res = list(ex.map(compile_unit, UNITS))
     tmp = LIB_PATH + f".tmp{os.getpid()}"
-    cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(_ROOT, "include"), "-o", tmp, SOURCES[0]]
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + [o for o, _ in res]
     r = subprocess.run(cmd, capture_output=True, text=True)
+    for o, _ in res:
+        os.remove(o)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{r.stderr}")
+        raise RuntimeError(f"nvcc link failed ({' '.join(cmd)}):\n{r.stderr}")
     if verbose:
-        print(r.stderr)
+        print("".join(e for _, e in res))
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

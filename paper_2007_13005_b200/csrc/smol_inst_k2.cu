@@ -1,0 +1,36 @@
+// smol_inst_k2.cu -- instantiations of the fused kernel at decode scale
+// 1/2 (smol_kernels.cuh); one translation unit per scale so the library
+// builds in parallel.
+#include "smol_kernels.cuh"
+#include "smol_launch.h"
+
+namespace smol {
+namespace {
+
+template <int NT> struct CfgYP {
+  static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
+};
+
+template <bool PK, int NT>
+KernelFn pick(bool f16, bool dbg) {
+  constexpr int YP = CfgYP<NT>::yp;
+  if (dbg) return f16 ? smol_fused_kernel<2, true, true, PK, NT, YP> : smol_fused_kernel<2, false, true, PK, NT, YP>;
+  return f16 ? smol_fused_kernel<2, true, false, PK, NT, YP> : smol_fused_kernel<2, false, false, PK, NT, YP>;
+}
+
+template <int NT>
+KernelFn pick_nt(bool f16, bool dbg, bool packed) {
+  return packed ? pick<true, NT>(f16, dbg) : pick<false, NT>(f16, dbg);
+}
+
+}  // namespace
+
+KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt) {
+  return nt == kThreadsNarrow ? pick_nt<kThreadsNarrow>(f16, dbg, packed)
+       : nt == kThreadsTiny   ? pick_nt<kThreadsTiny>(f16, dbg, packed)
+                              : pick_nt<kThreadsWide>(f16, dbg, packed);
+}
+
+cudaError_t upload_basis_k2(const Basis& b) { return cudaMemcpyToSymbol(c_basis, &b, sizeof(Basis)); }
+
+}  // namespace smol

@@ -53,7 +53,12 @@ struct Basis {
   float2 tp[4][4];   // column pass pairs: tp[k][y] = (t[2k][y], t[2k+1][y])
 };
 
+// One copy per translation unit (internal linkage; the library is built
+// without relocatable device code): every TU that instantiates kernels
+// exports an upload function (smol_launch.h) and the runtime fills all.
+namespace {
 __constant__ Basis c_basis;
+}
 
 // ------------------------------------------------------------ 1-D IDCTs ---
 // Reading R1 (Definition A), separable form of the oracle's sum.  The

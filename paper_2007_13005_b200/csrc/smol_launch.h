@@ -1,0 +1,25 @@
+// smol_launch.h -- kernel instantiation units of the fused kernel (one per
+// decode scale, compiled in parallel: smol_inst_k{1,2,4,8}.cu) and the host
+// runtime (smol_preproc.cu) meet here.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace smol {
+
+struct KParams;
+struct Basis;
+using KernelFn = void (*)(const KParams);
+
+// fused kernel instantiation for (scale 1/K, output dtype, debug store,
+// packed layout, threads per CTA); K fixed per unit
+KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt);
+KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt);
+KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt);
+KernelFn select_fused_k8(bool f16, bool dbg, bool packed, int nt);
+// upload the basis constants into each unit's constant bank (current device)
+cudaError_t upload_basis_k1(const Basis& b);
+cudaError_t upload_basis_k2(const Basis& b);
+cudaError_t upload_basis_k4(const Basis& b);
+cudaError_t upload_basis_k8(const Basis& b);
+
+}  // namespace smol

@@ -21,6 +21,7 @@
 #include "smol_kernels.cuh"
 #include "smol_compact.cuh"
 #include "smol_thumb.cuh"
+#include "smol_launch.h"
 
 using namespace smol;
 
@@ -94,7 +95,11 @@ int32_t ensure_basis(int dev) {
   if (g_basis_done[dev]) return SMOL_OK;
   Basis b;
   init_basis(b);
-  SMOL_CUDA(cudaMemcpyToSymbol(c_basis, &b, sizeof(Basis)));
+  SMOL_CUDA(cudaMemcpyToSymbol(c_basis, &b, sizeof(Basis)));     // this unit (thumbnail kernel)
+  SMOL_CUDA(upload_basis_k1(b));
+  SMOL_CUDA(upload_basis_k2(b));
+  SMOL_CUDA(upload_basis_k4(b));
+  SMOL_CUDA(upload_basis_k8(b));
   g_basis_done[dev] = true;
   return SMOL_OK;
 }
@@ -131,6 +136,10 @@ int32_t validate_params(const smol_preproc_params* p) {
     return fail(SMOL_ERR_INVALID, "params.tile_rows=%d", p->tile_rows);
   return SMOL_OK;
 }
+
+// coefficients per block the scale uses (reading R1: the box-averaged basis
+// of the others is exactly zero): 64 / 49 / 25 / 1 at 1, 1/2, 1/4, 1/8
+int used_coefs(int K) { return K == 1 ? 64 : K == 2 ? 49 : K == 4 ? 25 : 1; }
 
 // int16 elements per coefficient block of a layout at scale 1/K (smol_kernels.cuh BlockFmt)
 int block_elems(int K, int layout) {
@@ -249,36 +258,16 @@ int auto_tile_rows(int OH, int n_images, int slots) {
   return ceil_div(OH, best_t);
 }
 
-using KernelFn = void (*)(const KParams);
-
 int Cfg_yp(int nt) { return nt == kThreadsNarrow ? kYPNarrow : nt == kThreadsTiny ? kYPTiny : kYPWide; }
-
-template <int NT> struct Cfg {
-  static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
-};
-
-template <int K, bool PK, int NT>
-KernelFn pick_kernel(bool f16, bool dbg) {
-  constexpr int YP = Cfg<NT>::yp;
-  if (dbg) return f16 ? smol_fused_kernel<K, true, true, PK, NT, YP> : smol_fused_kernel<K, false, true, PK, NT, YP>;
-  return f16 ? smol_fused_kernel<K, true, false, PK, NT, YP> : smol_fused_kernel<K, false, false, PK, NT, YP>;
-}
-
-template <int NT>
-KernelFn select_kernel_nt(int K, bool f16, bool dbg, bool packed) {
-  switch (K) {
-    case 1: return pick_kernel<1, false, NT>(f16, dbg);
-    case 2: return packed ? pick_kernel<2, true, NT>(f16, dbg) : pick_kernel<2, false, NT>(f16, dbg);
-    case 4: return packed ? pick_kernel<4, true, NT>(f16, dbg) : pick_kernel<4, false, NT>(f16, dbg);
-    default: return packed ? pick_kernel<8, true, NT>(f16, dbg) : pick_kernel<8, false, NT>(f16, dbg);
-  }
-}
 
 // scale 1 has no packed variant: the packed layout of scale 1 is DENSE64
 KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt) {
-  return nt == kThreadsNarrow ? select_kernel_nt<kThreadsNarrow>(K, f16, dbg, packed)
-       : nt == kThreadsTiny   ? select_kernel_nt<kThreadsTiny>(K, f16, dbg, packed)
-                              : select_kernel_nt<kThreadsWide>(K, f16, dbg, packed);
+  switch (K) {
+    case 1: return select_fused_k1(f16, dbg, packed, nt);
+    case 2: return select_fused_k2(f16, dbg, packed, nt);
+    case 4: return select_fused_k4(f16, dbg, packed, nt);
+    default: return select_fused_k8(f16, dbg, packed, nt);
+  }
 }
 
 // Largest dynamic smem per CTA that keeps `ctas` CTAs resident per SM:
@@ -386,10 +375,14 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
     out->bx0[c] = L.bx0[c]; out->bx1[c] = L.bx1[c]; out->by0[c] = L.by0[c]; out->by1[c] = L.by1[c];
   }
   out->roi_blocks = tile_roi_blocks(L);
-  // algorithmic coefficient bytes: whole blocks of the layout, except dense-64
-  // at scale 1/8 where only the DC's 32-B sector is needed
+  // algorithmic coefficient bytes: the K_s coefficients the
+  // scale uses per ROI block (reading R1: 64 / 49 / 25 / 1), 2 B each, in any
+  // layout; storage bytes: what the layout holds for those blocks (PACKED
+  // pads to 8 B; dense-64 at scale 1/8 reads only the DC's 32-B sector)
+  out->roi_coef_bytes = out->roi_blocks * 2 * used_coefs(params->scale_denom);
   const int bb = 2 * block_elems(params->scale_denom, params->layout);
-  out->roi_coef_bytes = out->roi_blocks * ((params->scale_denom == 8 && params->layout == SMOL_LAYOUT_DENSE64) ? 32 : bb);
+  out->storage_coef_bytes =
+      out->roi_blocks * ((params->scale_denom == 8 && params->layout == SMOL_LAYOUT_DENSE64) ? 32 : bb);
   return SMOL_OK;
 }
 

@@ -3,8 +3,11 @@
 Images are independent units: the batch is partitioned into contiguous
 ranges, one per rank, balanced by ROI block count (the decode work of an
 image under the plan), and every rank runs the fused kernel on its own range.
-There is no data-path collective; ranks only exchange their device timings
-(max over ranks) through torch.distributed.
+There is no data-path collective and no NCCL communicator: ranks only
+exchange their device timings (max over ranks) through a gloo (host)
+process group.  Shard invariance -- every image's output is bit-identical
+whichever rank (plan, stream) processes it -- is tested on one GPU in
+tests/test_shard_gpu.py.
 """
 from __future__ import annotations
 
@@ -47,13 +50,12 @@ def roi_weights(params, images) -> List[int]:
     return out
 
 
-def max_over_ranks(value: float, device=None) -> float:
-    """Max of a per-rank scalar (e.g. elapsed ms) over the process group."""
+def max_over_ranks(value: float) -> float:
+    """Max of a per-rank scalar (e.g. elapsed ms) over the (gloo) process group."""
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64,
-                     device=device if device is not None else "cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())

@@ -280,6 +280,13 @@ def distinct_images(cfg: Config, mode: str = "natural", quality: Optional[int] =
     nd = min(cfg.n, 64) if n_distinct is None else n_distinct
     ss = np.random.SeedSequence(SEED_BASE + cfg.index + 1000 * seed_offset)
     rngs = [np.random.default_rng(s) for s in ss.spawn(nd)]
+    if nd >= 4 and cfg.width * cfg.height >= 1 << 18:
+        # large frames: one thread per image (each has its own generator, so
+        # the result does not depend on the thread count)
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(min(nd, os.cpu_count() or 1)) as ex:
+            return list(ex.map(lambda r: make_image(r, cfg.width, cfg.height, qt, mode), rngs)), qt
     return [make_image(r, cfg.width, cfg.height, qt, mode) for r in rngs], qt
 
 

@@ -41,9 +41,23 @@ def test_pack_plane_shapes_and_content(k, e):
 
 
 def test_geometry_bytes_per_layout():
-    for k, dense, packed in ((1, 128, 128), (2, 128, 104), (4, 128, 56), (8, 32, 2)):
+    # algorithmic bytes: K_s used coefficients per ROI block,
+    # independent of the layout; storage bytes: what each layout holds
+    for k, ks, dense, packed in ((1, 64, 128, 128), (2, 49, 128, 104), (4, 25, 128, 56), (8, 1, 32, 2)):
         gd = smol.geometry(smol.make_params(scale_denom=k, resize_mode="exact", resize_w=64, resize_h=64), 500, 375)
         gp = smol.geometry(smol.make_params(scale_denom=k, resize_mode="exact", resize_w=64, resize_h=64,
                                             layout="packed"), 500, 375)
-        assert gd["roi_coef_bytes"] == gd["roi_blocks"] * dense
-        assert gp["roi_coef_bytes"] == gp["roi_blocks"] * packed
+        assert gd["roi_coef_bytes"] == gp["roi_coef_bytes"] == gd["roi_blocks"] * 2 * ks
+        assert ks == len(layout.index_set(k))
+        assert gd["storage_coef_bytes"] == gd["roi_blocks"] * dense
+        assert gp["storage_coef_bytes"] == gp["roi_blocks"] * packed
+
+
+def test_survey_8d_bytes_per_image():
+    """packed ROI coefficient bytes per image."""
+    import synth
+    want = {"c2": 344064, "c3a": 271852, "c3b": 138700, "c4": 1366, "c5": 2436000}
+    for name, b in want.items():
+        cfg = synth.CONFIGS[name]
+        g = smol.geometry(smol.params_from_config(cfg, layout="packed"), cfg.width, cfg.height)
+        assert g["roi_coef_bytes"] == b, (name, g["roi_coef_bytes"])

@@ -1,5 +1,7 @@
 """Multi-process (world_size 2, gloo, CPU) coverage of the N > 1 path:
-batch partition across ranks and the max-over-ranks timing reduction."""
+batch partition across ranks, each rank's host-side geometry of its own
+shard (smol_debug_geometry, no GPU), the max-over-ranks timing reduction,
+and bench.py's torchrun launch of the reference arm over gloo."""
 import os
 import socket
 
@@ -53,7 +55,20 @@ def _worker(rank, world, port, q):
         import torch
         t = torch.tensor([len(mine)])
         dist.all_reduce(t)
-        q.put((rank, lo, hi, got, int(t.item())))
+        # per-rank geometry of its own shard of a heterogeneous c2-style
+        # batch, gathered over gloo: every image exactly once, and each
+        # image's ROI block count equals the single-process value
+        import paper_2007_13005_b200 as smol
+        import synth
+        ps = smol.params_from_config(synth.CONFIGS["c2"])
+        sizes = [(500, 375), (375, 500), (640, 480), (97, 61), (1920, 1080), (161, 161)] * 5
+        ims = [type("I", (), {"width": a, "height": b})() for a, b in sizes]
+        wts = shard.roi_weights(ps, ims)
+        a, b = shard.partition(wts, world)[rank]
+        mine_geo = [(i, smol.geometry(ps, *sizes[i])["roi_blocks"]) for i in range(a, b)]
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine_geo)
+        q.put((rank, lo, hi, got, int(t.item()), gathered, wts))
     finally:
         dist.destroy_process_group()
 
@@ -74,3 +89,29 @@ def test_gloo_world2_shards_and_max_time():
     assert res[0][1] == 0 and res[0][2] == res[1][1] and res[1][2] == 64
     assert all(r[3] == 11.0 for r in res)          # max over ranks
     assert all(r[4] == 64 for r in res)            # every image exactly once
+    gathered, wts = res[0][5], res[0][6]
+    flat = [x for part in gathered for x in part]
+    assert [i for i, _ in flat] == list(range(len(wts)))        # disjoint, contiguous, complete
+    assert [b for _, b in flat] == wts                           # per-rank geometry == single process
+    sums = [sum(b for _, b in part) for part in gathered]
+    assert max(sums) <= sum(wts) / 2 + max(wts)                  # ROI-balanced
+
+
+def test_bench_reference_arm_torchrun_gloo(tmp_path):
+    """bench.py --impl reference under torchrun with 2 ranks (gloo, CPU):
+    rank 0 prints one JSON line, rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py"), "--impl", "reference", "--config", "c1", "--gpus", "2",
+           "--steps", "2", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"] == {"workload": d["config"]["workload"]}
