@@ -72,6 +72,8 @@ void init_basis(Basis& b) {
   };
   for (int k = 0; k < 4; ++k)
     for (int y = 0; y < 4; ++y) b.tp[k][y] = make_float2((float)t[2 * k][y], (float)t[2 * k + 1][y]);
+  for (int u = 0; u < 8; ++u)
+    for (int j = 0; j < 2; ++j) b.rp[u][j] = make_float2(basis_t(u, 2 * j), basis_t(u, 2 * j + 1));
   for (int j = 0; j < 2; ++j)
     for (int u = 0; u < 8; ++u) b.a2[j][u] = (float)box(2, u, j);
   for (int u = 0; u < 8; ++u) b.a4[u] = (float)box(4, u, 0);
