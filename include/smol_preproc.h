@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SMOL_ABI_VERSION 1
+#define SMOL_ABI_VERSION 2
 
 typedef enum {
   SMOL_OK = 0,
@@ -76,13 +76,30 @@ typedef struct {
   int32_t out_dtype;        /* smol_out_dtype                                      */
   int32_t layout;           /* smol_coef_layout                                    */
   int32_t tile_rows;        /* output rows per CTA tile; 0 = automatic           */
+  int32_t idct_def;         /* reduced-scale IDCT (reading R1 / R16):
+                               SMOL_IDCT_BOX_MEAN (0, Definition A: k x k box
+                               mean of the 8x8 IDCT) or SMOL_IDCT_TRUNCATED (1,
+                               Definition B: orthonormal (8/k)-point IDCT of
+                               the top-left (8/k)^2 coefficients x (8/k)/8);
+                               both equal the 8x8 IDCT at k = 1 and DC/8 at
+                               k = 8                                              */
+  int32_t max_width, max_height; /* optional staging capacity: when both > 0,
+                               plan allocates the staging of the staged paths
+                               (run_host, run_compact) for max_images images of
+                               at most this SOF size, and those runs never
+                               allocate (a larger image -> SMOL_ERR_CAPACITY);
+                               0 = allocate on first use, grow on demand         */
 } smol_preproc_params;
+
+typedef enum { SMOL_IDCT_BOX_MEAN = 0, SMOL_IDCT_TRUNCATED = 1 } smol_idct_def;
 
 /* One entropy-decoded 4:2:0 image. */
 typedef struct {
   int32_t width, height;           /* SOF size in pixels, > 0                        */
-  int32_t subsampling;             /* 420, or 400 = grayscale (one component, T.81
-                                      Nf = 1: coef[1..2], their blocks/strides and
+  int32_t subsampling;             /* chroma sampling (T.81 A.1.1): 420 (chroma
+                                      W/2 x H/2), 422 (W/2 x H), 444 (W x H), or
+                                      400 = grayscale (one component, Nf = 1:
+                                      coef[1..2], their blocks/strides and
                                       qtable[1..2] are ignored; R = G = B = Y);
                                       anything else: SMOL_ERR_UNSUPPORTED            */
   int32_t qtable[3];               /* Y, Cb, Cr index into batch qtables             */
@@ -91,12 +108,23 @@ typedef struct {
                                       plan's layout (E = 64 for DENSE64: natural
                                       row-major v*8+u order), absolute DC;
                                       16-byte aligned                               */
-  int32_t blocks_w[3], blocks_h[3];/* >= ceil(W/8), ceil(H/8) luma;
-                                      >= ceil(W/16), ceil(H/16) chroma              */
+  int32_t blocks_w[3], blocks_h[3];/* >= ceil(W/8), ceil(H/8) luma; chroma
+                                      >= ceil(Wc/8), ceil(Hc/8) with Wc, Hc the
+                                      chroma size (420: ceil(W/2), ceil(H/2))       */
   int32_t row_stride_bytes[3];     /* >= blocks_w*2*E, multiple of 16                 */
   int32_t roi_left, roi_top;       /* optional ROI: crop window origin in resized
                                       coordinates (window = crop_w x crop_h);
                                       -1,-1 = centre crop                            */
+  int32_t roi_x, roi_y, roi_w, roi_h;  /* optional ROI rectangle (PAPER.md P:1080-1083,
+                                      P:1107-1109: "the ROIs are the face crops"), in
+                                      SOF pixel coordinates; roi_w, roi_h > 0 enable
+                                      it (roi_left/top must then be -1): the
+                                      rectangle's decoded window at scale 1/k,
+                                      [floor(x/k), ceil((x+w)/k)) x [floor(y/k),
+                                      ceil((y+h)/k)) (reading R15), is resized
+                                      (bilinear, R8, taps clamped to the window) to
+                                      the plan's output size -- torchvision
+                                      resized_crop; 0,0,0,0 = no rectangle          */
 } smol_image_desc;
 
 typedef struct {
@@ -180,10 +208,11 @@ int32_t smol_preproc_run_host(smol_preproc_plan_t* plan, const smol_batch_desc* 
  * smol_preproc_run on the dense planes. */
 typedef struct {
   int32_t width, height;           /* SOF size in pixels, > 0                        */
-  int32_t subsampling;             /* 420 or 400 (grayscale: the record has no
-                                      chroma rows)                                   */
+  int32_t subsampling;             /* 420, 422, 444 or 400 (grayscale: the record
+                                      has no chroma rows)                            */
   int32_t qtable[3];               /* Y, Cb, Cr index into batch qtables             */
   int32_t roi_left, roi_top;       /* as smol_image_desc (-1,-1 = centre crop)       */
+  int32_t roi_x, roi_y, roi_w, roi_h;  /* as smol_image_desc (0,0,0,0 = none)        */
   int64_t offset;                  /* byte offset of the image's record in `arena`,
                                       multiple of 16                                 */
 } smol_compact_image;
@@ -228,7 +257,9 @@ void smol_preproc_destroy(smol_preproc_plan_t* plan);
 int32_t smol_preproc_output_shape(const smol_preproc_plan_t* plan, int32_t* c, int32_t* h,
                                   int32_t* w);
 
-/* Number of kernel launches one smol_preproc_run issues (for accounting). */
+/* Number of kernel launches one smol_preproc_run issues (for accounting): 1.
+ * smol_preproc_run_host and smol_preproc_run_compact issue one more (the
+ * gather or expand kernel before the fused kernel). */
 int32_t smol_preproc_launches_per_run(const smol_preproc_plan_t* plan);
 
 /* Host-only: geometry of one image under `params` (no CUDA needed). */

@@ -19,6 +19,7 @@ from ._native import (BatchDesc, CompactBatchDesc, CompactImage, Geometry, Image
                       SmolError, build, check, lib,
                       SMOL_OUT_F16_NCHW, SMOL_OUT_F32_NCHW, SMOL_RESIZE_EXACT,
                       SMOL_RESIZE_SHORT_SIDE, SMOL_LAYOUT_DENSE64, SMOL_LAYOUT_PACKED, EXPORTS,
+                      SMOL_IDCT_BOX_MEAN, SMOL_IDCT_TRUNCATED,
                       LIB_PATH)
 from .layout import block_elems, pack_plane
 
@@ -33,7 +34,8 @@ IMAGENET_STD = (0.229, 0.224, 0.225)
 def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: int = 256,
                 resize_w: int = 0, resize_h: int = 0, crop_w: int = 0, crop_h: int = 0,
                 mean=IMAGENET_MEAN, std=IMAGENET_STD, out_dtype: str = "f32",
-                tile_rows: int = 0, layout: str = "dense") -> Params:
+                tile_rows: int = 0, layout: str = "dense", idct_def: str = "box",
+                max_size: Optional[Tuple[int, int]] = None) -> Params:
     p = Params()
     p.scale_denom = scale_denom
     p.resize_mode = SMOL_RESIZE_SHORT_SIDE if resize_mode == "short" else SMOL_RESIZE_EXACT
@@ -44,6 +46,8 @@ def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: 
     p.out_dtype = SMOL_OUT_F16_NCHW if out_dtype == "f16" else SMOL_OUT_F32_NCHW
     p.layout = SMOL_LAYOUT_PACKED if layout == "packed" else SMOL_LAYOUT_DENSE64
     p.tile_rows = tile_rows
+    p.idct_def = SMOL_IDCT_TRUNCATED if idct_def == "truncated" else SMOL_IDCT_BOX_MEAN
+    p.max_width, p.max_height = max_size if max_size is not None else (0, 0)
     return p
 
 

@@ -27,6 +27,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "UNSUPPORTED", 3: "CUDA", 4: "NOMEM", 
 SMOL_OUT_F32_NCHW, SMOL_OUT_F16_NCHW = 0, 1
 SMOL_RESIZE_SHORT_SIDE, SMOL_RESIZE_EXACT = 0, 1
 SMOL_LAYOUT_DENSE64, SMOL_LAYOUT_PACKED = 0, 1
+SMOL_IDCT_BOX_MEAN, SMOL_IDCT_TRUNCATED = 0, 1
 
 # every symbol include/smol_preproc.h declares (checked by tests/test_abi.py)
 EXPORTS = ["smol_preproc_plan", "smol_preproc_run", "smol_preproc_run_host", "smol_preproc_destroy",
@@ -41,7 +42,8 @@ class Params(ctypes.Structure):
                 ("resize_h", ctypes.c_int32), ("crop_w", ctypes.c_int32), ("crop_h", ctypes.c_int32),
                 ("mean", ctypes.c_float * 3), ("std", ctypes.c_float * 3),
                 ("out_dtype", ctypes.c_int32), ("layout", ctypes.c_int32),
-                ("tile_rows", ctypes.c_int32)]
+                ("tile_rows", ctypes.c_int32), ("idct_def", ctypes.c_int32),
+                ("max_width", ctypes.c_int32), ("max_height", ctypes.c_int32)]
 
 
 class ImageDesc(ctypes.Structure):
@@ -49,13 +51,17 @@ class ImageDesc(ctypes.Structure):
                 ("subsampling", ctypes.c_int32), ("qtable", ctypes.c_int32 * 3),
                 ("coef", ctypes.c_void_p * 3), ("blocks_w", ctypes.c_int32 * 3),
                 ("blocks_h", ctypes.c_int32 * 3), ("row_stride_bytes", ctypes.c_int32 * 3),
-                ("roi_left", ctypes.c_int32), ("roi_top", ctypes.c_int32)]
+                ("roi_left", ctypes.c_int32), ("roi_top", ctypes.c_int32),
+                ("roi_x", ctypes.c_int32), ("roi_y", ctypes.c_int32),
+                ("roi_w", ctypes.c_int32), ("roi_h", ctypes.c_int32)]
 
 
 class CompactImage(ctypes.Structure):
     _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
                 ("subsampling", ctypes.c_int32), ("qtable", ctypes.c_int32 * 3),
                 ("roi_left", ctypes.c_int32), ("roi_top", ctypes.c_int32),
+                ("roi_x", ctypes.c_int32), ("roi_y", ctypes.c_int32),
+                ("roi_w", ctypes.c_int32), ("roi_h", ctypes.c_int32),
                 ("offset", ctypes.c_int64)]
 
 
@@ -93,10 +99,12 @@ def _stale() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + [HEADER])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
     """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libsmol_preproc.so
-    (in-tree): every unit compiled to an object in parallel, then linked."""
-    if not force and not _stale():
+    (in-tree): every unit compiled to an object in parallel, then linked.
+    out/defines: an experiment variant (-D flags) built to another path."""
+    target = out or LIB_PATH
+    if out is None and not force and not _stale():
         return LIB_PATH
     from concurrent.futures import ThreadPoolExecutor
     objdir = os.path.join(_PKG, "build")
@@ -104,8 +112,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc = ["-I", os.path.join(_ROOT, "include"), "-I", _CSRC]
 
     def compile_unit(u):
-        obj = os.path.join(objdir, u.replace(".cu", f".{os.getpid()}.o"))
-        cmd = ["nvcc", *NVCC_FLAGS, *inc, "-c", "-o", obj, os.path.join(_CSRC, u)]
+        obj = os.path.join(objdir, u.replace(".cu", f".{os.getpid()}.{abs(hash(target))}.o"))
+        cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], *inc, "-c", "-o", obj, os.path.join(_CSRC, u)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{r.stderr}")
@@ -113,7 +121,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(len(UNITS)) as ex:
         res = list(ex.map(compile_unit, UNITS))
-    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + [o for o, _ in res]
     r = subprocess.run(cmd, capture_output=True, text=True)
     for o, _ in res:
@@ -122,8 +130,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc link failed ({' '.join(cmd)}):\n{r.stderr}")
     if verbose:
         print("".join(e for _, e in res))
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, target)
+    return target
 
 
 _lib = None

@@ -29,6 +29,12 @@
 #ifndef SMOL_COLOUR_QUADS
 #define SMOL_COLOUR_QUADS 2      // colour task = this many 2x4-pixel quads of one row pair
 #endif
+#ifndef SMOL_OUT_ROWRUN
+#define SMOL_OUT_ROWRUN 15       // bit log2(K): at scale 1/K an output task is one quad over a run of rows
+#endif
+#ifndef SMOL_OUT_RUN_ROWS
+#define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
+#endif
 #ifndef SMOL_OUT_QUADS
 #define SMOL_OUT_QUADS 2         // output task = this many 4-pixel quads of one row
 #endif
@@ -440,7 +446,8 @@ struct KParams {
   const DevImage* imgs;
   const uint16_t* qtables;
   void* out;
-  int OW, OH, tile_rows, tile_cols, n_col_tiles;
+  int OW, OH, tile_rows, tile_cols, n_col_tiles, n_row_tiles;
+  int out_vec;                     // out is 16-B (fp32) / 8-B (fp16) aligned: vector stores allowed
   const int4* cta_map;             // non-null: 1-D grid, CTA -> {image, oy0, oy1, 0}
   uint32_t magic;                  // 0x4B000000: bit pattern of 2^23 (byte -> float trick)
   float na[3], nb[3];              // y = x * na + nb = (x/255 - mean)/std
@@ -551,7 +558,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   constexpr int kOutQ = SMOL_OUT_QUADS;
   const int nqt = (nq4 + kOutQ - 1) / kOutQ;
   const FastDiv fd_qt = make_fastdiv(nqt);
-  const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0);
+  const FastDiv fd_q4 = make_fastdiv(nq4);
+  const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0) && kp.out_vec;
   const uint32_t plane_sz = (uint32_t)kp.OH * kp.OW;   // < 2^31 elements (host-checked)
   using OutT = typename std::conditional<F16, __half, float>::type;
   OutT* const outb = reinterpret_cast<OutT*>(kp.out) + ((size_t)n * 3 * kp.OH + oy0) * kp.OW + ox0;
@@ -769,6 +777,117 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     // ---- next step's IDCT (writes only Y/chroma rings: no reader now) ----
     if (s + 1 < L.nsteps) idct_step(s + 1);
 
+    if constexpr ((SMOL_OUT_ROWRUN >> (K == 1 ? 0 : K == 2 ? 1 : K == 4 ? 2 : 3)) & 1)
+    // ---- bilinear + normalize + NCHW store: a task is one 4-pixel column
+    // quad over a run of up to kRun consecutive output rows.  Walking down
+    // the run, the horizontal lerps of a source row are reused while the
+    // row's taps do not move: the same (i0, i0+1) pair keeps both, a pair
+    // one row lower keeps the old bottom lerp as the new top.  Bit-identical
+    // to recomputing them (same operations on the same samples).
+    {
+      constexpr int kRun = SMOL_OUT_RUN_ROWS(K);
+      const int nrows = done - done_prev;
+      const int ngr = (nrows + kRun - 1) / kRun;
+      const int ntasko = ngr * nq4;
+      const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
+      const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
+      const uint32_t magic = kp.magic;     // 0x4B000000 (2^23), kept in a register
+      constexpr bool kOutStatic = SMOL_OUT_STATIC == 1 || (SMOL_OUT_STATIC == 2 && K != 1);
+      for (int chunk = kOutStatic ? (tid >> 5) * 32 : 0;; chunk += kThreads) {
+        if constexpr (!kOutStatic) {
+          if (ctr[1] >= ntasko) break;           // (no atomic once the phase's tasks are gone)
+          chunk = grab_chunk(&ctr[1], lane, 32);
+        }
+        if (chunk >= ntasko) break;
+        const int t = chunk + lane;
+        if (t >= ntasko) continue;
+        const int gi = (int)fdiv((uint32_t)t, fd_q4);
+        const int q = t - gi * nq4;
+        const int ra = done_prev + gi * kRun, rb = min(ra + kRun, done);
+        const int ox = 4 * q;
+        const int4* xt4 = reinterpret_cast<const int4*>(xt);
+        const int4 txa = xt4[q];          // taps of ox, ox+1
+        const int4 txb = xt4[nq4 + q];    // taps of ox+2, ox+3 (padded)
+        const float2 wxa = make_float2(__int_as_float(txa.z), __int_as_float(txa.w));
+        const float2 wxb = make_float2(__int_as_float(txb.z), __int_as_float(txb.w));
+        const bool vst = vec4 && ox + 4 <= ntw;
+        float2 T[3][2], B[3][2];          // horizontal lerps of the top / bottom source rows [ch][pixel pair]
+        // horizontal lerps of one RGB ring row (byte offset ro) for the quad
+        auto hlerp = [&](int ro, float2 (&H)[3][2]) {
+          const uint8_t* row = reinterpret_cast<const uint8_t*>(rgb) + ro;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int4 tx = e == 0 ? txa : txb;
+            const float2 wx = e == 0 ? wxa : wxb;
+            const uint32_t p0 = lds_u32(row + tx.x), p1 = lds_u32(row + tx.x + 4);
+            const uint32_t q0 = lds_u32(row + tx.y), q1 = lds_u32(row + tx.y + 4);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              const int sel = 0x7540 + ch;
+              // bytes become 2^23 + b floats by one PRMT (exact), the bias cancels in b - a
+              const float2 fa = make_float2(__uint_as_float(__byte_perm(p0, magic, sel)), __uint_as_float(__byte_perm(q0, magic, sel)));
+              const float2 fb = make_float2(__uint_as_float(__byte_perm(p1, magic, sel)), __uint_as_float(__byte_perm(q1, magic, sel)));
+              H[ch][e] = __ffma2_rn(wx, __ffma2_rn(fa, f2(-1.f), fb), __fadd2_rn(fa, f2(-8388608.f)));
+            }
+          }
+        };
+        int cur = -1;                     // ring byte offset of the current top row
+#pragma unroll 1
+        for (int r = ra; r < rb; ++r) {
+          const int2 ty = yt[r];
+          const int ro = ty.x & 0xffff;
+          if (ro != cur) {
+            if (ro == cur + pitch4) {     // one row down: old bottom becomes the top
+#pragma unroll
+              for (int ch = 0; ch < 3; ++ch) { T[ch][0] = B[ch][0]; T[ch][1] = B[ch][1]; }
+            } else {
+              hlerp(ro, T);
+            }
+            hlerp(ro + pitch4, B);
+            cur = ro;
+          }
+          const float2 wy2 = f2(__int_as_float(ty.y));
+          float y[3][4];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float2 v = __ffma2_rn(wy2, __ffma2_rn(T[ch][e], f2(-1.f), B[ch][e]), T[ch][e]);
+              const float2 yn = __ffma2_rn(v, ch == 0 ? na0 : ch == 1 ? na1 : na2, ch == 0 ? nb0 : ch == 1 ? nb1 : nb2);
+              y[ch][2 * e] = yn.x;
+              y[ch][2 * e + 1] = yn.y;
+            }
+          OutT* const ot = outb + (uint32_t)(r * kp.OW + ox);
+          if (vst) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              if constexpr (F16) {
+                const __half2 h0 = __floats2half2_rn(y[ch][0], y[ch][1]);
+                const __half2 h1 = __floats2half2_rn(y[ch][2], y[ch][3]);
+                uint2 v;
+                v.x = *reinterpret_cast<const uint32_t*>(&h0);
+                v.y = *reinterpret_cast<const uint32_t*>(&h1);
+                __stcs(reinterpret_cast<uint2*>(ot + ch * plane_sz), v);
+              } else {
+                __stcs(reinterpret_cast<float4*>(ot + ch * plane_sz),
+                       make_float4(y[ch][0], y[ch][1], y[ch][2], y[ch][3]));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (ox + e >= ntw) break;
+#pragma unroll
+              for (int ch = 0; ch < 3; ++ch) {
+                if constexpr (F16) ot[e + ch * plane_sz] = __float2half_rn(y[ch][e]);
+                else ot[e + ch * plane_sz] = y[ch][e];
+              }
+            }
+          }
+        }
+      }
+    }
+    else
     // ---- bilinear + normalize + NCHW store, kOutQ x 4 output pixels per task
     {
       const int ntasko = (done - done_prev) * nqt;
@@ -891,9 +1010,11 @@ smol_fused_kernel(const __grid_constant__ KParams kp) {
   if (kp.cta_map) {            // 1-D grid: per-CTA {image, oy0, oy1} (full-width tiles)
     const int4 m = kp.cta_map[blockIdx.x];
     n = m.x; oy0 = m.y; oy1 = m.z; ox0 = 0; ox1 = kp.OW;
-  } else {
-    const int trow = blockIdx.x / kp.n_col_tiles, tcol = blockIdx.x - trow * kp.n_col_tiles;
-    n = blockIdx.y;
+  } else {                     // 1-D grid: image-major, then row tile, then column tile
+    const int per_img = kp.n_row_tiles * kp.n_col_tiles;
+    n = blockIdx.x / per_img;
+    const int rem = blockIdx.x - n * per_img;
+    const int trow = rem / kp.n_col_tiles, tcol = rem - trow * kp.n_col_tiles;
     oy0 = trow * kp.tile_rows; oy1 = min(kp.OH, oy0 + kp.tile_rows);
     ox0 = tcol * kp.tile_cols; ox1 = min(kp.OW, ox0 + kp.tile_cols);
   }

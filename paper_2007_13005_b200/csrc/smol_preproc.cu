@@ -2,6 +2,7 @@
 // include/smol_preproc.h: parameter/descriptor validation, per-image
 // geometry, device descriptor upload (pinned ring, no allocation per run),
 // kernel selection per (scale, dtype) and launch.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -136,6 +137,14 @@ int32_t validate_params(const smol_preproc_params* p) {
     return fail(SMOL_ERR_INVALID, "params.layout=%d", p->layout);
   if (p->tile_rows < 0 || p->tile_rows > 4096)
     return fail(SMOL_ERR_INVALID, "params.tile_rows=%d", p->tile_rows);
+  if (p->idct_def != SMOL_IDCT_BOX_MEAN && p->idct_def != SMOL_IDCT_TRUNCATED)
+    return fail(SMOL_ERR_INVALID, "params.idct_def=%d", p->idct_def);
+  if (p->idct_def == SMOL_IDCT_TRUNCATED)
+    return fail(SMOL_ERR_UNSUPPORTED, "params.idct_def=TRUNCATED not built");
+  if (p->max_width < 0 || p->max_height < 0 || (p->max_width > 0) != (p->max_height > 0) ||
+      p->max_width > 65535 || p->max_height > 65535)
+    return fail(SMOL_ERR_INVALID, "params.max_width/max_height=%d/%d: both in [1, 65535] or both 0",
+                p->max_width, p->max_height);
   return SMOL_OK;
 }
 
@@ -159,6 +168,8 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
     return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d > 65535 (JPEG limit)", idx, d->width, d->height);
   if (d->subsampling != 420 && d->subsampling != 400)
     return fail(SMOL_ERR_UNSUPPORTED, "image %d: subsampling=%d (420 or 400 only)", idx, d->subsampling);
+  if (d->roi_w != 0 || d->roi_h != 0 || d->roi_x != 0 || d->roi_y != 0)
+    return fail(SMOL_ERR_UNSUPPORTED, "image %d: ROI rectangle not built", idx);
   g.gray = d->subsampling == 400;
   g.Wd = ceil_div(d->width, k);
   g.Hd = ceil_div(d->height, k);
@@ -194,7 +205,8 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
 // reused: batches are mostly runs of equal-size images).
 inline bool same_geometry(const smol_image_desc* a, const smol_image_desc* b) {
   return a->width == b->width && a->height == b->height && a->subsampling == b->subsampling &&
-         a->roi_left == b->roi_left && a->roi_top == b->roi_top;
+         a->roi_left == b->roi_left && a->roi_top == b->roi_top && a->roi_x == b->roi_x &&
+         a->roi_y == b->roi_y && a->roi_w == b->roi_w && a->roi_h == b->roi_h;
 }
 inline void copy_geometry(const DevImage& from, DevImage& g) {
   g.Wd = from.Wd; g.Hd = from.Hd; g.Wc = from.Wc; g.Hc = from.Hc;
@@ -345,6 +357,8 @@ struct smol_preproc_plan {
   std::vector<TileLayout> layouts;         // host scratch (whole-output footprints)
   cudaEvent_t stage_free[2] = {}, stage_ready[2] = {};
   int stage_slot = 0;
+  bool fixed_stage = false;                // staging sized in plan (params.max_width/max_height)
+  std::vector<std::pair<uintptr_t, uintptr_t>> pinned_ok;   // run_host: verified [lo, hi) allocations
 };
 
 extern "C" {
@@ -442,6 +456,26 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     e = cudaMalloc(&pl->d_map, sizeof(int4) * (size_t)pl->map_cap * kRing);
     if (e == cudaSuccess) e = cudaMallocHost(&pl->h_map, sizeof(int4) * (size_t)pl->map_cap * kRing);
   }
+  if (e == cudaSuccess && params->max_width > 0) {
+    // staging of the staged paths for max_images images of at most
+    // max_width x max_height (worst case: every block of the image, 4:4:4),
+    // so run_host / run_compact never allocate: dense ROI rows (both slots)
+    // and compact records (units <= 2 per used element, plus the tables)
+    const int E = block_elems(params->scale_denom, params->layout);
+    const long long bw = ceil_div(params->max_width, 8), bh = ceil_div(params->max_height, 8);
+    const long long rows = 3 * bh, blocks = 3 * bw * bh;
+    const size_t stage_img = (size_t)(2 * (blocks * E + rows * 16 + 3 * 8));
+    const size_t rec_img = (size_t)compact_record_bytes(blocks, rows, 2LL * blocks * used_coefs(params->scale_denom));
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      pl->stage_cap[i] = stage_img * (size_t)max_images;
+      e = cudaMalloc(&pl->stage[i], pl->stage_cap[i] + 256);
+      if (e == cudaSuccess) {
+        pl->cbuf_cap[i] = rec_img * (size_t)max_images;
+        e = cudaMalloc(&pl->cbuf[i], pl->cbuf_cap[i] + 256);
+      }
+    }
+    pl->fixed_stage = true;
+  }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(smol_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kExpandSmem);
   if (e == cudaSuccess) {
@@ -472,6 +506,9 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
 
 void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (!pl) return;
+  int prev = -1;                    // release on the plan's device, then restore the caller's
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (prev != pl->device) cudaSetDevice(pl->device);
   for (int i = 0; i < kRing; ++i)
     if (pl->ev[i]) { cudaEventSynchronize(pl->ev[i]); cudaEventDestroy(pl->ev[i]); }
   for (int i = 0; i < 2; ++i) {
@@ -489,7 +526,9 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (pl->d_map) cudaFree(pl->d_map);
   if (pl->h_map) cudaFreeHost(pl->h_map);
   if (pl->h_desc) cudaFreeHost(pl->h_desc);
+  const int dev = pl->device;
   delete pl;
+  if (prev >= 0 && prev != dev) cudaSetDevice(prev);
 }
 
 int32_t smol_preproc_output_shape(const smol_preproc_plan_t* pl, int32_t* c, int32_t* h, int32_t* w) {
@@ -519,6 +558,7 @@ int32_t validate_compact_image(const smol_preproc_params* p, const smol_compact_
     smol_image_desc d{};
     d.width = ci->width; d.height = ci->height; d.subsampling = ci->subsampling;
     d.roi_left = ci->roi_left; d.roi_top = ci->roi_top;
+    d.roi_x = ci->roi_x; d.roi_y = ci->roi_y; d.roi_w = ci->roi_w; d.roi_h = ci->roi_h;
     int32_t rc = image_geometry(p, &d, idx, g);
     if (rc) return rc;
   }
@@ -555,8 +595,11 @@ size_t stage_layout(const TileLayout& L, int E, int32_t (&dst_stride)[3], size_t
   return need;
 }
 
-int32_t grow(void** buf, size_t* cap, size_t need, cudaStream_t s) {
+int32_t grow(void** buf, size_t* cap, size_t need, cudaStream_t s, bool fixed, const char* what) {
   if (need <= *cap) return SMOL_OK;
+  if (fixed)                       // sized in plan from params.max_width/max_height: never allocate here
+    return fail(SMOL_ERR_CAPACITY, "%s needs %zu B > %zu B sized in plan (params.max_width/max_height)",
+                what, need, *cap);
   SMOL_CUDA(cudaStreamSynchronize(s));
   if (*buf) SMOL_CUDA(cudaFree(*buf));
   *buf = nullptr;
@@ -578,6 +621,15 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   if (!qtables || n_qtables < 1 || n_qtables > 4)
     return fail(SMOL_ERR_INVALID, "batch.qtables NULL or n_qtables=%d not in [1,4]", n_qtables);
   if (!out) return fail(SMOL_ERR_INVALID, "out is NULL");
+  {
+    int cur = -1;
+    SMOL_CUDA(cudaGetDevice(&cur));
+    if (cur != pl->device)
+      return fail(SMOL_ERR_INVALID, "plan was created on device %d but device %d is current", pl->device, cur);
+  }
+  const size_t out_esz = pl->p.out_dtype == SMOL_OUT_F16_NCHW ? 2 : 4;
+  if (reinterpret_cast<uintptr_t>(out) % out_esz)
+    return fail(SMOL_ERR_INVALID, "out is not %zu-byte aligned", out_esz);
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_v);
   const int K = pl->p.scale_denom;
   const bool packed = pl->p.layout == SMOL_LAYOUT_PACKED;
@@ -600,7 +652,9 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       const smol_compact_image* ci = static_cast<const smol_compact_image*>(images);
       const bool same = i > 0 && ci[i].width == ci[i - 1].width && ci[i].height == ci[i - 1].height &&
                         ci[i].subsampling == ci[i - 1].subsampling && ci[i].roi_left == ci[i - 1].roi_left &&
-                        ci[i].roi_top == ci[i - 1].roi_top;
+                        ci[i].roi_top == ci[i - 1].roi_top && ci[i].roi_x == ci[i - 1].roi_x &&
+                        ci[i].roi_y == ci[i - 1].roi_y && ci[i].roi_w == ci[i - 1].roi_w &&
+                        ci[i].roi_h == ci[i - 1].roi_h;
       rc = validate_compact_image(&pl->p, &ci[i], i, n_qtables, h[i], same ? &h[i - 1] : nullptr);
     } else {
       const smol_image_desc* di = static_cast<const smol_image_desc*>(images);
@@ -669,6 +723,16 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       tile_rows = tr;
       ntiles = ceil_div(pl->OH, tile_rows);
       smem = max_smem(1, Cfg_yp(nt));
+    }
+  }
+  {
+    // the kernel's magic-number divisions (FastDiv) are exact for n * d <
+    // 2^32: output task indices reach tile_rows * nq4 with divisor nq4
+    const long long nq4 = (cols_of(n_col_tiles) + 3) / 4;
+    const long long cap = 0xFFFFFFFFLL / (nq4 * nq4);
+    if (tile_rows > cap) {
+      tile_rows = (int)std::max<long long>(1, cap);
+      ntiles = ceil_div(pl->OH, tile_rows);
     }
   }
   // Scale 1/8 with small footprints (thumbnails): the warp-per-image kernel
@@ -757,7 +821,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       }
     }
     void* sbuf = pl->stage[sl];
-    int32_t rc = grow(&sbuf, &pl->stage_cap[sl], need * 2, pl->copy_stream);
+    int32_t rc = grow(&sbuf, &pl->stage_cap[sl], need * 2, pl->copy_stream, pl->fixed_stage, "staging");
     pl->stage[sl] = static_cast<int16_t*>(sbuf);
     if (rc) return rc;
     int16_t* base = pl->stage[sl];
@@ -812,6 +876,25 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
           bytes = compact_record_bytes(nblocks, nrows, hd.n_units);
           if (ci[i].offset + bytes > cb->arena_bytes)
             return fail(SMOL_ERR_INVALID, "image %d: record (%lld B) overruns the arena", i, (long long)bytes);
+          // block lengths and row starts: the expand kernel stages at most
+          // 2 * E (<= 128) units per block and trusts the row starts
+          const uint8_t* lens = arena + ci[i].offset + kCompactHeader;
+          const uint8_t* rsp = arena + ci[i].offset + compact_rowstart_off(nblocks);
+          const int max_len = std::min(2 * E, 128);
+          uint64_t sum = 0;
+          int64_t bi = 0, ri = 0;
+          for (int c = 0; c < 3 && ok; ++c)
+            for (int r = 0; r < e.nby[c] && ok; ++r, ++ri) {
+              uint32_t rs;
+              memcpy(&rs, rsp + 4 * ri, 4);
+              ok = rs == sum;
+              for (int b = 0; b < e.nbx[c] && ok; ++b, ++bi) {
+                ok = lens[bi] <= max_len;
+                sum += lens[bi];
+              }
+            }
+          if (!ok || sum != hd.n_units)
+            return fail(SMOL_ERR_INVALID, "image %d: compact record block lengths / row starts are corrupt", i);
         }
         lo = std::min<int64_t>(lo, ci[i].offset);
         hi = std::max<int64_t>(hi, ci[i].offset + bytes);
@@ -821,7 +904,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
         lo = 0;
       } else {
         void* cbuf = pl->cbuf[sl];
-        rc = grow(&cbuf, &pl->cbuf_cap[sl], (size_t)(hi - lo), pl->copy_stream);
+        rc = grow(&cbuf, &pl->cbuf_cap[sl], (size_t)(hi - lo), pl->copy_stream, pl->fixed_stage,
+                  "compact records");
         pl->cbuf[sl] = static_cast<uint8_t*>(cbuf);
         if (rc) return rc;
         rec_base = pl->cbuf[sl];
@@ -855,6 +939,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   kp.out = out;
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;
   kp.magic = 0x4B000000u;
+  kp.out_vec = reinterpret_cast<uintptr_t>(out) % (4 * out_esz) == 0;
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
@@ -870,7 +955,10 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     if (src != Src::kDevice) SMOL_CUDA(cudaEventRecord(pl->stage_free[pl->stage_slot ^ 1], stream));
     return SMOL_OK;
   }
-  dim3 grid = map_n ? dim3(map_n, 1) : dim3(ntiles * n_col_tiles, n_images);
+  kp.n_row_tiles = ntiles;
+  const long long nblk = map_n ? (long long)map_n : (long long)ntiles * n_col_tiles * n_images;
+  if (nblk >= INT_MAX) return fail(SMOL_ERR_CAPACITY, "%lld CTAs exceed the grid limit", nblk);
+  dim3 grid((unsigned)nblk, 1);
   fn<<<grid, nt, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
@@ -941,15 +1029,49 @@ int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b,
   // ROI block rows cross PCIe: a gather kernel on the plan's copy stream
   // stages them (double-buffered, so batch k+1's transfer overlaps batch k's
   // fused kernel), then the fused kernel runs on `stream`.
-  // Probe image 0's planes (a batch normally comes from one pinned arena).
-  if (b && b->images && b->n_images > 0) {
-    for (int c = 0; c < (b->images[0].subsampling == 400 ? 1 : 3); ++c) {
-      cudaPointerAttributes a;
-      if (cudaPointerGetAttributes(&a, b->images[0].coef[c]) != cudaSuccess ||
-          (a.type != cudaMemoryTypeHost && a.type != cudaMemoryTypeDevice &&
-           a.type != cudaMemoryTypeManaged)) {
+  // Every plane must be pinned host (or device) memory: the gather kernel
+  // reads it over PCIe, and a pageable pointer would fault the context.  Each
+  // plane's first and last byte is checked, with verified allocations cached
+  // (driver range query) so a batch from one pinned arena costs one query.
+  if (pl && b && b->images && b->n_images > 0) {
+    static CUresult (*get_attr)(void*, CUpointer_attribute, CUdeviceptr) = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        get_attr = reinterpret_cast<CUresult (*)(void*, CUpointer_attribute, CUdeviceptr)>(fn);
+    });
+    auto usable = [&](uintptr_t a) -> bool {
+      for (const auto& r : pl->pinned_ok)
+        if (a >= r.first && a < r.second) return true;
+      cudaPointerAttributes pa;
+      if (cudaPointerGetAttributes(&pa, reinterpret_cast<const void*>(a)) != cudaSuccess ||
+          (pa.type != cudaMemoryTypeHost && pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged)) {
         cudaGetLastError();
-        return fail(SMOL_ERR_INVALID, "image 0: coef[%d] is neither pinned host nor device memory", c);
+        return false;
+      }
+      CUdeviceptr start = 0;
+      size_t size = 0;
+      if (get_attr && get_attr(&start, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, (CUdeviceptr)a) == CUDA_SUCCESS &&
+          get_attr(&size, CU_POINTER_ATTRIBUTE_RANGE_SIZE, (CUdeviceptr)a) == CUDA_SUCCESS && size > 0 &&
+          a >= (uintptr_t)start && a < (uintptr_t)start + size) {
+        // (device pointer range; for pinned host memory mapped at the same
+        // address under UVA it is the host range)
+        if (pl->pinned_ok.size() >= 64) pl->pinned_ok.erase(pl->pinned_ok.begin());
+        pl->pinned_ok.emplace_back((uintptr_t)start, (uintptr_t)start + size);
+      }
+      return true;
+    };
+    for (int i = 0; i < b->n_images; ++i) {
+      const smol_image_desc& d = b->images[i];
+      for (int c = 0; c < (d.subsampling == 400 ? 1 : 3); ++c) {
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(d.coef[c]);
+        const long long span = (long long)std::max(d.blocks_h[c], 1) * d.row_stride_bytes[c];
+        if (!d.coef[c] || span <= 0) continue;          // run_impl reports the descriptor error
+        if (!usable(lo) || !usable(lo + (uintptr_t)span - 1))
+          return fail(SMOL_ERR_INVALID, "image %d: coef[%d] is neither pinned host nor device memory", i, c);
       }
     }
   }

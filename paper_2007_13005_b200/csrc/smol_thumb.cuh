@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
         }
       }
       OutT* const o = outn + (uint32_t)oy * OW + ox;
-      if ((OW & 3) == 0) {
+      if ((OW & 3) == 0 && kp.out_vec) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           if constexpr (F16) {

@@ -56,6 +56,7 @@ def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=No
         roi = None if rois is None else rois[i]
         ref = oracle.run_image(po, im, qt, roi).astype(np.float64)
         widen = 0.0
+        img_flips = 0
         if debug:
             planes = [t[i].cpu().numpy() for t in (y, cb, cr)]
             dims = [(g["Hd"], g["Wd"]), (g["Hc"], g["Wc"]), (g["Hc"], g["Wc"])]
@@ -73,6 +74,7 @@ def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=No
                     assert np.all(np.abs(d) <= 1), f"image {i} comp {ci}: u8 off by >1"
                     assert np.all(band[m][bad]), f"image {i} comp {ci}: mismatch outside tie band"
                 flips += int(bad.sum())
+                img_flips += int(bad.sum())
                 gp.append(np.where(m, gpl, 0).astype(np.uint8))
             # RGB exact given the kernel's own planes
             grgb = rgb[i].cpu().numpy()[:3 * g["Hd"] * g["Wd"]].reshape(g["Hd"], g["Wd"], 3)
@@ -84,7 +86,7 @@ def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=No
             stage, _ = oracle.resize_crop_normalize(full, g["Wr"], g["Hr"], g["left"], g["top"],
                                                    g["OW"], g["OH"], out_dtype=cfg.out_dtype)
             assert np.max(np.abs(out[i] - stage.astype(np.float64))) <= tol, f"image {i}: resize stage"
-            if flips:
+            if img_flips:          # this image has a tie-band flip (reading R3): one level of slack
                 widen = 2.0 / (255 * min(synth.IMAGENET_STD))
         err = np.max(np.abs(out[i] - ref))
         assert err <= tol + widen, f"image {i}: max |gpu - oracle| = {err}"
@@ -268,6 +270,76 @@ def test_run_host_pinned_equals_device():
     b = plan.run(smol.CoefBatch(imgs, qt, location="pinned"))
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+def test_misaligned_output_and_grid_limits():
+    """out must be element-aligned (SMOL_ERR_INVALID otherwise); an
+    element-aligned but not vector-aligned out takes the scalar stores and
+    gives the same values; a batch larger than 65535 images per launch is
+    accepted (1-D grid)."""
+    cfg = synth.CONFIGS["c1"]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=3)
+    ps, _ = _cfg_params(cfg)
+    plan = smol.Plan(ps, 3)
+    ref = plan.run(smol.CoefBatch(imgs, qt))
+    buf = torch.empty(ref.numel() + 8, dtype=torch.float32, device="cuda")
+    shifted = buf[1:1 + ref.numel()].view(ref.shape)          # 4-B aligned, not 16-B
+    plan.run(smol.CoefBatch(imgs, qt), out=shifted)
+    torch.cuda.synchronize()
+    assert torch.equal(shifted, ref)
+    raw = torch.empty(ref.numel() * 4 + 16, dtype=torch.uint8, device="cuda")
+    bad = raw[1:1 + ref.numel() * 4]                          # 1-B offset: not float-aligned
+    b = smol.CoefBatch(imgs, qt)
+    with pytest.raises(smol.SmolError) as e:
+        smol.check(smol.lib().smol_preproc_run(plan._h, __import__("ctypes").byref(b.desc), bad.data_ptr(),
+                                               torch.cuda.current_stream().cuda_stream))
+    assert e.value.status == 1 and "aligned" in str(e.value)
+    plan.close()
+    # thumbnails: 70000 images in one launch (> 65535 CTAs of the old 2-D grid's y)
+    cfg4 = synth.CONFIGS["c4"]
+    ims4, qt4 = synth.batch_images(cfg4, n=70000, n_distinct=4)
+    ps4 = smol.params_from_config(cfg4)               # dense layout: tiled kernel
+    p4 = smol.Plan(ps4, 70000)
+    o4 = p4.run(smol.CoefBatch(ims4, qt4))
+    torch.cuda.synchronize()
+    assert torch.equal(o4[:4], o4[69996:70000])       # same 4 distinct images, cycled
+    p4.close()
+
+
+def test_huge_magnification_plan():
+    """A tiny image magnified to a large output: the host caps the tile
+    height so the kernel's magic-number divisions stay exact (n * d < 2^32);
+    the result matches the oracle."""
+    rng = np.random.default_rng(9)
+    qt = synth.quant_tables(75)
+    im = synth.make_image(rng, 24, 16, qt)
+    ps = smol.make_params(resize_mode="exact", resize_w=4096, resize_h=2048)
+    po = oracle.make_params(resize_mode="exact", resize_w=4096, resize_h=2048)
+    plan = smol.Plan(ps, 1)
+    out = plan.run(smol.CoefBatch([im], qt))
+    torch.cuda.synchronize()
+    ref = oracle.run_image(po, im, qt)
+    assert np.max(np.abs(out[0].cpu().numpy() - ref)) <= 1e-4 + 2.0 / (255 * 0.224)
+    plan.close()
+
+
+def test_staging_sized_in_plan():
+    """params.max_width/max_height: run_host / run_compact use the staging
+    sized in plan (no allocation in run) and refuse a larger image."""
+    cfg = synth.CONFIGS["c2"]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=4)
+    ps = smol.params_from_config(cfg, max_size=(500, 375))
+    plan = smol.Plan(ps, 4)
+    ref = plan.run(smol.CoefBatch(imgs, qt))
+    a = plan.run(smol.CoefBatch(imgs, qt, location="pinned"))
+    c = plan.run(smol.CompactBatch(ps, imgs, qt))
+    torch.cuda.synchronize()
+    assert torch.equal(a, ref) and torch.equal(c, ref)
+    big = [synth.make_image(np.random.default_rng(1), 1000, 750, qt)]
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(smol.CoefBatch(big, qt, location="pinned"))
+    assert e.value.status == 5
+    plan.close()
 
 
 def test_errors_and_empty():
