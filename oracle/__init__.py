@@ -43,7 +43,8 @@ class _Plane(ctypes.Structure):
 
 
 class _Image(ctypes.Structure):
-    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("comp", _Plane * 3)]
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("comp", _Plane * 3),
+                ("hs", ctypes.c_int32), ("vs", ctypes.c_int32)]
 
 
 class _Params(ctypes.Structure):
@@ -51,7 +52,8 @@ class _Params(ctypes.Structure):
                 ("resize_short", ctypes.c_int32), ("resize_w", ctypes.c_int32),
                 ("resize_h", ctypes.c_int32), ("crop_w", ctypes.c_int32),
                 ("crop_h", ctypes.c_int32), ("mean", ctypes.c_double * 3),
-                ("std", ctypes.c_double * 3), ("out_f16", ctypes.c_int32)]
+                ("std", ctypes.c_double * 3), ("out_f16", ctypes.c_int32),
+                ("idct_def", ctypes.c_int32)]
 
 
 class Geometry(ctypes.Structure):
@@ -68,8 +70,17 @@ def lib():
         L = ctypes.CDLL(build())
         P = ctypes.POINTER
         L.oracle_geometry_of.argtypes = [P(_Params), ctypes.c_int32, ctypes.c_int32, P(Geometry)]
+        L.oracle_geometry_of2.argtypes = [P(_Params), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32, P(Geometry)]
         L.oracle_decode_plane.argtypes = [P(_Plane), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_decode_plane2.argtypes = [P(_Plane), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_upsample_color2.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                             ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_run_image2.argtypes = [P(_Params), P(_Image)] + [ctypes.c_int32] * 6 + [ctypes.c_void_p]
         L.oracle_upsample_color.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
                                             ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
@@ -95,7 +106,7 @@ def _ptr(a: np.ndarray) -> int:
 
 def make_params(scale_denom=1, resize_mode="short", resize_short=256, resize_w=0, resize_h=0,
                 crop_w=0, crop_h=0, mean=(0.485, 0.456, 0.406), std=(0.229, 0.224, 0.225),
-                out_dtype="f32") -> _Params:
+                out_dtype="f32", idct_def="box") -> _Params:
     p = _Params()
     p.scale_denom = scale_denom
     p.resize_mode = 0 if resize_mode == "short" else 1
@@ -104,11 +115,12 @@ def make_params(scale_denom=1, resize_mode="short", resize_short=256, resize_w=0
     p.mean = (ctypes.c_double * 3)(*mean)
     p.std = (ctypes.c_double * 3)(*std)
     p.out_f16 = 1 if out_dtype == "f16" else 0
+    p.idct_def = 1 if idct_def == "truncated" else 0
     return p
 
 
-def params_from_config(cfg, mean=None, std=None) -> _Params:
-    kw = {}
+def params_from_config(cfg, mean=None, std=None, idct_def="box") -> _Params:
+    kw = {"idct_def": idct_def}
     if mean is not None:
         kw["mean"] = mean
     if std is not None:
@@ -117,9 +129,13 @@ def params_from_config(cfg, mean=None, std=None) -> _Params:
                        cfg.resize_h, cfg.crop_w, cfg.crop_h, out_dtype=cfg.out_dtype, **kw)
 
 
-def geometry(p: _Params, width: int, height: int) -> Geometry:
+SUBSAMPLING = {420: (2, 2), 422: (2, 1), 444: (1, 1), 400: (2, 2)}
+
+
+def geometry(p: _Params, width: int, height: int, subsampling: int = 420) -> Geometry:
     g = Geometry()
-    rc = lib().oracle_geometry_of(ctypes.byref(p), width, height, ctypes.byref(g))
+    hs, vs = SUBSAMPLING[subsampling]
+    rc = lib().oracle_geometry_of2(ctypes.byref(p), width, height, hs, vs, ctypes.byref(g))
     if rc:
         raise ValueError(f"oracle_geometry_of failed rc={rc}")
     return g
@@ -134,29 +150,32 @@ def _plane(coef: np.ndarray, q: np.ndarray) -> _Plane:
     return pl
 
 
-def decode_plane(coef: np.ndarray, q: np.ndarray, k: int, out_w: int, out_h: int
+def decode_plane(coef: np.ndarray, q: np.ndarray, k: int, out_w: int, out_h: int, idct_def: int = 0
                  ) -> Tuple[np.ndarray, np.ndarray]:
-    """-> (v [out_h][out_w] f64 before level shift, u8 [out_h][out_w])."""
+    """-> (v [out_h][out_w] f64 before level shift, u8 [out_h][out_w]);
+    idct_def 0 = Definition A (R1), 1 = Definition B (R16)."""
     coef = np.ascontiguousarray(coef, dtype=np.int16)
     q = np.ascontiguousarray(q, dtype=np.uint16)
     v = np.empty((out_h, out_w), np.float64)
     u8 = np.empty((out_h, out_w), np.uint8)
     pl = _plane(coef, q)
-    rc = lib().oracle_decode_plane(ctypes.byref(pl), k, out_w, out_h, _ptr(v), _ptr(u8))
+    rc = lib().oracle_decode_plane2(ctypes.byref(pl), k, idct_def, out_w, out_h, _ptr(v), _ptr(u8))
     if rc:
         raise ValueError(f"oracle_decode_plane rc={rc}")
     return v, u8
 
 
-def upsample_color(Y: np.ndarray, Cb: np.ndarray, Cr: np.ndarray
+def upsample_color(Y: np.ndarray, Cb: np.ndarray, Cr: np.ndarray, subsampling: int = 420
                    ) -> Tuple[np.ndarray, np.ndarray]:
     """-> (c16 [Hd][Wd][2] int32, rgb [Hd][Wd][3] u8)."""
+    hs, vs = SUBSAMPLING[subsampling]
     Y, Cb, Cr = (np.ascontiguousarray(a, dtype=np.uint8) for a in (Y, Cb, Cr))
     Hd, Wd = Y.shape
     Hc, Wc = Cb.shape
     c16 = np.empty((Hd, Wd, 2), np.int32)
     rgb = np.empty((Hd, Wd, 3), np.uint8)
-    rc = lib().oracle_upsample_color(_ptr(Y), Wd, Hd, _ptr(Cb), _ptr(Cr), Wc, Hc, _ptr(c16), _ptr(rgb))
+    rc = lib().oracle_upsample_color2(_ptr(Y), Wd, Hd, _ptr(Cb), _ptr(Cr), Wc, Hc, hs, vs, _ptr(c16),
+                                      _ptr(rgb))
     if rc:
         raise ValueError(f"oracle_upsample_color rc={rc}")
     return c16, rgb
@@ -188,6 +207,7 @@ def resize_crop_normalize(rgb: np.ndarray, Wr: int, Hr: int, left: int, top: int
 def _image(im, qtables: np.ndarray, keep: list) -> _Image:
     c = _Image()
     c.width, c.height = im.width, im.height
+    c.hs, c.vs = SUBSAMPLING[getattr(im, "subsampling", 420)]
     for ci in range(3):
         if ci >= len(im.coef):               # grayscale: one component
             c.comp[ci] = _Plane()
@@ -199,15 +219,22 @@ def _image(im, qtables: np.ndarray, keep: list) -> _Image:
     return c
 
 
-def run_image(p: _Params, im, qtables: np.ndarray, roi: Optional[Tuple[int, int]] = None
-              ) -> np.ndarray:
-    """Whole pipeline for one synth.CoefImage -> [3][OH][OW] (f32 or f16)."""
-    g = geometry(p, im.width, im.height)
+def run_image(p: _Params, im, qtables: np.ndarray, roi: Optional[Tuple[int, int]] = None,
+              roi_rect: Optional[Tuple[int, int, int, int]] = None) -> np.ndarray:
+    """Whole pipeline for one synth.CoefImage -> [3][OH][OW] (f32 or f16).
+    roi: crop-window origin in resized coordinates; roi_rect: (x, y, w, h) ROI
+    rectangle in SOF pixels, resized to the plan's output size (R15)."""
+    g = geometry(p, im.width, im.height, getattr(im, "subsampling", 420))
     keep: list = []
     c = _image(im, qtables, keep)
-    out = np.empty((3, g.OH, g.OW), np.float16 if p.out_f16 else np.float32)
+    OW, OH = g.OW, g.OH
+    if roi_rect is not None:
+        OW = p.crop_w if p.crop_w > 0 else p.resize_w
+        OH = p.crop_h if p.crop_w > 0 else p.resize_h
+    out = np.empty((3, OH, OW), np.float16 if p.out_f16 else np.float32)
     left, top = roi if roi is not None else (-1, -1)
-    rc = lib().oracle_run_image(ctypes.byref(p), ctypes.byref(c), left, top, _ptr(out))
+    rx, ry, rw, rh = roi_rect if roi_rect is not None else (0, 0, 0, 0)
+    rc = lib().oracle_run_image2(ctypes.byref(p), ctypes.byref(c), left, top, rx, ry, rw, rh, _ptr(out))
     if rc:
         raise ValueError(f"oracle_run_image rc={rc}")
     return out
@@ -228,12 +255,12 @@ def run_batch(p: _Params, imgs: Sequence, qtables: np.ndarray, threads: int = 1,
 def decode_image_planes(p: _Params, im, qtables: np.ndarray, with_v: bool = False):
     """Decoded u8 Y, Cb, Cr planes (Y only for a grayscale image) and optional
     unrounded v at p's scale."""
-    g = geometry(p, im.width, im.height)
+    g = geometry(p, im.width, im.height, getattr(im, "subsampling", 420))
     k = p.scale_denom
     out = []
     for ci in range(len(im.coef)):
         w, h = (g.Wd, g.Hd) if ci == 0 else (g.Wc, g.Hc)
-        v, u8 = decode_plane(im.coef[ci], qtables[im.qidx[ci]], k, w, h)
+        v, u8 = decode_plane(im.coef[ci], qtables[im.qidx[ci]], k, w, h, p.idct_def)
         out.append((v, u8) if with_v else u8)
     return out
 

@@ -49,15 +49,38 @@ static double oracle_a(int k, int u, int j) {
   return s / (double)k;
 }
 
+/* Reading R16 (Definition B, the alternative of R1): at scale 1/k, with
+ * N = 8/k, the N x N output is the orthonormal N-point 2-D IDCT of the
+ * top-left N x N coefficients scaled by N/8 (the N-point DCT of a block's
+ * low-pass content is sqrt(N/8) times the 8-point one per axis; libjpeg >= 7
+ * jpeg_idct_NxN).  Orthonormal N-point IDCT:
+ *   f(i,j) = sum_v sum_u alpha(v) alpha(u) F(v,u) cos((2i+1)v pi/2N) cos((2j+1)u pi/2N),
+ *   alpha(0) = sqrt(1/N), alpha(u>0) = sqrt(2/N);  with F = (N/8) D this is
+ *   f(i,j) = 1/8 sum_v sum_u D(v,u) b_N(v,i) b_N(u,j),
+ *   b_N(u,x) = sqrt2 C(u) cos((2x+1) u pi / 2N)   (b_8 = t).
+ * b_N(0,x) = 1 and b_N(N/2,x) = sqrt2 cos((2x+1) pi/4) = +-1 exactly; those
+ * entries are stored exactly (DC and u = N/2 ties stay exact, R3).  At N = 1
+ * (k = 8) this is DC/8, Definition A's value. */
+static double oracle_b(int N, int u, int x) {
+  if (u == 0) return 1.0;
+  if (2 * u == N) {
+    int m = (2 * x + 1) % 8;          /* angle (2x+1) pi/4 */
+    return (m == 1 || m == 7) ? 1.0 : -1.0;
+  }
+  return sqrt(2.0) * cos((double)((2 * x + 1) * u) * ORACLE_PI / (2.0 * N));
+}
+
 /* Dequantize (D = coef * Q, "inverse transform") and decode one
  * block at scale 1/k: v[i*P+j] = 1/8 sum_v sum_u D(v,u) a_k(v,i) a_k(u,j),
- * P = 8/k samples per side, before the level shift. */
-static void oracle_idct_block(const int16_t* coef, const uint16_t* q, int k, double* v) {
+ * P = 8/k samples per side, before the level shift (Definition A); with
+ * def = 1 the basis is b_P over u, v < P (Definition B, zero elsewhere). */
+static void oracle_idct_block_def(const int16_t* coef, const uint16_t* q, int k, int def, double* v) {
   const int P = 8 / k;
   double a[8][8];
   long long D[64];
   for (int u = 0; u < 8; ++u)
-    for (int j = 0; j < P; ++j) a[u][j] = oracle_a(k, u, j);
+    for (int j = 0; j < P; ++j)
+      a[u][j] = def == 0 ? oracle_a(k, u, j) : (u < P ? oracle_b(P, u, j) : 0.0);
   for (int i = 0; i < 64; ++i) D[i] = (long long)coef[i] * (long long)q[i];
   for (int i = 0; i < P; ++i)
     for (int j = 0; j < P; ++j) {
@@ -67,6 +90,7 @@ static void oracle_idct_block(const int16_t* coef, const uint16_t* q, int k, dou
       v[i * P + j] = s / 8.0;
     }
 }
+
 
 /* Reading R3: u8 = clamp(floor(v + 128 + 1/2), 0, 255) (round half up). */
 static uint8_t oracle_round_u8(double v) {
@@ -78,7 +102,13 @@ static uint8_t oracle_round_u8(double v) {
 
 int oracle_decode_plane(const oracle_plane* pl, int32_t k, int32_t out_w, int32_t out_h,
                         double* v_out, uint8_t* u8_out) {
+  return oracle_decode_plane2(pl, k, 0, out_w, out_h, v_out, u8_out);
+}
+
+int oracle_decode_plane2(const oracle_plane* pl, int32_t k, int32_t idct_def, int32_t out_w,
+                         int32_t out_h, double* v_out, uint8_t* u8_out) {
   if (!pl || !pl->coef || !pl->q || !u8_out) return 1;
+  if (idct_def != 0 && idct_def != 1) return 4;
   if (k != 1 && k != 2 && k != 4 && k != 8) return 2;
   const int P = 8 / k;                      /* output samples per block side */
   const int nbx = (out_w + P - 1) / P, nby = (out_h + P - 1) / P;
@@ -87,7 +117,7 @@ int oracle_decode_plane(const oracle_plane* pl, int32_t k, int32_t out_w, int32_
   for (int by = 0; by < nby; ++by)
     for (int bx = 0; bx < nbx; ++bx) {
       const int16_t* blk = pl->coef + (size_t)by * pl->row_stride + (size_t)bx * 64;
-      oracle_idct_block(blk, pl->q, k, v);
+      oracle_idct_block_def(blk, pl->q, k, idct_def, v);
       for (int i = 0; i < P; ++i)
         for (int j = 0; j < P; ++j) {
           int y = by * P + i, x = bx * P + j;
@@ -145,6 +175,32 @@ static int32_t oracle_upsample_at(const uint8_t* C, int32_t Wc, int32_t Hc, int3
          3 * C[(size_t)j2 * Wc + i] + 1 * C[(size_t)j2 * Wc + i2];
 }
 
+/* Reading R2 per axis (4:2:2, 4:4:4 and 4:2:0): along an axis subsampled by
+ * 2, luma position X takes 3/4 C[X/2] + 1/4 C[X/2 -+ 1] (- for even X, +
+ * for odd), clamped to the valid chroma size; along an axis that is not
+ * subsampled it takes C[X] (weight 4/4).  The 2-D value is the product of
+ * the two axis filters, kept exact in 1/16 units (4:2:0: 9/3/3/1, as above). */
+static void oracle_axis_taps(int32_t X, int32_t f, int32_t n, int32_t* i, int32_t* i2, int32_t* w, int32_t* w2) {
+  if (f == 1) {
+    *i = X < n ? X : n - 1; *i2 = *i; *w = 4; *w2 = 0;
+    return;
+  }
+  *i = X / 2;
+  *i2 = (X % 2 == 0) ? *i - 1 : *i + 1;
+  if (*i2 < 0) *i2 = 0;
+  if (*i2 > n - 1) *i2 = n - 1;
+  if (*i > n - 1) *i = n - 1;
+  *w = 3; *w2 = 1;
+}
+static int32_t oracle_upsample_at2(const uint8_t* C, int32_t Wc, int32_t Hc, int32_t X, int32_t Yr,
+                                   int32_t hs, int32_t vs) {
+  int32_t i, i2, wx, wx2, j, j2, wy, wy2;
+  oracle_axis_taps(X, hs, Wc, &i, &i2, &wx, &wx2);
+  oracle_axis_taps(Yr, vs, Hc, &j, &j2, &wy, &wy2);
+  return wy * (wx * C[(size_t)j * Wc + i] + wx2 * C[(size_t)j * Wc + i2]) +
+         wy2 * (wx * C[(size_t)j2 * Wc + i] + wx2 * C[(size_t)j2 * Wc + i2]);
+}
+
 int oracle_upsample_color(const uint8_t* Y, int32_t Wd, int32_t Hd,
                           const uint8_t* Cb, const uint8_t* Cr, int32_t Wc, int32_t Hc,
                           int32_t* c16_out, uint8_t* rgb_out) {
@@ -153,6 +209,24 @@ int oracle_upsample_color(const uint8_t* Y, int32_t Wd, int32_t Hd,
     for (int32_t x = 0; x < Wd; ++x) {
       int32_t cb = oracle_upsample_at(Cb, Wc, Hc, x, y);
       int32_t cr = oracle_upsample_at(Cr, Wc, Hc, x, y);
+      if (c16_out) {
+        c16_out[((size_t)y * Wd + x) * 2 + 0] = cb;
+        c16_out[((size_t)y * Wd + x) * 2 + 1] = cr;
+      }
+      oracle_color(Y[(size_t)y * Wd + x], cb, cr, rgb_out + ((size_t)y * Wd + x) * 3);
+    }
+  return 0;
+}
+
+int oracle_upsample_color2(const uint8_t* Y, int32_t Wd, int32_t Hd,
+                           const uint8_t* Cb, const uint8_t* Cr, int32_t Wc, int32_t Hc,
+                           int32_t hs, int32_t vs, int32_t* c16_out, uint8_t* rgb_out) {
+  if (!Y || !Cb || !Cr || !rgb_out || Wd <= 0 || Hd <= 0 || Wc <= 0 || Hc <= 0) return 1;
+  if ((hs != 1 && hs != 2) || (vs != 1 && vs != 2)) return 2;
+  for (int32_t y = 0; y < Hd; ++y)
+    for (int32_t x = 0; x < Wd; ++x) {
+      int32_t cb = oracle_upsample_at2(Cb, Wc, Hc, x, y, hs, vs);
+      int32_t cr = oracle_upsample_at2(Cr, Wc, Hc, x, y, hs, vs);
       if (c16_out) {
         c16_out[((size_t)y * Wd + x) * 2 + 0] = cb;
         c16_out[((size_t)y * Wd + x) * 2 + 1] = cr;
@@ -251,13 +325,20 @@ static int32_t oracle_round_half_even_half(int32_t n) {   /* round(n / 2) */
 }
 
 int oracle_geometry_of(const oracle_params* p, int32_t width, int32_t height, oracle_geometry* g) {
+  return oracle_geometry_of2(p, width, height, 2, 2, g);
+}
+
+int oracle_geometry_of2(const oracle_params* p, int32_t width, int32_t height, int32_t hs,
+                        int32_t vs, oracle_geometry* g) {
   if (!p || !g || width <= 0 || height <= 0) return 1;
   int32_t k = p->scale_denom;
   if (k != 1 && k != 2 && k != 4 && k != 8) return 2;
+  if ((hs != 1 && hs != 2) || (vs != 1 && vs != 2)) return 5;
   g->Wd = oracle_ceil_div(width, k);
   g->Hd = oracle_ceil_div(height, k);
-  g->Wc = oracle_ceil_div(width, 2 * k);
-  g->Hc = oracle_ceil_div(height, 2 * k);
+  /* component size ceil(X/hs) (T.81 A.1.1), decoded at 1/k: ceil(X/(hs k)) */
+  g->Wc = oracle_ceil_div(width, hs * k);
+  g->Hc = oracle_ceil_div(height, vs * k);
   if (p->resize_mode == 0) {
     int32_t S = p->resize_short;
     if (S <= 0) return 3;
@@ -279,29 +360,62 @@ int oracle_geometry_of(const oracle_params* p, int32_t width, int32_t height, or
 }
 
 int oracle_run_image(const oracle_params* p, const oracle_image* im, int32_t left, int32_t top, void* out) {
+  return oracle_run_image2(p, im, left, top, 0, 0, 0, 0, out);
+}
+
+int oracle_run_image2(const oracle_params* p, const oracle_image* im, int32_t left, int32_t top,
+                      int32_t roi_x, int32_t roi_y, int32_t roi_w, int32_t roi_h, void* out) {
   oracle_geometry g;
-  int rc = oracle_geometry_of(p, im->width, im->height, &g);
+  const int32_t hs = im->comp[1].coef == NULL ? 2 : im->hs, vs = im->comp[1].coef == NULL ? 2 : im->vs;
+  int rc = oracle_geometry_of2(p, im->width, im->height, hs, vs, &g);
   if (rc) return rc;
   if (left >= 0 && top >= 0) { g.left = left; g.top = top; }
+  int32_t wx0 = 0, wy0 = 0, ww = 0, wh = 0;     /* decoded ROI window (reading R15) */
+  if (roi_w > 0 || roi_h > 0) {
+    const int32_t k = p->scale_denom;
+    if (roi_w <= 0 || roi_h <= 0 || roi_x < 0 || roi_y < 0 || roi_x + roi_w > im->width ||
+        roi_y + roi_h > im->height)
+      return 20;
+    wx0 = roi_x / k; wy0 = roi_y / k;
+    ww = oracle_ceil_div(roi_x + roi_w, k) - wx0;
+    wh = oracle_ceil_div(roi_y + roi_h, k) - wy0;
+    /* output = the plan's size; the window is resized to it, no crop */
+    g.OW = p->crop_w > 0 ? p->crop_w : p->resize_w;
+    g.OH = p->crop_w > 0 ? p->crop_h : p->resize_h;
+    if (g.OW <= 0 || g.OH <= 0) return 21;
+  }
   uint8_t* Y = (uint8_t*)malloc((size_t)g.Wd * g.Hd);
   uint8_t* Cb = (uint8_t*)malloc((size_t)g.Wc * g.Hc);
   uint8_t* Cr = (uint8_t*)malloc((size_t)g.Wc * g.Hc);
   uint8_t* rgb = (uint8_t*)malloc((size_t)g.Wd * g.Hd * 3);
   rc = 10;
   if (Y && Cb && Cr && rgb) {
-    rc = oracle_decode_plane(&im->comp[0], p->scale_denom, g.Wd, g.Hd, NULL, Y);
+    rc = oracle_decode_plane2(&im->comp[0], p->scale_denom, p->idct_def, g.Wd, g.Hd, NULL, Y);
     if (im->comp[1].coef == NULL) {
       /* grayscale (one component, T.81 A.1.1 Nf = 1): the JFIF colour space
        * is Y only, i.e. R = G = B = Y (R6 with Cb = Cr = 128) */
       for (int32_t i = 0; !rc && i < g.Wd * g.Hd; ++i)
         rgb[3 * i] = rgb[3 * i + 1] = rgb[3 * i + 2] = Y[i];
     } else {
-      if (!rc) rc = oracle_decode_plane(&im->comp[1], p->scale_denom, g.Wc, g.Hc, NULL, Cb);
-      if (!rc) rc = oracle_decode_plane(&im->comp[2], p->scale_denom, g.Wc, g.Hc, NULL, Cr);
-      if (!rc) rc = oracle_upsample_color(Y, g.Wd, g.Hd, Cb, Cr, g.Wc, g.Hc, NULL, rgb);
+      if (!rc) rc = oracle_decode_plane2(&im->comp[1], p->scale_denom, p->idct_def, g.Wc, g.Hc, NULL, Cb);
+      if (!rc) rc = oracle_decode_plane2(&im->comp[2], p->scale_denom, p->idct_def, g.Wc, g.Hc, NULL, Cr);
+      if (!rc) rc = oracle_upsample_color2(Y, g.Wd, g.Hd, Cb, Cr, g.Wc, g.Hc, hs, vs, NULL, rgb);
     }
-    if (!rc) rc = oracle_resize_crop_normalize(rgb, g.Wd, g.Hd, g.Wr, g.Hr, g.left, g.top,
-                                               g.OW, g.OH, p->mean, p->std, p->out_f16, out, NULL);
+    if (!rc && ww > 0) {
+      /* crop the decoded RGB image to the ROI window, then resize the
+       * window to the output size (P:1080-1083 face crops at a fixed DNN
+       * input size; reading R15) */
+      uint8_t* win = (uint8_t*)malloc((size_t)ww * wh * 3);
+      if (!win) rc = 11;
+      for (int32_t y = 0; !rc && y < wh; ++y)
+        memcpy(win + (size_t)y * ww * 3, rgb + ((size_t)(wy0 + y) * g.Wd + wx0) * 3, (size_t)ww * 3);
+      if (!rc) rc = oracle_resize_crop_normalize(win, ww, wh, g.OW, g.OH, 0, 0, g.OW, g.OH, p->mean,
+                                                 p->std, p->out_f16, out, NULL);
+      free(win);
+    } else if (!rc) {
+      rc = oracle_resize_crop_normalize(rgb, g.Wd, g.Hd, g.Wr, g.Hr, g.left, g.top,
+                                        g.OW, g.OH, p->mean, p->std, p->out_f16, out, NULL);
+    }
   }
   free(Y); free(Cb); free(Cr); free(rgb);
   return rc;

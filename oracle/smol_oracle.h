@@ -11,8 +11,10 @@
  *   1. decode (§6.4 "entropy decoding, inverse transform,
  *      post-processing"; entropy decoding done by the host):
  *      dequantize + 8x8 IDCT (ITU-T T.81 A.3.3) at scale 1, or the k x k box
- *      mean of it at scale 1/k (reading R1) + level shift, round half up,
- *      clamp to u8 (R3);  4:2:0 centred triangle chroma upsample (R2);
+ *      mean of it at scale 1/k (reading R1; Definition B, R16, as an
+ *      option) + level shift, round half up, clamp to u8 (R3);  centred
+ *      triangle chroma upsample per subsampled axis (4:2:0, 4:2:2; 4:4:4
+ *      needs none) (R2);
  *      exact JFIF YCbCr->RGB (R6);
  *   2. resize (short edge -> S, or exact) with half-pixel bilinear, no
  *      antialias (readings R7/R8), centre crop (R7);
@@ -41,8 +43,10 @@ typedef struct {
 
 typedef struct {
   int32_t width, height;      /* SOF size in pixels */
-  oracle_plane comp[3];       /* Y, Cb, Cr (4:2:0); comp[1].coef == NULL: grayscale
+  oracle_plane comp[3];       /* Y, Cb, Cr; comp[1].coef == NULL: grayscale
                                  (one component; R = G = B = Y) */
+  int32_t hs, vs;             /* chroma subsampling factors (T.81 A.1.1: Hmax/Hc,
+                                 Vmax/Vc): 2,2 = 4:2:0; 2,1 = 4:2:2; 1,1 = 4:4:4 */
 } oracle_image;
 
 typedef struct {
@@ -52,6 +56,9 @@ typedef struct {
   int32_t crop_w, crop_h;     /* 0,0 = no crop */
   double mean[3], std[3];
   int32_t out_f16;            /* 0 = fp32 output, 1 = fp16 (RNE) */
+  int32_t idct_def;           /* reduced-scale IDCT: 0 = Definition A (box mean,
+                                 reading R1), 1 = Definition B (truncated
+                                 (8/k)-point IDCT, reading R16) */
 } oracle_params;
 
 typedef struct {
@@ -62,15 +69,24 @@ typedef struct {
   int32_t OW, OH;             /* output size */
 } oracle_geometry;
 
-/* Geometry per readings R4 (decoded sizes), R7 (torchvision resize/crop). */
+/* Geometry per readings R4 (decoded sizes), R7 (torchvision resize/crop),
+ * 4:2:0 chroma. */
 int oracle_geometry_of(const oracle_params* p, int32_t width, int32_t height,
                        oracle_geometry* g);
+/* Same for chroma subsampled by hs x vs (T.81 A.1.1: component size
+ * ceil(X / hs) x ceil(Y / vs), then ceil(./k) at scale 1/k, reading R4). */
+int oracle_geometry_of2(const oracle_params* p, int32_t width, int32_t height, int32_t hs,
+                        int32_t vs, oracle_geometry* g);
 
 /* Decode one component at scale 1/k into an out_w x out_h plane.
  * v_out (nullable): unrounded IDCT value before the +128 level shift.
  * u8_out: clamp(floor(v + 128 + 1/2), 0, 255). */
 int oracle_decode_plane(const oracle_plane* pl, int32_t k, int32_t out_w, int32_t out_h,
                         double* v_out, uint8_t* u8_out);
+/* Same with the reduced-scale definition idct_def (0: A, box mean; 1: B,
+ * truncated (8/k)-point IDCT of the top-left (8/k)^2 coefficients). */
+int oracle_decode_plane2(const oracle_plane* pl, int32_t k, int32_t idct_def, int32_t out_w,
+                         int32_t out_h, double* v_out, uint8_t* u8_out);
 
 /* 4:2:0 upsample + YCbCr->RGB.  Y: [Hd][Wd]; Cb, Cr: [Hc][Wc].
  * c16_out (nullable): [Hd][Wd][2] upsampled Cb, Cr in 1/16 units.
@@ -78,6 +94,12 @@ int oracle_decode_plane(const oracle_plane* pl, int32_t k, int32_t out_w, int32_
 int oracle_upsample_color(const uint8_t* Y, int32_t Wd, int32_t Hd,
                           const uint8_t* Cb, const uint8_t* Cr, int32_t Wc, int32_t Hc,
                           int32_t* c16_out, uint8_t* rgb_out);
+
+/* Upsample (hs x vs subsampled chroma; reading R2 per axis: factor 2 = the
+ * centred triangle 3/4, 1/4, factor 1 = identity) + YCbCr->RGB. */
+int oracle_upsample_color2(const uint8_t* Y, int32_t Wd, int32_t Hd,
+                           const uint8_t* Cb, const uint8_t* Cr, int32_t Wc, int32_t Hc,
+                           int32_t hs, int32_t vs, int32_t* c16_out, uint8_t* rgb_out);
 
 /* JFIF colour conversion of one sample, chroma in 1/16 units (0..4080). */
 void oracle_color(int32_t Y, int32_t cb16, int32_t cr16, uint8_t rgb[3]);
@@ -96,6 +118,17 @@ int oracle_resize_crop_normalize(const uint8_t* rgb, int32_t Wd, int32_t Hd,
  * P:1107-1109).  out: [3][OH][OW]. */
 int oracle_run_image(const oracle_params* p, const oracle_image* im,
                      int32_t left, int32_t top, void* out);
+
+/* Whole pipeline with an optional ROI rectangle (P:1080-1083, P:1107-1109:
+ * "the ROIs are the face crops"; reading R15): roi_w, roi_h > 0 select the
+ * SOF-pixel rectangle [roi_x, roi_x + roi_w) x [roi_y, roi_y + roi_h); its
+ * decoded window at scale 1/k is [floor(x/k), ceil((x+w)/k)) x likewise;
+ * the decoded RGB image is cropped to that window, which is resized to the
+ * plan's output size (crop_w x crop_h, else resize_w x resize_h) -- crop,
+ * then resize (torchvision resized_crop); normalize; channels-first.
+ * roi_w = roi_h = 0: oracle_run_image(p, im, left, top, out). */
+int oracle_run_image2(const oracle_params* p, const oracle_image* im, int32_t left, int32_t top,
+                      int32_t roi_x, int32_t roi_y, int32_t roi_w, int32_t roi_h, void* out);
 
 /* Algorithm 1 crop window in source coordinates, SPEC
  * convention: l',t' floored, r',b' ceiled.  Geometry helper only

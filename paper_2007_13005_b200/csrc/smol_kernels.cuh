@@ -26,23 +26,11 @@
 // scale 1 the output tasks share the phase with the next step's IDCT and are
 // grabbed dynamically, two per lane per grab, interleaved by the compiler; at
 // scales 1/2..1/8 that IDCT is small and a static stride wins.
-#ifndef SMOL_COLOUR_QUADS
-#define SMOL_COLOUR_QUADS 2      // colour task = this many 2x4-pixel quads of one row pair
-#endif
-#ifndef SMOL_OUT_ROWRUN
-#define SMOL_OUT_ROWRUN 15       // bit log2(K): at scale 1/K an output task is one quad over a run of rows
-#endif
 #ifndef SMOL_OUT_RUN_ROWS
 #define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
 #endif
-#ifndef SMOL_OUT_QUADS
-#define SMOL_OUT_QUADS 2         // output task = this many 4-pixel quads of one row
-#endif
 #ifndef SMOL_OUT_PER_GRAB
-#define SMOL_OUT_PER_GRAB (SMOL_OUT_QUADS == 1 ? 2 : 1)   // scale 1: output tasks per lane per work-counter grab
-#endif
-#ifndef SMOL_IDCT_V2
-#define SMOL_IDCT_V2 1           // scale-1 IDCT: both passes on packed column pairs
+#define SMOL_OUT_PER_GRAB 2      // scale 1: output tasks per lane per work-counter grab
 #endif
 #ifndef SMOL_OUT_STATIC
 #define SMOL_OUT_STATIC 2        // 0: dynamic everywhere; 1: static everywhere; 2: static at scales 1/2..1/8
@@ -66,7 +54,6 @@ struct Basis {
   float kR, kB, cR, cB;
   uint32_t gK1, gCb, gCr;          // G = Y + (gK1 + gCb cb16 + gCr cr16) / 2e6 - 136 (mod 2^32; see colour())
   float2 tp[4][4];   // column pass pairs: tp[k][y] = (t[2k][y], t[2k+1][y])
-  float2 rp[8][2];   // row pass column pairs: rp[u][j] = (t(u, 2j), t(u, 2j+1)), j < 2 (= basis_t)
 };
 
 // One copy per translation unit (internal linkage; the library is built
@@ -219,66 +206,6 @@ __device__ __forceinline__ void idct_rows(const int4 (&raw)[8], const float* q, 
   }
 }
 
-// Scale-1 block, v2 (SMOL_IDCT_V2): every pass two samples per packed FP32x2
-// instruction, no register transposes.  Row pass, per row v with inputs
-// d[u] = coef * Q/8 (FMUL2 on element pairs): lanes are COLUMN pairs --
-//   E01 = d0 + d4 (1,-1) + d2 T2(0,1) + d6 T6(0,1),  O01 = sum_odd d_u Tu(0,1)
-//   (m0, m1) = E01 + O01,  (m7, m6) = E01 - O01     (t(u,7-x) = (-1)^u t(u,x))
-// and likewise (m2, m3) / (m5, m4) from the (2,3) constant pairs; the scalar
-// d_u is broadcast into both lanes (FFMA2 .F32 operand) and the constant
-// pairs come from the constant bank (uniform registers).  The column pass
-// then runs on those column pairs with scalar immediates (idct8x2).  Each
-// lane sees exactly the IEEE operations, in the same order, of the scalar
-// idct8 row and column passes (DC and u=4 paths exact, reading R3).
-template <int H>
-__device__ __forceinline__ void idct_block_v2(const int4 (&raw)[8], const float* q, uint32_t (&px)[8][2]) {
-  float2 r[4][8];                        // r[k][v]: k = column pair (0,1), (2,3), (5,4), (7,6)
-#pragma unroll
-  for (int v = 0; v < 8; ++v) {
-    if (v >= H) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) r[k][v] = f2(0.f);
-      continue;
-    }
-    float a[8];
-    unpack_row(raw[v], a);
-    const float4 q0 = *reinterpret_cast<const float4*>(q + v * 8);
-    const float4 q1 = *reinterpret_cast<const float4*>(q + v * 8 + 4);
-    const float2 d01 = __fmul2_rn(make_float2(a[0], a[1]), make_float2(q0.x, q0.y));
-    const float2 d23 = __fmul2_rn(make_float2(a[2], a[3]), make_float2(q0.z, q0.w));
-    const float2 d45 = __fmul2_rn(make_float2(a[4], a[5]), make_float2(q1.x, q1.y));
-    const float2 d67 = __fmul2_rn(make_float2(a[6], a[7]), make_float2(q1.z, q1.w));
-    const float d0 = (v == 0) ? d01.x + 128.5f : d01.x;    // level shift + rounding offset on the DC
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      float2 e = __ffma2_rn(f2(d45.x), j == 0 ? make_float2(1.f, -1.f) : make_float2(-1.f, 1.f), f2(d0));
-      e = __ffma2_rn(f2(d23.x), c_basis.rp[2][j], e);
-      e = __ffma2_rn(f2(d67.x), c_basis.rp[6][j], e);
-      float2 od = __fmul2_rn(f2(d01.y), c_basis.rp[1][j]);
-      od = __ffma2_rn(f2(d23.y), c_basis.rp[3][j], od);
-      od = __ffma2_rn(f2(d45.y), c_basis.rp[5][j], od);
-      od = __ffma2_rn(f2(d67.y), c_basis.rp[7][j], od);
-      r[j][v] = __fadd2_rn(e, od);                        // (m[2j], m[2j+1])
-      r[3 - j][v] = __ffma2_rn(od, f2(-1.f), e);          // (m[7-2j], m[6-2j])
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    float2 f[8];
-    idct8x2<H>(r[k], f);
-    // lanes of pair k are columns (x0, x1): (0,1), (2,3), (5,4), (7,6)
-    const int x0 = k == 0 ? 0 : k == 1 ? 2 : k == 2 ? 5 : 7;
-#pragma unroll
-    for (int y = 0; y < 8; ++y) {
-      const uint32_t b0 = floor_u8(f[y].x), b1 = floor_u8(f[y].y);
-      const uint32_t pr = (k < 2) ? __byte_perm(b0, b1, 0x3340) : __byte_perm(b1, b0, 0x3340);  // ascending x
-      uint32_t& w = px[y][x0 >> 2];
-      if ((x0 & 3) < 2) w = pr;                             // bytes 0, 1 of the word
-      else w = __byte_perm(w, pr, 0x5410);                  // bytes 2, 3
-    }
-  }
-}
-
 template <int H>
 __device__ __forceinline__ void idct_cols(const float (&m)[8][8], uint32_t (&px)[8][2]) {
   // column x's bytes are merged into the row words as they are produced
@@ -341,14 +268,11 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     // prune by the warp's highest nonzero coefficient row (one code variant
     // per extent: more variants cost more in I-cache misses than they save)
     const int H = (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows));
-#if SMOL_IDCT_V2
-    if (H <= 6) idct_block_v2<6>(raw, q, px);
-    else idct_block_v2<8>(raw, q, px);
-#else
+    // (a column pass on FFMA2 row pairs, and both passes on packed column
+    // pairs, measured no faster: r02 A/B)
     float m[8][8];
     if (H <= 6) { idct_rows<8, 6>(raw, q, m); idct_cols<6>(m, px); }
     else { idct_rows<8, 8>(raw, q, m); idct_cols<8>(m, px); }
-#endif
   } else {
     // K = 2 (4x4 out, u,v != 4) and K = 4 (2x2 out, u,v in {0,1,3,5,7}):
     // rows/columns outside the index set have an exactly-zero basis.
@@ -448,6 +372,7 @@ struct KParams {
   void* out;
   int OW, OH, tile_rows, tile_cols, n_col_tiles, n_row_tiles;
   int out_vec;                     // out is 16-B (fp32) / 8-B (fp16) aligned: vector stores allowed
+  int rowrun;                      // output tasks walk runs of rows, reusing horizontal lerps (vertical magnification)
   const int4* cta_map;             // non-null: 1-D grid, CTA -> {image, oy0, oy1, 0}
   uint32_t magic;                  // 0x4B000000: bit pattern of 2^23 (byte -> float trick)
   float na[3], nb[3];              // y = x * na + nb = (x/255 - mean)/std
@@ -550,14 +475,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     for (int i = tid; i < 2 * kCStride / 4; i += kThreads) reinterpret_cast<uint32_t*>(cring)[i] = 0x80808080u;
   const int nbx0 = L.bx1[0] - L.bx0[0] + 1, nbxc = L.bx1[1] - L.bx0[1] + 1;
   const FastDiv fd_y = make_fastdiv(nbx0), fd_c = make_fastdiv(nbxc);
-  const int ntask4 = L.rgb_w >> 2;          // 4-column colour quads per quad row
-  constexpr int kColQ = SMOL_COLOUR_QUADS;  // quads per colour task
-  const int ntaskt = (ntask4 + kColQ - 1) / kColQ;
-  const FastDiv fd_tt = make_fastdiv(ntaskt);
-  // output tasks: kOutQ quads (4 px) of one output row
-  constexpr int kOutQ = SMOL_OUT_QUADS;
-  const int nqt = (nq4 + kOutQ - 1) / kOutQ;
-  const FastDiv fd_qt = make_fastdiv(nqt);
+  const int ntask4 = L.rgb_w >> 2;          // 4-column colour tasks per quad row
+  const FastDiv fd_t4 = make_fastdiv(ntask4);
   const FastDiv fd_q4 = make_fastdiv(nq4);
   const bool vec4 = ((kp.OW & 3) == 0) && ((ox0 & 3) == 0) && kp.out_vec;
   const uint32_t plane_sz = (uint32_t)kp.OH * kp.OW;   // < 2^31 elements (host-checked)
@@ -694,34 +613,24 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     }
 
     // ---- upsample + colour of the RGB rows that became ready -------------
-    // A task is kColQ quads of 2x4 luma pixels (rows 2j, 2j+1; cols 2i ..
-    // 2i+4 kColQ - 1); a quad's 2x4 pixels share a 3x4 chroma neighbourhood.
-    // Steps end on odd rows (ready_after), so quads never straddle steps; at
-    // the footprint's first/last row a quad may include one row outside it
-    // (computed, never read).
+    // A task is 2x4 luma pixels (rows 2j, 2j+1; cols 2i .. 2i+3) sharing a
+    // 3x4 chroma neighbourhood.  Steps end on odd rows (ready_after), so
+    // quads never straddle steps; at the footprint's first/last row a quad
+    // may include one row outside it (computed, never read).
     {
       const int j0 = (ready_prev + 1) >> 1;
       const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
-      const int ntaskc = nq * ntaskt;
+      const int ntaskc = nq * ntask4;
       // colour tasks all cost the same and nothing else runs in this phase:
       // a static round-robin needs no work counter
       for (int t = tid; t < ntaskc; t += kThreads) {
-        const int rr = (int)fdiv((uint32_t)t, fd_tt);
-        const int p0 = kColQ * (t - rr * ntaskt);
+        const int rr = (int)fdiv((uint32_t)t, fd_t4);
+        const int p = t - rr * ntask4;
         const int j = j0 + rr;                               // chroma row of the quads
-        const int i0 = (L.rgb_x0 >> 1) + 2 * p0;             // chroma column of the first quad
-        const uint8_t* c1b = cring + ((j & (kCRing - 1)) + 1) * kCP + (i0 - L.xbase[1] + kCPad);
-        const int up = j > 0 ? -kCP : 0;                     // row j-1 (clamped at the top)
-        const int dn = j < im.Hc - 1 ? kCP : 0;              // row j+1 (clamped at the bottom)
-        const uint8_t* yrb = yring + ((2 * j) & (kYRing - 1)) * kYP + (2 * i0 - L.xbase[0]);
-        const int slot = rgb_slot(2 * j);
-        uint32_t* r0b = rgb + slot * rgb_p + (2 * i0 - L.rgb_x0);
-#pragma unroll
-        for (int qq = 0; qq < kColQ; ++qq) {
-        if (kColQ > 1 && qq > 0 && p0 + qq >= ntask4) break;
-        const uint8_t* c1 = c1b + 2 * qq;
-        const uint8_t* c0 = c1 + up;
-        const uint8_t* c2 = c1 + dn;
+        const int i = (L.rgb_x0 >> 1) + 2 * p;               // chroma column of the left quad
+        const uint8_t* c1 = cring + ((j & (kCRing - 1)) + 1) * kCP + (i - L.xbase[1] + kCPad);
+        const uint8_t* c0 = c1 + (j > 0 ? -kCP : 0);               // row j-1 (clamped at the top)
+        const uint8_t* c2 = c1 + (j < im.Hc - 1 ? kCP : 0);        // row j+1 (clamped at the bottom)
         int cbq[8], crq[8];                                  // [row 0: 4 cols][row 1: 4 cols]
 #pragma unroll
         for (int comp = 0; comp < 2; ++comp) {
@@ -744,10 +653,11 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
             qv[4 + x] = 3 * h[1][x] + h[2][x];   // row 2j+1
           }
         }
-        const uint8_t* yr = yrb + 4 * qq;
+        const uint8_t* yr = yring + ((2 * j) & (kYRing - 1)) * kYP + (2 * i - L.xbase[0]);
         const uint32_t y0 = *reinterpret_cast<const uint32_t*>(yr);
         const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
-        uint32_t* r0p = r0b + 4 * qq;
+        const int slot = rgb_slot(2 * j);
+        uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
         const uint32_t mg = 0x4B000000u;
         const uint2 t01 = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x7541), cbq[0], cbq[1], crq[0], crq[1]);
         const uint2 t23 = colour2m(__byte_perm(y0, mg, 0x7542), __byte_perm(y0, mg, 0x7543), cbq[2], cbq[3], crq[2], crq[3]);
@@ -757,7 +667,6 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         *reinterpret_cast<uint4*>(r0p) = top;
         *reinterpret_cast<uint4*>(r0p + rgb_p) = make_uint4(b01.x, b01.y, b23.x, b23.y);
         if (slot == 0) *reinterpret_cast<uint4*>(r0p + kRgbRing * rgb_p) = top;   // guard row
-        }
       }
     }
     __syncthreads();
@@ -777,7 +686,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     // ---- next step's IDCT (writes only Y/chroma rings: no reader now) ----
     if (s + 1 < L.nsteps) idct_step(s + 1);
 
-    if constexpr ((SMOL_OUT_ROWRUN >> (K == 1 ? 0 : K == 2 ? 1 : K == 4 ? 2 : 3)) & 1)
+    if (K != 1 && kp.rowrun)      // (scale 1: measured no gain at c2; keeps the K=1 kernel's registers)
     // ---- bilinear + normalize + NCHW store: a task is one 4-pixel column
     // quad over a run of up to kRun consecutive output rows.  Walking down
     // the run, the horizontal lerps of a source row are reused while the
@@ -888,9 +797,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       }
     }
     else
-    // ---- bilinear + normalize + NCHW store, kOutQ x 4 output pixels per task
+    // ---- bilinear + normalize + NCHW store, 4 output pixels per task -----
     {
-      const int ntasko = (done - done_prev) * nqt;
+      const int ntasko = (done - done_prev) * nq4;
       const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
       const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
       const uint32_t magic = kp.magic;     // 0x4B000000 (2^23), kept in a register
@@ -900,10 +809,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       constexpr bool kOutStatic = SMOL_OUT_STATIC == 1 || (SMOL_OUT_STATIC == 2 && K != 1);
       constexpr int kPer = kOutStatic ? 1 : SMOL_OUT_PER_GRAB;   // tasks per lane per grab (unrolled)
       for (int chunk = kOutStatic ? (tid >> 5) * 32 : 0;; chunk += kThreads * kPer) {
-        if constexpr (!kOutStatic) {
-          if (ctr[1] >= ntasko) break;           // (no atomic once the phase's tasks are gone)
-          chunk = grab_chunk(&ctr[1], lane, 32 * kPer);
-        }
+        if constexpr (!kOutStatic) chunk = grab_chunk(&ctr[1], lane, 32 * kPer);
         if (chunk >= ntasko) break;
 #pragma unroll
        for (int h = 0; h < kPer; ++h) {
@@ -912,23 +818,18 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         const bool live = t0 < ntasko;
         if (kPer == 1 && !live) break;
         const int t = live ? t0 : ntasko - 1;
-        const int rr = (int)fdiv((uint32_t)t, fd_qt);
+        const int rr = (int)fdiv((uint32_t)t, fd_q4);
         const int r = done_prev + rr;
-        const int q0 = kOutQ * (t - rr * nqt);  // first quad of the task
+        const int ox = 4 * (t - rr * nq4);
         const int2 ty = yt[r];
-        const float2 wy2 = f2(__int_as_float(ty.y));
+        const float wy = __int_as_float(ty.y);
         const uint8_t* row0 = reinterpret_cast<const uint8_t*>(rgb) + (ty.x & 0xffff);
         const uint8_t* row1 = row0 + pitch4;
-        OutT* const orow = outb + (uint32_t)(r * kp.OW);
-        const int4* xt4 = reinterpret_cast<const int4*>(xt);
-#pragma unroll
-        for (int qq = 0; qq < kOutQ; ++qq) {
-        const int q = q0 + qq;
-        if (kOutQ > 1 && q >= nq4) break;
-        const int ox = 4 * q;
         float y[3][4];
-        const int4 txa = xt4[q];          // taps of ox, ox+1
-        const int4 txb = xt4[nq4 + q];    // taps of ox+2, ox+3 (padded)
+        const int4* xt4 = reinterpret_cast<const int4*>(xt);
+        const int4 txa = xt4[ox >> 2];          // taps of ox, ox+1
+        const int4 txb = xt4[nq4 + (ox >> 2)];  // taps of ox+2, ox+3 (padded)
+        const float2 wy2 = f2(wy);
 #pragma unroll
         for (int e = 0; e < 4; e += 2) {
           // two output pixels per packed FP32x2 instruction; bytes become
@@ -954,7 +855,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
             y[ch][e + 1] = yn.y;
           }
         }
-        OutT* const ot = orow + ox;
+        OutT* const ot = outb + (uint32_t)(r * kp.OW + ox);
         if (!live) {
         } else if (vec4 && ox + 4 <= ntw) {
 #pragma unroll
@@ -981,7 +882,6 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
               else ot[e + ch * plane_sz] = y[ch][e];
             }
           }
-        }
         }
        }
       }
