@@ -81,6 +81,7 @@ class CoefImage:
     height: int
     coef: List[np.ndarray]                 # Y, Cb, Cr  (or Y only)
     qidx: Tuple[int, ...] = (0, 1, 1)
+    subsampling: int = 420                 # 420, 422, 444 (chroma W/hs x H/vs), or 400 (gray)
 
     @property
     def gray(self) -> bool:
@@ -231,13 +232,39 @@ def encode_420(rgb: np.ndarray, qtables: np.ndarray) -> CoefImage:
     return CoefImage(w, h, coef)
 
 
+# chroma subsampling factors (hs, vs) per T.81 A.1.1 (Hmax/Hc, Vmax/Vc)
+SUBSAMPLING = {420: (2, 2), 422: (2, 1), 444: (1, 1)}
+
+
+def encode_ycc(rgb: np.ndarray, qtables: np.ndarray, subsampling: int = 420) -> CoefImage:
+    """Encoder stand-in for any of the 3-component samplings: JFIF forward
+    transform, hs x vs mean chroma downsample, MCU (8 hs x 8 vs luma px)
+    edge padding, FDCT + quantize."""
+    if subsampling == 420:
+        return encode_420(rgb, qtables)
+    hs, vs = SUBSAMPLING[subsampling]
+    h, w, _ = rgb.shape
+    ycc = _rgb_to_ycbcr(rgb)
+    mh, mw = -(-h // (8 * vs)), -(-w // (8 * hs))           # MCU grid
+    planes = [_pad_edge(ycc[..., 0], 8 * vs * mh, 8 * hs * mw)]
+    ch, cw = -(-h // vs), -(-w // hs)
+    for ci in (1, 2):
+        c = _pad_edge(ycc[..., ci], vs * ch, hs * cw)
+        c = c.reshape(ch, vs, cw, hs).mean(axis=(1, 3))     # hs x vs mean downsample
+        planes.append(_pad_edge(c, 8 * mh, 8 * mw))
+    coef = [_fdct_quantize(planes[0], qtables[0]),
+            _fdct_quantize(planes[1], qtables[1]),
+            _fdct_quantize(planes[2], qtables[1])]
+    return CoefImage(w, h, coef, subsampling=subsampling)
+
+
 def encode_gray(rgb: np.ndarray, qtables: np.ndarray) -> CoefImage:
     """Encoder stand-in for a grayscale JPEG: JFIF luma of the RGB field, one
     component, 8x8 MCUs (T.81 A.2.2: non-interleaved single component)."""
     h, w, _ = rgb.shape
     Y = _rgb_to_ycbcr(rgb)[..., 0]
     Y = _pad_edge(Y, 8 * -(-h // 8), 8 * -(-w // 8))
-    return CoefImage(w, h, [_fdct_quantize(Y, qtables[0])], (0,))
+    return CoefImage(w, h, [_fdct_quantize(Y, qtables[0])], (0,), subsampling=400)
 
 
 def stress_image(rng: np.random.Generator, width: int, height: int,
@@ -268,6 +295,8 @@ def make_image(rng: np.random.Generator, width: int, height: int, qtables: np.nd
         return stress_image(rng, width, height, qtables)
     if mode == "gray":
         return encode_gray(natural_rgb(rng, width, height), qtables)
+    if mode in ("natural422", "natural444"):
+        return encode_ycc(natural_rgb(rng, width, height), qtables, int(mode[-3:]))
     raise ValueError(mode)
 
 

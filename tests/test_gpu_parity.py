@@ -335,7 +335,9 @@ def test_staging_sized_in_plan():
     c = plan.run(smol.CompactBatch(ps, imgs, qt))
     torch.cuda.synchronize()
     assert torch.equal(a, ref) and torch.equal(c, ref)
-    big = [synth.make_image(np.random.default_rng(1), 1000, 750, qt)]
+    # capacity is for max_images images of at most 500x375: four 2000x1500
+    # images' ROI rows do not fit
+    big = [synth.make_image(np.random.default_rng(1), 2000, 1500, qt)] * 4
     with pytest.raises(smol.SmolError) as e:
         plan.run(smol.CoefBatch(big, qt, location="pinned"))
     assert e.value.status == 5
