@@ -151,6 +151,8 @@ typedef struct {
                                    (SURVEY 8(d)): roi_blocks x 2 B x the K_s
                                    coefficients scale 1/k uses (64/49/25/1 at
                                    k = 1/2/4/8, reading R1), in any layout     */
+  int32_t sx0, sy0, sw, sh;     /* source window of the resize (decoded px): the
+                                   whole image, or the ROI rectangle's window   */
   int64_t storage_coef_bytes;   /* bytes the plan's layout stores for those
                                    blocks: 128 (DENSE64; 32 at k = 8, the DC's
                                    sector) or 128/104/56/2 (PACKED)            */

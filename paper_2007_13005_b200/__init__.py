@@ -54,7 +54,7 @@ def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: 
 def batch_for(params: Params, images, qtables, **kw) -> "CoefBatch":
     """CoefBatch in the layout the plan's params expect."""
     return CoefBatch(images, qtables, layout="packed" if params.layout == SMOL_LAYOUT_PACKED else "dense",
-                     scale_denom=params.scale_denom, **kw)
+                     scale_denom=params.scale_denom, truncated=params.idct_def == SMOL_IDCT_TRUNCATED, **kw)
 
 
 def params_from_config(cfg, **kw) -> Params:
@@ -66,12 +66,18 @@ def params_from_config(cfg, **kw) -> Params:
     return make_params(**args)
 
 
-def _desc_for(width, height, blocks_w, blocks_h, qidx=(0, 1, 1), roi=None, strides=None) -> ImageDesc:
-    """Descriptor of a 4:2:0 image (3 planes) or a grayscale one (1 plane:
-    subsampling 400, chroma fields zero)."""
+def _desc_for(width, height, blocks_w, blocks_h, qidx=(0, 1, 1), roi=None, strides=None,
+              subsampling=None, roi_rect=None) -> ImageDesc:
+    """Descriptor of a 3-plane image (4:2:0 unless `subsampling` says 422 /
+    444) or a grayscale one (1 plane: subsampling 400, chroma fields zero).
+    roi: crop-window origin (left, top) in resized coordinates; roi_rect:
+    (x, y, w, h) ROI rectangle in SOF pixels."""
     d = ImageDesc()
     gray = len(blocks_w) == 1
-    d.width, d.height, d.subsampling = width, height, 400 if gray else 420
+    d.width, d.height = width, height
+    d.subsampling = 400 if gray else (subsampling or 420)
+    if roi_rect is not None:
+        d.roi_x, d.roi_y, d.roi_w, d.roi_h = roi_rect
     d.qtable = (ctypes.c_int32 * 3)(*(tuple(qidx) + (0, 0, 0))[:3])
     for c in range(len(blocks_w)):
         d.blocks_w[c], d.blocks_h[c] = blocks_w[c], blocks_h[c]
@@ -80,11 +86,17 @@ def _desc_for(width, height, blocks_w, blocks_h, qidx=(0, 1, 1), roi=None, strid
     return d
 
 
-def geometry(params: Params, width: int, height: int, roi=None, gray: bool = False) -> dict:
+SUBSAMPLING = {420: (2, 2), 422: (2, 1), 444: (1, 1)}
+
+
+def geometry(params: Params, width: int, height: int, roi=None, gray: bool = False,
+             subsampling: int = 420, roi_rect=None) -> dict:
     """Host-only geometry of one image (smol_debug_geometry)."""
     n = 1 if gray else 3
-    d = _desc_for(width, height, [(width + 7) // 8, (width + 15) // 16, (width + 15) // 16][:n],
-                  [(height + 7) // 8, (height + 15) // 16, (height + 15) // 16][:n], roi=roi)
+    hs, vs = SUBSAMPLING.get(subsampling, (2, 2))
+    bw = [(width + 7) // 8] + [-(-width // (8 * hs))] * 2
+    bh = [(height + 7) // 8] + [-(-height // (8 * vs))] * 2
+    d = _desc_for(width, height, bw[:n], bh[:n], roi=roi, subsampling=subsampling, roi_rect=roi_rect)
     g = Geometry()
     check(lib().smol_debug_geometry(ctypes.byref(params), ctypes.byref(d), ctypes.byref(g)))
     return g.as_dict()
@@ -103,7 +115,8 @@ class CoefBatch:
 
     def __init__(self, images: Sequence, qtables: np.ndarray, location: str = "device",
                  device: Optional[int] = None, rois: Optional[Sequence] = None,
-                 layout: str = "dense", scale_denom: int = 1):
+                 layout: str = "dense", scale_denom: int = 1, roi_rects: Optional[Sequence] = None,
+                 truncated: bool = False):
         import torch
         self.n = len(images)
         k = scale_denom if layout == "packed" else 1
@@ -112,7 +125,7 @@ class CoefBatch:
         for im in images:
             key = id(im)
             if key not in cache:
-                cache[key] = [pack_plane(np.ascontiguousarray(c, dtype=np.int16), k) for c in im.coef]
+                cache[key] = [pack_plane(np.ascontiguousarray(c, dtype=np.int16), k, truncated) for c in im.coef]
             planes.append(cache[key])
         sizes = [[int(p.size) for p in ps] for ps in planes]
         total = int(sum(sum(s) for s in sizes))
@@ -144,7 +157,9 @@ class CoefBatch:
             roi = rois[i] if rois is not None else None
             d = _desc_for(im.width, im.height, [c.shape[1] for c in im.coef],
                           [c.shape[0] for c in im.coef], tuple(im.qidx), roi,
-                          strides=[2 * p.shape[1] for p in planes[i]])
+                          strides=[2 * p.shape[1] for p in planes[i]],
+                          subsampling=getattr(im, "subsampling", 420),
+                          roi_rect=None if roi_rects is None else roi_rects[i])
             for ci in range(len(im.coef)):
                 d.coef[ci] = base + 2 * oo[ci]
             self.descs[i] = d
@@ -155,7 +170,7 @@ class CoefBatch:
         self.desc.n_qtables = int(qtables.shape[0])
 
 
-def compact_encode(params: Params, im, roi=None) -> np.ndarray:
+def compact_encode(params: Params, im, roi=None, roi_rect=None) -> np.ndarray:
     """One image's compact record (smol_compact_encode, host only) as uint8.
 
     im: object with .width, .height, .coef (3 int16 [bh][bw][64]) and .qidx;
@@ -163,9 +178,11 @@ def compact_encode(params: Params, im, roi=None) -> np.ndarray:
     decoder holds), then the C encoder keeps the ROI blocks' nonzero used
     coefficients (include/smol_preproc.h "Compact coefficient transport")."""
     k = params.scale_denom if params.layout == SMOL_LAYOUT_PACKED else 1
-    planes = [pack_plane(np.ascontiguousarray(c, dtype=np.int16), k) for c in im.coef]
+    planes = [pack_plane(np.ascontiguousarray(c, dtype=np.int16), k, params.idct_def == SMOL_IDCT_TRUNCATED)
+              for c in im.coef]
     d = _desc_for(im.width, im.height, [c.shape[1] for c in im.coef], [c.shape[0] for c in im.coef],
-                  tuple(im.qidx), roi, strides=[2 * p.shape[1] for p in planes])
+                  tuple(im.qidx), roi, strides=[2 * p.shape[1] for p in planes],
+                  subsampling=getattr(im, "subsampling", 420), roi_rect=roi_rect)
     for ci in range(len(planes)):
         d.coef[ci] = planes[ci].ctypes.data
     n = ctypes.c_int64()
@@ -183,16 +200,18 @@ class CompactBatch:
     for `params` (layout, scale and crop fix the ROI and element set)."""
 
     def __init__(self, params: Params, images: Sequence, qtables: np.ndarray, location: str = "pinned",
-                 device: Optional[int] = None, rois: Optional[Sequence] = None):
+                 device: Optional[int] = None, rois: Optional[Sequence] = None,
+                 roi_rects: Optional[Sequence] = None):
         import torch
         self.n = len(images)
         cache = {}
         recs = []
         for i, im in enumerate(images):
             roi = rois[i] if rois is not None else None
-            key = (id(im), roi)
+            rr = roi_rects[i] if roi_rects is not None else None
+            key = (id(im), roi, rr)
             if key not in cache:
-                cache[key] = compact_encode(params, im, roi)
+                cache[key] = compact_encode(params, im, roi, rr)
             recs.append(cache[key])
         offs, o = [], 0
         for r in recs:
@@ -216,10 +235,12 @@ class CompactBatch:
         for i, (im, oo) in enumerate(zip(images, offs)):
             ci = CompactImage()
             ci.width, ci.height = im.width, im.height
-            ci.subsampling = 400 if len(im.coef) == 1 else 420
+            ci.subsampling = 400 if len(im.coef) == 1 else getattr(im, "subsampling", 420)
             ci.qtable = (ctypes.c_int32 * 3)(*(tuple(im.qidx) + (0, 0, 0))[:3])
             roi = rois[i] if rois is not None else None
             ci.roi_left, ci.roi_top = roi if roi is not None else (-1, -1)
+            if roi_rects is not None and roi_rects[i] is not None:
+                ci.roi_x, ci.roi_y, ci.roi_w, ci.roi_h = roi_rects[i]
             ci.offset = oo
             self.images[i] = ci
         self.desc = CompactBatchDesc()

@@ -81,8 +81,9 @@ class Geometry(ctypes.Structure):
                                                "OW", "OH", "lx0", "lx1", "ly0", "ly1",
                                                "cx0", "cx1", "cy0", "cy1")] +
                 [(n, ctypes.c_int32 * 3) for n in ("bx0", "bx1", "by0", "by1")] +
-                [("roi_blocks", ctypes.c_int64), ("roi_coef_bytes", ctypes.c_int64),
-                 ("storage_coef_bytes", ctypes.c_int64)])
+                [("roi_blocks", ctypes.c_int64), ("roi_coef_bytes", ctypes.c_int64)] +
+                [(n, ctypes.c_int32) for n in ("sx0", "sy0", "sw", "sh")] +
+                [("storage_coef_bytes", ctypes.c_int64)])
 
     def as_dict(self):
         d = {}

@@ -19,12 +19,21 @@ struct CompactHeader {            // the 64-byte record header
 static_assert(sizeof(CompactHeader) == kCompactHeader, "compact header is 64 bytes");
 
 // Bit e set <=> element e of a stored block (layout DENSE64 or PACKED at
-// scale 1/K) enters the decode at that scale (reading R1: the box-averaged
+// scale 1/K) enters the decode at that scale (Definition B: u, v < 8/K;
+// Definition A, reading R1: the box-averaged
 // basis of frequency u vanishes exactly for u = 4 at K = 2, u in {2, 4, 6} at
 // K = 4, u > 0 at K = 8).  PACKED blocks store exactly the used set (49 / 25
 // / 1 elements) followed by zero padding.
-inline uint64_t used_mask(int K, bool packed) {
+inline uint64_t used_mask(int K, bool packed, bool db = false) {
   if (K == 1) return ~0ull;
+  if (db) {                       // Definition B (R16): the top-left N x N, N = 8/K
+    const int N = 8 / K;
+    if (packed) return N * N >= 64 ? ~0ull : (1ull << (N * N)) - 1;
+    uint64_t m = 0;
+    for (int v = 0; v < N; ++v)
+      for (int u = 0; u < N; ++u) m |= 1ull << (v * 8 + u);
+    return m;
+  }
   if (packed) return K == 2 ? (1ull << 49) - 1 : K == 4 ? (1ull << 25) - 1 : 1ull;
   auto keep = [K](int f) {
     return K == 2 ? f != 4 : K == 4 ? (f == 0 || (f & 1)) : f == 0;

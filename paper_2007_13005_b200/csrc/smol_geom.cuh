@@ -42,6 +42,8 @@ struct __align__(16) DevImage {
   int32_t Wr, Hr;           // resized size
   int32_t left, top;        // crop origin in resized coordinates
   int32_t gray;             // 1: one component (subsampling 400): no chroma blocks, Cb = Cr = 128
+  int32_t sx0, sy0, sw, sh; // source window of the resize in decoded luma px: the whole
+                            // image (0, 0, Wd, Hd), or an ROI rectangle's window (R15)
 };
 
 // Reading R9: the half-pixel bilinear source index of destination index d
@@ -65,6 +67,18 @@ SMOL_HD void src_tap(int d, int in, int out, int& i0, int& i1, float& w) {
   }
   if (i0 > in - 1) i0 = in - 1;
   i1 = imin(i0 + 1, in - 1);
+}
+
+// Taps of the resize of an image's source window (the whole decoded image,
+// or an ROI rectangle's window): R9 within the window, then offset to
+// decoded coordinates.
+SMOL_HD void src_tap_x(const DevImage& im, int d, int& i0, int& i1, float& w) {
+  src_tap(d, im.sw, im.Wr, i0, i1, w);
+  i0 += im.sx0; i1 += im.sx0;
+}
+SMOL_HD void src_tap_y(const DevImage& im, int d, int& i0, int& i1, float& w) {
+  src_tap(d, im.sh, im.Hr, i0, i1, w);
+  i0 += im.sy0; i1 += im.sy0;
 }
 
 SMOL_HD int align16(int x) { return (x + 15) & ~15; }
@@ -111,10 +125,10 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   const int P = 8 / K;
   int a, b; float w;
   L.oy0 = oy0; L.oy1 = oy1; L.ox0 = ox0; L.ox1 = ox1;
-  src_tap(im.left + ox0, im.Wd, im.Wr, L.lx0, b, w);
-  src_tap(im.left + ox1 - 1, im.Wd, im.Wr, a, L.lx1, w);
-  src_tap(im.top + oy0, im.Hd, im.Hr, L.ly0, b, w);
-  src_tap(im.top + oy1 - 1, im.Hd, im.Hr, a, L.ly1, w);
+  src_tap_x(im, im.left + ox0, L.lx0, b, w);
+  src_tap_x(im, im.left + ox1 - 1, a, L.lx1, w);
+  src_tap_y(im, im.top + oy0, L.ly0, b, w);
+  src_tap_y(im, im.top + oy1 - 1, a, L.ly1, w);
   // chroma rows/cols used by the centred triangle filter of luma rows
   // [ly0, ly1]: floor((ly0-1)/2) .. floor((ly1+1)/2), clamped (reading R2)
   L.cy0 = imax(0, (L.ly0 - 1) >> 1);

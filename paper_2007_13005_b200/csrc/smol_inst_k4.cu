@@ -11,24 +11,25 @@ template <int NT> struct CfgYP {
   static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
 };
 
-template <bool PK, int NT>
+template <bool PK, int NT, bool DB = false>
 KernelFn pick(bool f16, bool dbg) {
   constexpr int YP = CfgYP<NT>::yp;
-  if (dbg) return f16 ? smol_fused_kernel<4, true, true, PK, NT, YP> : smol_fused_kernel<4, false, true, PK, NT, YP>;
-  return f16 ? smol_fused_kernel<4, true, false, PK, NT, YP> : smol_fused_kernel<4, false, false, PK, NT, YP>;
+  if (dbg) return f16 ? smol_fused_kernel<4, true, true, PK, NT, YP, DB> : smol_fused_kernel<4, false, true, PK, NT, YP, DB>;
+  return f16 ? smol_fused_kernel<4, true, false, PK, NT, YP, DB> : smol_fused_kernel<4, false, false, PK, NT, YP, DB>;
 }
 
 template <int NT>
-KernelFn pick_nt(bool f16, bool dbg, bool packed) {
+KernelFn pick_nt(bool f16, bool dbg, bool packed, bool db) {
+  if (db) return packed ? pick<true, NT, true>(f16, dbg) : pick<false, NT, true>(f16, dbg);
   return packed ? pick<true, NT>(f16, dbg) : pick<false, NT>(f16, dbg);
 }
 
 }  // namespace
 
-KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt) {
-  return nt == kThreadsNarrow ? pick_nt<kThreadsNarrow>(f16, dbg, packed)
-       : nt == kThreadsTiny   ? pick_nt<kThreadsTiny>(f16, dbg, packed)
-                              : pick_nt<kThreadsWide>(f16, dbg, packed);
+KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt, bool db) {
+  return nt == kThreadsNarrow ? pick_nt<kThreadsNarrow>(f16, dbg, packed, db)
+       : nt == kThreadsTiny   ? pick_nt<kThreadsTiny>(f16, dbg, packed, db)
+                              : pick_nt<kThreadsWide>(f16, dbg, packed, db);
 }
 
 cudaError_t upload_basis_k4(const Basis& b) { return cudaMemcpyToSymbol(c_basis, &b, sizeof(Basis)); }

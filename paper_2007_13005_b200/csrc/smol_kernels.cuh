@@ -233,9 +233,14 @@ __device__ __forceinline__ void idct_cols(const float (&m)[8][8], uint32_t (&px)
 //   K=2: u,v in {0,1,2,3,5,6,7}  49 -> 52 int16 (104 B)
 //   K=4: u,v in {0,1,3,5,7}      25 -> 28 int16 ( 56 B)
 //   K=8: DC only                  1 int16      (  2 B)
-template <int K, bool PACKED>
+// Definition B (reading R16, plan option SMOL_IDCT_TRUNCATED) uses only the
+// top-left N x N coefficients (N = 8/K); its PACKED blocks hold exactly
+// those, row-major: K=2: 16 int16 (32 B), K=4: 4 int16 (8 B), K=8: DC.
+template <int K, bool PACKED, bool DB = false>
 struct BlockFmt {
-  static constexpr int kElems = !PACKED ? 64 : (K == 1 ? 64 : K == 2 ? 52 : K == 4 ? 28 : 1);
+  static constexpr int kElems = !PACKED ? 64
+                              : DB ? (8 / K) * (8 / K)
+                                   : (K == 1 ? 64 : K == 2 ? 52 : K == 4 ? 28 : 1);
 };
 __host__ __device__ constexpr int packed_set(int K, int i) {   // i-th index of the K's set
   return K == 2 ? (i < 4 ? i : i + 1) : K == 4 ? (i == 0 ? 0 : 2 * i - 1) : i;
@@ -251,11 +256,62 @@ __device__ __forceinline__ float half_of(const uint32_t (&w)[NWORDS], int e) {
 // (little-endian bytes, 2 words per row at K = 1).  `act` = this lane has a
 // block; every lane of the warp must call it (warp reductions pick the
 // nonzero row extent).
-template <int K, bool PACKED>
+// Definition B, N = 8/K: N-point IDCT with b_N(u,x) = sqrt2 C(u)
+// cos((2x+1) u pi / 2N): b_4(1,.) = (c2, c6, -c6, -c2), b_4(3,.) = (c6, -c2,
+// c2, -c6) (c_k = sqrt2 cos(k pi/16) of the 8-point basis), b_4(2,.) =
+// (1,-1,-1,1) and b_2(1,.) = (1,-1) exactly, so DC and u = N/2 inputs are
+// transformed exactly (reading R3).
+template <int N>
+__device__ __forceinline__ void idct_trunc(const float (&d)[N], float (&o)[N]) {
+  if constexpr (N == 4) {
+    const float e0 = d[0] + d[2], e1 = d[0] - d[2];
+    const float od0 = fmaf(d[3], kC6, d[1] * kC2);
+    const float od1 = fmaf(d[3], -kC2, d[1] * kC6);
+    o[0] = e0 + od0; o[3] = e0 - od0;
+    o[1] = e1 + od1; o[2] = e1 - od1;
+  } else {
+    o[0] = d[0] + d[1];
+    o[1] = d[0] - d[1];
+  }
+}
+
+template <int K, bool PACKED, bool DB = false>
 __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const float* q,
                                              uint32_t (&px)[8][2]) {
   constexpr int P = 8 / K;
-  if constexpr (K == 8) {
+  if constexpr (DB && (K == 2 || K == 4)) {
+    // Definition B (reading R16): P-point IDCT of the top-left P x P
+    // coefficients (Q/8 folded in q: v = 1/8 sum D b_P b_P)
+    float g[P][P];
+#pragma unroll
+    for (int v = 0; v < P; ++v) {
+      float d[P];
+      if constexpr (K == 2) {
+        const int2 r = act ? __ldg(reinterpret_cast<const int2*>(src + (PACKED ? 4 * v : 8 * v))) : make_int2(0, 0);
+        d[0] = (float)(int16_t)(r.x & 0xffff); d[1] = (float)(r.x >> 16);
+        d[2] = (float)(int16_t)(r.y & 0xffff); d[3] = (float)(r.y >> 16);
+      } else {
+        const int r = act ? __ldg(reinterpret_cast<const int*>(src + (PACKED ? 2 * v : 8 * v))) : 0;
+        d[0] = (float)(int16_t)(r & 0xffff); d[1] = (float)(r >> 16);
+      }
+#pragma unroll
+      for (int u = 0; u < P; ++u) d[u] *= q[v * 8 + u];
+      if (v == 0) d[0] += 128.5f;           // level shift + rounding offset (b_P(0, .) = 1 exactly)
+      idct_trunc<P>(d, g[v]);
+    }
+#pragma unroll
+    for (int x = 0; x < P; ++x) {
+      float col[P], f[P];
+#pragma unroll
+      for (int v = 0; v < P; ++v) col[v] = g[v][x];
+      idct_trunc<P>(col, f);
+#pragma unroll
+      for (int y = 0; y < P; ++y) {
+        const uint32_t b = floor_u8(f[y]);
+        px[y][0] = (x == 0) ? b : (px[y][0] | (b << (8 * x)));
+      }
+    }
+  } else if constexpr (K == 8) {
     px[0][0] = act ? round_u8((float)__ldg(src) * q[0]) : 0u;
   } else if constexpr (K == 1) {
     int4 raw[8];
@@ -418,7 +474,7 @@ __device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
   return __shfl_sync(0xffffffffu, chunk, 0);
 }
 
-template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB>
 __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const int oy0, const int oy1,
                                        const int ox0, const int ox1) {
   constexpr int P = 8 / K;                 // decoded samples per block side
@@ -459,7 +515,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   const int nq4 = (ntw + 3) >> 2;
   for (int i = tid; i < 4 * nq4; i += kThreads) {
     int i0, i1; float w;
-    src_tap(im.left + ox0 + min(i, ntw - 1), im.Wd, im.Wr, i0, i1, w);
+    src_tap_x(im, im.left + ox0 + min(i, ntw - 1), i0, i1, w);
     int* e = reinterpret_cast<int*>(xt) + (((i >> 1) & 1) * nq4 + (i >> 2)) * 4 + (i & 1);
     e[0] = (i0 - L.rgb_x0) * 4;
     e[2] = __float_as_int(i1 == i0 ? 0.f : w);
@@ -468,7 +524,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   // (row i0 + 1 is at +pitch4: the ring's guard slot mirrors slot 0)
   for (int i = tid; i < nth; i += kThreads) {
     int i0, i1; float w;
-    src_tap(im.top + oy0 + i, im.Hd, im.Hr, i0, i1, w);
+    src_tap_y(im, im.top + oy0 + i, i0, i1, w);
     yt[i] = make_int2((rgb_slot(i0) * pitch4) | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
   }
   if (im.gray)       // grayscale: neutral chroma everywhere in the rings (read only by colour)
@@ -512,9 +568,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         bcol = tt - brow * nbxc;
         brow += cb0;
       }
-      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * BlockFmt<K, PACKED>::kElems;
+      const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * BlockFmt<K, PACKED, DB>::kElems;
       uint32_t px[8][2];
-      decode_block<K, PACKED>(act, src, qf + c * 64, px);
+      decode_block<K, PACKED, DB>(act, src, qf + c * 64, px);
       if (!act) continue;
       if (c == 0) {
         uint8_t* d = yring + bcol * P;
@@ -605,7 +661,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         int c = 0, brow = yb0 + k;
         if (k >= ny) { c = 1 + (k - ny >= nc); brow = cb0 + (k - ny) - (c - 1) * nc; }
         // 16-B aligned segment [bx0 * S, (bx1 + 1) * S) of the (16-B padded) block row
-        constexpr int SB = BlockFmt<K, PACKED>::kElems * 2;
+        constexpr int SB = BlockFmt<K, PACKED, DB>::kElems * 2;
         const uint32_t lo = ((uint32_t)L.bx0[c] * SB) & ~15u, hi = ((uint32_t)(L.bx1[c] + 1) * SB + 15u) & ~15u;
         const char* p = reinterpret_cast<const char*>(im.coef[c] + (size_t)brow * im.stride[c]) + lo;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(hi - lo) : "memory");
@@ -903,7 +959,8 @@ __host__ __device__ constexpr int kCtasPerSm(int threads) {
 }
 
 // The fused kernel: one (image, row band, column band) tile per CTA.
-template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP>
+// DB: Definition B reduced-scale IDCT (K = 2, 4 only; equal to A at 1, 1/8).
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm<K>(kThreads))
 smol_fused_kernel(const __grid_constant__ KParams kp) {
   int n, oy0, oy1, ox0, ox1;
@@ -918,7 +975,7 @@ smol_fused_kernel(const __grid_constant__ KParams kp) {
     oy0 = trow * kp.tile_rows; oy1 = min(kp.OH, oy0 + kp.tile_rows);
     ox0 = tcol * kp.tile_cols; ox1 = min(kp.OW, ox0 + kp.tile_cols);
   }
-  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP>(kp, n, oy0, oy1, ox0, ox1);
+  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP, DB>(kp, n, oy0, oy1, ox0, ox1);
 }
 
 }  // namespace smol

@@ -11,11 +11,12 @@ struct Basis;
 using KernelFn = void (*)(const KParams);
 
 // fused kernel instantiation for (scale 1/K, output dtype, debug store,
-// packed layout, threads per CTA); K fixed per unit
-KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt);
-KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt);
-KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt);
-KernelFn select_fused_k8(bool f16, bool dbg, bool packed, int nt);
+// packed layout, threads per CTA, Definition B IDCT); K fixed per unit
+// (db only exists at K = 2, 4: at 1 and 1/8 the definitions coincide)
+KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt, bool db);
+KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db);
+KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt, bool db);
+KernelFn select_fused_k8(bool f16, bool dbg, bool packed, int nt, bool db);
 // upload the basis constants into each unit's constant bank (current device)
 cudaError_t upload_basis_k1(const Basis& b);
 cudaError_t upload_basis_k2(const Basis& b);

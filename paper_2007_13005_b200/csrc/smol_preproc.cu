@@ -137,8 +137,6 @@ int32_t validate_params(const smol_preproc_params* p) {
     return fail(SMOL_ERR_INVALID, "params.tile_rows=%d", p->tile_rows);
   if (p->idct_def != SMOL_IDCT_BOX_MEAN && p->idct_def != SMOL_IDCT_TRUNCATED)
     return fail(SMOL_ERR_INVALID, "params.idct_def=%d", p->idct_def);
-  if (p->idct_def == SMOL_IDCT_TRUNCATED)
-    return fail(SMOL_ERR_UNSUPPORTED, "params.idct_def=TRUNCATED not built");
   if (p->max_width < 0 || p->max_height < 0 || (p->max_width > 0) != (p->max_height > 0) ||
       p->max_width > 65535 || p->max_height > 65535)
     return fail(SMOL_ERR_INVALID, "params.max_width/max_height=%d/%d: both in [1, 65535] or both 0",
@@ -146,13 +144,19 @@ int32_t validate_params(const smol_preproc_params* p) {
   return SMOL_OK;
 }
 
-// coefficients per block the scale uses (reading R1: the box-averaged basis
-// of the others is exactly zero): 64 / 49 / 25 / 1 at 1, 1/2, 1/4, 1/8
-int used_coefs(int K) { return K == 1 ? 64 : K == 2 ? 49 : K == 4 ? 25 : 1; }
+// coefficients per block the scale uses: Definition A (reading R1: the
+// box-averaged basis of the others is exactly zero) 64 / 49 / 25 / 1 at 1,
+// 1/2, 1/4, 1/8; Definition B (R16) the top-left (8/k)^2: 64 / 16 / 4 / 1
+int used_coefs(int K, int def) {
+  if (def == SMOL_IDCT_TRUNCATED) return (8 / K) * (8 / K);
+  return K == 1 ? 64 : K == 2 ? 49 : K == 4 ? 25 : 1;
+}
 
-// int16 elements per coefficient block of a layout at scale 1/K (smol_kernels.cuh BlockFmt)
-int block_elems(int K, int layout) {
+// int16 elements per coefficient block of a layout at scale 1/K
+// (smol_kernels.cuh BlockFmt)
+int block_elems(int K, int layout, int def) {
   if (layout != SMOL_LAYOUT_PACKED || K == 1) return 64;
+  if (def == SMOL_IDCT_TRUNCATED) return (8 / K) * (8 / K);
   return K == 2 ? 52 : K == 4 ? 28 : 1;
 }
 
@@ -166,8 +170,6 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
     return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d > 65535 (JPEG limit)", idx, d->width, d->height);
   if (d->subsampling != 420 && d->subsampling != 400)
     return fail(SMOL_ERR_UNSUPPORTED, "image %d: subsampling=%d (420 or 400 only)", idx, d->subsampling);
-  if (d->roi_w != 0 || d->roi_h != 0 || d->roi_x != 0 || d->roi_y != 0)
-    return fail(SMOL_ERR_UNSUPPORTED, "image %d: ROI rectangle not built", idx);
   g.gray = d->subsampling == 400;
   g.Wd = ceil_div(d->width, k);
   g.Hd = ceil_div(d->height, k);
@@ -182,6 +184,27 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
     g.Wr = p->resize_w; g.Hr = p->resize_h;
   }
   if (p->crop_w > 0) { OW = p->crop_w; OH = p->crop_h; } else { OW = g.Wr; OH = g.Hr; }
+  g.sx0 = 0; g.sy0 = 0; g.sw = g.Wd; g.sh = g.Hd;
+  if (d->roi_w != 0 || d->roi_h != 0 || d->roi_x != 0 || d->roi_y != 0) {
+    // ROI rectangle (reading R15): its decoded
+    // window [floor(x/k), ceil((x+w)/k)) x [floor(y/k), ceil((y+h)/k)) is
+    // resized straight to the plan's output size (no crop)
+    if (d->roi_w <= 0 || d->roi_h <= 0 || d->roi_x < 0 || d->roi_y < 0 ||
+        (long long)d->roi_x + d->roi_w > d->width || (long long)d->roi_y + d->roi_h > d->height)
+      return fail(SMOL_ERR_INVALID, "image %d: ROI rectangle (%d,%d,%d,%d) outside the %dx%d image", idx,
+                  d->roi_x, d->roi_y, d->roi_w, d->roi_h, d->width, d->height);
+    if (d->roi_left >= 0 || d->roi_top >= 0)
+      return fail(SMOL_ERR_INVALID, "image %d: ROI rectangle and crop origin both given", idx);
+    const int plan_ow = p->crop_w > 0 ? p->crop_w : p->resize_w;
+    const int plan_oh = p->crop_w > 0 ? p->crop_h : p->resize_h;
+    g.sx0 = d->roi_x / k;
+    g.sy0 = d->roi_y / k;
+    g.sw = ceil_div(d->roi_x + d->roi_w, k) - g.sx0;
+    g.sh = ceil_div(d->roi_y + d->roi_h, k) - g.sy0;
+    g.Wr = plan_ow; g.Hr = plan_oh;
+    g.left = 0; g.top = 0;
+    return SMOL_OK;
+  }
   if (OW > g.Wr || OH > g.Hr)
     return fail(SMOL_ERR_INVALID, "image %d: crop %dx%d larger than resized %dx%d", idx, OW, OH, g.Wr, g.Hr);
   if (d->roi_left < 0 && d->roi_top < 0) {
@@ -210,11 +233,12 @@ inline void copy_geometry(const DevImage& from, DevImage& g) {
   g.Wd = from.Wd; g.Hd = from.Hd; g.Wc = from.Wc; g.Hc = from.Hc;
   g.Wr = from.Wr; g.Hr = from.Hr; g.left = from.left; g.top = from.top;
   g.gray = from.gray;
+  g.sx0 = from.sx0; g.sy0 = from.sy0; g.sw = from.sw; g.sh = from.sh;
 }
 inline bool same_layout_inputs(const DevImage& a, const DevImage& b) {
   return a.Wd == b.Wd && a.Hd == b.Hd && a.Wc == b.Wc && a.Hc == b.Hc && a.Wr == b.Wr && a.Hr == b.Hr &&
          a.left == b.left && a.top == b.top && a.nbw[0] == b.nbw[0] && a.nbw[1] == b.nbw[1] &&
-         a.gray == b.gray;
+         a.gray == b.gray && a.sx0 == b.sx0 && a.sy0 == b.sy0 && a.sw == b.sw && a.sh == b.sh;
 }
 
 int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, int idx, int n_qtables,
@@ -238,7 +262,7 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
     if (d->blocks_w[c] < need_w[c] || d->blocks_h[c] < need_h[c])
       return fail(SMOL_ERR_INVALID, "image %d: blocks_w[%d]=%d / blocks_h[%d]=%d < required %d / %d", idx, c,
                   d->blocks_w[c], c, d->blocks_h[c], need_w[c], need_h[c]);
-    const int bb = 2 * block_elems(p->scale_denom, p->layout);
+    const int bb = 2 * block_elems(p->scale_denom, p->layout, p->idct_def);
     if (d->row_stride_bytes[c] < d->blocks_w[c] * bb || d->row_stride_bytes[c] % 16)
       return fail(SMOL_ERR_INVALID, "image %d: row_stride_bytes[%d]=%d (need >= %d, multiple of 16)", idx, c,
                   d->row_stride_bytes[c], d->blocks_w[c] * bb);
@@ -273,12 +297,12 @@ int auto_tile_rows(int OH, int n_images, int slots) {
 int Cfg_yp(int nt) { return nt == kThreadsNarrow ? kYPNarrow : nt == kThreadsTiny ? kYPTiny : kYPWide; }
 
 // scale 1 has no packed variant: the packed layout of scale 1 is DENSE64
-KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt) {
+KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt, bool db) {
   switch (K) {
-    case 1: return select_fused_k1(f16, dbg, packed, nt);
-    case 2: return select_fused_k2(f16, dbg, packed, nt);
-    case 4: return select_fused_k4(f16, dbg, packed, nt);
-    default: return select_fused_k8(f16, dbg, packed, nt);
+    case 1: return select_fused_k1(f16, dbg, packed, nt, db);
+    case 2: return select_fused_k2(f16, dbg, packed, nt, db);
+    case 4: return select_fused_k4(f16, dbg, packed, nt, db);
+    default: return select_fused_k8(f16, dbg, packed, nt, db);
   }
 }
 
@@ -379,6 +403,7 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
   out->Wr = g.Wr; out->Hr = g.Hr; out->left = g.left; out->top = g.top;
   out->OW = params->crop_w > 0 ? params->crop_w : g.Wr;
   out->OH = params->crop_w > 0 ? params->crop_h : g.Hr;
+  out->sx0 = g.sx0; out->sy0 = g.sy0; out->sw = g.sw; out->sh = g.sh;
   g.nbw[0] = ceil_div(image->width, 8);
   g.nbw[1] = g.nbw[2] = ceil_div(image->width, 16);
   TileLayout L;
@@ -393,8 +418,8 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
   // scale uses per ROI block (reading R1: 64 / 49 / 25 / 1), 2 B each, in any
   // layout; storage bytes: what the layout holds for those blocks (PACKED
   // pads to 8 B; dense-64 at scale 1/8 reads only the DC's 32-B sector)
-  out->roi_coef_bytes = out->roi_blocks * 2 * used_coefs(params->scale_denom);
-  const int bb = 2 * block_elems(params->scale_denom, params->layout);
+  out->roi_coef_bytes = out->roi_blocks * 2 * used_coefs(params->scale_denom, params->idct_def);
+  const int bb = 2 * block_elems(params->scale_denom, params->layout, params->idct_def);
   out->storage_coef_bytes =
       out->roi_blocks * ((params->scale_denom == 8 && params->layout == SMOL_LAYOUT_DENSE64) ? 32 : bb);
   return SMOL_OK;
@@ -459,11 +484,11 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     // max_width x max_height (worst case: every block of the image, 4:4:4),
     // so run_host / run_compact never allocate: dense ROI rows (both slots)
     // and compact records (units <= 2 per used element, plus the tables)
-    const int E = block_elems(params->scale_denom, params->layout);
+    const int E = block_elems(params->scale_denom, params->layout, params->idct_def);
     const long long bw = ceil_div(params->max_width, 8), bh = ceil_div(params->max_height, 8);
     const long long rows = 3 * bh, blocks = 3 * bw * bh;
     const size_t stage_img = (size_t)(2 * (blocks * E + rows * 16 + 3 * 8));
-    const size_t rec_img = (size_t)compact_record_bytes(blocks, rows, 2LL * blocks * used_coefs(params->scale_denom));
+    const size_t rec_img = (size_t)compact_record_bytes(blocks, rows, 2LL * blocks * used_coefs(params->scale_denom, params->idct_def));
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
       pl->stage_cap[i] = stage_img * (size_t)max_images;
       e = cudaMalloc(&pl->stage[i], pl->stage_cap[i] + 256);
@@ -484,7 +509,8 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     for (int v = 0; v < 6 && e == cudaSuccess; ++v) {
       const int dbg = v & 1, nt = v < 2 ? kThreadsWide : v < 4 ? kThreadsNarrow : kThreadsTiny;
       cudaFuncAttributes fa;
-      KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED, nt);
+      KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED, nt,
+                                  params->idct_def == SMOL_IDCT_TRUNCATED);
       e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) break;
       const int dyn = pl->smem_optin - (int)fa.sharedSizeBytes;
@@ -671,9 +697,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     const DevImage* prev = nullptr;
     for (int i = 0; i < n_images; ++i) {
       const DevImage& g = h[i];
-      if (prev && g.Wd == prev->Wd && g.Hd == prev->Hd && g.left == prev->left && g.top == prev->top &&
-          g.nbw[0] == prev->nbw[0] && g.nbw[1] == prev->nbw[1])
-        continue;
+      if (prev && same_layout_inputs(g, *prev)) continue;
       for (int t = 0; t < ntiles; ++t)
         for (int u = 0; u < n_col_tiles; ++u) {
           TileLayout L;
@@ -709,7 +733,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     }
   }
   // resident CTAs per SM of the chosen kernel at this shared-memory size
-  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt);
+  KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt,
+                              pl->p.idct_def == SMOL_IDCT_TRUNCATED);
   int occ = 768 / nt;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
@@ -781,7 +806,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     const int sl = pl->stage_slot;
     pl->stage_slot ^= 1;
     SMOL_CUDA(cudaEventSynchronize(pl->stage_free[sl]));     // host side: descriptor slot reusable
-    const int E = block_elems(K, pl->p.layout);
+    const int E = block_elems(K, pl->p.layout, pl->p.idct_def);
     GatherDesc* hg = pl->h_gather + (size_t)sl * pl->max_images;
     GatherDesc* dg = pl->d_gather + (size_t)sl * pl->max_images;
     ExpandDesc* he = pl->h_expand + (size_t)sl * pl->max_images;
@@ -942,7 +967,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // rows, i.e. under vertical magnification (measured r02: c3b 0.0556 ->
   // 0.0488 ms, c3a 0.0822 -> 0.0800; slower where rows are skipped: c2, c5).
   kp.rowrun = 1;
-  for (int i = 0; i < n_images && kp.rowrun; ++i) kp.rowrun = h[i].Hr >= h[i].Hd;
+  for (int i = 0; i < n_images && kp.rowrun; ++i) kp.rowrun = h[i].Hr >= h[i].sh;
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }
@@ -1102,8 +1127,8 @@ int32_t smol_compact_encode(const smol_preproc_params* p, const smol_image_desc*
   const int OW = p->crop_w > 0 ? p->crop_w : g.Wr, OH = p->crop_w > 0 ? p->crop_h : g.Hr;
   TileLayout L;
   tile_layout(g, p->scale_denom, 0, OH, 0, OW, L);
-  const int E = block_elems(p->scale_denom, p->layout);
-  const uint64_t mask = used_mask(p->scale_denom, p->layout == SMOL_LAYOUT_PACKED);
+  const int E = block_elems(p->scale_denom, p->layout, p->idct_def);
+  const uint64_t mask = used_mask(p->scale_denom, p->layout == SMOL_LAYOUT_PACKED, p->idct_def == SMOL_IDCT_TRUNCATED);
   uint32_t nv = 0;
   const int64_t bytes = compact_encode_pass(d, L, E, mask, nullptr, &nv);
   *written = bytes;

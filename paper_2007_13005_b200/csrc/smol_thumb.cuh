@@ -53,14 +53,14 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     // byte -> float trick keeps even stale words finite)
     for (int q = lane; q < (OW + 1) >> 1; q += 32) {
       int a0, a1, b0, b1; float wa, wb;
-      src_tap(im.left + 2 * q, im.Wd, im.Wr, a0, a1, wa);
-      src_tap(im.left + min(2 * q + 1, OW - 1), im.Wd, im.Wr, b0, b1, wb);
+      src_tap_x(im, im.left + 2 * q, a0, a1, wa);
+      src_tap_x(im, im.left + min(2 * q + 1, OW - 1), b0, b1, wb);
       S.xp[q] = make_int4(4 * (a0 - lx0), 4 * (b0 - lx0), __float_as_int(a1 == a0 ? 0.f : wa),
                           __float_as_int(b1 == b0 ? 0.f : wb));
     }
     for (int i = lane; i < OH; i += 32) {
       int i0, i1; float w;
-      src_tap(im.top + i, im.Hd, im.Hr, i0, i1, w);
+      src_tap_y(im, im.top + i, i0, i1, w);
       S.yt[i] = make_int2((i0 - ly0) | ((i1 - ly0) << 16), __float_as_int(i1 == i0 ? 0.f : w));
     }
     // 1/8 decode (reading R1/R3): u8 = clamp(floor(DC * Q0 / 8 + 128 + 1/2))

@@ -44,9 +44,10 @@ def oracle_planes(p, im, qt):
     return res
 
 
-def make_tie_free(im, qt, k: int, max_iter: int = 50):
+def make_tie_free(im, qt, k: int, max_iter: int = 50, idct_def: int = 0):
     """Perturb AC coefficients of blocks having a sample within delta_b of a
-    tie (exact ties excluded as well) until none does, at decode scale 1/k."""
+    tie (exact ties excluded as well) until none does, at decode scale 1/k
+    (Definition A, or B with idct_def = 1: nudges stay in the top-left)."""
     P = 8 // k
     coef = [c.copy() for c in im.coef]
     rng = np.random.default_rng(12345)
@@ -54,7 +55,7 @@ def make_tie_free(im, qt, k: int, max_iter: int = 50):
         q = qt[im.qidx[ci]]
         bh, bw = coef[ci].shape[:2]
         for _ in range(max_iter):
-            v, _ = oracle.decode_plane(coef[ci], q, k, bw * P, bh * P)
+            v, _ = oracle.decode_plane(coef[ci], q, k, bw * P, bh * P, idct_def)
             delta = block_delta(coef[ci], q)
             d = tie_distance(v).reshape(bh, P, bw, P).min(axis=(1, 3))
             bad = d <= delta
@@ -64,11 +65,12 @@ def make_tie_free(im, qt, k: int, max_iter: int = 50):
             for (by, bx) in idx:
                 # an odd-u AC nudge shifts samples by irrational amounts; at
                 # scale 1/8 only the DC matters
-                j = 0 if k == 8 else int(rng.choice([1, 3, 8, 24, 9]))
+                choices = [1, 8, 9] if (idct_def and k == 4) else [1, 3, 8, 24, 9]
+                j = 0 if k == 8 else int(rng.choice(choices))
                 coef[ci][by, bx, j] += 1 if rng.random() < 0.5 else -1
         else:
             raise RuntimeError("tie-free regeneration did not converge")
-    return synth.CoefImage(im.width, im.height, coef, im.qidx)
+    return synth.CoefImage(im.width, im.height, coef, im.qidx, getattr(im, "subsampling", 420))
 
 
 def rgb_from_planes(Y, Cb, Cr):

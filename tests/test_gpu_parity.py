@@ -528,3 +528,84 @@ def test_large_footprints_column_tiles(w, h, k, out_wh):
     assert err[~aff].max(initial=0) <= TOL[cfg.out_dtype], err[~aff].max()
     assert err.max() <= TOL[cfg.out_dtype] + 2.0 / (255 * min(synth.IMAGENET_STD))
     plan.close()
+
+
+def _band_widen(po, im, qt, tol):
+    """Per-image bound: tolerance, plus one u8 level if the image has a
+    decoded sample in the reading-R3 tie band."""
+    in_band = any(bool(b.any()) for _, _, b in helpers.oracle_planes(po, im, qt))
+    return tol + (2.0 / (255 * min(synth.IMAGENET_STD)) if in_band else 0.0)
+
+
+@pytest.mark.parametrize("k,layout", [(1, "dense"), (2, "packed"), (4, "dense"), (8, "packed")])
+def test_roi_rectangle(k, layout):
+    """Arbitrary per-image ROI rectangles (face-crop style, PAPER.md
+    P:1080-1083; reading R15) resized to the plan's output,
+    through run, run_host and run_compact, against the oracle."""
+    rng = np.random.default_rng(40 + k)
+    qt = synth.quant_tables(75)
+    imgs = [synth.make_image(rng, w, h, qt) for (w, h) in [(500, 375), (375, 500), (161, 161), (97, 61)] * 2]
+    rects = [(120, 80, 160, 200), (0, 0, 375, 500), (40, 33, 64, 64), (3, 5, 90, 50),
+             (499 - 17, 374 - 9, 17, 9), (10, 250, 300, 249), (0, 100, 161, 61), (96, 60, 1, 1)]
+    out_wh = (64, 64) if k == 8 else (112, 96)
+    ps = smol.make_params(scale_denom=k, resize_mode="exact", resize_w=out_wh[0], resize_h=out_wh[1],
+                          layout=layout)
+    po = oracle.make_params(scale_denom=k, resize_mode="exact", resize_w=out_wh[0], resize_h=out_wh[1])
+    plan = smol.Plan(ps, len(imgs))
+    outs = [plan.run(smol.batch_for(ps, imgs, qt, roi_rects=rects))]
+    outs.append(plan.run(smol.batch_for(ps, imgs, qt, roi_rects=rects, location="pinned")))
+    if k != 8:
+        outs.append(plan.run(smol.CompactBatch(ps, imgs, qt, roi_rects=rects)))
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    got = outs[0].float().cpu().numpy()
+    for i, (im, r) in enumerate(zip(imgs, rects)):
+        ref = oracle.run_image(po, im, qt, roi_rect=r).astype(np.float64)
+        err = np.max(np.abs(got[i] - ref))
+        assert err <= _band_widen(po, im, qt, 1e-4), (k, i, r, err)
+    # ROI rectangle poison: blocks outside the reported ROI ranges never read
+    g = smol.geometry(ps, imgs[0].width, imgs[0].height, roi_rect=rects[0])
+    pim = synth.CoefImage(imgs[0].width, imgs[0].height, [c.copy() for c in imgs[0].coef])
+    for ci in range(3):
+        m = np.ones(pim.coef[ci].shape[:2], bool)
+        m[g["by0"][ci]:g["by1"][ci] + 1, g["bx0"][ci]:g["bx1"][ci] + 1] = False
+        pim.coef[ci][m] = 32767
+    p2 = plan.run(smol.batch_for(ps, [pim], qt, roi_rects=rects[:1]))
+    torch.cuda.synchronize()
+    assert torch.equal(p2[0], outs[0][0])
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(smol.batch_for(ps, imgs[:1], qt, roi_rects=[(400, 300, 200, 100)]))
+    assert e.value.status == 1
+    plan.close()
+
+
+@pytest.mark.parametrize("name", ["c3a", "c3b"])
+@pytest.mark.parametrize("layout", ["dense", "packed"])
+def test_definition_b_idct(name, layout):
+    """Plan option SMOL_IDCT_TRUNCATED (reading R16): u8 planes bit-exact to
+    the oracle's Definition B (tie band only), RGB exact, output within
+    tolerance; the packed (top-left N x N) and compact transports give the
+    same bytes as dense."""
+    cfg = synth.CONFIGS[name]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=3)
+    ps = smol.params_from_config(cfg, layout=layout, idct_def="truncated")
+    po = oracle.params_from_config(cfg, idct_def="truncated")
+    out = _check(cfg, imgs, qt, ps, po)
+    plan = smol.Plan(ps, 3)
+    c = plan.run(smol.CompactBatch(ps, imgs, qt)).float().cpu().numpy()
+    d = plan.run(smol.batch_for(smol.params_from_config(cfg, idct_def="truncated"), imgs, qt)).float().cpu().numpy()
+    assert np.array_equal(c, out) and np.array_equal(d, out)
+    plan.close()
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_definition_b_tie_free_and_dc(k):
+    """Strict bit-exact u8 on a tie-free corpus, and the DC closed form."""
+    rng = np.random.default_rng(77 + k)
+    qt = synth.quant_tables(95)
+    cfg = synth.Config("tb", 4, 96, 72, k, "exact", resize_w=48, resize_h=40)
+    ps = smol.params_from_config(cfg, idct_def="truncated")
+    po = oracle.params_from_config(cfg, idct_def="truncated")
+    imgs = [helpers.make_tie_free(synth.make_image(rng, 96, 72, qt), qt, k, idct_def=1) for _ in range(3)]
+    _check(cfg, imgs, qt, ps, po, strict=True)
