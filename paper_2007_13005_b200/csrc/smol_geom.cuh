@@ -44,6 +44,9 @@ struct __align__(16) DevImage {
   int32_t gray;             // 1: one component (subsampling 400): no chroma blocks, Cb = Cr = 128
   int32_t sx0, sy0, sw, sh; // source window of the resize in decoded luma px: the whole
                             // image (0, 0, Wd, Hd), or an ROI rectangle's window (R15)
+  int32_t hs, vs;           // chroma subsampling factors (T.81 A.1.1): 2,2 = 4:2:0 (and
+                            // gray); 2,1 = 4:2:2; 1,1 = 4:4:4
+  int32_t pad_[2];
 };
 
 // Reading R9: the half-pixel bilinear source index of destination index d
@@ -103,9 +106,20 @@ constexpr int kYPWide = 512, kYPNarrow = 384, kYPTiny = 128;
 __host__ __device__ constexpr int rgb_pitch(int yp) { return yp - SMOL_RGB_PITCH_PAD; }
 constexpr int kCPad = 8;
 constexpr int kCSlots = 18;
+// Generic-chroma kernels (4:2:2 / 4:4:4 / mixed batches; template flag GC):
+// chroma rings as tall and as wide as the luma ring (vertically
+// unsubsampled chroma advances 16 rows per step, horizontally unsubsampled
+// chroma is as wide as luma): 32 rows + 2 guard slots, pitch yp.
+constexpr int kCRingG = 32;
+constexpr int kCSlotsG = kCRingG + 2;
+__host__ __device__ constexpr int c_ring(bool gc) { return gc ? kCRingG : kCRing; }
+__host__ __device__ constexpr int c_slots(bool gc) { return gc ? kCSlotsG : kCSlots; }
+__host__ __device__ constexpr int c_pitch(int yp, bool gc) { return gc ? yp : yp / 2; }
 __host__ __device__ constexpr int off_c(int yp) { return kYRing * yp; }                  // Cb ring, then Cr ring (Y ring at 0)
-__host__ __device__ constexpr int off_q(int yp) { return off_c(yp) + 2 * kCSlots * (yp / 2); }   // dequant tables (3 x 64 float)
-__host__ __device__ constexpr int off_rgb(int yp) { return off_q(yp) + 3 * 64 * 4; }     // RGB ring (size depends on the tile)
+__host__ __device__ constexpr int off_q(int yp, bool gc = false) {                         // dequant tables (3 x 64 float)
+  return off_c(yp) + 2 * c_slots(gc) * c_pitch(yp, gc);
+}
+__host__ __device__ constexpr int off_rgb(int yp, bool gc = false) { return off_q(yp, gc) + 3 * 64 * 4; }  // RGB ring (size depends on the tile)
 
 struct TileLayout {
   int oy0, oy1, ox0, ox1;          // output tile
@@ -121,7 +135,7 @@ struct TileLayout {
 };
 
 SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, int ox1, TileLayout& L,
-                         int yp = kYPWide) {
+                         int yp = kYPWide, bool gc = false) {
   const int P = 8 / K;
   int a, b; float w;
   L.oy0 = oy0; L.oy1 = oy1; L.ox0 = ox0; L.ox1 = ox1;
@@ -130,11 +144,12 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   src_tap_y(im, im.top + oy0, L.ly0, b, w);
   src_tap_y(im, im.top + oy1 - 1, a, L.ly1, w);
   // chroma rows/cols used by the centred triangle filter of luma rows
-  // [ly0, ly1]: floor((ly0-1)/2) .. floor((ly1+1)/2), clamped (reading R2)
-  L.cy0 = imax(0, (L.ly0 - 1) >> 1);
-  L.cy1 = imin(im.Hc - 1, (L.ly1 + 1) >> 1);
-  L.cx0 = imax(0, (L.lx0 - 1) >> 1);
-  L.cx1 = imin(im.Wc - 1, (L.lx1 + 1) >> 1);
+  // [ly0, ly1] along a subsampled axis: floor((ly0-1)/2) .. floor((ly1+1)/2),
+  // clamped (reading R2); along an unsubsampled axis the same rows
+  L.cy0 = im.vs == 2 ? imax(0, (L.ly0 - 1) >> 1) : imin(L.ly0, im.Hc - 1);
+  L.cy1 = imin(im.Hc - 1, im.vs == 2 ? (L.ly1 + 1) >> 1 : L.ly1);
+  L.cx0 = im.hs == 2 ? imax(0, (L.lx0 - 1) >> 1) : imin(L.lx0 & ~3, im.Wc - 1);
+  L.cx1 = imin(im.Wc - 1, im.hs == 2 ? (L.lx1 + 1) >> 1 : (L.lx1 | 3));
   // luma columns are processed 4 at a time (two 2x2 quads): widen to
   // 4-alignment (never beyond the image's valid block columns)
   L.by0[0] = L.ly0 / P; L.by1[0] = L.ly1 / P;
@@ -153,18 +168,19 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.rgb_w = ((L.lx1 | 3) - L.rgb_x0 + 1);
   L.rgb_p = rgb_pitch(yp);         // fixed pitch (u32): row r+1 is an immediate offset from row r
   L.r0 = L.ly0 & ~(kStepRows - 1);
-  // the last step must cover luma row ly1 and chroma row cy1 (luma 2 cy1)
-  L.nsteps = ((imax(L.ly1, 2 * L.cy1) - L.r0) / kStepRows) + 1;
-  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= yp) && ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= yp / 2) &&
-           (L.rgb_w + 4 <= L.rgb_p);
+  // the last step must cover luma row ly1 and chroma row cy1 (luma vs cy1)
+  L.nsteps = ((imax(L.ly1, im.vs * L.cy1) - L.r0) / kStepRows) + 1;
+  L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= yp) &&
+           ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= c_pitch(yp, gc)) && (L.rgb_w + 4 <= L.rgb_p) &&
+           (gc || (im.hs == 2 && im.vs == 2));
   int off = 0;
   // fixed-size regions first, at compile-time offsets (kOff*), so the hot
   // loops address them as immediates instead of keeping base pointers live
   L.off_y = 0;
   L.off_c = off_c(yp);
-  L.off_q = off_q(yp);
-  L.off_rgb = off_rgb(yp);
-  off = off_rgb(yp) + align16(L.rgb_p * 4 * (kRgbRing + 1));
+  L.off_q = off_q(yp, gc);
+  L.off_rgb = off_rgb(yp, gc);
+  off = off_rgb(yp, gc) + align16(L.rgb_p * 4 * (kRgbRing + 1));
   L.off_xt = off;  off += ((ox1 - ox0 + 3) >> 2) * 32;       // x taps per pixel pair: {4 x0 a, 4 x0 b, w a, w b}
   L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {ring byte offset of row y0 | y1<<16, w}
   L.off_st = off;  off += align16(L.nsteps * 8);              // per-step {ready, done}
@@ -182,10 +198,11 @@ SMOL_HD long long tile_roi_blocks(const TileLayout& L) {
 // luma row L needs chroma rows L>>1 and, for odd L, min(L>>1 + 1, Hc - 1).
 // While chroma is the limit the step ends on an odd row (2 chi - 1), so the
 // next step starts on an even row and 2x2 quads never straddle steps.
-SMOL_HD int ready_after(const TileLayout& L, int Hc, int s) {
+SMOL_HD int ready_after(const TileLayout& L, int Hc, int s, int vs = 2) {
   const int R = L.r0 + kStepRows * s;
-  const int chi = imin(L.cy1, (R >> 1) + kStepRows / 2 - 1);
   int r = imin(L.ly1, R + kStepRows - 1);
+  if (vs == 1) return r;             // unsubsampled rows: luma row L needs chroma row L only
+  const int chi = imin(L.cy1, (R >> 1) + kStepRows / 2 - 1);
   if (chi < Hc - 1) r = imin(r, chi < L.cy1 ? 2 * chi - 1 : 2 * chi);
   return r;
 }

@@ -11,11 +11,11 @@ template <int NT> struct CfgYP {
   static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
 };
 
-template <bool PK, int NT, bool DB = false>
+template <bool PK, int NT, bool DB = false, bool GC = false>
 KernelFn pick(bool f16, bool dbg) {
   constexpr int YP = CfgYP<NT>::yp;
-  if (dbg) return f16 ? smol_fused_kernel<2, true, true, PK, NT, YP, DB> : smol_fused_kernel<2, false, true, PK, NT, YP, DB>;
-  return f16 ? smol_fused_kernel<2, true, false, PK, NT, YP, DB> : smol_fused_kernel<2, false, false, PK, NT, YP, DB>;
+  if (dbg) return f16 ? smol_fused_kernel<2, true, true, PK, NT, YP, DB, GC> : smol_fused_kernel<2, false, true, PK, NT, YP, DB, GC>;
+  return f16 ? smol_fused_kernel<2, true, false, PK, NT, YP, DB, GC> : smol_fused_kernel<2, false, false, PK, NT, YP, DB, GC>;
 }
 
 template <int NT>
@@ -26,7 +26,12 @@ KernelFn pick_nt(bool f16, bool dbg, bool packed, bool db) {
 
 }  // namespace
 
-KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db) {
+KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db, bool gc) {
+  if (gc) {
+    constexpr int W = kThreadsWide;
+    if (db) return packed ? pick<true, W, true, true>(f16, dbg) : pick<false, W, true, true>(f16, dbg);
+    return packed ? pick<true, W, false, true>(f16, dbg) : pick<false, W, false, true>(f16, dbg);
+  }
   return nt == kThreadsNarrow ? pick_nt<kThreadsNarrow>(f16, dbg, packed, db)
        : nt == kThreadsTiny   ? pick_nt<kThreadsTiny>(f16, dbg, packed, db)
                               : pick_nt<kThreadsWide>(f16, dbg, packed, db);

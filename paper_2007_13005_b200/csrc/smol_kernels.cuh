@@ -474,7 +474,7 @@ __device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
   return __shfl_sync(0xffffffffu, chunk, 0);
 }
 
-template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB>
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB, bool GC>
 __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const int oy0, const int oy1,
                                        const int ox0, const int ox1) {
   constexpr int P = 8 / K;                 // decoded samples per block side
@@ -485,18 +485,23 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   __shared__ int ctr[2];                   // dynamic work counter of the output phase (ctr[1])
   if (tid == 0) {
     im = kp.imgs[n];
-    tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP);
+    tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP, GC);
     ctr[1] = 0;
   }
   __syncthreads();
-  constexpr int kCP = kYP / 2;              // chroma ring pitch
-  float* qf = reinterpret_cast<float*>(smem + off_q(kYP));
+  // chroma rings: 4:2:0 kernels (GC = false) keep 16 rows of half-width
+  // chroma; generic-chroma kernels 32 rows of full width (4:2:2, 4:4:4)
+  constexpr int kCP = c_pitch(kYP, GC);     // chroma ring pitch
+  constexpr int kCR = c_ring(GC);           // chroma ring rows (power of 2)
+  constexpr int kCS = c_slots(GC);          // + 2 guard slots
+  const int cvs = GC ? im.vs : 2, chs = GC ? im.hs : 2;   // chroma subsampling factors
+  float* qf = reinterpret_cast<float*>(smem + off_q(kYP, GC));
   int2* xt = reinterpret_cast<int2*>(smem + L.off_xt);
   int2* yt = reinterpret_cast<int2*>(smem + L.off_yt);
   uint8_t* yring = smem;
   uint8_t* cring = smem + off_c(kYP);
-  uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + off_rgb(kYP));
-  constexpr int kCStride = kCSlots * kCP;  // Cr ring follows the Cb ring
+  uint32_t* rgb = reinterpret_cast<uint32_t*>(smem + off_rgb(kYP, GC));
+  constexpr int kCStride = kCS * kCP;      // Cr ring follows the Cb ring
   const int ntw = ox1 - ox0, nth = oy1 - oy0;
   constexpr int rgb_p = rgb_pitch(kYP);     // RGB ring row pitch (u32), = L.rgb_p
   constexpr int pitch4 = rgb_p * 4;         // in bytes
@@ -544,8 +549,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   auto idct_step = [&](int s) {
     const int R = L.r0 + kStepRows * s;
     const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
-    const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P);
-    const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
+    const int Rc = GC ? R / cvs : (R >> 1), crows = GC ? kStepRows / cvs : kStepRows / 2;  // chroma rows of the step
+    const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], Rc / P);
+    const int cb1 = min(L.by1[1], (Rc + crows) / P - 1);
     const int ny = max(0, yb1 - yb0 + 1) * nbx0;
     const int nc = max(0, cb1 - cb0 + 1) * nbxc;
     const int ntask = ny + 2 * nc;
@@ -583,10 +589,10 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
 #pragma unroll
         for (int y = 0; y < P; ++y) {
           const int r = brow * P + y;
-          const int rs = r & (kCRing - 1);
-          // slot rs+1, plus the guard mirrors (slot 0 = 16, slot 17 = 1)
-          for (int k = 0; k < 1 + (rs == 15 || rs == 0); ++k) {
-            uint8_t* row = d + (k == 0 ? rs + 1 : (rs == 15 ? 0 : kCSlots - 1)) * kCP;
+          const int rs = r & (kCR - 1);
+          // slot rs+1, plus the guard mirrors (slot 0 = kCR, slot kCR+1 = 1)
+          for (int k = 0; k < 1 + (rs == kCR - 1 || rs == 0); ++k) {
+            uint8_t* row = d + (k == 0 ? rs + 1 : (rs == kCR - 1 ? 0 : kCS - 1)) * kCP;
             put_row<P>(row, px[y]);
             if (edge) {
               // replicate image-edge chroma columns into the neighbours the
@@ -606,7 +612,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   // (taps are monotone: binary search)
   int2* st = reinterpret_cast<int2*>(smem + L.off_st);
   for (int s = tid; s < L.nsteps; s += kThreads) {
-    const int ready = max(L.ly0 - 1, ready_after(L, im.Hc, s));
+    const int ready = max(L.ly0 - 1, ready_after(L, im.Hc, s, cvs));
     int lo = 0, hi = nth;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -632,8 +638,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         int rlo, rhi;
         if (c == 0) { rlo = max(max(L.by0[0], R / P) * P, L.ly0); rhi = min(min(L.by1[0], (R + kStepRows) / P - 1) * P + P - 1, L.ly1); }
         else {
-          rlo = max(((s == 0) ? L.by0[1] : max(L.by0[1], (R >> 1) / P)) * P, L.cy0);
-          rhi = min(min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1) * P + P - 1, L.cy1);
+          const int Rc = R / cvs;
+          rlo = max(((s == 0) ? L.by0[1] : max(L.by0[1], Rc / P)) * P, L.cy0);
+          rhi = min(min(L.by1[1], (Rc + kStepRows / cvs) / P - 1) * P + P - 1, L.cy1);
         }
         const int x0 = c ? L.cx0 : L.lx0, x1 = c ? L.cx1 : L.lx1;
         int16_t* dst = kp.dbg_pl[c] + n * (c ? kp.dbg_stride_c : kp.dbg_stride_y);
@@ -641,7 +648,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
           for (int x = x0 + tid; x <= x1; x += kThreads)
             if (y < Hh && x < W)
               dst[(size_t)y * W + x] = c == 0 ? yring[(y & (kYRing - 1)) * kYP + (x - L.xbase[0])]
-                                              : cring[(c - 1) * kCStride + ((y & (kCRing - 1)) + 1) * kCP +
+                                              : cring[(c - 1) * kCStride + ((y & (kCR - 1)) + 1) * kCP +
                                                       (x - L.xbase[c] + kCPad)];
       }
     }
@@ -654,8 +661,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     if ((K != 8 || PACKED) && s + 1 < L.nsteps && tid >= kThreads - 32) {
       const int R = L.r0 + kStepRows * (s + 1);
       const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
-      const int cb0 = max(L.by0[1], (R >> 1) / P);
-      const int cb1 = min(L.by1[1], ((R >> 1) + kStepRows / 2) / P - 1);
+      const int Rc = GC ? R / cvs : (R >> 1), crows = GC ? kStepRows / cvs : kStepRows / 2;
+      const int cb0 = max(L.by0[1], Rc / P);
+      const int cb1 = min(L.by1[1], (Rc + crows) / P - 1);
       const int ny = max(0, yb1 - yb0 + 1), nc = max(0, cb1 - cb0 + 1);
       for (int k = lane; k < ny + 2 * nc; k += 32) {
         int c = 0, brow = yb0 + k;
@@ -673,6 +681,65 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     // 3x4 chroma neighbourhood.  Steps end on odd rows (ready_after), so
     // quads never straddle steps; at the footprint's first/last row a quad
     // may include one row outside it (computed, never read).
+    if constexpr (GC) {
+      // generic chroma (4:2:2, 4:4:4; reading R2 per axis): along a
+      // subsampled axis the triangle 3/4, 1/4, along an unsubsampled one the
+      // sample itself (weight 4/4); values in 1/16 units as for 4:2:0
+      const int j0 = (ready_prev + 1) >> 1;
+      const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
+      const int ntaskc = nq * ntask4;
+      for (int t = tid; t < ntaskc; t += kThreads) {
+        const int rr = (int)fdiv((uint32_t)t, fd_t4);
+        const int p = t - rr * ntask4;
+        const int j = j0 + rr;                               // luma rows 2j, 2j+1
+        const int lx = L.rgb_x0 + 4 * p;                     // luma column of the quad
+        const int cc = (chs == 2 ? lx >> 1 : lx) - L.xbase[1] + kCPad;   // ring column of its chroma
+        int cbq[8], crq[8];
+#pragma unroll
+        for (int comp = 0; comp < 2; ++comp) {
+          const uint8_t* base = cring + comp * kCStride + cc;
+          auto hrow = [&](int crow, int (&h)[4]) {           // horizontal filter of chroma row crow
+            const uint8_t* r = base + ((crow & (kCR - 1)) + 1) * kCP;
+            if (chs == 2) {
+              const int a = ldu8(r - 1), m = ldu8(r), n2 = ldu8(r + 1), z = ldu8(r + 2);
+              h[0] = 3 * m + a; h[1] = 3 * m + n2; h[2] = 3 * n2 + m; h[3] = 3 * n2 + z;
+            } else {
+#pragma unroll
+              for (int x = 0; x < 4; ++x) h[x] = 4 * ldu8(r + x);
+            }
+          };
+          int* qv = comp ? crq : cbq;
+          if (cvs == 2) {
+            int h0[4], h1[4], h2[4];
+            hrow(j > 0 ? j - 1 : 0, h0);
+            hrow(j, h1);
+            hrow(j < im.Hc - 1 ? j + 1 : j, h2);
+#pragma unroll
+            for (int x = 0; x < 4; ++x) { qv[x] = 3 * h1[x] + h0[x]; qv[4 + x] = 3 * h1[x] + h2[x]; }
+          } else {
+            int ha[4], hb[4];
+            hrow(min(2 * j, im.Hc - 1), ha);
+            hrow(min(2 * j + 1, im.Hc - 1), hb);
+#pragma unroll
+            for (int x = 0; x < 4; ++x) { qv[x] = 4 * ha[x]; qv[4 + x] = 4 * hb[x]; }
+          }
+        }
+        const uint8_t* yr = yring + ((2 * j) & (kYRing - 1)) * kYP + (lx - L.xbase[0]);
+        const uint32_t y0 = *reinterpret_cast<const uint32_t*>(yr);
+        const uint32_t y1 = *reinterpret_cast<const uint32_t*>(yr + kYP);
+        const int slot = rgb_slot(2 * j);
+        uint32_t* r0p = rgb + slot * rgb_p + (lx - L.rgb_x0);
+        const uint32_t mg = 0x4B000000u;
+        const uint2 t01 = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x7541), cbq[0], cbq[1], crq[0], crq[1]);
+        const uint2 t23 = colour2m(__byte_perm(y0, mg, 0x7542), __byte_perm(y0, mg, 0x7543), cbq[2], cbq[3], crq[2], crq[3]);
+        const uint2 b01 = colour2m(__byte_perm(y1, mg, 0x7540), __byte_perm(y1, mg, 0x7541), cbq[4], cbq[5], crq[4], crq[5]);
+        const uint2 b23 = colour2m(__byte_perm(y1, mg, 0x7542), __byte_perm(y1, mg, 0x7543), cbq[6], cbq[7], crq[6], crq[7]);
+        const uint4 top = make_uint4(t01.x, t01.y, t23.x, t23.y);
+        *reinterpret_cast<uint4*>(r0p) = top;
+        *reinterpret_cast<uint4*>(r0p + rgb_p) = make_uint4(b01.x, b01.y, b23.x, b23.y);
+        if (slot == 0) *reinterpret_cast<uint4*>(r0p + kRgbRing * rgb_p) = top;   // guard row
+      }
+    } else
     {
       const int j0 = (ready_prev + 1) >> 1;
       const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
@@ -684,7 +751,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         const int p = t - rr * ntask4;
         const int j = j0 + rr;                               // chroma row of the quads
         const int i = (L.rgb_x0 >> 1) + 2 * p;               // chroma column of the left quad
-        const uint8_t* c1 = cring + ((j & (kCRing - 1)) + 1) * kCP + (i - L.xbase[1] + kCPad);
+        const uint8_t* c1 = cring + ((j & (kCR - 1)) + 1) * kCP + (i - L.xbase[1] + kCPad);
         const uint8_t* c0 = c1 + (j > 0 ? -kCP : 0);               // row j-1 (clamped at the top)
         const uint8_t* c2 = c1 + (j < im.Hc - 1 ? kCP : 0);        // row j+1 (clamped at the bottom)
         int cbq[8], crq[8];                                  // [row 0: 4 cols][row 1: 4 cols]
@@ -960,7 +1027,7 @@ __host__ __device__ constexpr int kCtasPerSm(int threads) {
 
 // The fused kernel: one (image, row band, column band) tile per CTA.
 // DB: Definition B reduced-scale IDCT (K = 2, 4 only; equal to A at 1, 1/8).
-template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB = false>
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB = false, bool GC = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm<K>(kThreads))
 smol_fused_kernel(const __grid_constant__ KParams kp) {
   int n, oy0, oy1, ox0, ox1;
@@ -975,7 +1042,7 @@ smol_fused_kernel(const __grid_constant__ KParams kp) {
     oy0 = trow * kp.tile_rows; oy1 = min(kp.OH, oy0 + kp.tile_rows);
     ox0 = tcol * kp.tile_cols; ox1 = min(kp.OW, ox0 + kp.tile_cols);
   }
-  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP, DB>(kp, n, oy0, oy1, ox0, ox1);
+  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP, DB, GC>(kp, n, oy0, oy1, ox0, ox1);
 }
 
 }  // namespace smol

@@ -12,11 +12,13 @@ using KernelFn = void (*)(const KParams);
 
 // fused kernel instantiation for (scale 1/K, output dtype, debug store,
 // packed layout, threads per CTA, Definition B IDCT); K fixed per unit
-// (db only exists at K = 2, 4: at 1 and 1/8 the definitions coincide)
-KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt, bool db);
-KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db);
-KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt, bool db);
-KernelFn select_fused_k8(bool f16, bool dbg, bool packed, int nt, bool db);
+// (db only exists at K = 2, 4: at 1 and 1/8 the definitions coincide);
+// gc: generic-chroma kernel (4:2:2 / 4:4:4), built for the wide CTA only
+// (nt is ignored)
+KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
+KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
+KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
+KernelFn select_fused_k8(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
 // upload the basis constants into each unit's constant bank (current device)
 cudaError_t upload_basis_k1(const Basis& b);
 cudaError_t upload_basis_k2(const Basis& b);

@@ -168,13 +168,15 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
     return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d must be > 0", idx, d->width, d->height);
   if (d->width > 65535 || d->height > 65535)
     return fail(SMOL_ERR_INVALID, "image %d: width/height=%d/%d > 65535 (JPEG limit)", idx, d->width, d->height);
-  if (d->subsampling != 420 && d->subsampling != 400)
-    return fail(SMOL_ERR_UNSUPPORTED, "image %d: subsampling=%d (420 or 400 only)", idx, d->subsampling);
+  if (d->subsampling != 420 && d->subsampling != 400 && d->subsampling != 422 && d->subsampling != 444)
+    return fail(SMOL_ERR_UNSUPPORTED, "image %d: subsampling=%d (420, 422, 444 or 400)", idx, d->subsampling);
   g.gray = d->subsampling == 400;
+  g.hs = d->subsampling == 444 ? 1 : 2;      // T.81 A.1.1: Hmax / H_chroma, Vmax / V_chroma
+  g.vs = (d->subsampling == 444 || d->subsampling == 422) ? 1 : 2;
   g.Wd = ceil_div(d->width, k);
   g.Hd = ceil_div(d->height, k);
-  g.Wc = ceil_div(d->width, 2 * k);
-  g.Hc = ceil_div(d->height, 2 * k);
+  g.Wc = ceil_div(d->width, g.hs * k);      // chroma ceil(W/hs) decoded at 1/k (R4)
+  g.Hc = ceil_div(d->height, g.vs * k);
   int OW, OH;
   if (p->resize_mode == SMOL_RESIZE_SHORT_SIDE) {
     const long long S = p->resize_short;
@@ -247,8 +249,8 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
   if (geom) copy_geometry(*geom, g);
   else rc = image_geometry(p, d, idx, g);
   if (rc) return rc;
-  const int need_w[3] = {ceil_div(d->width, 8), ceil_div(d->width, 16), ceil_div(d->width, 16)};
-  const int need_h[3] = {ceil_div(d->height, 8), ceil_div(d->height, 16), ceil_div(d->height, 16)};
+  const int need_w[3] = {ceil_div(d->width, 8), ceil_div(d->width, 8 * g.hs), ceil_div(d->width, 8 * g.hs)};
+  const int need_h[3] = {ceil_div(d->height, 8), ceil_div(d->height, 8 * g.vs), ceil_div(d->height, 8 * g.vs)};
   static const char* names[3] = {"Y", "Cb", "Cr"};
   for (int c = 0; c < 3; ++c) {
     g.nbw[c] = need_w[c];
@@ -297,12 +299,12 @@ int auto_tile_rows(int OH, int n_images, int slots) {
 int Cfg_yp(int nt) { return nt == kThreadsNarrow ? kYPNarrow : nt == kThreadsTiny ? kYPTiny : kYPWide; }
 
 // scale 1 has no packed variant: the packed layout of scale 1 is DENSE64
-KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt, bool db) {
+KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt, bool db, bool gc = false) {
   switch (K) {
-    case 1: return select_fused_k1(f16, dbg, packed, nt, db);
-    case 2: return select_fused_k2(f16, dbg, packed, nt, db);
-    case 4: return select_fused_k4(f16, dbg, packed, nt, db);
-    default: return select_fused_k8(f16, dbg, packed, nt, db);
+    case 1: return select_fused_k1(f16, dbg, packed, nt, db, gc);
+    case 2: return select_fused_k2(f16, dbg, packed, nt, db, gc);
+    case 4: return select_fused_k4(f16, dbg, packed, nt, db, gc);
+    default: return select_fused_k8(f16, dbg, packed, nt, db, gc);
   }
 }
 
@@ -405,9 +407,9 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
   out->OH = params->crop_w > 0 ? params->crop_h : g.Hr;
   out->sx0 = g.sx0; out->sy0 = g.sy0; out->sw = g.sw; out->sh = g.sh;
   g.nbw[0] = ceil_div(image->width, 8);
-  g.nbw[1] = g.nbw[2] = ceil_div(image->width, 16);
+  g.nbw[1] = g.nbw[2] = ceil_div(image->width, 8 * g.hs);
   TileLayout L;
-  tile_layout(g, params->scale_denom, 0, out->OH, 0, out->OW, L);
+  tile_layout(g, params->scale_denom, 0, out->OH, 0, out->OW, L, kYPWide, true);
   out->lx0 = L.lx0; out->lx1 = L.lx1; out->ly0 = L.ly0; out->ly1 = L.ly1;
   out->cx0 = L.cx0; out->cx1 = L.cx1; out->cy0 = L.cy0; out->cy1 = L.cy1;
   for (int c = 0; c < 3; ++c) {
@@ -506,11 +508,11 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     // dynamic smem the device allows next to the kernel's static smem
     const bool f16 = params->out_dtype == SMOL_OUT_F16_NCHW;
     int limit = pl->smem_optin;
-    for (int v = 0; v < 6 && e == cudaSuccess; ++v) {
+    for (int v = 0; v < 8 && e == cudaSuccess; ++v) {
       const int dbg = v & 1, nt = v < 2 ? kThreadsWide : v < 4 ? kThreadsNarrow : kThreadsTiny;
       cudaFuncAttributes fa;
       KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED, nt,
-                                  params->idct_def == SMOL_IDCT_TRUNCATED);
+                                  params->idct_def == SMOL_IDCT_TRUNCATED, v >= 6);
       e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) break;
       const int dyn = pl->smem_optin - (int)fa.sharedSizeBytes;
@@ -596,7 +598,7 @@ int32_t validate_compact_image(const smol_preproc_params* p, const smol_compact_
         return fail(SMOL_ERR_INVALID, "image %d: qtable[%d]=%d not in [0,%d)", idx, c, ci->qtable[c], n_qtables);
       g.qidx[c] = ci->qtable[c];
     }
-    g.nbw[c] = ceil_div(ci->width, c ? 16 : 8);
+    g.nbw[c] = ceil_div(ci->width, c ? 8 * g.hs : 8);
     g.coef[c] = nullptr;
     g.stride[c] = 0;
   }
@@ -690,6 +692,10 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // shared memory of the largest tile over the batch's distinct geometries
   // (a tile whose footprint exceeds the fixed ring pitches reports INT_MAX/2)
   auto cols_of = [&](int n_col_tiles) { return (ceil_div(pl->OW, n_col_tiles) + 3) & ~3; };  // multiple of 4
+  // a batch with any 4:2:2 / 4:4:4 image runs the generic-chroma kernel
+  // (wide CTA only; its chroma rings are full-size)
+  bool gc = false;
+  for (int i = 0; i < n_images && !gc; ++i) gc = h[i].hs != 2 || h[i].vs != 2;
   auto max_smem = [&](int n_col_tiles, int yp) {
     const int tile_cols = cols_of(n_col_tiles);
     n_col_tiles = ceil_div(pl->OW, tile_cols);
@@ -702,7 +708,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
         for (int u = 0; u < n_col_tiles; ++u) {
           TileLayout L;
           tile_layout(g, K, t * tile_rows, imin(pl->OH, (t + 1) * tile_rows), u * tile_cols,
-                      imin(pl->OW, (u + 1) * tile_cols), L, yp);
+                      imin(pl->OW, (u + 1) * tile_cols), L, yp, gc);
           m = imax(m, L.fits ? L.total : (1 << 30));
         }
       prev = &g;
@@ -715,10 +721,10 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // adding column tiles only when a tile would not leave 2 CTAs/SM.
   int n_col_tiles = 1;
   int nt = kThreadsTiny;
-  int smem = max_smem(1, kYPTiny);
+  int smem = gc ? INT_MAX : max_smem(1, kYPTiny);
   if (smem > smem_budget(6) || (pl->nt_mode != 0 && pl->nt_mode != kThreadsTiny) || pl->min_col_tiles > 1) {
     nt = kThreadsNarrow;
-    smem = max_smem(1, kYPNarrow);
+    smem = gc ? INT_MAX : max_smem(1, kYPNarrow);
   }
   if (smem > smem_budget(4) || pl->nt_mode == kThreadsWide || pl->min_col_tiles > 1) {
     nt = kThreadsWide;
@@ -734,7 +740,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   }
   // resident CTAs per SM of the chosen kernel at this shared-memory size
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt,
-                              pl->p.idct_def == SMOL_IDCT_TRUNCATED);
+                              pl->p.idct_def == SMOL_IDCT_TRUNCATED, gc);
   int occ = 768 / nt;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
@@ -763,7 +769,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // Packed layout only: with dense-64 blocks each DC is a separate 32-B
   // sector and the tiled kernel hides that latency better (measured r01s:
   // c4 packed 47.5 M -> 52.1 M img/s, dense 33.6 M -> 27.0 M).
-  bool thumb = K == 8 && packed && !dbg && pl->thumb_mode && pl->OW <= kThumbMaxOut && pl->OH <= kThumbMaxOut;
+  bool thumb = K == 8 && packed && !dbg && !gc && pl->thumb_mode && pl->OW <= kThumbMaxOut &&
+               pl->OH <= kThumbMaxOut;
   for (int i = 0; thumb && i < n_images; ++i) {
     if (i > 0 && same_layout_inputs(h[i], h[i - 1])) continue;
     TileLayout L;
@@ -819,7 +826,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     for (int i = 0; i < n_images; ++i) {
       TileLayout& L = Ls[i];
       if (i > 0 && same_layout_inputs(h[i], h[i - 1])) L = Ls[i - 1];
-      else tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L);
+      else tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L, kYPWide, true);
       need = stage_layout(L, E, strides, offs, need);
       for (int c = 0; c < 3; ++c) {
         if (src == Src::kGather) {
@@ -1126,7 +1133,7 @@ int32_t smol_compact_encode(const smol_preproc_params* p, const smol_image_desc*
   if (rc) return rc;
   const int OW = p->crop_w > 0 ? p->crop_w : g.Wr, OH = p->crop_w > 0 ? p->crop_h : g.Hr;
   TileLayout L;
-  tile_layout(g, p->scale_denom, 0, OH, 0, OW, L);
+  tile_layout(g, p->scale_denom, 0, OH, 0, OW, L, kYPWide, true);
   const int E = block_elems(p->scale_denom, p->layout, p->idct_def);
   const uint64_t mask = used_mask(p->scale_denom, p->layout == SMOL_LAYOUT_PACKED, p->idct_def == SMOL_IDCT_TRUNCATED);
   uint32_t nv = 0;

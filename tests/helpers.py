@@ -25,14 +25,38 @@ def tie_distance(v: np.ndarray) -> np.ndarray:
     return np.abs(x - (np.floor(x) + 0.5))
 
 
-def plane_band(coef, q, k, v):
-    """Boolean [h][w]: sample within delta_b of a tie but not exactly on it."""
+def exact_basis_mask(k: int, idct_def: int = 0) -> np.ndarray:
+    """[64] bool: coefficient (v, u) whose basis entries at scale 1/k are all
+    exact (0 or +-1 times a power of two): u and v in {0, 4} at scale 1
+    (t(4, x) = +-1), {0} plus the vanishing frequencies under Definition A
+    (R1), {0, N/2} under Definition B (R16, N = 8/k)."""
+    if idct_def and k > 1:
+        N = 8 // k
+        ok = {0, N // 2} if N > 1 else {0}
+        ok |= set(range(N, 8))                  # unused: zero basis
+    elif k == 1:
+        ok = {0, 4}
+    else:
+        ok = {0} | {u for u in range(1, 8) if (k * u) % 16 == 0 or all(
+            (k * u * (2 * j + 1)) % 16 == 8 for j in range(8 // k))}
+    return np.array([(v in ok) and (u in ok) for v in range(8) for u in range(8)])
+
+
+def plane_band(coef, q, k, v, idct_def: int = 0):
+    """Boolean [h][w], reading R3: the sample lies within delta_b of a
+    rounding tie but not exactly on it -- or exactly on it in a block with a
+    nonzero coefficient whose basis is irrational: such a tie is reached only
+    by cancellation of irrational terms (e.g. D(0,1) = D(1,0) at mirrored
+    positions), which fp32 evaluation cannot reproduce exactly.  Exact ties
+    of blocks whose arithmetic is exact (DC, u = 4 / N/2 paths) must match."""
     P = 8 // k
     h, w = v.shape
     delta = block_delta(coef, q)
     dl = np.repeat(np.repeat(delta, P, axis=0), P, axis=1)[:h, :w]
+    inexact = ((coef != 0) & ~exact_basis_mask(k, idct_def)).any(axis=-1)
+    il = np.repeat(np.repeat(inexact, P, axis=0), P, axis=1)[:h, :w]
     d = tie_distance(v)
-    return (d <= dl) & (d > 0)
+    return (d <= dl) & ((d > 0) | il)
 
 
 def oracle_planes(p, im, qt):
@@ -40,7 +64,7 @@ def oracle_planes(p, im, qt):
     res = []
     for ci, (v, u8) in enumerate(oracle.decode_image_planes(p, im, qt, with_v=True)):
         q = qt[im.qidx[ci]]
-        res.append((v, u8, plane_band(im.coef[ci], q, p.scale_denom, v)))
+        res.append((v, u8, plane_band(im.coef[ci], q, p.scale_denom, v, p.idct_def)))
     return res
 
 
@@ -73,8 +97,8 @@ def make_tie_free(im, qt, k: int, max_iter: int = 50, idct_def: int = 0):
     return synth.CoefImage(im.width, im.height, coef, im.qidx, getattr(im, "subsampling", 420))
 
 
-def rgb_from_planes(Y, Cb, Cr):
-    return oracle.upsample_color(Y, Cb, Cr)[1]
+def rgb_from_planes(Y, Cb, Cr, subsampling=420):
+    return oracle.upsample_color(Y, Cb, Cr, subsampling)[1]
 
 
 def _taps(n_out, offset, n_in, n_res):

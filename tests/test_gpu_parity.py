@@ -41,7 +41,8 @@ def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=No
     n = len(imgs)
     plan = smol.Plan(ps, n)
     batch = smol.CoefBatch(imgs, qt, rois=rois)
-    geoms = [smol.geometry(ps, im.width, im.height, roi=None if rois is None else rois[i])
+    geoms = [smol.geometry(ps, im.width, im.height, roi=None if rois is None else rois[i],
+                           subsampling=getattr(im, "subsampling", 420))
              for i, im in enumerate(imgs)]
     if debug:
         out, y, cb, cr, rgb = plan.debug_run(batch, geoms)
@@ -79,7 +80,7 @@ def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=No
             # RGB exact given the kernel's own planes
             grgb = rgb[i].cpu().numpy()[:3 * g["Hd"] * g["Wd"]].reshape(g["Hd"], g["Wd"], 3)
             mrgb = grgb[..., 0] >= 0
-            exp_rgb = helpers.rgb_from_planes(*gp)
+            exp_rgb = helpers.rgb_from_planes(*gp, subsampling=getattr(im, "subsampling", 420))
             assert np.array_equal(grgb[mrgb], exp_rgb[mrgb].astype(np.int16)), f"image {i}: RGB mismatch"
             # resize/normalize given the kernel's own RGB
             full = np.where(mrgb[..., None], grgb, 0).astype(np.uint8)
@@ -609,3 +610,31 @@ def test_definition_b_tie_free_and_dc(k):
     po = oracle.params_from_config(cfg, idct_def="truncated")
     imgs = [helpers.make_tie_free(synth.make_image(rng, 96, 72, qt), qt, k, idct_def=1) for _ in range(3)]
     _check(cfg, imgs, qt, ps, po, strict=True)
+
+
+@pytest.mark.parametrize("ss", [422, 444])
+@pytest.mark.parametrize("k,layout", [(1, "dense"), (2, "packed"), (4, "dense"), (8, "packed")])
+def test_chroma_subsampling_variants(ss, k, layout):
+    """4:2:2 and 4:4:4 JPEGs (T.81 A.1.1): the generic-chroma
+    kernel's u8 planes are bit-exact to the oracle (tie band only), its RGB
+    exact given its planes, the output within tolerance; a batch mixing
+    4:2:0, 4:2:2, 4:4:4 and grayscale images gives each image the same
+    bytes as a batch of its own mode."""
+    rng = np.random.default_rng(ss + k)
+    qt = synth.quant_tables(75)
+    cfg = synth.Config("ss", 4, 160, 120, k, "exact", resize_w=96, resize_h=72)
+    ps = smol.params_from_config(cfg, layout=layout)
+    po = oracle.params_from_config(cfg)
+    imgs = [synth.make_image(rng, w, h, qt, f"natural{ss}") for (w, h) in [(160, 120), (97, 61), (333, 250)]]
+    out = _check(cfg, imgs, qt, ps, po)
+    mixed = [imgs[0], synth.make_image(rng, 160, 120, qt), synth.make_image(rng, 96, 80, qt, "gray"), imgs[1]]
+    plan = smol.Plan(ps, 4)
+    m = plan.run(smol.batch_for(ps, mixed, qt)).float().cpu().numpy()
+    solo = plan.run(smol.batch_for(ps, [mixed[1], mixed[2]], qt)).float().cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(m[0], out[0]) and np.array_equal(m[3], out[1])
+    assert np.array_equal(m[1], solo[0]) and np.array_equal(m[2], solo[1])
+    if k != 8:
+        c = plan.run(smol.CompactBatch(ps, mixed, qt)).float().cpu().numpy()
+        assert np.array_equal(c, m)
+    plan.close()
