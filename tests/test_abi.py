@@ -108,9 +108,17 @@ def test_param_validation(native, bad, msg):
 def test_unsupported_subsampling_and_crop_too_big(native):
     p = smol.make_params(scale_denom=1, resize_short=256, crop_w=224, crop_h=224)
     d = smol._desc_for(500, 375, [63, 32, 32], [47, 24, 24])
-    d.subsampling = 444
+    d.subsampling = 411                      # (4:1:1 is not a supported sampling)
     g = _native.Geometry()
     assert native.smol_debug_geometry(ctypes.byref(p), ctypes.byref(d), ctypes.byref(g)) == _native.SMOL_ERR_UNSUPPORTED
+    # 4:2:2 / 4:4:4 chroma sizes (T.81 A.1.1) agree with the oracle
+    import oracle
+    po = oracle.make_params(scale_denom=2, resize_mode="exact", resize_w=64, resize_h=64)
+    for ss in (420, 422, 444):
+        gs = smol.geometry(smol.make_params(scale_denom=2, resize_mode="exact", resize_w=64, resize_h=64),
+                           500, 375, subsampling=ss)
+        go = oracle.geometry(po, 500, 375, ss)
+        assert (gs["Wc"], gs["Hc"], gs["Wd"], gs["Hd"]) == (go.Wc, go.Hc, go.Wd, go.Hd)
     p2 = smol.make_params(scale_denom=8, resize_short=16, crop_w=224, crop_h=224)
     with pytest.raises(smol.SmolError):
         smol.geometry(p2, 500, 375)
