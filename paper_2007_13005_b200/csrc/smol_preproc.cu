@@ -236,11 +236,13 @@ inline void copy_geometry(const DevImage& from, DevImage& g) {
   g.Wr = from.Wr; g.Hr = from.Hr; g.left = from.left; g.top = from.top;
   g.gray = from.gray;
   g.sx0 = from.sx0; g.sy0 = from.sy0; g.sw = from.sw; g.sh = from.sh;
+  g.hs = from.hs; g.vs = from.vs;
 }
 inline bool same_layout_inputs(const DevImage& a, const DevImage& b) {
   return a.Wd == b.Wd && a.Hd == b.Hd && a.Wc == b.Wc && a.Hc == b.Hc && a.Wr == b.Wr && a.Hr == b.Hr &&
          a.left == b.left && a.top == b.top && a.nbw[0] == b.nbw[0] && a.nbw[1] == b.nbw[1] &&
-         a.gray == b.gray && a.sx0 == b.sx0 && a.sy0 == b.sy0 && a.sw == b.sw && a.sh == b.sh;
+         a.gray == b.gray && a.sx0 == b.sx0 && a.sy0 == b.sy0 && a.sw == b.sw && a.sh == b.sh &&
+         a.hs == b.hs && a.vs == b.vs;
 }
 
 int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, int idx, int n_qtables,
