@@ -40,7 +40,7 @@ def _cfg_params(cfg, **kw):
 def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=None):
     n = len(imgs)
     plan = smol.Plan(ps, n)
-    batch = smol.CoefBatch(imgs, qt, rois=rois)
+    batch = smol.batch_for(ps, imgs, qt, rois=rois)         # the plan's layout
     geoms = [smol.geometry(ps, im.width, im.height, roi=None if rois is None else rois[i],
                            subsampling=getattr(im, "subsampling", 420))
              for i, im in enumerate(imgs)]
