@@ -29,12 +29,6 @@
 #ifndef SMOL_KO
 #define SMOL_KO 0                // diagnostic knockouts (1 IDCT, 2 colour, 4 output math); 0 in products
 #endif
-#ifndef SMOL_ALU_I2F
-#define SMOL_ALU_I2F 0           // coefficient low halves converted on the ALU pipe (A/B)
-#endif
-#ifndef SMOL_L1_PREFETCH
-#define SMOL_L1_PREFETCH 0       // prefetch step s+1's coefficient lines into L1 during colour(s) (A/B)
-#endif
 #ifndef SMOL_OUT_RUN_ROWS
 #define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
 #endif
@@ -148,16 +142,7 @@ __device__ __forceinline__ uint32_t floor_u8(float v) {
   return r;
 }
 
-#if SMOL_ALU_I2F
-// low half: PRMT sign-extension + I2FP (ALU pipe) instead of I2F.S16 (XU)
-__device__ __forceinline__ float lo16f(int x) {
-  float f;
-  asm("cvt.rn.f32.s32 %0, %1;" : "=f"(f) : "r"((int)__byte_perm(x, 0, 0x9910)));
-  return f;
-}
-#else
 __device__ __forceinline__ float lo16f(int x) { return (float)(int16_t)(x & 0xffff); }
-#endif
 __device__ __forceinline__ void unpack_row(const int4 r, float (&d)[8]) {
   d[0] = lo16f(r.x); d[1] = (float)(r.x >> 16);
   d[2] = lo16f(r.y); d[3] = (float)(r.y >> 16);
@@ -701,33 +686,6 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       }
     }
 
-#if SMOL_L1_PREFETCH
-    // ---- L1 prefetch of step s+1's coefficient blocks (one thread per
-    // block: first and last byte) so the next IDCT phase hits L1
-    if (K != 8 && s + 1 < L.nsteps) {
-      const int R = L.r0 + kStepRows * (s + 1);
-      const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
-      const int Rc = GC ? R / cvs : (R >> 1), crows = GC ? kStepRows / cvs : kStepRows / 2;
-      const int cb0 = max(L.by0[1], Rc / P);
-      const int cb1 = min(L.by1[1], (Rc + crows) / P - 1);
-      const int ny = max(0, yb1 - yb0 + 1) * nbx0, nc = max(0, cb1 - cb0 + 1) * nbxc;
-      for (int t = tid; t < ny + 2 * nc; t += kThreads) {
-        int c = 0, brow, bcol;
-        if (t < ny) { brow = (int)fdiv((uint32_t)t, fd_y); bcol = t - brow * nbx0; brow += yb0; }
-        else {
-          int tt = t - ny;
-          c = 1 + (tt >= nc);
-          tt -= (c - 1) * nc;
-          brow = (int)fdiv((uint32_t)tt, fd_c); bcol = tt - brow * nbxc; brow += cb0;
-        }
-        constexpr int SB = BlockFmt<K, PACKED, DB>::kElems * 2;
-        const char* p = reinterpret_cast<const char*>(im.coef[c] + (size_t)brow * im.stride[c] +
-                                                      (size_t)(L.bx0[c] + bcol) * BlockFmt<K, PACKED, DB>::kElems);
-        asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
-        asm volatile("prefetch.global.L1 [%0];" :: "l"(p + SB - 1));
-      }
-    }
-#endif
 
     // ---- upsample + colour of the RGB rows that became ready -------------
     // A task is 2x4 luma pixels (rows 2j, 2j+1; cols 2i .. 2i+3) sharing a

@@ -595,9 +595,12 @@ def test_definition_b_idct(name, layout):
     out = _check(cfg, imgs, qt, ps, po)
     plan = smol.Plan(ps, 3)
     c = plan.run(smol.CompactBatch(ps, imgs, qt)).float().cpu().numpy()
-    d = plan.run(smol.batch_for(smol.params_from_config(cfg, idct_def="truncated"), imgs, qt)).float().cpu().numpy()
+    pd = smol.params_from_config(cfg, idct_def="truncated")              # dense-64 layout
+    plan_d = smol.Plan(pd, 3)
+    d = plan_d.run(smol.batch_for(pd, imgs, qt)).float().cpu().numpy()
     assert np.array_equal(c, out) and np.array_equal(d, out)
     plan.close()
+    plan_d.close()
 
 
 @pytest.mark.parametrize("k", [2, 4])
