@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
         const int wpb = E / 4;                              // 8-byte words per block
         uint2* to8 = reinterpret_cast<uint2*>(drow + (int64_t)ch * E);
         for (int w = lane; w < nb * wpb; w += 32) {
-          const int bb = (int)__umulhi((uint32_t)w, fd_wpb);   // w / wpb (w < 2^16)
+          const int bb = wpb == 1 ? w : (int)__umulhi((uint32_t)w, fd_wpb);   // w / wpb (w < 2^16)
           to8[w] = reinterpret_cast<const uint2*>(blk + bb * ls)[w - bb * wpb];
         }
       }
