@@ -366,6 +366,7 @@ struct smol_preproc_plan {
   int thumb_mode = 1;          // SMOL_THUMB=0 disables the warp-per-image 1/8 kernel (A/B)
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
   cudaEvent_t ev[kRing] = {};
+  cudaEvent_t desc_ready[kRing] = {};      // descriptor upload of a ring slot done (copy stream)
   int ring = 0;
   float na[3], nb[3];
   // end-to-end (run_host) staging: ROI block rows gathered from pinned host
@@ -467,7 +468,10 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
-  for (int i = 0; i < kRing && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
+  for (int i = 0; i < kRing && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->desc_ready[i], cudaEventDisableTiming);
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&pl->stage_free[i], cudaEventDisableTiming);
@@ -537,8 +541,10 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   int prev = -1;                    // release on the plan's device, then restore the caller's
   if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
   if (prev != pl->device) cudaSetDevice(pl->device);
-  for (int i = 0; i < kRing; ++i)
+  for (int i = 0; i < kRing; ++i) {
     if (pl->ev[i]) { cudaEventSynchronize(pl->ev[i]); cudaEventDestroy(pl->ev[i]); }
+    if (pl->desc_ready[i]) cudaEventDestroy(pl->desc_ready[i]);
+  }
   for (int i = 0; i < 2; ++i) {
     if (pl->stage_free[i]) { cudaEventSynchronize(pl->stage_free[i]); cudaEventDestroy(pl->stage_free[i]); }
     if (pl->stage_ready[i]) cudaEventDestroy(pl->stage_ready[i]);
@@ -961,10 +967,22 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     }
   }
 
-  if (src == Src::kDevice)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  SMOL_CUDA(cudaStreamIsCapturing(stream, &cap));
+  if (src == Src::kDevice && cap != cudaStreamCaptureStatusNone) {
+    // (being captured into a CUDA graph: keep every operation on `stream`)
     SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, stream));
-  if (map_n && src == Src::kDevice)
-    SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, stream));
+    if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, stream));
+  } else if (src == Src::kDevice) {
+    // descriptors (and the CTA map) go up on the plan's copy stream, so the
+    // copy for run k+1 overlaps run k's kernel instead of sitting between
+    // the kernels on `stream` (4096 thumbnails: 512 KB per run); the ring
+    // slot is free (host waited on ev[slot] above)
+    SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+    if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, pl->copy_stream));
+    SMOL_CUDA(cudaEventRecord(pl->desc_ready[slot], pl->copy_stream));
+    SMOL_CUDA(cudaStreamWaitEvent(stream, pl->desc_ready[slot], 0));
+  }
   KParams kp = dbg ? *dbg : KParams{};
   kp.imgs = d;
   kp.qtables = qtables;

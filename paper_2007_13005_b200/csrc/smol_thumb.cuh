@@ -19,6 +19,7 @@ constexpr int kThumbWarps = 4;                 // images in flight per CTA
 constexpr int kThumbMaxFoot = 32;              // decoded luma footprint limit (px per side)
 constexpr int kThumbMaxOut = 128;              // output width / height limit
 constexpr int kThumbCP = kThumbMaxFoot / 2 + 2;   // chroma footprint pitch
+constexpr int kThumbRun = 8;                   // output rows per lane task (row-run reuse)
 struct ThumbWarpSmem {
   uint32_t rgb[kThumbMaxFoot * kThumbMaxFoot + 1];  // RGBx of the luma footprint (+1: x0 + 1 read at the end)
   uint8_t y[kThumbMaxFoot * kThumbMaxFoot];
@@ -107,60 +108,83 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     const uint32_t magic = kp.magic;
     const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
     const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
-    for (int t = lane; t < nq * OH; t += 32) {
-      const int oy = (int)fdiv((uint32_t)t, fd_nq), ox = 4 * (t - oy * nq);
-      const int2 ty = S.yt[oy];
-      const float2 wy2 = f2(__int_as_float(ty.y));
-      const uint32_t* r0 = S.rgb + (ty.x & 0xffff) * kThumbMaxFoot;
-      const uint32_t* r1 = S.rgb + (ty.x >> 16) * kThumbMaxFoot;
-      float v[3][4];
+    // a lane walks one 4-pixel column quad down a run of kThumbRun rows:
+    // the horizontal lerps of a source row are reused while the row taps
+    // stay put (thumbnails magnify: 21 -> 64 rows at c4), the old bottom
+    // becomes the new top when they move down one row (bit-identical)
+    const int ngr = (OH + kThumbRun - 1) / kThumbRun;
+    for (int t = lane; t < nq * ngr; t += 32) {
+      const int g = (int)fdiv((uint32_t)t, fd_nq), q = t - g * nq, ox = 4 * q;
+      const int ra = g * kThumbRun, rb = min(ra + kThumbRun, OH);
+      const int4 txa = S.xp[min(ox >> 1, ((OW + 1) >> 1) - 1)];
+      const int4 txb = S.xp[min((ox + 2) >> 1, ((OW + 1) >> 1) - 1)];
+      float2 T[3][2], B[3][2];
+      auto hlerp = [&](int row, float2 (&H)[3][2]) {
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(S.rgb + row * kThumbMaxFoot);
 #pragma unroll
-      for (int e = 0; e < 4; e += 2) {
-        const int4 tx = S.xp[min((ox + e) >> 1, ((OW + 1) >> 1) - 1)];
-        const float2 wx = make_float2(__int_as_float(tx.z), __int_as_float(tx.w));
-        const uint8_t* a0 = reinterpret_cast<const uint8_t*>(r0) + tx.x;
-        const uint8_t* a1 = reinterpret_cast<const uint8_t*>(r1) + tx.x;
-        const uint8_t* b0 = reinterpret_cast<const uint8_t*>(r0) + tx.y;
-        const uint8_t* b1 = reinterpret_cast<const uint8_t*>(r1) + tx.y;
-        const uint32_t p00 = lds_u32(a0), p01 = lds_u32(a0 + 4), p10 = lds_u32(a1), p11 = lds_u32(a1 + 4);
-        const uint32_t q00 = lds_u32(b0), q01 = lds_u32(b0 + 4), q10 = lds_u32(b1), q11 = lds_u32(b1 + 4);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int sel = 0x7540 + c;
-          const float2 fa = make_float2(__uint_as_float(__byte_perm(p00, magic, sel)), __uint_as_float(__byte_perm(q00, magic, sel)));
-          const float2 fb = make_float2(__uint_as_float(__byte_perm(p01, magic, sel)), __uint_as_float(__byte_perm(q01, magic, sel)));
-          const float2 fc = make_float2(__uint_as_float(__byte_perm(p10, magic, sel)), __uint_as_float(__byte_perm(q10, magic, sel)));
-          const float2 fd = make_float2(__uint_as_float(__byte_perm(p11, magic, sel)), __uint_as_float(__byte_perm(q11, magic, sel)));
-          const float2 tp = __ffma2_rn(wx, __ffma2_rn(fa, f2(-1.f), fb), __fadd2_rn(fa, f2(-8388608.f)));
-          const float2 bt = __ffma2_rn(wx, __ffma2_rn(fc, f2(-1.f), fd), __fadd2_rn(fc, f2(-8388608.f)));
-          const float2 vv = __ffma2_rn(wy2, __ffma2_rn(tp, f2(-1.f), bt), tp);
-          const float2 yn = __ffma2_rn(vv, c == 0 ? na0 : c == 1 ? na1 : na2, c == 0 ? nb0 : c == 1 ? nb1 : nb2);
-          v[c][e] = yn.x;
-          v[c][e + 1] = yn.y;
-        }
-      }
-      OutT* const o = outn + (uint32_t)oy * OW + ox;
-      if ((OW & 3) == 0 && kp.out_vec) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if constexpr (F16) {
-            const __half2 h0 = __floats2half2_rn(v[c][0], v[c][1]), h1 = __floats2half2_rn(v[c][2], v[c][3]);
-            uint2 u;
-            u.x = *reinterpret_cast<const uint32_t*>(&h0);
-            u.y = *reinterpret_cast<const uint32_t*>(&h1);
-            __stcs(reinterpret_cast<uint2*>(o + c * plane), u);
-          } else {
-            __stcs(reinterpret_cast<float4*>(o + c * plane), make_float4(v[c][0], v[c][1], v[c][2], v[c][3]));
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (ox + e >= OW) break;
+        for (int e = 0; e < 2; ++e) {
+          const int4 tx = e == 0 ? txa : txb;
+          const float2 wx = make_float2(__int_as_float(tx.z), __int_as_float(tx.w));
+          const uint32_t p0 = lds_u32(base + tx.x), p1 = lds_u32(base + tx.x + 4);
+          const uint32_t q0 = lds_u32(base + tx.y), q1 = lds_u32(base + tx.y + 4);
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            if constexpr (F16) o[e + c * plane] = __float2half_rn(v[c][e]);
-            else o[e + c * plane] = v[c][e];
+            const int sel = 0x7540 + c;
+            const float2 fa = make_float2(__uint_as_float(__byte_perm(p0, magic, sel)), __uint_as_float(__byte_perm(q0, magic, sel)));
+            const float2 fb = make_float2(__uint_as_float(__byte_perm(p1, magic, sel)), __uint_as_float(__byte_perm(q1, magic, sel)));
+            H[c][e] = __ffma2_rn(wx, __ffma2_rn(fa, f2(-1.f), fb), __fadd2_rn(fa, f2(-8388608.f)));
+          }
+        }
+      };
+      int c0 = -1, c1 = -1;                       // source rows of T and B
+#pragma unroll 1
+      for (int oy = ra; oy < rb; ++oy) {
+        const int2 ty = S.yt[oy];
+        const int i0 = ty.x & 0xffff, i1 = ty.x >> 16;
+        if (i0 != c0 || i1 != c1) {
+          if (i0 == c1) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) { T[c][0] = B[c][0]; T[c][1] = B[c][1]; }
+          } else {
+            hlerp(i0, T);
+          }
+          hlerp(i1, B);
+          c0 = i0; c1 = i1;
+        }
+        const float2 wy2 = f2(__int_as_float(ty.y));
+        float v[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float2 vv = __ffma2_rn(wy2, __ffma2_rn(T[c][e], f2(-1.f), B[c][e]), T[c][e]);
+            const float2 yn = __ffma2_rn(vv, c == 0 ? na0 : c == 1 ? na1 : na2, c == 0 ? nb0 : c == 1 ? nb1 : nb2);
+            v[c][2 * e] = yn.x;
+            v[c][2 * e + 1] = yn.y;
+          }
+        OutT* const o = outn + (uint32_t)oy * OW + ox;
+        if ((OW & 3) == 0 && kp.out_vec) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if constexpr (F16) {
+              const __half2 h0 = __floats2half2_rn(v[c][0], v[c][1]), h1 = __floats2half2_rn(v[c][2], v[c][3]);
+              uint2 u;
+              u.x = *reinterpret_cast<const uint32_t*>(&h0);
+              u.y = *reinterpret_cast<const uint32_t*>(&h1);
+              __stcs(reinterpret_cast<uint2*>(o + c * plane), u);
+            } else {
+              __stcs(reinterpret_cast<float4*>(o + c * plane), make_float4(v[c][0], v[c][1], v[c][2], v[c][3]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (ox + e >= OW) break;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              if constexpr (F16) o[e + c * plane] = __float2half_rn(v[c][e]);
+              else o[e + c * plane] = v[c][e];
+            }
           }
         }
       }
