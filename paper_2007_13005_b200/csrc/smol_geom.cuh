@@ -49,6 +49,16 @@ struct __align__(16) DevImage {
   int32_t pad_[2];
 };
 
+// Per-image reference of a run (32 B): the image's coefficient planes and
+// the index of its "kind" -- the DevImage holding everything else, shared by
+// consecutive images with equal descriptors (a batch of equal-size images
+// has one kind, so the host writes and uploads 32 B per image).
+struct __align__(16) DevRef {
+  const int16_t* coef[3];
+  int32_t kind;
+  int32_t pad_;
+};
+
 // Reading R9: the half-pixel bilinear source index of destination index d
 // (R8: src = max(0, (d + 1/2) in/out - 1/2)), from exact integers:
 //   num = max(0, (2d+1) in - out),  i0 = num div 2out,  w = (num mod 2out) / 2out,

@@ -433,7 +433,8 @@ __device__ __forceinline__ uint2 colour2m(uint32_t m0, uint32_t m1, int cb0, int
 __device__ __forceinline__ int ldu8(const uint8_t* p) { return *p; }
 
 struct KParams {
-  const DevImage* imgs;
+  const DevRef* refs;              // per image: coefficient planes + kind
+  const DevImage* kinds;           // per kind: geometry, strides, quant table ids
   const uint16_t* qtables;
   void* out;
   int OW, OH, tile_rows, tile_cols, n_col_tiles, n_row_tiles;
@@ -494,7 +495,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   __shared__ TileLayout L;
   __shared__ int ctr[2];                   // dynamic work counter of the output phase (ctr[1])
   if (tid == 0) {
-    im = kp.imgs[n];
+    const DevRef r = kp.refs[n];
+    im = kp.kinds[r.kind];
+    im.coef[0] = r.coef[0]; im.coef[1] = r.coef[1]; im.coef[2] = r.coef[2];
     tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP, GC);
     ctr[1] = 0;
   }

@@ -358,13 +358,15 @@ struct smol_preproc_plan {
   int num_sms = 148;
   int min_col_tiles = 1;                  // SMOL_COL_TILES=k forces >= k column tiles (A/B)
   int nt_mode = 0;                        // SMOL_THREADS=192|256 forces the CTA size (A/B)
-  DevImage* d_desc = nullptr;  // [kRing][max_images]
+  DevImage* d_desc = nullptr;  // [kRing][max_images] image kinds
+  DevRef* d_ref = nullptr;     // [kRing][max_images] per-image references
   int4* d_map = nullptr;       // [kRing][map_cap] balanced CTA map (see run_impl)
   int4* h_map = nullptr;       // pinned
   int map_cap = 0;
   int cta_map_mode = 1;        // SMOL_CTA_MAP=0 disables the balanced map (A/B)
   int thumb_mode = 1;          // SMOL_THUMB=0 disables the warp-per-image 1/8 kernel (A/B)
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
+  DevRef* h_ref = nullptr;     // pinned [kRing][max_images]
   cudaEvent_t ev[kRing] = {};
   cudaEvent_t desc_ready[kRing] = {};      // descriptor upload of a ring slot done (copy stream)
   int ring = 0;
@@ -468,6 +470,8 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_ref, sizeof(DevRef) * (size_t)max_images * kRing);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_ref, sizeof(DevRef) * (size_t)max_images * kRing);
   for (int i = 0; i < kRing && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->desc_ready[i], cudaEventDisableTiming);
@@ -560,6 +564,8 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (pl->d_map) cudaFree(pl->d_map);
   if (pl->h_map) cudaFreeHost(pl->h_map);
   if (pl->h_desc) cudaFreeHost(pl->h_desc);
+  if (pl->d_ref) cudaFree(pl->d_ref);
+  if (pl->h_ref) cudaFreeHost(pl->h_ref);
   const int dev = pl->device;
   delete pl;
   if (prev >= 0 && prev != dev) cudaSetDevice(prev);
@@ -672,28 +678,58 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   const int slot = pl->ring;
   pl->ring = (pl->ring + 1) % kRing;
   SMOL_CUDA(cudaEventSynchronize(pl->ev[slot]));
-  DevImage* h = pl->h_desc + (size_t)slot * pl->max_images;
+  DevImage* h = pl->h_desc + (size_t)slot * pl->max_images;   // kinds
   DevImage* d = pl->d_desc + (size_t)slot * pl->max_images;
+  DevRef* hr = pl->h_ref + (size_t)slot * pl->max_images;      // per image
+  DevRef* dr = pl->d_ref + (size_t)slot * pl->max_images;
 
   // provisional tile height (4 CTAs per SM); final once the CTA size is known
   const bool auto_rows = pl->tile_rows <= 0;
   int tile_rows = auto_rows ? auto_tile_rows(pl->OH, n_images, pl->num_sms * 4) : imin(pl->tile_rows, pl->OH);
   int ntiles = ceil_div(pl->OH, tile_rows);
-  // validate every descriptor once
+  // validate every descriptor once; consecutive images whose descriptors
+  // differ only in their coefficient pointers (compact: record offsets)
+  // share one kind, so per image only the pointers are checked and written
+  int nk = 0;
   for (int i = 0; i < n_images; ++i) {
-    int32_t rc;
+    int32_t rc = SMOL_OK;
     if (src == Src::kCompact) {
       const smol_compact_image* ci = static_cast<const smol_compact_image*>(images);
-      const bool same = i > 0 && ci[i].width == ci[i - 1].width && ci[i].height == ci[i - 1].height &&
+      const bool same = i > 0 && memcmp(&ci[i], &ci[i - 1], offsetof(smol_compact_image, offset)) == 0;
+      if (!same) {
+        const bool sg = i > 0 && ci[i].width == ci[i - 1].width && ci[i].height == ci[i - 1].height &&
                         ci[i].subsampling == ci[i - 1].subsampling && ci[i].roi_left == ci[i - 1].roi_left &&
                         ci[i].roi_top == ci[i - 1].roi_top && ci[i].roi_x == ci[i - 1].roi_x &&
                         ci[i].roi_y == ci[i - 1].roi_y && ci[i].roi_w == ci[i - 1].roi_w &&
                         ci[i].roi_h == ci[i - 1].roi_h;
-      rc = validate_compact_image(&pl->p, &ci[i], i, n_qtables, h[i], same ? &h[i - 1] : nullptr);
+        rc = validate_compact_image(&pl->p, &ci[i], i, n_qtables, h[nk], sg ? &h[nk - 1] : nullptr);
+        ++nk;
+      } else if (ci[i].offset < 0 || ci[i].offset % 16) {
+        rc = fail(SMOL_ERR_INVALID, "image %d: record offset %lld not a non-negative multiple of 16", i,
+                  (long long)ci[i].offset);
+      }
+      hr[i].kind = nk - 1;
+      hr[i].coef[0] = hr[i].coef[1] = hr[i].coef[2] = nullptr;
     } else {
       const smol_image_desc* di = static_cast<const smol_image_desc*>(images);
-      const bool same = i > 0 && same_geometry(&di[i], &di[i - 1]);
-      rc = validate_image(&pl->p, &di[i], i, n_qtables, h[i], true, same ? &h[i - 1] : nullptr);
+      // (fields before and after the coefficient pointers)
+      const bool same = i > 0 && memcmp(&di[i], &di[i - 1], offsetof(smol_image_desc, coef)) == 0 &&
+                        memcmp(&di[i].blocks_w, &di[i - 1].blocks_w,
+                               sizeof(smol_image_desc) - offsetof(smol_image_desc, blocks_w)) == 0;
+      if (!same) {
+        const bool sg = i > 0 && same_geometry(&di[i], &di[i - 1]);
+        rc = validate_image(&pl->p, &di[i], i, n_qtables, h[nk], true, sg ? &h[nk - 1] : nullptr);
+        ++nk;
+      } else {
+        for (int c = 0; c < (h[nk - 1].gray ? 1 : 3) && !rc; ++c)
+          if (!di[i].coef[c] || reinterpret_cast<uintptr_t>(di[i].coef[c]) % 16)
+            rc = fail(SMOL_ERR_INVALID, "image %d: coef[%d] NULL or not 16-byte aligned", i, c);
+      }
+      hr[i].kind = nk - 1;
+      const bool gray = h[nk - 1].gray;
+      hr[i].coef[0] = di[i].coef[0];
+      hr[i].coef[1] = gray ? nullptr : di[i].coef[1];
+      hr[i].coef[2] = gray ? nullptr : di[i].coef[2];
     }
     if (rc) return rc;
   }
@@ -703,13 +739,13 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // a batch with any 4:2:2 / 4:4:4 image runs the generic-chroma kernel
   // (wide CTA only; its chroma rings are full-size)
   bool gc = false;
-  for (int i = 0; i < n_images && !gc; ++i) gc = h[i].hs != 2 || h[i].vs != 2;
+  for (int i = 0; i < nk && !gc; ++i) gc = h[i].hs != 2 || h[i].vs != 2;
   auto max_smem = [&](int n_col_tiles, int yp) {
     const int tile_cols = cols_of(n_col_tiles);
     n_col_tiles = ceil_div(pl->OW, tile_cols);
     int m = 0;
     const DevImage* prev = nullptr;
-    for (int i = 0; i < n_images; ++i) {
+    for (int i = 0; i < nk; ++i) {
       const DevImage& g = h[i];
       if (prev && same_layout_inputs(g, *prev)) continue;
       for (int t = 0; t < ntiles; ++t)
@@ -779,7 +815,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // c4 packed 47.5 M -> 52.1 M img/s, dense 33.6 M -> 27.0 M).
   bool thumb = K == 8 && packed && !dbg && !gc && pl->thumb_mode && pl->OW <= kThumbMaxOut &&
                pl->OH <= kThumbMaxOut;
-  for (int i = 0; thumb && i < n_images; ++i) {
+  for (int i = 0; thumb && i < nk; ++i) {
     if (i > 0 && same_layout_inputs(h[i], h[i - 1])) continue;
     TileLayout L;
     tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L, kYPTiny);
@@ -829,18 +865,22 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     size_t need = 0;
     size_t offs[3];
     int32_t strides[3];
-    std::vector<TileLayout>& Ls = pl->layouts;
-    Ls.resize(n_images);
+    std::vector<TileLayout>& Ls = pl->layouts;      // per kind (images of a kind share their ROI ranges)
+    Ls.resize(nk);
+    for (int k = 0; k < nk; ++k) {
+      if (k > 0 && same_layout_inputs(h[k], h[k - 1])) Ls[k] = Ls[k - 1];
+      else tile_layout(h[k], K, 0, pl->OH, 0, pl->OW, Ls[k], kYPWide, true);
+    }
     for (int i = 0; i < n_images; ++i) {
-      TileLayout& L = Ls[i];
-      if (i > 0 && same_layout_inputs(h[i], h[i - 1])) L = Ls[i - 1];
-      else tile_layout(h[i], K, 0, pl->OH, 0, pl->OW, L, kYPWide, true);
+      const int kd = hr[i].kind;
+      const TileLayout& L = Ls[kd];
       need = stage_layout(L, E, strides, offs, need);
       for (int c = 0; c < 3; ++c) {
         if (src == Src::kGather) {
           GatherDesc& g = hg[i];
-          g.src[c] = h[i].coef[c];
-          g.src_stride[c] = h[i].stride[c];
+          const smol_image_desc& di = static_cast<const smol_image_desc*>(images)[i];
+          g.src[c] = hr[i].coef[c];
+          g.src_stride[c] = di.row_stride_bytes[c] / 2;
           g.by0[c] = L.by0[c];
           g.rows[c] = L.by1[c] - L.by0[c] + 1;
           g.col0[c] = L.bx0[c] * E;
@@ -855,21 +895,23 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
           e.nby[c] = L.by1[c] - L.by0[c] + 1;
           e.E = E;
         }
-        h[i].stride[c] = strides[c];
       }
     }
+    for (int k = 0; k < nk; ++k)            // staged planes: the kind's rows have the staged stride
+      stage_layout(Ls[k], E, h[k].stride, offs, 0);
     void* sbuf = pl->stage[sl];
     int32_t rc = grow(&sbuf, &pl->stage_cap[sl], need * 2, pl->copy_stream, pl->fixed_stage, "staging");
     pl->stage[sl] = static_cast<int16_t*>(sbuf);
     if (rc) return rc;
     int16_t* base = pl->stage[sl];
     for (int i = 0; i < n_images; ++i) {
-      const TileLayout& L = Ls[i];
+      const int kd = hr[i].kind;
+      const TileLayout& L = Ls[kd];
       for (int c = 0; c < 3; ++c) {
         int16_t** dp = src == Src::kGather ? &hg[i].dst[c] : &he[i].dst[c];
         *dp = base + reinterpret_cast<size_t>(*dp);
-        // descriptor of the staged plane: same absolute block indexing
-        h[i].coef[c] = *dp - (ptrdiff_t)L.by0[c] * h[i].stride[c] - (ptrdiff_t)L.bx0[c] * E;
+        // reference to the staged plane: same absolute block indexing
+        hr[i].coef[c] = *dp - (ptrdiff_t)L.by0[c] * h[kd].stride[c] - (ptrdiff_t)L.bx0[c] * E;
       }
     }
     // Every host->device copy of a staged run goes on the copy stream, small
@@ -878,7 +920,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     SMOL_CUDA(cudaStreamWaitEvent(pl->copy_stream, pl->stage_free[sl], 0));   // previous user done
     if (src == Src::kGather) {
       SMOL_CUDA(cudaMemcpyAsync(dg, hg, sizeof(GatherDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
-      SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
+    SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       smol_gather_kernel<<<n_images, 256, 0, pl->copy_stream>>>(dg);
       SMOL_CUDA(cudaGetLastError());
     } else {
@@ -906,7 +949,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
           memcpy(&hd, arena + ci[i].offset, sizeof(hd));
           bool ok = hd.magic == kCompactMagic && (int)hd.E == E;
           for (int c = 0; c < 3 && ok; ++c)
-            ok = hd.bx0[c] == Ls[i].bx0[c] && hd.by0[c] == Ls[i].by0[c] && hd.nbx[c] == e.nbx[c] &&
+            ok = hd.bx0[c] == Ls[hr[i].kind].bx0[c] && hd.by0[c] == Ls[hr[i].kind].by0[c] && hd.nbx[c] == e.nbx[c] &&
                  hd.nby[c] == e.nby[c];
           if (!ok)
             return fail(SMOL_ERR_INVALID, "image %d: compact record header does not match this plan's "
@@ -950,7 +993,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       }
       for (int i = 0; i < n_images; ++i) he[i].rec = rec_base + (ci[i].offset - lo);
       SMOL_CUDA(cudaMemcpyAsync(de, he, sizeof(ExpandDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
-      SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
+    SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       if (!on_device)
         SMOL_CUDA(cudaMemcpyAsync(pl->cbuf[sl], arena + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice,
                                   pl->copy_stream));
@@ -971,20 +1015,23 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   SMOL_CUDA(cudaStreamIsCapturing(stream, &cap));
   if (src == Src::kDevice && cap != cudaStreamCaptureStatusNone) {
     // (being captured into a CUDA graph: keep every operation on `stream`)
-    SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, stream));
+    SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, stream));
+    SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, stream));
     if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, stream));
   } else if (src == Src::kDevice) {
     // descriptors (and the CTA map) go up on the plan's copy stream, so the
     // copy for run k+1 overlaps run k's kernel instead of sitting between
     // the kernels on `stream` (4096 thumbnails: 512 KB per run); the ring
     // slot is free (host waited on ev[slot] above)
-    SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+    SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
+    SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
     if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaEventRecord(pl->desc_ready[slot], pl->copy_stream));
     SMOL_CUDA(cudaStreamWaitEvent(stream, pl->desc_ready[slot], 0));
   }
   KParams kp = dbg ? *dbg : KParams{};
-  kp.imgs = d;
+  kp.refs = dr;
+  kp.kinds = d;
   kp.qtables = qtables;
   kp.out = out;
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;
@@ -994,7 +1041,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   // rows, i.e. under vertical magnification (measured r02: c3b 0.0556 ->
   // 0.0488 ms, c3a 0.0822 -> 0.0800; slower where rows are skipped: c2, c5).
   kp.rowrun = 1;
-  for (int i = 0; i < n_images && kp.rowrun; ++i) kp.rowrun = h[i].Hr >= h[i].sh;
+  for (int i = 0; i < nk && kp.rowrun; ++i) kp.rowrun = h[i].Hr >= h[i].sh;
   kp.tile_cols = cols_of(n_col_tiles);
   kp.n_col_tiles = n_col_tiles = ceil_div(pl->OW, kp.tile_cols);
   for (int c = 0; c < 3; ++c) { kp.na[c] = pl->na[c]; kp.nb[c] = pl->nb[c]; }

@@ -41,7 +41,9 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
   const int OW = kp.OW, OH = kp.OH;
   const uint32_t plane = (uint32_t)OW * OH;
   for (int n = blockIdx.x * kThumbWarps + warp; n < n_images; n += gridDim.x * kThumbWarps) {
-    const DevImage im = kp.imgs[n];
+    const DevRef ref = kp.refs[n];
+    DevImage im = kp.kinds[ref.kind];
+    im.coef[0] = ref.coef[0]; im.coef[1] = ref.coef[1]; im.coef[2] = ref.coef[2];
     if (lane == 0) tile_layout(im, 8, 0, OH, 0, OW, S.L, kYPTiny);
     __syncwarp();
     const int lx0 = S.L.lx0, ly0 = S.L.ly0, fw = S.L.lx1 - lx0 + 1, fh = S.L.ly1 - ly0 + 1;
