@@ -435,6 +435,8 @@ __device__ __forceinline__ int ldu8(const uint8_t* p) { return *p; }
 struct KParams {
   const DevRef* refs;              // per image: coefficient planes + kind
   const DevImage* kinds;           // per kind: geometry, strides, quant table ids
+  const TileLayout* lays;          // per (kind, tile): the tile's layout (null: computed in the kernel)
+  int lay_stride;                  // layouts per kind
   const uint16_t* qtables;
   void* out;
   int OW, OH, tile_rows, tile_cols, n_col_tiles, n_row_tiles;
@@ -487,7 +489,7 @@ __device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
 
 template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB, bool GC>
 __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const int oy0, const int oy1,
-                                       const int ox0, const int ox1) {
+                                       const int ox0, const int ox1, const int lay_local) {
   constexpr int P = 8 / K;                 // decoded samples per block side
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -498,7 +500,10 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     const DevRef r = kp.refs[n];
     im = kp.kinds[r.kind];
     im.coef[0] = r.coef[0]; im.coef[1] = r.coef[1]; im.coef[2] = r.coef[2];
-    tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP, GC);
+    // the tile's layout: precomputed by the host per (image kind, tile), or
+    // computed here when the table did not fit
+    if (kp.lays) L = kp.lays[r.kind * kp.lay_stride + lay_local];
+    else tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP, GC);
     ctr[1] = 0;
   }
   __syncthreads();
@@ -1059,19 +1064,19 @@ __host__ __device__ constexpr int kCtasPerSm(int threads) {
 template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB = false, bool GC = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm<K>(kThreads))
 smol_fused_kernel(const __grid_constant__ KParams kp) {
-  int n, oy0, oy1, ox0, ox1;
-  if (kp.cta_map) {            // 1-D grid: per-CTA {image, oy0, oy1} (full-width tiles)
+  int n, oy0, oy1, ox0, ox1, local;
+  if (kp.cta_map) {            // 1-D grid: per-CTA {image, oy0, oy1, layout} (full-width tiles)
     const int4 m = kp.cta_map[blockIdx.x];
-    n = m.x; oy0 = m.y; oy1 = m.z; ox0 = 0; ox1 = kp.OW;
+    n = m.x; oy0 = m.y; oy1 = m.z; ox0 = 0; ox1 = kp.OW; local = m.w;
   } else {                     // 1-D grid: image-major, then row tile, then column tile
     const int per_img = kp.n_row_tiles * kp.n_col_tiles;
     n = blockIdx.x / per_img;
-    const int rem = blockIdx.x - n * per_img;
-    const int trow = rem / kp.n_col_tiles, tcol = rem - trow * kp.n_col_tiles;
+    local = blockIdx.x - n * per_img;
+    const int trow = local / kp.n_col_tiles, tcol = local - trow * kp.n_col_tiles;
     oy0 = trow * kp.tile_rows; oy1 = min(kp.OH, oy0 + kp.tile_rows);
     ox0 = tcol * kp.tile_cols; ox1 = min(kp.OW, ox0 + kp.tile_cols);
   }
-  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP, DB, GC>(kp, n, oy0, oy1, ox0, ox1);
+  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP, DB, GC>(kp, n, oy0, oy1, ox0, ox1, local);
 }
 
 }  // namespace smol

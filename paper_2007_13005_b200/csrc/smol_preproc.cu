@@ -367,6 +367,9 @@ struct smol_preproc_plan {
   int thumb_mode = 1;          // SMOL_THUMB=0 disables the warp-per-image 1/8 kernel (A/B)
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
   DevRef* h_ref = nullptr;     // pinned [kRing][max_images]
+  TileLayout* d_lay = nullptr; // [kRing][lay_cap] tile layouts per (kind, tile)
+  TileLayout* h_lay = nullptr; // pinned
+  int lay_cap = 0;
   cudaEvent_t ev[kRing] = {};
   cudaEvent_t desc_ready[kRing] = {};      // descriptor upload of a ring slot done (copy stream)
   int ring = 0;
@@ -472,6 +475,9 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_desc, sizeof(DevImage) * (size_t)max_images * kRing);
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_ref, sizeof(DevRef) * (size_t)max_images * kRing);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_ref, sizeof(DevRef) * (size_t)max_images * kRing);
+  pl->lay_cap = std::min(4 * max_images, 4096) + 256;
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_lay, sizeof(TileLayout) * (size_t)pl->lay_cap * kRing);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_lay, sizeof(TileLayout) * (size_t)pl->lay_cap * kRing);
   for (int i = 0; i < kRing && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->desc_ready[i], cudaEventDisableTiming);
@@ -565,6 +571,8 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (pl->h_map) cudaFreeHost(pl->h_map);
   if (pl->h_desc) cudaFreeHost(pl->h_desc);
   if (pl->d_ref) cudaFree(pl->d_ref);
+  if (pl->d_lay) cudaFree(pl->d_lay);
+  if (pl->h_lay) cudaFreeHost(pl->h_lay);
   if (pl->h_ref) cudaFreeHost(pl->h_ref);
   const int dev = pl->device;
   delete pl;
@@ -841,13 +849,39 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
         for (int i = pass == 0 ? extra : 0; i < (pass == 0 ? n_images : extra); ++i) {
           const int t = ntiles + (i < extra ? 1 : 0);
           for (int j = 0; j < t; ++j)
-            hm[map_n++] = make_int4(i, (int)((long long)j * pl->OH / t), (int)((long long)(j + 1) * pl->OH / t), 0);
+            hm[map_n++] = make_int4(i, (int)((long long)j * pl->OH / t), (int)((long long)(j + 1) * pl->OH / t),
+                                    t == ntiles ? j : ntiles + j);      // layout: t-tile slot j
         }
       smem += 64;      // tile positions differ from the uniform grid's: one step of slack
     }
   }
   if (smem > pl->smem_optin)
     return fail(SMOL_ERR_CAPACITY, "tile needs %d B of shared memory > %d; lower tile_rows", smem, pl->smem_optin);
+
+  // Tile layouts per (image kind, tile), so no CTA (or thumbnail warp)
+  // computes its own with a serial lane: the grid's row x column tiles, the
+  // balanced map's t- and (t+1)-tile splits, or the thumbnail's one tile.
+  // (Left to the kernel when the table would not fit its ring slot.)
+  const int lay_stride = thumb ? 1 : map_n ? 2 * ntiles + 1 : ntiles * n_col_tiles;
+  TileLayout* hl = pl->h_lay + (size_t)slot * pl->lay_cap;
+  TileLayout* dl = pl->d_lay + (size_t)slot * pl->lay_cap;
+  int nl = (long long)nk * lay_stride <= pl->lay_cap ? nk * lay_stride : 0;
+  {
+    const int tcols = cols_of(n_col_tiles), yp = thumb ? kYPTiny : Cfg_yp(nt);
+    for (int k = 0; k < nk && nl; ++k)
+      for (int j = 0; j < lay_stride; ++j) {
+        int oy0 = 0, oy1 = pl->OH, ox0 = 0, ox1 = pl->OW;
+        if (map_n) {                         // slot j < ntiles: j of ntiles; else j - ntiles of ntiles + 1
+          const int t = j < ntiles ? ntiles : ntiles + 1, jj = j < ntiles ? j : j - ntiles;
+          oy0 = (int)((long long)jj * pl->OH / t); oy1 = (int)((long long)(jj + 1) * pl->OH / t);
+        } else if (!thumb) {
+          const int trow = j / n_col_tiles, tcol = j - trow * n_col_tiles;
+          oy0 = trow * tile_rows; oy1 = imin(pl->OH, oy0 + tile_rows);
+          ox0 = tcol * tcols; ox1 = imin(pl->OW, ox0 + tcols);
+        }
+        tile_layout(h[k], K, oy0, oy1, ox0, ox1, hl[(size_t)k * lay_stride + j], yp, gc && !thumb);
+      }
+  }
 
   if (src != Src::kDevice) {
     // Staged paths: each image's ROI block rows (the whole output's tap
@@ -922,6 +956,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       SMOL_CUDA(cudaMemcpyAsync(dg, hg, sizeof(GatherDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, pl->copy_stream));
       smol_gather_kernel<<<n_images, 256, 0, pl->copy_stream>>>(dg);
       SMOL_CUDA(cudaGetLastError());
     } else {
@@ -995,6 +1030,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       SMOL_CUDA(cudaMemcpyAsync(de, he, sizeof(ExpandDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, pl->copy_stream));
       if (!on_device)
         SMOL_CUDA(cudaMemcpyAsync(pl->cbuf[sl], arena + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice,
                                   pl->copy_stream));
@@ -1017,6 +1053,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     // (being captured into a CUDA graph: keep every operation on `stream`)
     SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, stream));
     SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, stream));
+    if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, stream));
     if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, stream));
   } else if (src == Src::kDevice) {
     // descriptors (and the CTA map) go up on the plan's copy stream, so the
@@ -1025,6 +1062,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     // slot is free (host waited on ev[slot] above)
     SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+    if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, pl->copy_stream));
     if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaEventRecord(pl->desc_ready[slot], pl->copy_stream));
     SMOL_CUDA(cudaStreamWaitEvent(stream, pl->desc_ready[slot], 0));
@@ -1032,6 +1070,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   KParams kp = dbg ? *dbg : KParams{};
   kp.refs = dr;
   kp.kinds = d;
+  kp.lays = nl ? dl : nullptr;
+  kp.lay_stride = lay_stride;
   kp.qtables = qtables;
   kp.out = out;
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;

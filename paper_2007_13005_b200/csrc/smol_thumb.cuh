@@ -44,7 +44,10 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     const DevRef ref = kp.refs[n];
     DevImage im = kp.kinds[ref.kind];
     im.coef[0] = ref.coef[0]; im.coef[1] = ref.coef[1]; im.coef[2] = ref.coef[2];
-    if (lane == 0) tile_layout(im, 8, 0, OH, 0, OW, S.L, kYPTiny);
+    if (lane == 0) {
+      if (kp.lays) S.L = kp.lays[ref.kind * kp.lay_stride];     // precomputed per image kind
+      else tile_layout(im, 8, 0, OH, 0, OW, S.L, kYPTiny);
+    }
     __syncwarp();
     const int lx0 = S.L.lx0, ly0 = S.L.ly0, fw = S.L.lx1 - lx0 + 1, fh = S.L.ly1 - ly0 + 1;
     const int cx0 = S.L.cx0, cy0 = S.L.cy0, cw = S.L.cx1 - cx0 + 1, ch = S.L.cy1 - cy0 + 1;

@@ -10,4 +10,5 @@ for spec in $CFGS; do
   ncu -i gpurun_out/prof_${TAG}_$cfg.ncu-rep --page source --csv --print-source sass > gpurun_out/sass_${TAG}_$cfg.csv 2>/dev/null
   python scripts/tools_ncu.py gpurun_out/prof_${TAG}_$cfg.ncu-rep > gpurun_out/summary_${TAG}_$cfg.txt 2>&1
   head -12 gpurun_out/summary_${TAG}_$cfg.txt
+  [ "$cfg" != "c2" ] && rm -f gpurun_out/prof_${TAG}_$cfg.ncu-rep   # (gpurun_out merge cap: summaries + SASS CSVs kept)
 done
