@@ -110,6 +110,11 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
   const uint8_t* len_all = e.rec + kCompactHeader;
   const uint32_t* rowst = reinterpret_cast<const uint32_t*>(e.rec + compact_rowstart_off(nblocks));
   const uint16_t* units = reinterpret_cast<const uint16_t*>(e.rec + compact_entries_off(nblocks, nrows));
+  // record-supplied counts are clamped (a corrupt record must not make this
+  // kernel read or write out of bounds): units per block <= 2 E (<= 128),
+  // every staged unit inside the record's n_units
+  const uint32_t n_units = reinterpret_cast<const CompactHeader*>(e.rec)->n_units;
+  const int max_len = 2 * E < 128 ? 2 * E : 128;
   for (int gr = part * kExpandWarps + warp; gr < nrows; gr += kExpandWarps * kExpandSplit) {
     const int c = gr >= r2 ? 2 : gr >= r1 ? 1 : 0;
     const int r = gr - (c == 2 ? r2 : c == 1 ? r1 : 0);
@@ -118,17 +123,21 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
     int16_t* const dst_c = c == 2 ? e.dst[2] : c == 1 ? e.dst[1] : e.dst[0];
     const int stride_c = c == 2 ? e.dst_stride[2] : c == 1 ? e.dst_stride[1] : e.dst_stride[0];
     int16_t* drow = dst_c + (int64_t)r * stride_c;
-    uint32_t vbase = __ldg(rowst + gr);
+    uint32_t vbase = min(__ldg(rowst + gr), n_units);
     for (int ch = 0; ch < nbx; ch += 32) {
       const int b = ch + lane;
-      const int cnt = b < nbx ? (int)__ldg(lens + b) : 0;   // units of this block's entries
+      const int cnt = b < nbx ? min((int)__ldg(lens + b), max_len) : 0;   // units of this block's entries
       int inc = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += t;
       }
-      const int total = __shfl_sync(0xffffffffu, inc, 31);
+      // this lane's units are [inc - cnt, inc) of the chunk; a row overrunning
+      // the record is cut at n_units (later blocks' ranges shrink to nothing)
+      const int total = min(__shfl_sync(0xffffffffu, inc, 31), (int)(n_units - vbase));
+      const int first = min(inc - cnt, total);
+      const int cntc = min(inc, total) - first;
       // 2. stage the chunk's entry units (32-bit loads from the 4-B aligned start)
       const uint16_t* src = units + vbase;
       const int mis = (int)(reinterpret_cast<uintptr_t>(src) & 3) >> 1;     // 0 or 1 unit
@@ -137,12 +146,12 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
       uint32_t* b32 = reinterpret_cast<uint32_t*>(buf);
       for (int w = lane; w < nw; w += 32) b32[w] = __ldg(s32 + w);
       const int nb = min(32, nbx - ch);
-      const uint16_t* ub = reinterpret_cast<const uint16_t*>(buf) + mis + (inc - cnt);
+      const uint16_t* ub = reinterpret_cast<const uint16_t*>(buf) + mis + first;
       if (E == 1) {
         __syncwarp();
         if (b < nbx) {
           int16_t v = 0;
-          if (cnt) {
+          if (cntc) {
             v = (int16_t)ub[0] >> 6;
             if (v == kEscape) v = (int16_t)ub[1];
           }
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
         uint2* m8 = reinterpret_cast<uint2*>(mine);
         for (int q = 0; q < E / 4; ++q) m8[q] = make_uint2(0u, 0u);
         __syncwarp();                                       // staged entries visible
-        for (int j = 0; j < cnt; ++j) {
+        for (int j = 0; j < cntc; ++j) {
           const uint16_t u = ub[j];
           int16_t v = (int16_t)u >> 6;
           if (v == kEscape) v = (int16_t)ub[++j];

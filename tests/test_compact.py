@@ -250,3 +250,32 @@ def test_run_compact_int16_extremes_equal_dense():
         assert torch.equal(a, b), k
         assert torch.isfinite(a).all()
         plan.close()
+
+
+@pytest.mark.gpu
+def test_run_compact_corrupt_lengths_do_not_fault():
+    """Block lengths and row starts of a record are clamped inside the expand
+    kernel (not re-scanned on the host): a record with lengths of 255 and
+    row starts past its end gives garbage samples for that image but no
+    out-of-bounds access -- the context stays usable and the other images
+    of the batch are unaffected."""
+    import torch
+    cfg = synth.CONFIGS["c2"]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=3)
+    ps = smol.params_from_config(cfg)
+    plan = smol.Plan(ps, 3)
+    good = plan.run(smol.CompactBatch(ps, imgs, qt))
+    cb = smol.CompactBatch(ps, imgs, qt)
+    rec0 = cb.arena.numpy()                  # pinned host arena (a view)
+    g = smol.geometry(ps, imgs[0].width, imgs[0].height)
+    nblocks = sum((g["bx1"][c] - g["bx0"][c] + 1) * (g["by1"][c] - g["by0"][c] + 1) for c in range(3))
+    rec0[64:64 + nblocks] = 255              # image 0: every block length 255
+    rs = (64 + nblocks + 3) & ~3
+    rec0[rs:rs + 40] = 0xff                  # first row starts far past the record
+    bad = plan.run(cb)
+    torch.cuda.synchronize()                 # raises if the expand kernel faulted
+    assert torch.equal(bad[1:], good[1:])
+    again = plan.run(smol.CompactBatch(ps, imgs, qt))
+    torch.cuda.synchronize()
+    assert torch.equal(again, good)
+    plan.close()
