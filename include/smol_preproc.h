@@ -164,8 +164,16 @@ typedef struct {
 int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
                           smol_preproc_plan_t** out);
 
-/* Run the fused path on `stream`.  out: DEVICE [n][3][OH][OW] fp32/fp16.
- * Validates every descriptor before any launch (status + smol_last_error). */
+/* Run the fused path on `stream`.  out: DEVICE [n][3][OH][OW] fp32/fp16,
+ * aligned to its element size (vector stores are used when it is 16-B
+ * (fp32) / 8-B (fp16) aligned).  Validates every descriptor before any
+ * launch (status + smol_last_error); consecutive descriptors that differ only
+ * in their coef pointers share one validated "kind" (only the pointers are
+ * checked for them).  The per-run descriptors are uploaded on the plan's
+ * internal copy stream and `stream` waits on that upload, so the next run's
+ * upload overlaps this run's kernel (while `stream` is being captured into a
+ * CUDA graph every operation stays on `stream`).  The plan's device must be
+ * the current device (SMOL_ERR_INVALID otherwise). */
 int32_t smol_preproc_run(smol_preproc_plan_t* plan, const smol_batch_desc* batch,
                          void* out, void* stream);
 
@@ -174,8 +182,12 @@ int32_t smol_preproc_run(smol_preproc_plan_t* plan, const smol_batch_desc* batch
  * kernel on the plan's internal copy stream stages them into plan-owned device
  * memory (double-buffered: the next call's transfer overlaps this call's fused
  * kernel), then the fused kernel runs on `stream`.  The staging buffers are
- * allocated on first use and grown when a larger batch arrives (the only
- * allocation in any run call).  out: DEVICE. */
+ * sized in plan when params.max_width / max_height are set (no allocation in
+ * any run call; a batch that does not fit returns SMOL_ERR_CAPACITY), else
+ * allocated on first use and grown when a larger batch arrives.  Every
+ * plane's first and last byte must be pinned host (or device) memory:
+ * checked per image (SMOL_ERR_INVALID), verified allocation ranges cached.
+ * out: DEVICE. */
 int32_t smol_preproc_run_host(smol_preproc_plan_t* plan, const smol_batch_desc* batch,
                               void* out, void* stream);
 
@@ -246,10 +258,13 @@ int32_t smol_compact_encode(const smol_preproc_params* params, const smol_image_
  * call's expand + fused kernel).  Each record's header must match the ROI ranges
  * the plan computes for its image and lie inside the arena: checked on the
  * host (SMOL_ERR_INVALID) when the arena is host memory; a DEVICE arena is
- * not read by the host, so only its record offsets are checked and the
- * records are trusted to come from smol_compact_encode with this plan's
- * params.  Staging is allocated on first use and grown for a larger batch.
- * out: DEVICE. */
+ * not read by the host, so only its record offsets are checked.  Block
+ * lengths and row starts are not re-scanned on the host: the expand kernel
+ * clamps them (units per block <= 2E, every unit inside the record's
+ * n_units), so a corrupt record gives wrong samples for its image but never
+ * an out-of-bounds access.  Staging is sized in plan when params.max_width /
+ * max_height are set (a batch that does not fit: SMOL_ERR_CAPACITY), else
+ * allocated on first use and grown for a larger batch.  out: DEVICE. */
 int32_t smol_preproc_run_compact(smol_preproc_plan_t* plan, const smol_compact_batch* batch,
                                  void* out, void* stream);
 
