@@ -26,9 +26,6 @@
 // scale 1 the output tasks share the phase with the next step's IDCT and are
 // grabbed dynamically, two per lane per grab, interleaved by the compiler; at
 // scales 1/2..1/8 that IDCT is small and a static stride wins.
-#ifndef SMOL_KO
-#define SMOL_KO 0                // diagnostic knockouts (1 IDCT, 2 colour, 4 output math); 0 in products
-#endif
 #ifndef SMOL_OUT_RUN_ROWS
 #define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
 #endif
@@ -327,12 +324,6 @@ __device__ __forceinline__ void decode_block(bool act, const int16_t* src, const
     for (int v = 0; v < 8; ++v) rows |= ((raw[v].x | raw[v].y | raw[v].z | raw[v].w) != 0) << v;
     // prune by the warp's highest nonzero coefficient row (one code variant
     // per extent: more variants cost more in I-cache misses than they save)
-#if SMOL_KO & 1
-    // diagnostic knockout (never a product build): loads kept, IDCT math dropped
-#pragma unroll
-    for (int y = 0; y < 8; ++y) { px[y][0] = raw[y].x ^ raw[y].z; px[y][1] = raw[y].y ^ raw[y].w; }
-    return;
-#endif
     const int H = (int)__reduce_max_sync(0xffffffffu, 32 - __clz(rows));
     // (a column pass on FFMA2 row pairs, and both passes on packed column
     // pairs, measured no faster: r02 A/B)
@@ -801,17 +792,10 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         const int slot = rgb_slot(2 * j);
         uint32_t* r0p = rgb + slot * rgb_p + (2 * i - L.rgb_x0);
         const uint32_t mg = 0x4B000000u;
-        #if SMOL_KO & 2
-        // diagnostic knockout: upsample kept, colour conversion dropped
-        const uint2 t01 = make_uint2(y0 ^ cbq[0], y1 ^ crq[0]), t23 = make_uint2(y0 ^ cbq[2], y1 ^ crq[2]);
-        const uint2 b01 = make_uint2(y0 ^ cbq[4], y1 ^ crq[4]), b23 = make_uint2(y0 ^ cbq[6], y1 ^ crq[6]);
-        (void)mg;
-#else
-const uint2 t01 = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x7541), cbq[0], cbq[1], crq[0], crq[1]);
+        const uint2 t01 = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x7541), cbq[0], cbq[1], crq[0], crq[1]);
         const uint2 t23 = colour2m(__byte_perm(y0, mg, 0x7542), __byte_perm(y0, mg, 0x7543), cbq[2], cbq[3], crq[2], crq[3]);
         const uint2 b01 = colour2m(__byte_perm(y1, mg, 0x7540), __byte_perm(y1, mg, 0x7541), cbq[4], cbq[5], crq[4], crq[5]);
         const uint2 b23 = colour2m(__byte_perm(y1, mg, 0x7542), __byte_perm(y1, mg, 0x7543), cbq[6], cbq[7], crq[6], crq[7]);
-        #endif
         const uint4 top = make_uint4(t01.x, t01.y, t23.x, t23.y);
         *reinterpret_cast<uint4*>(r0p) = top;
         *reinterpret_cast<uint4*>(r0p + rgb_p) = make_uint4(b01.x, b01.y, b23.x, b23.y);
@@ -990,14 +974,6 @@ const uint2 t01 = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x75
           const uint32_t q00 = lds_u32(row0 + tx.y), q01 = lds_u32(row0 + tx.y + 4);
           const uint32_t q10 = lds_u32(row1 + tx.y), q11 = lds_u32(row1 + tx.y + 4);
 #pragma unroll
-#if SMOL_KO & 4
-          // diagnostic knockout: loads and stores kept, bilinear + normalize dropped
-          for (int ch = 0; ch < 3; ++ch) {
-            y[ch][e] = __uint_as_float((p00 ^ p11) + ch);
-            y[ch][e + 1] = __uint_as_float((q00 ^ q11 ^ p01 ^ p10 ^ q01 ^ q10) + ch);
-          }
-          if (false)
-#endif
           for (int ch = 0; ch < 3; ++ch) {
             const int sel = 0x7540 + ch;
             const float2 fa = make_float2(__uint_as_float(__byte_perm(p00, magic, sel)), __uint_as_float(__byte_perm(q00, magic, sel)));
