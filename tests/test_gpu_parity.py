@@ -641,3 +641,53 @@ def test_chroma_subsampling_variants(ss, k, layout):
         c = plan.run(smol.CompactBatch(ps, mixed, qt)).float().cpu().numpy()
         assert np.array_equal(c, m)
     plan.close()
+
+
+@pytest.mark.parametrize("k,ss,f16", [(2, 444, True), (4, 422, False), (1, 444, True)])
+def test_variants_combined(k, ss, f16):
+    """Variants together: 4:2:2 / 4:4:4 images, per-image ROI rectangles,
+    Definition B (at 1/2, 1/4), fp16 output -- against the oracle."""
+    rng = np.random.default_rng(900 + k + ss)
+    qt = synth.quant_tables(95)
+    imgs = [synth.make_image(rng, w, h, qt, f"natural{ss}") for (w, h) in [(320, 240), (241, 187), (160, 160)]]
+    rects = [(33, 17, 200, 150), (0, 0, 241, 187), (80, 40, 45, 99)]
+    kw = dict(scale_denom=k, resize_mode="exact", resize_w=72, resize_h=56, out_dtype="f16" if f16 else "f32")
+    ps = smol.make_params(idct_def="truncated" if k in (2, 4) else "box", layout="packed", **kw)
+    po = oracle.make_params(idct_def="truncated" if k in (2, 4) else "box", **kw)
+    plan = smol.Plan(ps, len(imgs))
+    a = plan.run(smol.batch_for(ps, imgs, qt, roi_rects=rects))
+    c = plan.run(smol.CompactBatch(ps, imgs, qt, roi_rects=rects))
+    torch.cuda.synchronize()
+    assert torch.equal(a, c)
+    got = a.float().cpu().numpy()
+    tol = 2e-3 if f16 else 1e-4
+    for i, (im, r) in enumerate(zip(imgs, rects)):
+        ref = oracle.run_image(po, im, qt, roi_rect=r).astype(np.float64)
+        assert np.max(np.abs(got[i] - ref)) <= _band_widen(po, im, qt, tol), (i, r)
+    plan.close()
+
+
+def test_thumbnail_kernel_with_roi_rectangles(monkeypatch):
+    """Scale 1/8 thumbnails with per-image ROI rectangles take the
+    warp-per-image kernel (small windows) and equal the tiled kernel
+    (SMOL_THUMB=0) and the oracle."""
+    rng = np.random.default_rng(31)
+    qt = synth.quant_tables(75)
+    imgs = [synth.make_image(rng, 161, 161, qt) for _ in range(6)]
+    rects = [(0, 0, 161, 161), (20, 30, 100, 90), (64, 64, 8, 8), (150, 0, 11, 161), (1, 2, 3, 4), (40, 40, 81, 81)]
+    ps = smol.make_params(scale_denom=8, resize_mode="exact", resize_w=64, resize_h=64, layout="packed")
+    po = oracle.make_params(scale_denom=8, resize_mode="exact", resize_w=64, resize_h=64)
+    plan = smol.Plan(ps, len(imgs))
+    a = plan.run(smol.batch_for(ps, imgs, qt, roi_rects=rects))
+    torch.cuda.synchronize()
+    monkeypatch.setenv("SMOL_THUMB", "0")
+    plan2 = smol.Plan(ps, len(imgs))
+    b = plan2.run(smol.batch_for(ps, imgs, qt, roi_rects=rects))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    got = a.cpu().numpy()
+    for i, (im, r) in enumerate(zip(imgs, rects)):
+        ref = oracle.run_image(po, im, qt, roi_rect=r)
+        assert np.max(np.abs(got[i] - ref)) <= 1e-4, (i, r)
+    plan.close()
+    plan2.close()
