@@ -74,21 +74,20 @@ struct ExpandDesc {
 
 #if defined(__CUDACC__)
 constexpr int kExpandWarps = 4;
-constexpr int kExpandChunkVals = 32 * 128 + 8; // entry units of one 32-block chunk (worst case: all escaped) + slack
 // per-lane block buffers are padded by 8 bytes (lane stride 2E + 8 bytes) so
 // the lanes' zeroing/scatter stores do not all land in one shared-memory bank
 constexpr int kExpandLanePad = 4;               // int16 elements
 constexpr int kExpandBlkBuf = 32 * (64 + kExpandLanePad);
-// dynamic shared memory per CTA: per warp a 32-block output buffer + the chunk's values
-constexpr int kExpandSmem = kExpandWarps * (kExpandBlkBuf * 2 + kExpandChunkVals * 2);
+// dynamic shared memory per CTA: per warp a 32-block output buffer
+constexpr int kExpandSmem = kExpandWarps * kExpandBlkBuf * 2;
 constexpr int kExpandSplit = 8;                 // CTAs per image (block rows interleaved)
 
 // kExpandSplit CTAs per image (block rows interleaved); a warp expands one ROI
 // block row at a time, 32 blocks (one per lane) per chunk:
 //   1. each lane reads its block's entry length; a warp scan gives each
 //      block's first entry;
-//   2. the chunk's entries (contiguous in the record) are copied to shared
-//      memory with independent coalesced loads;
+//   2. each lane reads its block's entries straight from the record (the
+//      chunk's entries are contiguous, so neighbouring lanes share L1 lines);
 //   3. each lane zeroes its block in a shared buffer and scatters its entries
 //      into it;
 //   4. the chunk's 32 blocks are contiguous in the staged row: the warp copies
@@ -100,7 +99,6 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
   const int part = blockIdx.x % kExpandSplit;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int16_t* blk = reinterpret_cast<int16_t*>(esm) + warp * kExpandBlkBuf;
-  int16_t* buf = reinterpret_cast<int16_t*>(esm + kExpandWarps * kExpandBlkBuf * 2) + warp * kExpandChunkVals;
   const int E = e.E;
   const uint32_t fd_wpb = make_fastdiv((uint32_t)(E / 4 > 0 ? E / 4 : 1)).m;
   // component bases without dynamically indexed arrays (no local memory)
@@ -138,22 +136,18 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
       const int total = min(__shfl_sync(0xffffffffu, inc, 31), (int)(n_units - vbase));
       const int first = min(inc - cnt, total);
       const int cntc = min(inc, total) - first;
-      // 2. stage the chunk's entry units (32-bit loads from the 4-B aligned start)
-      const uint16_t* src = units + vbase;
-      const int mis = (int)(reinterpret_cast<uintptr_t>(src) & 3) >> 1;     // 0 or 1 unit
-      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src - mis);
-      const int nw = (total + mis + 1) >> 1;
-      uint32_t* b32 = reinterpret_cast<uint32_t*>(buf);
-      for (int w = lane; w < nw; w += 32) b32[w] = __ldg(s32 + w);
+      // 2. each lane reads its own entries straight from the record (the
+      // chunk's units are contiguous: neighbouring lanes share L1 lines), so
+      // no shared staging -- 3x more resident warps to hide the load latency
+      const uint16_t* ub = units + vbase + first;
       const int nb = min(32, nbx - ch);
-      const uint16_t* ub = reinterpret_cast<const uint16_t*>(buf) + mis + first;
       if (E == 1) {
         __syncwarp();
         if (b < nbx) {
           int16_t v = 0;
           if (cntc) {
-            v = (int16_t)ub[0] >> 6;
-            if (v == kEscape) v = (int16_t)ub[1];
+            v = (int16_t)__ldg(ub) >> 6;
+            if (v == kEscape) v = (int16_t)__ldg(ub + 1);
           }
           drow[b] = v;
         }
@@ -165,9 +159,9 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
         for (int q = 0; q < E / 4; ++q) m8[q] = make_uint2(0u, 0u);
         __syncwarp();                                       // staged entries visible
         for (int j = 0; j < cntc; ++j) {
-          const uint16_t u = ub[j];
+          const uint16_t u = __ldg(ub + j);
           int16_t v = (int16_t)u >> 6;
-          if (v == kEscape) v = (int16_t)ub[++j];
+          if (v == kEscape) v = (int16_t)__ldg(ub + (++j));
           mine[u & 63] = v;
         }
         __syncwarp();

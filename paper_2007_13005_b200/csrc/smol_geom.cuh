@@ -131,6 +131,13 @@ __host__ __device__ constexpr int off_q(int yp, bool gc = false) {              
 }
 __host__ __device__ constexpr int off_rgb(int yp, bool gc = false) { return off_q(yp, gc) + 3 * 64 * 4; }  // RGB ring (size depends on the tile)
 
+// Magic-number division: exact for n * d < 2^32 (the host caps the tile
+// height so every kernel division meets it).
+struct FastDiv {
+  uint32_t d, m;
+};
+SMOL_HD FastDiv make_fastdiv(uint32_t d) { return FastDiv{d, d <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / d) + 1u}; }
+
 struct TileLayout {
   int oy0, oy1, ox0, ox1;          // output tile
   int ly0, ly1, lx0, lx1;          // luma (decoded) tap footprint, inclusive
@@ -142,6 +149,10 @@ struct TileLayout {
   int fits;                        // footprint fits the fixed ring pitches
   // byte offsets in dynamic shared memory
   int off_q, off_xt, off_yt, off_st, off_y, off_c, off_rgb, total;
+  // the kernel's task-index divisors: luma / chroma blocks per block row,
+  // 4-column colour tasks per quad row, 4-pixel output quads per row
+  FastDiv fd_y, fd_c, fd_t4, fd_q4;
+  FastDiv fd_fw, fd_cw;            // luma / chroma footprint widths (thumbnail kernel)
 };
 
 SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, int ox1, TileLayout& L,
@@ -195,6 +206,12 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {ring byte offset of row y0 | y1<<16, w}
   L.off_st = off;  off += align16(L.nsteps * 8);              // per-step {ready, done}
   L.total = off;
+  L.fd_y = make_fastdiv(L.bx1[0] - L.bx0[0] + 1);
+  L.fd_c = make_fastdiv(L.bx1[1] - L.bx0[1] + 1);
+  L.fd_t4 = make_fastdiv(L.rgb_w >> 2);
+  L.fd_q4 = make_fastdiv((ox1 - ox0 + 3) >> 2);
+  L.fd_fw = make_fastdiv(L.lx1 - L.lx0 + 1);
+  L.fd_cw = make_fastdiv(L.cx1 - L.cx0 + 1);
 }
 
 SMOL_HD long long tile_roi_blocks(const TileLayout& L) {
@@ -217,10 +234,5 @@ SMOL_HD int ready_after(const TileLayout& L, int Hc, int s, int vs = 2) {
   return r;
 }
 
-// Magic-number division for 0 <= n < 2^16, 1 <= d < 2^16.
-struct FastDiv {
-  uint32_t d, m;
-};
-SMOL_HD FastDiv make_fastdiv(uint32_t d) { return FastDiv{d, d <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / d) + 1u}; }
 
 }  // namespace smol

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     const int lx0 = S.L.lx0, ly0 = S.L.ly0, fw = S.L.lx1 - lx0 + 1, fh = S.L.ly1 - ly0 + 1;
     const int cx0 = S.L.cx0, cy0 = S.L.cy0, cw = S.L.cx1 - cx0 + 1, ch = S.L.cy1 - cy0 + 1;
     // magic-number divisions by the runtime widths (all operands < 2^16)
-    const FastDiv fd_fw = make_fastdiv(fw), fd_cw = make_fastdiv(cw), fd_nq = make_fastdiv((OW + 3) >> 2);
+    const FastDiv fd_fw = S.L.fd_fw, fd_cw = S.L.fd_cw, fd_nq = S.L.fd_q4;   // (precomputed with the layout)
     // taps (reading R9: exact integers); a clamped upper tap gets weight 0
     // column taps per output pair, byte offsets of x0 in an RGB row; the
     // kernel always reads x0 + 1 (a clamped upper tap has weight 0, and the
