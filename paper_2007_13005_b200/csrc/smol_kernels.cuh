@@ -26,9 +26,6 @@
 // scale 1 the output tasks share the phase with the next step's IDCT and are
 // grabbed dynamically, two per lane per grab, interleaved by the compiler; at
 // scales 1/2..1/8 that IDCT is small and a static stride wins.
-#ifndef SMOL_COLOUR_TAIL
-#define SMOL_COLOUR_TAIL 1       // run the colour phase's partial last round as half tasks
-#endif
 #ifndef SMOL_OUT_RUN_ROWS
 #define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
 #endif
@@ -758,11 +755,9 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       const int nq = ready > ready_prev ? (ready >> 1) - j0 + 1 : 0;
       const int ntaskc = nq * ntask4;
       // colour tasks all cost the same and nothing else runs in this phase:
-      // a static round-robin needs no work counter.  The last, partial round
-      // is run as half tasks (2x2 pixels) over all the threads, so it takes
-      // about half a task's time instead of a whole one (SMOL_COLOUR_TAIL).
-      const int nfull = SMOL_COLOUR_TAIL ? ntaskc - ntaskc % kThreads : ntaskc;
-      for (int t = tid; t < nfull; t += kThreads) {
+      // a static round-robin needs no work counter (running the partial last
+      // round as half tasks measured slower, r02)
+      for (int t = tid; t < ntaskc; t += kThreads) {
         const int rr = (int)fdiv((uint32_t)t, fd_t4);
         const int p = t - rr * ntask4;
         const int j = j0 + rr;                               // chroma row of the quads
@@ -806,50 +801,6 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         *reinterpret_cast<uint4*>(r0p) = top;
         *reinterpret_cast<uint4*>(r0p + rgb_p) = make_uint4(b01.x, b01.y, b23.x, b23.y);
         if (slot == 0) *reinterpret_cast<uint4*>(r0p + kRgbRing * rgb_p) = top;   // guard row
-      }
-      if (SMOL_COLOUR_TAIL) {
-        // tail: half task h of task nfull + (h >> 1): luma cols 2i + 2e, +1
-        // (e = h & 1) of rows 2j, 2j+1 -- the same arithmetic on 2 columns
-        for (int hx = tid; hx < 2 * (ntaskc - nfull); hx += kThreads) {
-          const int t = nfull + (hx >> 1), e = hx & 1;
-          const int rr = (int)fdiv((uint32_t)t, fd_t4);
-          const int p = t - rr * ntask4;
-          const int j = j0 + rr;
-          const int i = (L.rgb_x0 >> 1) + 2 * p;
-          const uint8_t* c1 = cring + ((j & (kCR - 1)) + 1) * kCP + (i + e - L.xbase[1] + kCPad);  // centre col i+e
-          const uint8_t* c0 = c1 + (j > 0 ? -kCP : 0);
-          const uint8_t* c2 = c1 + (j < im.Hc - 1 ? kCP : 0);
-          int cbq[4], crq[4];                                // [row 0: 2 cols][row 1: 2 cols]
-#pragma unroll
-          for (int comp = 0; comp < 2; ++comp) {
-            const int o = comp * kCStride;
-            int h[3][2];
-            const uint8_t* rows[3] = {c0, c1, c2};
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-              const int a = ldu8(rows[r] + o - 1), m = ldu8(rows[r] + o), n2 = ldu8(rows[r] + o + 1);
-              h[r][0] = 3 * m + a;     // col 2(i+e)
-              h[r][1] = 3 * m + n2;    // col 2(i+e)+1
-            }
-            int* qv = comp ? crq : cbq;
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-              qv[x] = 3 * h[1][x] + h[0][x];
-              qv[2 + x] = 3 * h[1][x] + h[2][x];
-            }
-          }
-          const uint8_t* yr = yring + ((2 * j) & (kYRing - 1)) * kYP + (2 * (i + e) - L.xbase[0]);
-          const uint32_t y0 = *reinterpret_cast<const uint16_t*>(yr);
-          const uint32_t y1 = *reinterpret_cast<const uint16_t*>(yr + kYP);
-          const int slot = rgb_slot(2 * j);
-          uint32_t* r0p = rgb + slot * rgb_p + (2 * (i + e) - L.rgb_x0);
-          const uint32_t mg = 0x4B000000u;
-          const uint2 tt = colour2m(__byte_perm(y0, mg, 0x7540), __byte_perm(y0, mg, 0x7541), cbq[0], cbq[1], crq[0], crq[1]);
-          const uint2 bb = colour2m(__byte_perm(y1, mg, 0x7540), __byte_perm(y1, mg, 0x7541), cbq[2], cbq[3], crq[2], crq[3]);
-          *reinterpret_cast<uint2*>(r0p) = tt;
-          *reinterpret_cast<uint2*>(r0p + rgb_p) = bb;
-          if (slot == 0) *reinterpret_cast<uint2*>(r0p + kRgbRing * rgb_p) = tt;   // guard row
-        }
       }
     }
     __syncthreads();
