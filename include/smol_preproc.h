@@ -89,6 +89,12 @@ typedef struct {
                                at most this SOF size, and those runs never
                                allocate (a larger image -> SMOL_ERR_CAPACITY);
                                0 = allocate on first use, grow on demand         */
+  int32_t chroma_2s;        /* 1: libjpeg-turbo-style scaled decoding of 4:2:0
+                               (reading R18): chroma blocks IDCT'd at twice the
+                               luma scale (1/(k/2)), giving chroma at the luma
+                               resolution, and no upsampling; k >= 2, DENSE64,
+                               Definition A, 4:2:0 (and gray) images only;
+                               0 = all components at 1/k + triangle upsample (R2) */
 } smol_preproc_params;
 
 typedef enum { SMOL_IDCT_BOX_MEAN = 0, SMOL_IDCT_TRUNCATED = 1 } smol_idct_def;

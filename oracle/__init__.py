@@ -53,7 +53,7 @@ class _Params(ctypes.Structure):
                 ("resize_h", ctypes.c_int32), ("crop_w", ctypes.c_int32),
                 ("crop_h", ctypes.c_int32), ("mean", ctypes.c_double * 3),
                 ("std", ctypes.c_double * 3), ("out_f16", ctypes.c_int32),
-                ("idct_def", ctypes.c_int32)]
+                ("idct_def", ctypes.c_int32), ("chroma_2s", ctypes.c_int32)]
 
 
 class Geometry(ctypes.Structure):
@@ -106,7 +106,7 @@ def _ptr(a: np.ndarray) -> int:
 
 def make_params(scale_denom=1, resize_mode="short", resize_short=256, resize_w=0, resize_h=0,
                 crop_w=0, crop_h=0, mean=(0.485, 0.456, 0.406), std=(0.229, 0.224, 0.225),
-                out_dtype="f32", idct_def="box") -> _Params:
+                out_dtype="f32", idct_def="box", chroma_2s=False) -> _Params:
     p = _Params()
     p.scale_denom = scale_denom
     p.resize_mode = 0 if resize_mode == "short" else 1
@@ -116,11 +116,12 @@ def make_params(scale_denom=1, resize_mode="short", resize_short=256, resize_w=0
     p.std = (ctypes.c_double * 3)(*std)
     p.out_f16 = 1 if out_dtype == "f16" else 0
     p.idct_def = 1 if idct_def == "truncated" else 0
+    p.chroma_2s = 1 if chroma_2s else 0
     return p
 
 
-def params_from_config(cfg, mean=None, std=None, idct_def="box") -> _Params:
-    kw = {"idct_def": idct_def}
+def params_from_config(cfg, mean=None, std=None, idct_def="box", chroma_2s=False) -> _Params:
+    kw = {"idct_def": idct_def, "chroma_2s": chroma_2s}
     if mean is not None:
         kw["mean"] = mean
     if std is not None:
@@ -257,10 +258,12 @@ def decode_image_planes(p: _Params, im, qtables: np.ndarray, with_v: bool = Fals
     unrounded v at p's scale."""
     g = geometry(p, im.width, im.height, getattr(im, "subsampling", 420))
     k = p.scale_denom
+    c2s = bool(p.chroma_2s) and len(im.coef) == 3 and getattr(im, "subsampling", 420) == 420
     out = []
     for ci in range(len(im.coef)):
-        w, h = (g.Wd, g.Hd) if ci == 0 else (g.Wc, g.Hc)
-        v, u8 = decode_plane(im.coef[ci], qtables[im.qidx[ci]], k, w, h, p.idct_def)
+        w, h = (g.Wd, g.Hd) if ci == 0 or c2s else (g.Wc, g.Hc)
+        kk = k // 2 if (ci > 0 and c2s) else k          # reading R18: chroma at twice the scale
+        v, u8 = decode_plane(im.coef[ci], qtables[im.qidx[ci]], kk, w, h, p.idct_def)
         out.append((v, u8) if with_v else u8)
     return out
 

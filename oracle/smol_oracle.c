@@ -366,9 +366,19 @@ int oracle_run_image(const oracle_params* p, const oracle_image* im, int32_t lef
 int oracle_run_image2(const oracle_params* p, const oracle_image* im, int32_t left, int32_t top,
                       int32_t roi_x, int32_t roi_y, int32_t roi_w, int32_t roi_h, void* out) {
   oracle_geometry g;
-  const int32_t hs = im->comp[1].coef == NULL ? 2 : im->hs, vs = im->comp[1].coef == NULL ? 2 : im->vs;
+  int32_t hs = im->comp[1].coef == NULL ? 2 : im->hs, vs = im->comp[1].coef == NULL ? 2 : im->vs;
   int rc = oracle_geometry_of2(p, im->width, im->height, hs, vs, &g);
   if (rc) return rc;
+  /* reading R18 (libjpeg-turbo scaled decoding of 4:2:0): chroma blocks are
+   * decoded at scale 1/(k/2), which puts chroma on the luma grid
+   * (ceil(W/k) x ceil(H/k)); no upsampling follows (factors 1, 1) */
+  int32_t ck = p->scale_denom;
+  if (p->chroma_2s && im->comp[1].coef != NULL) {
+    if (p->scale_denom < 2 || hs != 2 || vs != 2) return 22;
+    ck = p->scale_denom / 2;
+    g.Wc = g.Wd; g.Hc = g.Hd;
+    hs = vs = 1;
+  }
   if (left >= 0 && top >= 0) { g.left = left; g.top = top; }
   int32_t wx0 = 0, wy0 = 0, ww = 0, wh = 0;     /* decoded ROI window (reading R15) */
   if (roi_w > 0 || roi_h > 0) {
@@ -397,8 +407,8 @@ int oracle_run_image2(const oracle_params* p, const oracle_image* im, int32_t le
       for (int32_t i = 0; !rc && i < g.Wd * g.Hd; ++i)
         rgb[3 * i] = rgb[3 * i + 1] = rgb[3 * i + 2] = Y[i];
     } else {
-      if (!rc) rc = oracle_decode_plane2(&im->comp[1], p->scale_denom, p->idct_def, g.Wc, g.Hc, NULL, Cb);
-      if (!rc) rc = oracle_decode_plane2(&im->comp[2], p->scale_denom, p->idct_def, g.Wc, g.Hc, NULL, Cr);
+      if (!rc) rc = oracle_decode_plane2(&im->comp[1], ck, p->idct_def, g.Wc, g.Hc, NULL, Cb);
+      if (!rc) rc = oracle_decode_plane2(&im->comp[2], ck, p->idct_def, g.Wc, g.Hc, NULL, Cr);
       if (!rc) rc = oracle_upsample_color2(Y, g.Wd, g.Hd, Cb, Cr, g.Wc, g.Hc, hs, vs, NULL, rgb);
     }
     if (!rc && ww > 0) {

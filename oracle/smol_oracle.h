@@ -59,6 +59,9 @@ typedef struct {
   int32_t idct_def;           /* reduced-scale IDCT: 0 = Definition A (box mean,
                                  reading R1), 1 = Definition B (truncated
                                  (8/k)-point IDCT, reading R16) */
+  int32_t chroma_2s;          /* 1 (k >= 2, 4:2:0): chroma decoded at scale
+                                 1/(k/2), i.e. at the luma resolution, and used
+                                 without upsampling (reading R18) */
 } oracle_params;
 
 typedef struct {

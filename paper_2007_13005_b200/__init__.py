@@ -35,7 +35,7 @@ def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: 
                 resize_w: int = 0, resize_h: int = 0, crop_w: int = 0, crop_h: int = 0,
                 mean=IMAGENET_MEAN, std=IMAGENET_STD, out_dtype: str = "f32",
                 tile_rows: int = 0, layout: str = "dense", idct_def: str = "box",
-                max_size: Optional[Tuple[int, int]] = None) -> Params:
+                max_size: Optional[Tuple[int, int]] = None, chroma_2s: bool = False) -> Params:
     p = Params()
     p.scale_denom = scale_denom
     p.resize_mode = SMOL_RESIZE_SHORT_SIDE if resize_mode == "short" else SMOL_RESIZE_EXACT
@@ -48,6 +48,7 @@ def make_params(scale_denom: int = 1, resize_mode: str = "short", resize_short: 
     p.tile_rows = tile_rows
     p.idct_def = SMOL_IDCT_TRUNCATED if idct_def == "truncated" else SMOL_IDCT_BOX_MEAN
     p.max_width, p.max_height = max_size if max_size is not None else (0, 0)
+    p.chroma_2s = 1 if chroma_2s else 0
     return p
 
 

@@ -43,7 +43,8 @@ class Params(ctypes.Structure):
                 ("mean", ctypes.c_float * 3), ("std", ctypes.c_float * 3),
                 ("out_dtype", ctypes.c_int32), ("layout", ctypes.c_int32),
                 ("tile_rows", ctypes.c_int32), ("idct_def", ctypes.c_int32),
-                ("max_width", ctypes.c_int32), ("max_height", ctypes.c_int32)]
+                ("max_width", ctypes.c_int32), ("max_height", ctypes.c_int32),
+                ("chroma_2s", ctypes.c_int32)]
 
 
 class ImageDesc(ctypes.Structure):

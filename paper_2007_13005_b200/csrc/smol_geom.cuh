@@ -44,9 +44,11 @@ struct __align__(16) DevImage {
   int32_t gray;             // 1: one component (subsampling 400): no chroma blocks, Cb = Cr = 128
   int32_t sx0, sy0, sw, sh; // source window of the resize in decoded luma px: the whole
                             // image (0, 0, Wd, Hd), or an ROI rectangle's window (R15)
-  int32_t hs, vs;           // chroma subsampling factors (T.81 A.1.1): 2,2 = 4:2:0 (and
-                            // gray); 2,1 = 4:2:2; 1,1 = 4:4:4
-  int32_t pad_[2];
+  int32_t hs, vs;           // chroma factors of the decoded planes (T.81 A.1.1): 2,2 =
+                            // 4:2:0 (and gray); 2,1 = 4:2:2; 1,1 = 4:4:4, and 4:2:0
+                            // decoded with chroma at twice the scale (R18)
+  int32_t ck;               // decode scale denominator of the chroma blocks (K, or K/2)
+  int32_t pad_;
 };
 
 // Per-image reference of a run (32 B): the image's coefficient planes and
@@ -176,15 +178,16 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.by0[0] = L.ly0 / P; L.by1[0] = L.ly1 / P;
   L.bx0[0] = (L.lx0 & ~3) / P;
   L.bx1[0] = imin((L.lx1 | 3) / P, im.nbw[0] - 1);
+  const int PC = 8 / (im.ck > 0 ? im.ck : K);   // chroma samples per block side
   for (int c = 1; c < 3; ++c) {
-    L.by0[c] = L.cy0 / P; L.by1[c] = L.cy1 / P;
-    L.bx0[c] = L.cx0 / P; L.bx1[c] = L.cx1 / P;
+    L.by0[c] = L.cy0 / PC; L.by1[c] = L.cy1 / PC;
+    L.bx0[c] = L.cx0 / PC; L.bx1[c] = L.cx1 / PC;
   }
   // grayscale: no chroma block rows (the kernel fills the chroma rings with
   // 128, the neutral value, so colour conversion gives R = G = B = Y)
   if (im.gray)
     for (int c = 1; c < 3; ++c) L.by1[c] = L.by0[c] - 1;
-  for (int c = 0; c < 3; ++c) L.xbase[c] = L.bx0[c] * P;
+  for (int c = 0; c < 3; ++c) L.xbase[c] = L.bx0[c] * (c ? PC : P);
   L.rgb_x0 = L.lx0 & ~3;
   L.rgb_w = ((L.lx1 | 3) - L.rgb_x0 + 1);
   L.rgb_p = rgb_pitch(yp);         // fixed pitch (u32): row r+1 is an immediate offset from row r
@@ -192,7 +195,7 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   // the last step must cover luma row ly1 and chroma row cy1 (luma vs cy1)
   L.nsteps = ((imax(L.ly1, im.vs * L.cy1) - L.r0) / kStepRows) + 1;
   L.fits = ((L.bx1[0] - L.bx0[0] + 1) * P + 4 <= yp) &&
-           ((L.bx1[1] - L.bx0[1] + 1) * P + 2 * kCPad <= c_pitch(yp, gc)) && (L.rgb_w + 4 <= L.rgb_p) &&
+           ((L.bx1[1] - L.bx0[1] + 1) * PC + 2 * kCPad <= c_pitch(yp, gc)) && (L.rgb_w + 4 <= L.rgb_p) &&
            (gc || (im.hs == 2 && im.vs == 2));
   int off = 0;
   // fixed-size regions first, at compile-time offsets (kOff*), so the hot

@@ -11,11 +11,11 @@ template <int NT> struct CfgYP {
   static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
 };
 
-template <bool PK, int NT, bool DB = false, bool GC = false>
+template <bool PK, int NT, bool DB = false, bool GC = false, int CK = 1>
 KernelFn pick(bool f16, bool dbg) {
   constexpr int YP = CfgYP<NT>::yp;
-  if (dbg) return f16 ? smol_fused_kernel<1, true, true, PK, NT, YP, DB, GC> : smol_fused_kernel<1, false, true, PK, NT, YP, DB, GC>;
-  return f16 ? smol_fused_kernel<1, true, false, PK, NT, YP, DB, GC> : smol_fused_kernel<1, false, false, PK, NT, YP, DB, GC>;
+  if (dbg) return f16 ? smol_fused_kernel<1, true, true, PK, NT, YP, DB, GC, CK> : smol_fused_kernel<1, false, true, PK, NT, YP, DB, GC, CK>;
+  return f16 ? smol_fused_kernel<1, true, false, PK, NT, YP, DB, GC, CK> : smol_fused_kernel<1, false, false, PK, NT, YP, DB, GC, CK>;
 }
 
 template <int NT>
@@ -27,7 +27,8 @@ KernelFn pick_nt(bool f16, bool dbg, bool packed, bool db) {
 
 }  // namespace
 
-KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt, bool db, bool gc) {
+KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt, bool db, bool gc, bool c2s) {
+  (void)c2s;                    // (no chroma at twice the scale at scale 1)
   if (gc) return pick<false, kThreadsWide, false, true>(f16, dbg);
   return nt == kThreadsNarrow ? pick_nt<kThreadsNarrow>(f16, dbg, packed, db)
        : nt == kThreadsTiny   ? pick_nt<kThreadsTiny>(f16, dbg, packed, db)

@@ -11,11 +11,11 @@ template <int NT> struct CfgYP {
   static constexpr int yp = NT == kThreadsNarrow ? kYPNarrow : NT == kThreadsTiny ? kYPTiny : kYPWide;
 };
 
-template <bool PK, int NT, bool DB = false, bool GC = false>
+template <bool PK, int NT, bool DB = false, bool GC = false, int CK = 2>
 KernelFn pick(bool f16, bool dbg) {
   constexpr int YP = CfgYP<NT>::yp;
-  if (dbg) return f16 ? smol_fused_kernel<2, true, true, PK, NT, YP, DB, GC> : smol_fused_kernel<2, false, true, PK, NT, YP, DB, GC>;
-  return f16 ? smol_fused_kernel<2, true, false, PK, NT, YP, DB, GC> : smol_fused_kernel<2, false, false, PK, NT, YP, DB, GC>;
+  if (dbg) return f16 ? smol_fused_kernel<2, true, true, PK, NT, YP, DB, GC, CK> : smol_fused_kernel<2, false, true, PK, NT, YP, DB, GC, CK>;
+  return f16 ? smol_fused_kernel<2, true, false, PK, NT, YP, DB, GC, CK> : smol_fused_kernel<2, false, false, PK, NT, YP, DB, GC, CK>;
 }
 
 template <int NT>
@@ -26,7 +26,8 @@ KernelFn pick_nt(bool f16, bool dbg, bool packed, bool db) {
 
 }  // namespace
 
-KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db, bool gc) {
+KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db, bool gc, bool c2s) {
+  if (c2s) return pick<false, kThreadsWide, false, true, 1>(f16, dbg);   // chroma at 1/1 (R18)
   if (gc) {
     constexpr int W = kThreadsWide;
     if (db) return packed ? pick<true, W, true, true>(f16, dbg) : pick<false, W, true, true>(f16, dbg);

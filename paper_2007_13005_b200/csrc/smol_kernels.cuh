@@ -478,10 +478,12 @@ __device__ __forceinline__ int grab_chunk(int* ctr, int lane, int n = 32) {
   return __shfl_sync(0xffffffffu, chunk, 0);
 }
 
-template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB, bool GC>
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB, bool GC, int CK>
 __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const int oy0, const int oy1,
                                        const int ox0, const int ox1, const int lay_local) {
   constexpr int P = 8 / K;                 // decoded samples per block side
+  constexpr int PC = 8 / CK;               // per chroma block side (= P unless chroma at twice the scale)
+  static_assert(CK == K || GC, "chroma at another scale needs the generic-chroma rings");
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   __shared__ DevImage im;
@@ -559,8 +561,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     const int R = L.r0 + kStepRows * s;
     const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
     const int Rc = GC ? R / cvs : (R >> 1), crows = GC ? kStepRows / cvs : kStepRows / 2;  // chroma rows of the step
-    const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], Rc / P);
-    const int cb1 = min(L.by1[1], (Rc + crows) / P - 1);
+    const int cb0 = (s == 0) ? L.by0[1] : max(L.by0[1], Rc / PC);
+    const int cb1 = min(L.by1[1], (Rc + crows) / PC - 1);
     const int ny = max(0, yb1 - yb0 + 1) * nbx0;
     const int nc = max(0, cb1 - cb0 + 1) * nbxc;
     const int ntask = ny + 2 * nc;
@@ -585,30 +587,45 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       }
       const int16_t* src = im.coef[c] + (size_t)brow * im.stride[c] + (size_t)(L.bx0[c] + bcol) * BlockFmt<K, PACKED, DB>::kElems;
       uint32_t px[8][2];
-      decode_block<K, PACKED, DB>(act, src, qf + c * 64, px);
+      if constexpr (CK == K) {
+        decode_block<K, PACKED, DB>(act, src, qf + c * 64, px);
+      } else {
+        // luma and chroma blocks decode at different scales: each variant
+        // runs (warp-uniformly) for the warps holding such blocks
+        const bool isy = c == 0;
+        uint32_t pc[8][2];
+        if (__any_sync(0xffffffffu, act && isy)) decode_block<K, PACKED, DB>(act && isy, src, qf + c * 64, px);
+        if (__any_sync(0xffffffffu, act && !isy)) {
+          decode_block<CK, PACKED, DB>(act && !isy, src, qf + c * 64, pc);
+          if (!isy) {
+#pragma unroll
+            for (int y = 0; y < 8; ++y) { px[y][0] = pc[y][0]; px[y][1] = pc[y][1]; }
+          }
+        }
+      }
       if (!act) continue;
       if (c == 0) {
         uint8_t* d = yring + bcol * P;
 #pragma unroll
         for (int y = 0; y < P; ++y) put_row<P>(d + ((brow * P + y) & (kYRing - 1)) * kYP, px[y]);
       } else {
-        uint8_t* d = cring + (c - 1) * kCStride + bcol * P + kCPad;
-        const int gx0 = (L.bx0[c] + bcol) * P;
-        const bool edge = (gx0 == 0) || (gx0 <= im.Wc - 1 && im.Wc - 1 < gx0 + P);
+        uint8_t* d = cring + (c - 1) * kCStride + bcol * PC + kCPad;
+        const int gx0 = (L.bx0[c] + bcol) * PC;
+        const bool edge = (gx0 == 0) || (gx0 <= im.Wc - 1 && im.Wc - 1 < gx0 + PC);
 #pragma unroll
-        for (int y = 0; y < P; ++y) {
-          const int r = brow * P + y;
+        for (int y = 0; y < PC; ++y) {
+          const int r = brow * PC + y;
           const int rs = r & (kCR - 1);
           // slot rs+1, plus the guard mirrors (slot 0 = kCR, slot kCR+1 = 1)
           for (int k = 0; k < 1 + (rs == kCR - 1 || rs == 0); ++k) {
             uint8_t* row = d + (k == 0 ? rs + 1 : (rs == kCR - 1 ? 0 : kCS - 1)) * kCP;
-            put_row<P>(row, px[y]);
+            put_row<PC>(row, px[y]);
             if (edge) {
               // replicate image-edge chroma columns into the neighbours the
               // triangle filter reads (reading R2: indices clamp at the edges)
               if (gx0 == 0) row[-1] = (uint8_t)byte_of(px[y], 0);
               const int e = im.Wc - 1 - gx0;
-              if (e >= 0 && e < P) row[e + 1] = (uint8_t)byte_of(px[y], e);
+              if (e >= 0 && e < PC) row[e + 1] = (uint8_t)byte_of(px[y], e);
             }
           }
         }
@@ -648,8 +665,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
         if (c == 0) { rlo = max(max(L.by0[0], R / P) * P, L.ly0); rhi = min(min(L.by1[0], (R + kStepRows) / P - 1) * P + P - 1, L.ly1); }
         else {
           const int Rc = R / cvs;
-          rlo = max(((s == 0) ? L.by0[1] : max(L.by0[1], Rc / P)) * P, L.cy0);
-          rhi = min(min(L.by1[1], (Rc + kStepRows / cvs) / P - 1) * P + P - 1, L.cy1);
+          rlo = max(((s == 0) ? L.by0[1] : max(L.by0[1], Rc / PC)) * PC, L.cy0);
+          rhi = min(min(L.by1[1], (Rc + kStepRows / cvs) / PC - 1) * PC + PC - 1, L.cy1);
         }
         const int x0 = c ? L.cx0 : L.lx0, x1 = c ? L.cx1 : L.lx1;
         int16_t* dst = kp.dbg_pl[c] + n * (c ? kp.dbg_stride_c : kp.dbg_stride_y);
@@ -671,8 +688,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       const int R = L.r0 + kStepRows * (s + 1);
       const int yb0 = max(L.by0[0], R / P), yb1 = min(L.by1[0], (R + kStepRows) / P - 1);
       const int Rc = GC ? R / cvs : (R >> 1), crows = GC ? kStepRows / cvs : kStepRows / 2;
-      const int cb0 = max(L.by0[1], Rc / P);
-      const int cb1 = min(L.by1[1], (Rc + crows) / P - 1);
+      const int cb0 = max(L.by0[1], Rc / PC);
+      const int cb1 = min(L.by1[1], (Rc + crows) / PC - 1);
       const int ny = max(0, yb1 - yb0 + 1), nc = max(0, cb1 - cb0 + 1);
       for (int k = lane; k < ny + 2 * nc; k += 32) {
         int c = 0, brow = yb0 + k;
@@ -1038,7 +1055,11 @@ __host__ __device__ constexpr int kCtasPerSm(int threads) {
 
 // The fused kernel: one (image, row band, column band) tile per CTA.
 // DB: Definition B reduced-scale IDCT (K = 2, 4 only; equal to A at 1, 1/8).
-template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB = false, bool GC = false>
+// CK: decode scale of the chroma blocks: K, or K/2 for libjpeg-turbo-style
+// scaled decoding of 4:2:0 (chroma IDCT at twice the luma scale, no
+// upsampling; reading R18; generic-chroma kernels only).
+template <int K, bool F16, bool DEBUG, bool PACKED, int kThreads, int kYP, bool DB = false, bool GC = false,
+          int CK = K>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm<K>(kThreads))
 smol_fused_kernel(const __grid_constant__ KParams kp) {
   int n, oy0, oy1, ox0, ox1, local;
@@ -1053,7 +1074,7 @@ smol_fused_kernel(const __grid_constant__ KParams kp) {
     oy0 = trow * kp.tile_rows; oy1 = min(kp.OH, oy0 + kp.tile_rows);
     ox0 = tcol * kp.tile_cols; ox1 = min(kp.OW, ox0 + kp.tile_cols);
   }
-  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP, DB, GC>(kp, n, oy0, oy1, ox0, ox1, local);
+  smol_tile<K, F16, DEBUG, PACKED, kThreads, kYP, DB, GC, CK>(kp, n, oy0, oy1, ox0, ox1, local);
 }
 
 }  // namespace smol

@@ -14,11 +14,12 @@ using KernelFn = void (*)(const KParams);
 // packed layout, threads per CTA, Definition B IDCT); K fixed per unit
 // (db only exists at K = 2, 4: at 1 and 1/8 the definitions coincide);
 // gc: generic-chroma kernel (4:2:2 / 4:4:4), built for the wide CTA only
-// (nt is ignored)
-KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
-KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
-KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
-KernelFn select_fused_k8(bool f16, bool dbg, bool packed, int nt, bool db, bool gc);
+// (nt is ignored); c2s (with gc, K >= 2, dense, Definition A): chroma blocks
+// decoded at scale 1/(K/2) (reading R18)
+KernelFn select_fused_k1(bool f16, bool dbg, bool packed, int nt, bool db, bool gc, bool c2s);
+KernelFn select_fused_k2(bool f16, bool dbg, bool packed, int nt, bool db, bool gc, bool c2s);
+KernelFn select_fused_k4(bool f16, bool dbg, bool packed, int nt, bool db, bool gc, bool c2s);
+KernelFn select_fused_k8(bool f16, bool dbg, bool packed, int nt, bool db, bool gc, bool c2s);
 // upload the basis constants into each unit's constant bank (current device)
 cudaError_t upload_basis_k1(const Basis& b);
 cudaError_t upload_basis_k2(const Basis& b);

@@ -137,6 +137,11 @@ int32_t validate_params(const smol_preproc_params* p) {
     return fail(SMOL_ERR_INVALID, "params.tile_rows=%d", p->tile_rows);
   if (p->idct_def != SMOL_IDCT_BOX_MEAN && p->idct_def != SMOL_IDCT_TRUNCATED)
     return fail(SMOL_ERR_INVALID, "params.idct_def=%d", p->idct_def);
+  if (p->chroma_2s != 0 && p->chroma_2s != 1)
+    return fail(SMOL_ERR_INVALID, "params.chroma_2s=%d", p->chroma_2s);
+  if (p->chroma_2s && (p->scale_denom < 2 || p->layout != SMOL_LAYOUT_DENSE64 || p->idct_def != SMOL_IDCT_BOX_MEAN))
+    return fail(SMOL_ERR_UNSUPPORTED, "params.chroma_2s needs scale_denom >= 2, the DENSE64 layout and "
+                "Definition A");
   if (p->max_width < 0 || p->max_height < 0 || (p->max_width > 0) != (p->max_height > 0) ||
       p->max_width > 65535 || p->max_height > 65535)
     return fail(SMOL_ERR_INVALID, "params.max_width/max_height=%d/%d: both in [1, 65535] or both 0",
@@ -173,10 +178,20 @@ int32_t image_geometry(const smol_preproc_params* p, const smol_image_desc* d, i
   g.gray = d->subsampling == 400;
   g.hs = d->subsampling == 444 ? 1 : 2;      // T.81 A.1.1: Hmax / H_chroma, Vmax / V_chroma
   g.vs = (d->subsampling == 444 || d->subsampling == 422) ? 1 : 2;
+  g.ck = k;
   g.Wd = ceil_div(d->width, k);
   g.Hd = ceil_div(d->height, k);
   g.Wc = ceil_div(d->width, g.hs * k);      // chroma ceil(W/hs) decoded at 1/k (R4)
   g.Hc = ceil_div(d->height, g.vs * k);
+  if (p->chroma_2s && d->subsampling == 420) {
+    // reading R18: chroma blocks decoded at 1/(k/2) -> chroma at the luma
+    // size ceil(W/k) x ceil(H/k), used without upsampling (factors 1, 1)
+    g.ck = k / 2;
+    g.hs = g.vs = 1;
+    g.Wc = g.Wd; g.Hc = g.Hd;
+  } else if (p->chroma_2s && (d->subsampling == 422 || d->subsampling == 444)) {
+    return fail(SMOL_ERR_UNSUPPORTED, "image %d: chroma_2s is defined for 4:2:0 only", idx);
+  }
   int OW, OH;
   if (p->resize_mode == SMOL_RESIZE_SHORT_SIDE) {
     const long long S = p->resize_short;
@@ -236,13 +251,13 @@ inline void copy_geometry(const DevImage& from, DevImage& g) {
   g.Wr = from.Wr; g.Hr = from.Hr; g.left = from.left; g.top = from.top;
   g.gray = from.gray;
   g.sx0 = from.sx0; g.sy0 = from.sy0; g.sw = from.sw; g.sh = from.sh;
-  g.hs = from.hs; g.vs = from.vs;
+  g.hs = from.hs; g.vs = from.vs; g.ck = from.ck;
 }
 inline bool same_layout_inputs(const DevImage& a, const DevImage& b) {
   return a.Wd == b.Wd && a.Hd == b.Hd && a.Wc == b.Wc && a.Hc == b.Hc && a.Wr == b.Wr && a.Hr == b.Hr &&
          a.left == b.left && a.top == b.top && a.nbw[0] == b.nbw[0] && a.nbw[1] == b.nbw[1] &&
          a.gray == b.gray && a.sx0 == b.sx0 && a.sy0 == b.sy0 && a.sw == b.sw && a.sh == b.sh &&
-         a.hs == b.hs && a.vs == b.vs;
+         a.hs == b.hs && a.vs == b.vs && a.ck == b.ck;
 }
 
 int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, int idx, int n_qtables,
@@ -251,8 +266,11 @@ int32_t validate_image(const smol_preproc_params* p, const smol_image_desc* d, i
   if (geom) copy_geometry(*geom, g);
   else rc = image_geometry(p, d, idx, g);
   if (rc) return rc;
-  const int need_w[3] = {ceil_div(d->width, 8), ceil_div(d->width, 8 * g.hs), ceil_div(d->width, 8 * g.hs)};
-  const int need_h[3] = {ceil_div(d->height, 8), ceil_div(d->height, 8 * g.vs), ceil_div(d->height, 8 * g.vs)};
+  // block counts of the coded planes (the coded sampling, whatever scale
+  // the chroma is decoded at)
+  const int hsc = d->subsampling == 444 ? 1 : 2, vsc = (d->subsampling == 420 || d->subsampling == 400) ? 2 : 1;
+  const int need_w[3] = {ceil_div(d->width, 8), ceil_div(d->width, 8 * hsc), ceil_div(d->width, 8 * hsc)};
+  const int need_h[3] = {ceil_div(d->height, 8), ceil_div(d->height, 8 * vsc), ceil_div(d->height, 8 * vsc)};
   static const char* names[3] = {"Y", "Cb", "Cr"};
   for (int c = 0; c < 3; ++c) {
     g.nbw[c] = need_w[c];
@@ -301,12 +319,13 @@ int auto_tile_rows(int OH, int n_images, int slots) {
 int Cfg_yp(int nt) { return nt == kThreadsNarrow ? kYPNarrow : nt == kThreadsTiny ? kYPTiny : kYPWide; }
 
 // scale 1 has no packed variant: the packed layout of scale 1 is DENSE64
-KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt, bool db, bool gc = false) {
+KernelFn select_kernel(int K, bool f16, bool dbg, bool packed, int nt, bool db, bool gc = false,
+                       bool c2s = false) {
   switch (K) {
-    case 1: return select_fused_k1(f16, dbg, packed, nt, db, gc);
-    case 2: return select_fused_k2(f16, dbg, packed, nt, db, gc);
-    case 4: return select_fused_k4(f16, dbg, packed, nt, db, gc);
-    default: return select_fused_k8(f16, dbg, packed, nt, db, gc);
+    case 1: return select_fused_k1(f16, dbg, packed, nt, db, gc, false);
+    case 2: return select_fused_k2(f16, dbg, packed, nt, db, gc, c2s);
+    case 4: return select_fused_k4(f16, dbg, packed, nt, db, gc, c2s);
+    default: return select_fused_k8(f16, dbg, packed, nt, db, gc, c2s);
   }
 }
 
@@ -415,7 +434,7 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
   out->OH = params->crop_w > 0 ? params->crop_h : g.Hr;
   out->sx0 = g.sx0; out->sy0 = g.sy0; out->sw = g.sw; out->sh = g.sh;
   g.nbw[0] = ceil_div(image->width, 8);
-  g.nbw[1] = g.nbw[2] = ceil_div(image->width, 8 * g.hs);
+  g.nbw[1] = g.nbw[2] = ceil_div(image->width, image->subsampling == 444 ? 8 : 16);
   TileLayout L;
   tile_layout(g, params->scale_denom, 0, out->OH, 0, out->OW, L, kYPWide, true);
   out->lx0 = L.lx0; out->lx1 = L.lx1; out->ly0 = L.ly0; out->ly1 = L.ly1;
@@ -428,7 +447,10 @@ int32_t smol_debug_geometry(const smol_preproc_params* params, const smol_image_
   // scale uses per ROI block (reading R1: 64 / 49 / 25 / 1), 2 B each, in any
   // layout; storage bytes: what the layout holds for those blocks (PACKED
   // pads to 8 B; dense-64 at scale 1/8 reads only the DC's 32-B sector)
-  out->roi_coef_bytes = out->roi_blocks * 2 * used_coefs(params->scale_denom, params->idct_def);
+  out->roi_coef_bytes = 0;
+  for (int c = 0; c < 3; ++c)
+    out->roi_coef_bytes += (int64_t)(L.by1[c] - L.by0[c] + 1) * (L.bx1[c] - L.bx0[c] + 1) * 2 *
+                           used_coefs(c ? g.ck : params->scale_denom, params->idct_def);
   const int bb = 2 * block_elems(params->scale_denom, params->layout, params->idct_def);
   out->storage_coef_bytes =
       out->roi_blocks * ((params->scale_denom == 8 && params->layout == SMOL_LAYOUT_DENSE64) ? 32 : bb);
@@ -524,11 +546,12 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     // dynamic smem the device allows next to the kernel's static smem
     const bool f16 = params->out_dtype == SMOL_OUT_F16_NCHW;
     int limit = pl->smem_optin;
-    for (int v = 0; v < 8 && e == cudaSuccess; ++v) {
+    for (int v = 0; v < 10 && e == cudaSuccess; ++v) {
+      if (v >= 8 && !params->chroma_2s) break;
       const int dbg = v & 1, nt = v < 2 ? kThreadsWide : v < 4 ? kThreadsNarrow : kThreadsTiny;
       cudaFuncAttributes fa;
       KernelFn fn = select_kernel(params->scale_denom, f16, dbg, params->layout == SMOL_LAYOUT_PACKED, nt,
-                                  params->idct_def == SMOL_IDCT_TRUNCATED, v >= 6);
+                                  params->idct_def == SMOL_IDCT_TRUNCATED, v >= 6, v >= 8);
       e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) break;
       const int dyn = pl->smem_optin - (int)fa.sharedSizeBytes;
@@ -620,7 +643,7 @@ int32_t validate_compact_image(const smol_preproc_params* p, const smol_compact_
         return fail(SMOL_ERR_INVALID, "image %d: qtable[%d]=%d not in [0,%d)", idx, c, ci->qtable[c], n_qtables);
       g.qidx[c] = ci->qtable[c];
     }
-    g.nbw[c] = ceil_div(ci->width, c ? 8 * g.hs : 8);
+    g.nbw[c] = ceil_div(ci->width, c ? (ci->subsampling == 444 ? 8 : 16) : 8);
     g.coef[c] = nullptr;
     g.stride[c] = 0;
   }
@@ -791,8 +814,10 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     }
   }
   // resident CTAs per SM of the chosen kernel at this shared-memory size
+  bool c2s = false;                        // some image decodes chroma at twice the scale (R18)
+  for (int i = 0; i < nk && !c2s; ++i) c2s = h[i].ck != K;
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt,
-                              pl->p.idct_def == SMOL_IDCT_TRUNCATED, gc);
+                              pl->p.idct_def == SMOL_IDCT_TRUNCATED, gc, c2s);
   int occ = 768 / nt;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
@@ -1102,8 +1127,8 @@ int32_t run_batch(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, 
 
 // Compact record of one image (format: include/smol_preproc.h).  Pass 1
 // (dst == NULL) counts, pass 2 writes.
-int64_t compact_encode_pass(const smol_image_desc* d, const TileLayout& L, int E, uint64_t mask,
-                            uint8_t* dst, uint32_t* n_units_out) {
+int64_t compact_encode_pass(const smol_image_desc* d, const TileLayout& L, int E, uint64_t mask_y,
+                            uint64_t mask_c, uint8_t* dst, uint32_t* n_units_out) {
   int64_t nblocks = 0, nrows = 0;
   for (int c = 0; c < 3; ++c) {
     nblocks += (int64_t)(L.bx1[c] - L.bx0[c] + 1) * (L.by1[c] - L.by0[c] + 1);
@@ -1116,6 +1141,7 @@ int64_t compact_encode_pass(const smol_image_desc* d, const TileLayout& L, int E
   int64_t bi = 0, ri = 0;
   for (int c = 0; c < 3; ++c) {
     const int stride = d->row_stride_bytes[c] / 2;
+    const uint64_t mask = c ? mask_c : mask_y;          // (chroma at twice the scale: its own set)
     for (int by = L.by0[c]; by <= L.by1[c]; ++by) {
       if (rs) rs[ri] = nu;
       ++ri;
@@ -1227,8 +1253,9 @@ int32_t smol_compact_encode(const smol_preproc_params* p, const smol_image_desc*
   tile_layout(g, p->scale_denom, 0, OH, 0, OW, L, kYPWide, true);
   const int E = block_elems(p->scale_denom, p->layout, p->idct_def);
   const uint64_t mask = used_mask(p->scale_denom, p->layout == SMOL_LAYOUT_PACKED, p->idct_def == SMOL_IDCT_TRUNCATED);
+  const uint64_t mask_c = used_mask(g.ck, p->layout == SMOL_LAYOUT_PACKED, p->idct_def == SMOL_IDCT_TRUNCATED);
   uint32_t nv = 0;
-  const int64_t bytes = compact_encode_pass(d, L, E, mask, nullptr, &nv);
+  const int64_t bytes = compact_encode_pass(d, L, E, mask, mask_c, nullptr, &nv);
   *written = bytes;
   if (!dst) return SMOL_OK;
   if (capacity < bytes)
@@ -1245,7 +1272,7 @@ int32_t smol_compact_encode(const smol_preproc_params* p, const smol_image_desc*
     hd.nbx[c] = L.bx1[c] - L.bx0[c] + 1; hd.nby[c] = L.by1[c] - L.by0[c] + 1;
   }
   memcpy(o, &hd, sizeof(hd));
-  compact_encode_pass(d, L, E, mask, o, &nv);
+  compact_encode_pass(d, L, E, mask, mask_c, o, &nv);
   return SMOL_OK;
 }
 

@@ -62,9 +62,11 @@ def plane_band(coef, q, k, v, idct_def: int = 0):
 def oracle_planes(p, im, qt):
     """[(v, u8, band_mask)] for Y, Cb, Cr at the params' scale."""
     res = []
+    c2s = bool(getattr(p, "chroma_2s", 0)) and len(im.coef) == 3 and getattr(im, "subsampling", 420) == 420
     for ci, (v, u8) in enumerate(oracle.decode_image_planes(p, im, qt, with_v=True)):
         q = qt[im.qidx[ci]]
-        res.append((v, u8, plane_band(im.coef[ci], q, p.scale_denom, v, p.idct_def)))
+        k = p.scale_denom // 2 if (ci > 0 and c2s) else p.scale_denom     # reading R18
+        res.append((v, u8, plane_band(im.coef[ci], q, k, v, p.idct_def)))
     return res
 
 

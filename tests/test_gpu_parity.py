@@ -80,7 +80,10 @@ def _check(cfg, imgs, qt, ps, po, strict=False, debug=True, rois=None, report=No
             # RGB exact given the kernel's own planes
             grgb = rgb[i].cpu().numpy()[:3 * g["Hd"] * g["Wd"]].reshape(g["Hd"], g["Wd"], 3)
             mrgb = grgb[..., 0] >= 0
-            exp_rgb = helpers.rgb_from_planes(*gp, subsampling=getattr(im, "subsampling", 420))
+            ss = getattr(im, "subsampling", 420)
+            if getattr(ps, "chroma_2s", 0) and ss == 420:
+                ss = 444                      # reading R18: chroma already on the luma grid
+            exp_rgb = helpers.rgb_from_planes(*gp, subsampling=ss)
             assert np.array_equal(grgb[mrgb], exp_rgb[mrgb].astype(np.int16)), f"image {i}: RGB mismatch"
             # resize/normalize given the kernel's own RGB
             full = np.where(mrgb[..., None], grgb, 0).astype(np.uint8)
@@ -691,3 +694,23 @@ def test_thumbnail_kernel_with_roi_rectangles(monkeypatch):
         assert np.max(np.abs(got[i] - ref)) <= 1e-4, (i, r)
     plan.close()
     plan2.close()
+
+
+@pytest.mark.parametrize("name", ["c3a", "c3b"])
+def test_chroma_at_twice_the_scale(name):
+    """Plan option chroma_2s (reading R18, libjpeg-turbo scaled decoding of
+    4:2:0): chroma IDCT at 1/(k/2) onto the luma grid, no upsampling -- u8
+    planes bit-exact to the oracle (tie band only), RGB exact given them,
+    output within tolerance; compact transport equal to device planes."""
+    cfg = synth.CONFIGS[name]
+    imgs, qt = synth.distinct_images(cfg, n_distinct=3)
+    ps = smol.params_from_config(cfg, chroma_2s=True)
+    po = oracle.params_from_config(cfg, chroma_2s=True)
+    out = _check(cfg, imgs, qt, ps, po)
+    plan = smol.Plan(ps, 3)
+    c = plan.run(smol.CompactBatch(ps, imgs, qt)).float().cpu().numpy()
+    assert np.array_equal(c, out)
+    plan.close()
+    with pytest.raises(smol.SmolError) as e:                 # 1/8 needs the DC plane layout? no: dense only
+        smol.Plan(smol.params_from_config(cfg, chroma_2s=True, layout="packed"), 1)
+    assert e.value.status == 2

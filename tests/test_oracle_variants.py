@@ -83,11 +83,16 @@ def _colour_np(Y, cb16, cr16):
     return np.clip(np.stack([R, G, B]), 0, 255).astype(np.float64)
 
 
-def independent_pipeline(im, qt, k, Wr, Hr, idct_def="box", roi_rect=None):
+def independent_pipeline(im, qt, k, Wr, Hr, idct_def="box", roi_rect=None, chroma_2s=False):
     import torchvision.transforms.functional as TF
     hs, vs = HV[im.subsampling]
     Y, Cb, Cr = _decode_planes_scipy(im, qt, k, idct_def)
     Hd, Wd = Y.shape
+    if chroma_2s:
+        # reading R18: chroma decoded at 1/(k/2) onto the luma grid, no upsampling
+        _, Cb, Cr = _decode_planes_scipy(im, qt, k // 2, idct_def)
+        Cb, Cr = Cb[:Hd, :Wd], Cr[:Hd, :Wd]
+        hs = vs = 1
     rgb = _colour_np(Y, _upsample_np(Cb, Wd, Hd, hs, vs), _upsample_np(Cr, Wd, Hd, hs, vs))
     t = torch.from_numpy(rgb)
     if roi_rect is not None:
@@ -308,3 +313,39 @@ def test_roi_rect_window_rounding(oracle_mod):
     a = oracle_mod.run_image(p, im, qt, roi_rect=(5, 9, 22, 13))      # -> [1, 7) x [2, 6)
     b = oracle_mod.run_image(p, im, qt, roi_rect=(4, 8, 24, 16))      # exactly [1, 7) x [2, 6)
     np.testing.assert_array_equal(a, b)
+
+
+# ------------------------------------------------- chroma at twice the scale --
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_chroma_2s_vs_independent(oracle_mod, k):
+    """Reading R18 (libjpeg-turbo scaled decoding of 4:2:0): chroma blocks
+    decoded at 1/(k/2) land on the luma grid and are used without
+    upsampling -- against scipy box means at k/2 and the identity filter."""
+    rng = np.random.default_rng(1000 + k)
+    qt = synth.quant_tables(75)
+    for (w, h) in [(64, 48), (97, 61), (40, 40)]:
+        im = synth.make_image(rng, w, h, qt)
+        p = oracle_mod.make_params(scale_denom=k, resize_mode="exact", resize_w=13, resize_h=11, chroma_2s=True)
+        got = oracle_mod.run_image(p, im, qt)
+        ref = independent_pipeline(im, qt, k, 13, 11, chroma_2s=True)
+        assert np.max(np.abs(got - ref)) < 2e-6, (k, w, h)
+        Y, Cb, Cr = oracle_mod.decode_image_planes(p, im, qt)
+        assert Cb.shape == Y.shape == (-(-h // k), -(-w // k))
+
+
+def test_chroma_2s_equals_r2_on_constant_chroma(oracle_mod):
+    """With one chroma level everywhere both readings give the same image
+    (triangle of a constant = the constant; DC-only blocks decode to DC/8 at
+    any scale)."""
+    qt = synth.quant_tables(75)
+    rng = np.random.default_rng(7)
+    im = synth.make_image(rng, 64, 48, qt)
+    coef = [im.coef[0]] + [np.zeros_like(c) for c in im.coef[1:]]
+    coef[1][..., 0] = 5
+    coef[2][..., 0] = -3
+    im2 = synth.CoefImage(64, 48, coef)
+    for k in (2, 4, 8):
+        a = oracle_mod.run_image(oracle_mod.make_params(scale_denom=k, resize_mode="exact", resize_w=16, resize_h=12), im2, qt)
+        b = oracle_mod.run_image(oracle_mod.make_params(scale_denom=k, resize_mode="exact", resize_w=16, resize_h=12,
+                                                        chroma_2s=True), im2, qt)
+        np.testing.assert_array_equal(a, b)
