@@ -411,6 +411,11 @@ class Workload:
         torch.cuda.synchronize()
         ctx = clocks if clocks is not None else _Null()
         with ctx:
+            # a ~0.1 ms spin ahead of the start event lets the host queue the
+            # first steps before the clock starts, so the timed region holds K
+            # steps of device work and not the host's first-launch latency
+            with torch.cuda.stream(self.stream):
+                torch.cuda._sleep(200_000)
             ev0.record(self.stream)
             for k in range(steps):
                 self.step(k)
