@@ -26,6 +26,9 @@
 // scale 1 the output tasks share the phase with the next step's IDCT and are
 // grabbed dynamically, two per lane per grab, interleaved by the compiler; at
 // scales 1/2..1/8 that IDCT is small and a static stride wins.
+#ifndef SMOL_COLOUR_UNROLL
+#define SMOL_COLOUR_UNROLL 1     // colour tasks interleaved per thread (A/B)
+#endif
 #ifndef SMOL_OUT_RUN_ROWS
 #define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
 #endif
@@ -774,6 +777,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       // colour tasks all cost the same and nothing else runs in this phase:
       // a static round-robin needs no work counter (running the partial last
       // round as half tasks measured slower, r02)
+      constexpr int kColU = SMOL_COLOUR_UNROLL;
+#pragma unroll(kColU)
       for (int t = tid; t < ntaskc; t += kThreads) {
         const int rr = (int)fdiv((uint32_t)t, fd_t4);
         const int p = t - rr * ntask4;
