@@ -98,6 +98,10 @@ SMOL_HD void src_tap_y(const DevImage& im, int d, int& i0, int& i1, float& w) {
 
 SMOL_HD int align16(int x) { return (x + 15) & ~15; }
 
+// RGB ring slot of decoded row r >= 0 (kRgbRing is even, so an even row's
+// odd neighbour never wraps)
+SMOL_HD int rgb_slot(int r) { return (int)((uint32_t)r % (uint32_t)kRgbRing); }
+
 // Shared-memory rings (fixed pitches so neighbour loads use immediate offsets):
 //   Y   : kYRing slots x kYP bytes, column = x - xbase[0]
 //   Cb/Cr: kCSlots = 16 + 2 slots x kCP bytes each; row r lives in slot
@@ -149,6 +153,7 @@ struct TileLayout {
   int rgb_x0, rgb_w, rgb_p;        // RGB ring: first column, width, pitch (u32; rgb_pitch(yp), compile-time in the kernel)
   int r0, nsteps;                  // first rolling-step row (16-aligned) and step count
   int fits;                        // footprint fits the fixed ring pitches
+  int tap_off;                     // int4 index of the host-computed tap region (-1: computed by the CTA)
   // byte offsets in dynamic shared memory
   int off_q, off_xt, off_yt, off_st, off_y, off_c, off_rgb, total;
   // the kernel's task-index divisors: luma / chroma blocks per block row,
@@ -209,6 +214,7 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.off_yt = off;  off += align16((oy1 - oy0) * 8);           // y taps: {ring byte offset of row y0 | y1<<16, w}
   L.off_st = off;  off += align16(L.nsteps * 8);              // per-step {ready, done}
   L.total = off;
+  L.tap_off = -1;
   L.fd_y = make_fastdiv(L.bx1[0] - L.bx0[0] + 1);
   L.fd_c = make_fastdiv(L.bx1[1] - L.bx0[1] + 1);
   L.fd_t4 = make_fastdiv(L.rgb_w >> 2);
@@ -216,6 +222,57 @@ SMOL_HD void tile_layout(const DevImage& im, int K, int oy0, int oy1, int ox0, i
   L.fd_fw = make_fastdiv(L.lx1 - L.lx0 + 1);
   L.fd_cw = make_fastdiv(L.cx1 - L.cx0 + 1);
 }
+
+// Bilinear taps of a tile, in the layout of its shared-memory tap region
+// [off_xt, off_st) (computed per CTA, or once per (image kind, tile) by the
+// host and copied in -- the same function either way, so the same bits).
+// x entry i (output column ox0 + i, padded to a multiple of 4): pixel pairs
+// {byte offset of x0 (a), (b), w (a), w (b)}; output quad q reads pair A at
+// int4 [q] and pair B at [nq4 + q]; a clamped upper tap gets weight 0.
+SMOL_HD void tile_xtap(const DevImage& im, const TileLayout& L, int i, int* xt) {
+  const int ntw = L.ox1 - L.ox0, nq4 = (ntw + 3) >> 2;
+  int i0, i1; float w;
+  src_tap_x(im, im.left + L.ox0 + (i < ntw - 1 ? i : ntw - 1), i0, i1, w);
+  int* e = xt + (((i >> 1) & 1) * nq4 + (i >> 2)) * 4 + (i & 1);
+  e[0] = (i0 - L.rgb_x0) * 4;
+  union { float f; int i; } u;
+  u.f = i1 == i0 ? 0.f : w;
+  e[2] = u.i;
+}
+// y entry i (output row oy0 + i): {byte offset of RGB ring row i0 | i1 << 16, w}
+SMOL_HD void tile_ytap(const DevImage& im, const TileLayout& L, int i, int pitch4, int* yt) {
+  int i0, i1; float w;
+  src_tap_y(im, im.top + L.oy0 + i, i0, i1, w);
+  union { float f; int i; } u;
+  u.f = i1 == i0 ? 0.f : w;
+  yt[2 * i] = (rgb_slot(i0) * pitch4) | (i1 << 16);
+  yt[2 * i + 1] = u.i;
+}
+// bytes of the tap region (x taps then y taps)
+SMOL_HD int tile_tap_bytes(const TileLayout& L) { return L.off_st - L.off_xt; }
+
+// Thumbnail kernel taps (one tile = the whole output): column pair q {4 x0
+// (a), 4 x0 (b), w (a), w (b)} relative to the footprint, and row i
+// {y0 - ly0 | (y1 - ly0) << 16, w}.
+SMOL_HD void thumb_xp(const DevImage& im, const TileLayout& L, int OW, int q, int* e) {
+  int a0, a1, b0, b1; float wa, wb;
+  src_tap_x(im, im.left + 2 * q, a0, a1, wa);
+  src_tap_x(im, im.left + (2 * q + 1 < OW - 1 ? 2 * q + 1 : OW - 1), b0, b1, wb);
+  union { float f; int i; } u, v;
+  u.f = a1 == a0 ? 0.f : wa;
+  v.f = b1 == b0 ? 0.f : wb;
+  e[0] = 4 * (a0 - L.lx0); e[1] = 4 * (b0 - L.lx0); e[2] = u.i; e[3] = v.i;
+}
+SMOL_HD void thumb_yt(const DevImage& im, const TileLayout& L, int i, int* e) {
+  int i0, i1; float w;
+  src_tap_y(im, im.top + i, i0, i1, w);
+  union { float f; int i; } u;
+  u.f = i1 == i0 ? 0.f : w;
+  e[0] = (i0 - L.ly0) | ((i1 - L.ly0) << 16);
+  e[1] = u.i;
+}
+// int4 words of a thumbnail tap region: (OW+1)/2 column pairs, then OH rows (2 per int4)
+SMOL_HD int thumb_tap_words(int OW, int OH) { return ((OW + 1) >> 1) + ((OH + 1) >> 1); }
 
 SMOL_HD long long tile_roi_blocks(const TileLayout& L) {
   long long n = 0;

@@ -26,9 +26,6 @@
 // scale 1 the output tasks share the phase with the next step's IDCT and are
 // grabbed dynamically, two per lane per grab, interleaved by the compiler; at
 // scales 1/2..1/8 that IDCT is small and a static stride wins.
-#ifndef SMOL_COLOUR_UNROLL
-#define SMOL_COLOUR_UNROLL 1     // colour tasks interleaved per thread (A/B)
-#endif
 #ifndef SMOL_OUT_RUN_ROWS
 #define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
 #endif
@@ -430,6 +427,7 @@ struct KParams {
   const DevRef* refs;              // per image: coefficient planes + kind
   const DevImage* kinds;           // per kind: geometry, strides, quant table ids
   const TileLayout* lays;          // per (kind, tile): the tile's layout (null: computed in the kernel)
+  const int4* taps;                // tap regions referenced by TileLayout::tap_off
   int lay_stride;                  // layouts per kind
   const uint16_t* qtables;
   void* out;
@@ -463,9 +461,6 @@ __device__ __forceinline__ void put_row(uint8_t* d, const uint32_t (&w)[2]) {
   else *d = (uint8_t)w[0];
 }
 
-// RGB ring slot of decoded row r >= 0 (kRgbRing is even, so an even row's
-// odd neighbour never wraps)
-__device__ __forceinline__ int rgb_slot(int r) { return (int)((uint32_t)r % (uint32_t)kRgbRing); }
 
 __device__ __forceinline__ uint32_t lds_u32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
 
@@ -531,20 +526,18 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   // so a pair's weights load into an adjacent register pair for FFMA2.
   // Output task q (pixels 4q .. 4q+3) reads pair A at [q] and pair B at
   // [nq4 + q]: consecutive lanes read consecutive 16-B entries.
-  const int nq4 = (ntw + 3) >> 2;
-  for (int i = tid; i < 4 * nq4; i += kThreads) {
-    int i0, i1; float w;
-    src_tap_x(im, im.left + ox0 + min(i, ntw - 1), i0, i1, w);
-    int* e = reinterpret_cast<int*>(xt) + (((i >> 1) & 1) * nq4 + (i >> 2)) * 4 + (i & 1);
-    e[0] = (i0 - L.rgb_x0) * 4;
-    e[2] = __float_as_int(i1 == i0 ? 0.f : w);
-  }
   // y taps per output row: {byte offset of RGB ring row i0 | i1 << 16, w}
-  // (row i0 + 1 is at +pitch4: the ring's guard slot mirrors slot 0)
-  for (int i = tid; i < nth; i += kThreads) {
-    int i0, i1; float w;
-    src_tap_y(im, im.top + oy0 + i, i0, i1, w);
-    yt[i] = make_int2((rgb_slot(i0) * pitch4) | (i1 << 16), __float_as_int(i1 == i0 ? 0.f : w));
+  // (row i0 + 1 is at +pitch4: the ring's guard slot mirrors slot 0).
+  // Precomputed per (image kind, tile) by the host when it could (copied
+  // in), else computed here (smol_geom.cuh tile_xtap / tile_ytap).
+  const int nq4 = (ntw + 3) >> 2;
+  if (L.tap_off >= 0) {
+    const int4* src = kp.taps + L.tap_off;
+    int4* dst = reinterpret_cast<int4*>(smem + L.off_xt);
+    for (int i = tid; i < tile_tap_bytes(L) / 16; i += kThreads) dst[i] = src[i];
+  } else {
+    for (int i = tid; i < 4 * nq4; i += kThreads) tile_xtap(im, L, i, reinterpret_cast<int*>(xt));
+    for (int i = tid; i < nth; i += kThreads) tile_ytap(im, L, i, pitch4, reinterpret_cast<int*>(yt));
   }
   if (im.gray)       // grayscale: neutral chroma everywhere in the rings (read only by colour)
     for (int i = tid; i < 2 * kCStride / 4; i += kThreads) reinterpret_cast<uint32_t*>(cring)[i] = 0x80808080u;
@@ -776,9 +769,8 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
       const int ntaskc = nq * ntask4;
       // colour tasks all cost the same and nothing else runs in this phase:
       // a static round-robin needs no work counter (running the partial last
-      // round as half tasks measured slower, r02)
-      constexpr int kColU = SMOL_COLOUR_UNROLL;
-#pragma unroll(kColU)
+      // round as half tasks, or unrolling two tasks per thread, measured
+      // slower, r02)
       for (int t = tid; t < ntaskc; t += kThreads) {
         const int rr = (int)fdiv((uint32_t)t, fd_t4);
         const int p = t - rr * ntask4;

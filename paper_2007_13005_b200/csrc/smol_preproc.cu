@@ -49,6 +49,7 @@ int32_t fail(int32_t code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kRing = 4;           // descriptor ring depth (runs in flight per plan)
+constexpr int kTapCap = 8192;      // int4 words of host-computed taps per run (128 KB; the rest: per CTA)
 constexpr int kMaxDevices = 64;
 
 // ------------------------------------------------------------ basis upload --
@@ -384,11 +385,15 @@ struct smol_preproc_plan {
   int map_cap = 0;
   int cta_map_mode = 1;        // SMOL_CTA_MAP=0 disables the balanced map (A/B)
   int thumb_mode = 1;          // SMOL_THUMB=0 disables the warp-per-image 1/8 kernel (A/B)
+  int tap_mode = 1;            // SMOL_TAPS=0: every CTA computes its own bilinear taps (A/B)
   DevImage* h_desc = nullptr;  // pinned [kRing][max_images]
   DevRef* h_ref = nullptr;     // pinned [kRing][max_images]
   TileLayout* d_lay = nullptr; // [kRing][lay_cap] tile layouts per (kind, tile)
   TileLayout* h_lay = nullptr; // pinned
   int lay_cap = 0;
+  int4* d_tap = nullptr;       // [kRing][tap_cap] bilinear tap regions per (kind, tile)
+  int4* h_tap = nullptr;       // pinned
+  int tap_cap = 0;             // int4 words per ring slot
   cudaEvent_t ev[kRing] = {};
   cudaEvent_t desc_ready[kRing] = {};      // descriptor upload of a ring slot done (copy stream)
   int ring = 0;
@@ -487,6 +492,7 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (const char* e = std::getenv("SMOL_THREADS")) pl->nt_mode = std::atoi(e);
   if (const char* e = std::getenv("SMOL_CTA_MAP")) pl->cta_map_mode = std::atoi(e);
   if (const char* e = std::getenv("SMOL_THUMB")) pl->thumb_mode = std::atoi(e);
+  if (const char* e = std::getenv("SMOL_TAPS")) pl->tap_mode = std::atoi(e);
   for (int c = 0; c < 3; ++c) {
     pl->na[c] = (float)(1.0 / (255.0 * (double)params->std[c]));
     pl->nb[c] = (float)(-(double)params->mean[c] / (double)params->std[c]);
@@ -500,6 +506,9 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   pl->lay_cap = std::min(4 * max_images, 4096) + 256;
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_lay, sizeof(TileLayout) * (size_t)pl->lay_cap * kRing);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_lay, sizeof(TileLayout) * (size_t)pl->lay_cap * kRing);
+  pl->tap_cap = kTapCap;
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_tap, sizeof(int4) * (size_t)pl->tap_cap * kRing);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_tap, sizeof(int4) * (size_t)pl->tap_cap * kRing);
   for (int i = 0; i < kRing && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&pl->ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->desc_ready[i], cudaEventDisableTiming);
@@ -596,6 +605,8 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (pl->d_ref) cudaFree(pl->d_ref);
   if (pl->d_lay) cudaFree(pl->d_lay);
   if (pl->h_lay) cudaFreeHost(pl->h_lay);
+  if (pl->d_tap) cudaFree(pl->d_tap);
+  if (pl->h_tap) cudaFreeHost(pl->h_tap);
   if (pl->h_ref) cudaFreeHost(pl->h_ref);
   const int dev = pl->device;
   delete pl;
@@ -907,6 +918,36 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
         tile_layout(h[k], K, oy0, oy1, ox0, ox1, hl[(size_t)k * lay_stride + j], yp, gc && !thumb);
       }
   }
+  // Bilinear taps per (image kind, tile), in the layout of the tile's
+  // shared-memory tap region, so a CTA copies them in instead of dividing
+  // per output row and column (the same smol_geom.cuh functions either way:
+  // same bits).  Bounded by kTapCap; tiles past it compute their own.
+  int ntap = 0;
+  int4* ht = pl->h_tap + (size_t)slot * pl->tap_cap;
+  int4* dt = pl->d_tap + (size_t)slot * pl->tap_cap;
+  if (pl->tap_mode) {
+    const int pitch4 = rgb_pitch(thumb ? kYPTiny : Cfg_yp(nt)) * 4;
+    for (int j = 0; j < nl; ++j) {
+      TileLayout& L = hl[j];
+      const DevImage& im = h[j / lay_stride];
+      const int words = thumb ? thumb_tap_words(pl->OW, pl->OH) : tile_tap_bytes(L) / 16;
+      if (ntap + words > pl->tap_cap) break;
+      int* e = reinterpret_cast<int*>(ht + ntap);
+      memset(e, 0, sizeof(int4) * (size_t)words);
+      if (thumb) {
+        const int nxp = (pl->OW + 1) >> 1;
+        for (int q = 0; q < nxp; ++q) thumb_xp(im, L, pl->OW, q, e + 4 * q);
+        for (int i = 0; i < pl->OH; ++i) thumb_yt(im, L, i, e + 4 * nxp + 2 * i);
+      } else {
+        const int nq4 = (L.ox1 - L.ox0 + 3) >> 2;
+        for (int i = 0; i < 4 * nq4; ++i) tile_xtap(im, L, i, e);
+        int* yt = e + (L.off_yt - L.off_xt) / 4;
+        for (int i = 0; i < L.oy1 - L.oy0; ++i) tile_ytap(im, L, i, pitch4, yt);
+      }
+      L.tap_off = ntap;
+      ntap += words;
+    }
+  }
 
   if (src != Src::kDevice) {
     // Staged paths: each image's ROI block rows (the whole output's tap
@@ -980,8 +1021,9 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     if (src == Src::kGather) {
       SMOL_CUDA(cudaMemcpyAsync(dg, hg, sizeof(GatherDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
-    SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (ntap) SMOL_CUDA(cudaMemcpyAsync(dt, ht, sizeof(int4) * ntap, cudaMemcpyHostToDevice, pl->copy_stream));
       smol_gather_kernel<<<n_images, 256, 0, pl->copy_stream>>>(dg);
       SMOL_CUDA(cudaGetLastError());
     } else {
@@ -1038,8 +1080,9 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       for (int i = 0; i < n_images; ++i) he[i].rec = rec_base + (ci[i].offset - lo);
       SMOL_CUDA(cudaMemcpyAsync(de, he, sizeof(ExpandDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
-    SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (ntap) SMOL_CUDA(cudaMemcpyAsync(dt, ht, sizeof(int4) * ntap, cudaMemcpyHostToDevice, pl->copy_stream));
       if (!on_device)
         SMOL_CUDA(cudaMemcpyAsync(pl->cbuf[sl], arena + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice,
                                   pl->copy_stream));
@@ -1063,6 +1106,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, stream));
     SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, stream));
     if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, stream));
+    if (ntap) SMOL_CUDA(cudaMemcpyAsync(dt, ht, sizeof(int4) * ntap, cudaMemcpyHostToDevice, stream));
     if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, stream));
   } else if (src == Src::kDevice) {
     // descriptors (and the CTA map) go up on the plan's copy stream, so the
@@ -1072,6 +1116,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
     if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, pl->copy_stream));
+    if (ntap) SMOL_CUDA(cudaMemcpyAsync(dt, ht, sizeof(int4) * ntap, cudaMemcpyHostToDevice, pl->copy_stream));
     if (map_n) SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaEventRecord(pl->desc_ready[slot], pl->copy_stream));
     SMOL_CUDA(cudaStreamWaitEvent(stream, pl->desc_ready[slot], 0));
@@ -1081,6 +1126,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   kp.kinds = d;
   kp.lays = nl ? dl : nullptr;
   kp.lay_stride = lay_stride;
+  kp.taps = dt;
   kp.qtables = qtables;
   kp.out = out;
   kp.OW = pl->OW; kp.OH = pl->OH; kp.tile_rows = tile_rows;

@@ -57,17 +57,15 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     // column taps per output pair, byte offsets of x0 in an RGB row; the
     // kernel always reads x0 + 1 (a clamped upper tap has weight 0, and the
     // byte -> float trick keeps even stale words finite)
-    for (int q = lane; q < (OW + 1) >> 1; q += 32) {
-      int a0, a1, b0, b1; float wa, wb;
-      src_tap_x(im, im.left + 2 * q, a0, a1, wa);
-      src_tap_x(im, im.left + min(2 * q + 1, OW - 1), b0, b1, wb);
-      S.xp[q] = make_int4(4 * (a0 - lx0), 4 * (b0 - lx0), __float_as_int(a1 == a0 ? 0.f : wa),
-                          __float_as_int(b1 == b0 ? 0.f : wb));
-    }
-    for (int i = lane; i < OH; i += 32) {
-      int i0, i1; float w;
-      src_tap_y(im, im.top + i, i0, i1, w);
-      S.yt[i] = make_int2((i0 - ly0) | ((i1 - ly0) << 16), __float_as_int(i1 == i0 ? 0.f : w));
+    // (precomputed once per image kind by the host when it could: copied in)
+    if (S.L.tap_off >= 0) {
+      const int4* src = kp.taps + S.L.tap_off;
+      const int nxp = (OW + 1) >> 1;
+      for (int q = lane; q < nxp; q += 32) S.xp[q] = src[q];
+      for (int i = lane; i < (OH + 1) >> 1; i += 32) reinterpret_cast<int4*>(S.yt)[i] = src[nxp + i];
+    } else {
+      for (int q = lane; q < (OW + 1) >> 1; q += 32) thumb_xp(im, S.L, OW, q, reinterpret_cast<int*>(&S.xp[q]));
+      for (int i = lane; i < OH; i += 32) thumb_yt(im, S.L, i, reinterpret_cast<int*>(&S.yt[i]));
     }
     // 1/8 decode (reading R1/R3): u8 = clamp(floor(DC * Q0 / 8 + 128 + 1/2))
     const float qy = (float)kp.qtables[im.qidx[0] * 64] * 0.125f;

@@ -480,6 +480,39 @@ def test_balanced_cta_map_invariance(n, monkeypatch):
     assert err[~aff].max(initial=0) <= TOL[cfg.out_dtype]
 
 
+@pytest.mark.parametrize("name", ["c2", "c3b", "c4", "mixed"])
+def test_host_tap_tables_invariance(name, monkeypatch):
+    """Bilinear taps precomputed by the host per (image kind, tile) and copied
+    into shared memory (SMOL_TAPS=1, default) or computed by each CTA / warp
+    (SMOL_TAPS=0): the same smol_geom.cuh functions, so bit-identical
+    outputs.  "mixed": 12 image sizes, more tap words than one run's table
+    holds, so some tiles take each path in the same launch."""
+    rng = np.random.default_rng(77)
+    if name == "mixed":
+        cfg = synth.CONFIGS["c2"]
+        qt = synth.quant_tables(75)
+        imgs = [synth.make_image(rng, 300 + 37 * i, 240 + 23 * i, qt) for i in range(12)]
+    else:
+        cfg = synth.CONFIGS[name]
+        imgs, qt = synth.batch_images(cfg, n=16, n_distinct=8)
+    ps = smol.params_from_config(cfg, layout="packed" if name == "c4" else "dense")
+    outs = {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("SMOL_TAPS", m)
+        plan = smol.Plan(ps, len(imgs))
+        outs[m] = plan.run(smol.batch_for(ps, imgs, qt)).clone()
+        torch.cuda.synchronize()
+        plan.close()
+    assert torch.equal(outs["0"], outs["1"])
+    if name == "mixed":
+        po = oracle.params_from_config(cfg)
+        for i in (0, 11):
+            ref = oracle.run_image(po, imgs[i], qt).astype(np.float64)
+            err = np.abs(outs["1"][i].float().cpu().numpy() - ref).max(axis=0)
+            aff = helpers.affected_outputs(po, imgs[i], qt)
+            assert err[~aff].max(initial=0) <= TOL[cfg.out_dtype]
+
+
 @pytest.mark.parametrize("layout,out_dtype", [("packed", "f32"), ("dense", "f32"), ("packed", "f16")])
 def test_thumb_kernel_matches_tiled_kernel_and_oracle(layout, out_dtype, monkeypatch):
     """Scale 1/8 small images go to the warp-per-image kernel (smol_thumb.cuh),
