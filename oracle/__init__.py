@@ -21,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "smol_oracle.c")
+_SRC_JPEG = os.path.join(_HERE, "smol_oracle_jpeg.c")
 _LIB_PATH = os.path.join(_HERE, "libsmol_oracle.so")
 _lib = None
 
@@ -28,10 +29,11 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (plain -O2, no -ffast-math)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "smol_oracle.h"))):
+            os.path.getmtime(_SRC), os.path.getmtime(_SRC_JPEG),
+            os.path.getmtime(os.path.join(_HERE, "smol_oracle.h"))):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-fPIC", "-shared",
-                               "-fno-fast-math", "-o", tmp, _SRC, "-lm"])
+                               "-fno-fast-math", "-o", tmp, _SRC, _SRC_JPEG, "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -94,6 +96,8 @@ def lib():
                                        ctypes.c_void_p]
         L.oracle_alg1_crop_window.argtypes = [ctypes.c_int32] * 3 + [P(ctypes.c_int32)] * 4
         L.oracle_f64_to_f16.argtypes = [ctypes.c_double]
+        L.oracle_jpeg_info_of.argtypes = [ctypes.c_char_p, ctypes.c_int64, P(JpegInfo)]
+        L.oracle_jpeg_decode.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_void_p * 3]
         L.oracle_f64_to_f16.restype = ctypes.c_uint16
         _lib = L
     return _lib
@@ -278,3 +282,33 @@ def alg1_crop_window(height: int, width: int, target: int):
 
 def f64_to_f16_bits(x: float) -> int:
     return int(lib().oracle_f64_to_f16(float(x)))
+
+
+# ---- baseline JPEG entropy decoding (smol_oracle_jpeg.c, T.81 F.2.2) ----
+class JpegInfo(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("ncomp", ctypes.c_int32),
+                ("h", ctypes.c_int32 * 3), ("v", ctypes.c_int32 * 3), ("tq", ctypes.c_int32 * 3),
+                ("blocks_w", ctypes.c_int32 * 3), ("blocks_h", ctypes.c_int32 * 3),
+                ("mcus_x", ctypes.c_int32), ("mcus_y", ctypes.c_int32),
+                ("restart_interval", ctypes.c_int32), ("qt", (ctypes.c_uint16 * 64) * 4)]
+
+
+def jpeg_info(data: bytes) -> JpegInfo:
+    info = JpegInfo()
+    rc = lib().oracle_jpeg_info_of(data, len(data), ctypes.byref(info))
+    if rc:
+        raise ValueError(f"oracle_jpeg_info_of: {rc}")
+    return info
+
+
+def jpeg_decode(data: bytes):
+    """-> (info, [planes [bh][bw][64] int16 natural order, absolute DC],
+    qtables [4][64] uint16 natural order)."""
+    info = jpeg_info(data)
+    planes = [np.zeros((info.blocks_h[c], info.blocks_w[c], 64), dtype=np.int16) for c in range(info.ncomp)]
+    ptrs = (ctypes.c_void_p * 3)(*([_ptr(p) for p in planes] + [None] * (3 - info.ncomp)))
+    rc = lib().oracle_jpeg_decode(data, len(data), ptrs)
+    if rc:
+        raise ValueError(f"oracle_jpeg_decode: {rc}")
+    qt = np.array([[info.qt[t][k] for k in range(64)] for t in range(4)], dtype=np.uint16)
+    return info, planes, qt

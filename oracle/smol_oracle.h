@@ -142,6 +142,27 @@ int oracle_alg1_crop_window(int32_t height, int32_t width, int32_t target,
 /* Round a double to IEEE binary16 (round to nearest even); returns bits. */
 uint16_t oracle_f64_to_f16(double x);
 
+/* ---- baseline JPEG entropy decoding (smol_oracle_jpeg.c)
+ * ITU-T T.81 Annexes B, C, F.2.2 followed sequentially (see that file).
+ * Accepts one baseline (SOF0/SOF1, 8-bit, Huffman) interleaved scan of 1 or
+ * 3 components, with or without restart intervals. */
+typedef struct {
+  int32_t width, height, ncomp;
+  int32_t h[3], v[3];            /* sampling factors (SOF) */
+  int32_t tq[3];                 /* quantization table selectors */
+  int32_t blocks_w[3], blocks_h[3];   /* coefficient blocks per component incl.
+                                         MCU padding (A.2.2 / A.2.3) */
+  int32_t mcus_x, mcus_y;
+  int32_t restart_interval;      /* MCUs per restart interval (DRI), 0 = none */
+  uint16_t qt[4][64];            /* DQT tables, natural order */
+} oracle_jpeg_info;
+
+/* Header of a JPEG file (0 = ok; nonzero = not a supported baseline file). */
+int oracle_jpeg_info_of(const uint8_t* data, int64_t size, oracle_jpeg_info* info);
+/* Entropy-decode the scan into planes[c]: [blocks_h][blocks_w][64] int16,
+ * natural order, absolute DC (caller-allocated, sizes from the info). */
+int oracle_jpeg_decode(const uint8_t* data, int64_t size, int16_t* const planes[3]);
+
 #ifdef __cplusplus
 }
 #endif
