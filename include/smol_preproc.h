@@ -186,8 +186,8 @@ int32_t smol_preproc_run(smol_preproc_plan_t* plan, const smol_batch_desc* batch
 /* Same as smol_preproc_run, but coefficient pointers may be pinned HOST
  * memory (qtables stay DEVICE).  Only the ROI block rows cross PCIe: a gather
  * kernel on the plan's internal copy stream stages them into plan-owned device
- * memory (double-buffered: the next call's transfer overlaps this call's fused
- * kernel), then the fused kernel runs on `stream`.  The staging buffers are
+ * memory (3 staging slots: the next call's transfer overlaps this call's fused
+ * kernel while the host prepares the call after it), then the fused kernel runs on `stream`.  The staging buffers are
  * sized in plan when params.max_width / max_height are set (no allocation in
  * any run call; a batch that does not fit returns SMOL_ERR_CAPACITY), else
  * allocated on first use and grown when a larger batch arrives.  Every
@@ -260,8 +260,8 @@ int32_t smol_compact_encode(const smol_preproc_params* params, const smol_image_
  * uses is copied host->device in one DMA on the plan's copy stream (skipped
  * when the arena is DEVICE memory); then, on `stream`, an expand kernel
  * rebuilds the ROI blocks of the plan's layout in plan-owned staging and the
- * fused kernel runs (double-buffered: the next call's DMA overlaps this
- * call's expand + fused kernel).  Each record's header must match the ROI ranges
+ * fused kernel runs (3 staging slots: the next call's DMA overlaps this
+ * call's expand + fused kernel while the host prepares the call after it).  Each record's header must match the ROI ranges
  * the plan computes for its image and lie inside the arena: checked on the
  * host (SMOL_ERR_INVALID) when the arena is host memory; a DEVICE arena is
  * not read by the host, so only its record offsets are checked.  Block

@@ -49,6 +49,7 @@ int32_t fail(int32_t code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kRing = 4;           // descriptor ring depth (runs in flight per plan)
+constexpr int kStageMax = 4, kStageDefault = 3;   // staging slots of the staged paths (SMOL_STAGE_SLOTS)
 constexpr int kTapCap = 8192;      // int4 words of host-computed taps per run (128 KB; the rest: per CTA)
 constexpr int kMaxDevices = 64;
 
@@ -398,20 +399,28 @@ struct smol_preproc_plan {
   cudaEvent_t desc_ready[kRing] = {};      // descriptor upload of a ring slot done (copy stream)
   int ring = 0;
   float na[3], nb[3];
-  // end-to-end (run_host) staging: ROI block rows gathered from pinned host
-  // memory into device memory on a copy stream, double-buffered
+  // end-to-end (run_host / run_compact) staging: ROI block rows gathered
+  // from pinned host memory (or expanded from compact records) into device
+  // memory, n_stage slots deep (default 3: the host prepares run k while the
+  // copy engine moves run k-1 and the SMs run k-2)
   cudaStream_t copy_stream = nullptr;
-  int16_t* stage[2] = {nullptr, nullptr};
-  size_t stage_cap[2] = {0, 0};            // bytes
-  GatherDesc* d_gather = nullptr;          // [2][max_images]
-  GatherDesc* h_gather = nullptr;          // pinned [2][max_images]
+  int n_stage = kStageDefault;
+  int16_t* stage[kStageMax] = {};
+  size_t stage_cap[kStageMax] = {};        // bytes
+  GatherDesc* d_gather = nullptr;          // [n_stage][max_images]
+  GatherDesc* h_gather = nullptr;          // pinned [n_stage][max_images]
   // compact transport (run_compact): device copy of the records, expand descriptors
-  uint8_t* cbuf[2] = {nullptr, nullptr};
-  size_t cbuf_cap[2] = {0, 0};
-  ExpandDesc* d_expand = nullptr;          // [2][max_images]
-  ExpandDesc* h_expand = nullptr;          // pinned [2][max_images]
+  uint8_t* cbuf[kStageMax] = {};
+  size_t cbuf_cap[kStageMax] = {};
+  ExpandDesc* d_expand = nullptr;          // [n_stage][max_images]
+  ExpandDesc* h_expand = nullptr;          // pinned [n_stage][max_images]
   std::vector<TileLayout> layouts;         // host scratch (whole-output footprints)
-  cudaEvent_t stage_free[2] = {}, stage_ready[2] = {};
+  cudaEvent_t stage_free[kStageMax] = {}, stage_ready[kStageMax] = {};
+  // run_compact: the expand kernel runs on its own stream, so batch k+1's
+  // expansion fills the SMs the fused kernel of batch k leaves idle in its tail
+  cudaStream_t expand_stream = nullptr;
+  cudaEvent_t stage_expanded[kStageMax] = {};
+  int expand_own_stream = 1;               // SMOL_EXPAND_STREAM=0: expand on `stream` (A/B)
   int stage_slot = 0;
   bool fixed_stage = false;                // staging sized in plan (params.max_width/max_height)
   std::vector<std::pair<uintptr_t, uintptr_t>> pinned_ok;   // run_host: verified [lo, hi) allocations
@@ -514,14 +523,19 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->desc_ready[i], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking);
-  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+  if (const char* ev = std::getenv("SMOL_EXPAND_STREAM")) pl->expand_own_stream = std::atoi(ev);
+  if (const char* ev = std::getenv("SMOL_STAGE_SLOTS")) pl->n_stage = std::max(2, std::min(kStageMax, std::atoi(ev)));
+  const size_t nst = (size_t)pl->n_stage;
+  for (int i = 0; i < pl->n_stage && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&pl->stage_free[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->stage_ready[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->stage_expanded[i], cudaEventDisableTiming);
   }
-  if (e == cudaSuccess) e = cudaMalloc(&pl->d_gather, sizeof(GatherDesc) * (size_t)max_images * 2);
-  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_gather, sizeof(GatherDesc) * (size_t)max_images * 2);
-  if (e == cudaSuccess) e = cudaMalloc(&pl->d_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
-  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_expand, sizeof(ExpandDesc) * (size_t)max_images * 2);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->expand_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_gather, sizeof(GatherDesc) * (size_t)max_images * nst);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_gather, sizeof(GatherDesc) * (size_t)max_images * nst);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_expand, sizeof(ExpandDesc) * (size_t)max_images * nst);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_expand, sizeof(ExpandDesc) * (size_t)max_images * nst);
   if (e == cudaSuccess) pl->layouts.reserve(max_images);
   if (e == cudaSuccess) {
     pl->map_cap = pl->num_sms * 8;
@@ -531,14 +545,14 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess && params->max_width > 0) {
     // staging of the staged paths for max_images images of at most
     // max_width x max_height (worst case: every block of the image, 4:4:4),
-    // so run_host / run_compact never allocate: dense ROI rows (both slots)
+    // so run_host / run_compact never allocate: dense ROI rows (every slot)
     // and compact records (units <= 2 per used element, plus the tables)
     const int E = block_elems(params->scale_denom, params->layout, params->idct_def);
     const long long bw = ceil_div(params->max_width, 8), bh = ceil_div(params->max_height, 8);
     const long long rows = 3 * bh, blocks = 3 * bw * bh;
     const size_t stage_img = (size_t)(2 * (blocks * E + rows * 16 + 3 * 8));
     const size_t rec_img = (size_t)compact_record_bytes(blocks, rows, 2LL * blocks * used_coefs(params->scale_denom, params->idct_def));
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    for (int i = 0; i < pl->n_stage && e == cudaSuccess; ++i) {
       pl->stage_cap[i] = stage_img * (size_t)max_images;
       e = cudaMalloc(&pl->stage[i], pl->stage_cap[i] + 256);
       if (e == cudaSuccess) {
@@ -587,9 +601,10 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
     if (pl->ev[i]) { cudaEventSynchronize(pl->ev[i]); cudaEventDestroy(pl->ev[i]); }
     if (pl->desc_ready[i]) cudaEventDestroy(pl->desc_ready[i]);
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kStageMax; ++i) {
     if (pl->stage_free[i]) { cudaEventSynchronize(pl->stage_free[i]); cudaEventDestroy(pl->stage_free[i]); }
     if (pl->stage_ready[i]) cudaEventDestroy(pl->stage_ready[i]);
+    if (pl->stage_expanded[i]) cudaEventDestroy(pl->stage_expanded[i]);
     if (pl->stage[i]) cudaFree(pl->stage[i]);
     if (pl->cbuf[i]) cudaFree(pl->cbuf[i]);
   }
@@ -598,6 +613,7 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
   if (pl->d_gather) cudaFree(pl->d_gather);
   if (pl->h_gather) cudaFreeHost(pl->h_gather);
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
+  if (pl->expand_stream) cudaStreamDestroy(pl->expand_stream);
   if (pl->d_desc) cudaFree(pl->d_desc);
   if (pl->d_map) cudaFree(pl->d_map);
   if (pl->h_map) cudaFreeHost(pl->h_map);
@@ -949,13 +965,15 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     }
   }
 
+  int sl_used = -1;                 // staging slot of a staged run
   if (src != Src::kDevice) {
     // Staged paths: each image's ROI block rows (the whole output's tap
     // footprint) are rebuilt in a plan-owned device buffer on the plan's copy
     // stream -- gathered from pinned host planes (kGather) or expanded from
     // compact records (kCompact) -- then the descriptors point at it.
     const int sl = pl->stage_slot;
-    pl->stage_slot ^= 1;
+    sl_used = sl;
+    pl->stage_slot = (sl + 1) % pl->n_stage;
     SMOL_CUDA(cudaEventSynchronize(pl->stage_free[sl]));     // host side: descriptor slot reusable
     const int E = block_elems(K, pl->p.layout, pl->p.idct_def);
     GatherDesc* hg = pl->h_gather + (size_t)sl * pl->max_images;
@@ -1090,12 +1108,21 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     if (map_n)
       SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaEventRecord(pl->stage_ready[sl], pl->copy_stream));
-    SMOL_CUDA(cudaStreamWaitEvent(stream, pl->stage_ready[sl], 0));
     if (src == Src::kCompact) {
-      // expand on the compute stream: the copy stream carries only copies,
-      // so batch k+1's transfer overlaps batch k's expand + fused kernel
-      smol_expand_kernel<<<n_images * kExpandSplit, kExpandWarps * 32, kExpandSmem, stream>>>(de);
+      // expand on the plan's expand stream: the copy stream carries only
+      // copies (batch k+1's transfer overlaps batch k's kernels) and the
+      // expansion of batch k+1 runs in the tail of batch k's fused kernel
+      // instead of between the fused kernels on `stream`
+      cudaStream_t es = pl->expand_own_stream ? pl->expand_stream : stream;
+      SMOL_CUDA(cudaStreamWaitEvent(es, pl->stage_ready[sl], 0));
+      smol_expand_kernel<<<n_images * kExpandSplit, kExpandWarps * 32, kExpandSmem, es>>>(de);
       SMOL_CUDA(cudaGetLastError());
+      if (es != stream) {
+        SMOL_CUDA(cudaEventRecord(pl->stage_expanded[sl], es));
+        SMOL_CUDA(cudaStreamWaitEvent(stream, pl->stage_expanded[sl], 0));
+      }
+    } else {
+      SMOL_CUDA(cudaStreamWaitEvent(stream, pl->stage_ready[sl], 0));
     }
   }
 
@@ -1149,7 +1176,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
     tk<<<grid_t, kThumbWarps * 32, kThumbSmem, stream>>>(kp, n_images);
     SMOL_CUDA(cudaGetLastError());
     SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
-    if (src != Src::kDevice) SMOL_CUDA(cudaEventRecord(pl->stage_free[pl->stage_slot ^ 1], stream));
+    if (sl_used >= 0) SMOL_CUDA(cudaEventRecord(pl->stage_free[sl_used], stream));
     return SMOL_OK;
   }
   kp.n_row_tiles = ntiles;
@@ -1159,7 +1186,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   fn<<<grid, nt, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
-  if (src != Src::kDevice) SMOL_CUDA(cudaEventRecord(pl->stage_free[pl->stage_slot ^ 1], stream));
+  if (sl_used >= 0) SMOL_CUDA(cudaEventRecord(pl->stage_free[sl_used], stream));
   return SMOL_OK;
 }
 
@@ -1225,8 +1252,8 @@ int32_t smol_preproc_run(smol_preproc_plan_t* pl, const smol_batch_desc* b, void
 int32_t smol_preproc_run_host(smol_preproc_plan_t* pl, const smol_batch_desc* b, void* out, void* stream) {
   // Pinned host coefficient memory is device-addressable under UVA.  Only the
   // ROI block rows cross PCIe: a gather kernel on the plan's copy stream
-  // stages them (double-buffered, so batch k+1's transfer overlaps batch k's
-  // fused kernel), then the fused kernel runs on `stream`.
+  // stages them (3 staging slots, so batch k+1's transfer overlaps batch k's
+  // fused kernel while the host prepares batch k+2), then the fused kernel runs on `stream`.
   // Every plane must be pinned host (or device) memory: the gather kernel
   // reads it over PCIe, and a pageable pointer would fault the context.  Each
   // plane's first and last byte is checked, with verified allocations cached
