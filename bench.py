@@ -54,6 +54,7 @@ L2_BYTES = 126 * 2 ** 20
 LAYOUT = {"c1": "dense", "c2": "dense", "c3a": "packed", "c3b": "packed", "c4": "packed", "c5": "packed"}
 # distinct synthetic images per config (replicated into distinct buffers)
 N_DISTINCT = {"c5": 16}
+JPEG_RESTART_INTERVAL = 4          # MCUs per restart interval of the e2e JPEG files
 # PAPER.md context numbers (another machine's: AWS g4dn.xlarge, one T4 + 4 vCPUs)
 PAPER_CONTEXT = {
     "hardware": "AWS g4dn.xlarge: NVIDIA T4 GPU + 4 vCPU cores (PAPER.md P:384-392)",
@@ -484,8 +485,32 @@ class Workload:
         cbs = [smol.CompactBatch(self.params, self.imgs, self.qt, location="pinned") for _ in range(2)]
         compact_value, compact_ms = e2e_time(cbs)
         compact_h2d = cbs[0].arena_bytes * grp.world
+        # JPEG files: headers parsed on the host, restart
+        # markers indexed and Huffman decoded on the GPU, then the fused kernel
+        jpeg_entry = None
+        try:
+            from synth import jpeg as sjpeg
+            t0 = time.perf_counter()
+            files = sjpeg.encode_batch(self.imgs, self.qt, JPEG_RESTART_INTERVAL)
+            enc_s = time.perf_counter() - t0
+            jbs = [smol.JpegBatch(files) for _ in range(2)]
+            jpeg_value, jpeg_ms = e2e_time(jbs)
+            jpeg_h2d = jbs[0].file_bytes * grp.world
+            jpeg_entry = {"value": jpeg_value, "unit": UNIT, "h2d_bytes_per_step": jpeg_h2d,
+                          "d2h_bytes_per_step": d2h, "ms_per_step": jpeg_ms,
+                          "mean_file_bytes": jbs[0].file_bytes / max(len(files), 1),
+                          "restart_interval_mcus": JPEG_RESTART_INTERVAL,
+                          "path": "smol_preproc_run_jpeg: baseline JPEG files (synth encoder, T.81 Annex K "
+                                  "tables, DRI) in pinned host memory -> host header parse (one per distinct "
+                                  "header) + one H2D DMA + RST index kernel + Huffman decode kernel (thread "
+                                  "per restart interval, ROI blocks only) + fused kernel; D2H of one image's "
+                                  "output as the step's result read",
+                          "encode_s_host": enc_s}
+            del jbs
+        except Exception as e:  # noqa: BLE001
+            jpeg_entry = {"error": repr(e)}
         return {"value": compact_value, "unit": UNIT, "h2d_bytes_per_step": compact_h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": compact_ms,
+                "ms_per_step": compact_ms, "jpeg": jpeg_entry,
                 "path": "smol_preproc_run_compact: compact records (ROI blocks, nonzero used coefficients) "
                         "in pinned host memory -> one H2D DMA + expand kernel + fused kernel; D2H of one "
                         "image's output as the step's result read",
@@ -579,6 +604,10 @@ def main():
         e2e["pcie_achieved_gbs"] = e2e["h2d_bytes_per_step"] / grp.world / (e2e["ms_per_step"] / 1e3) / 1e9
         e2e["pcie_frac"] = e2e["pcie_achieved_gbs"] / pcie["gbs"]
         e2e["pcie_peak_how"] = pcie["how"]
+        je = e2e.get("jpeg")
+        if isinstance(je, dict) and "ms_per_step" in je:
+            je["pcie_achieved_gbs"] = je["h2d_bytes_per_step"] / grp.world / (je["ms_per_step"] / 1e3) / 1e9
+            je["pcie_frac"] = je["pcie_achieved_gbs"] / pcie["gbs"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": grp.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SMOL_ABI_VERSION 2
+#define SMOL_ABI_VERSION 3
 
 typedef enum {
   SMOL_OK = 0,
@@ -280,9 +280,83 @@ void smol_preproc_destroy(smol_preproc_plan_t* plan);
 int32_t smol_preproc_output_shape(const smol_preproc_plan_t* plan, int32_t* c, int32_t* h,
                                   int32_t* w);
 
+/* ---------------------------------------------------------------------
+ * JPEG input (entropy decoding on the GPU).
+ *
+ * The paper leaves Huffman decoding on the host because it "requires
+ * substantial branching" (§6.4).  This entry point takes the
+ * JPEG files themselves: the host parses only the headers (ITU-T T.81 Annex
+ * B markers: SOF0/SOF1, DQT, DHT, DRI, SOS; a header byte-identical to the
+ * previous image's is parsed once), then on the GPU one kernel finds the
+ * restart markers (RSTm, T.81 B.2.1) and one thread per restart interval
+ * Huffman-decodes its MCUs (T.81 F.2.2: DC prediction reset at every
+ * interval, F.2.1.3.1; run-length AC, Figure F.13; zig-zag, Figure A.6),
+ * writing only the blocks inside each image's ROI (the plan's tap footprint)
+ * in the plan's layout; the fused kernel follows as for run_compact.  The
+ * output equals smol_preproc_run on the entropy-decoded planes bit for bit.
+ * Parallelism comes from restart intervals: a file without DRI decodes on one
+ * thread (correct, slow).
+ *
+ * Supported: baseline sequential Huffman (SOF0, or SOF1 with 8-bit tables),
+ * 8-bit samples, one interleaved scan of 1 (grayscale) or 3 components with
+ * luma sampling 2x2 (4:2:0), 2x1 (4:2:2) or 1x1 (4:4:4) and chroma 1x1;
+ * else SMOL_ERR_UNSUPPORTED.  Quantization tables come from each file's DQT
+ * (at most 64 distinct tables and 16 distinct sets of Huffman tables per
+ * batch: SMOL_ERR_CAPACITY).
+ * Malformed entropy-coded data cannot make a kernel read or write out of
+ * bounds (the bit reader stops at the file end; runs past 63 end the block);
+ * it yields wrong samples.  A header error is SMOL_ERR_INVALID with the image
+ * index in smol_last_error(). */
+typedef struct {
+  int64_t offset;                  /* byte offset of the file (SOI..EOI) in arena,
+                                      multiple of 16                                 */
+  int64_t size;                    /* bytes                                         */
+  int32_t roi_left, roi_top;       /* as smol_image_desc (-1,-1 = centre crop)      */
+  int32_t roi_x, roi_y, roi_w, roi_h;  /* as smol_image_desc (0,0,0,0 = none)       */
+} smol_jpeg_image;
+
+typedef struct {
+  int32_t n_images;                /* 0 is allowed (no-op)                          */
+  const smol_jpeg_image* images;   /* HOST array of n_images                        */
+  const void* arena;               /* the files: pinned HOST memory (cudaMallocHost /
+                                      cudaHostRegister); read by the host (headers)
+                                      and copied to the device in one DMA            */
+  int64_t arena_bytes;             /* every file lies inside [0, arena_bytes)       */
+} smol_jpeg_batch;
+
+/* Header of one JPEG file as this library reads it (host only, no CUDA). */
+typedef struct {
+  int32_t width, height;           /* SOF size                                      */
+  int32_t subsampling;             /* 420, 422, 444 or 400                           */
+  int32_t ncomp;
+  int32_t blocks_w[3], blocks_h[3];/* coefficient blocks per component incl. MCU padding */
+  int32_t mcus_x, mcus_y;
+  int32_t restart_interval;        /* MCUs per interval (0 = none)                   */
+  int32_t n_segments;              /* restart intervals in the scan                 */
+  int32_t scan_offset;             /* first byte of the entropy-coded data          */
+} smol_jpeg_header;
+
+int32_t smol_jpeg_parse_header(const void* data, int64_t size, smol_jpeg_header* out);
+
+/* Files -> output tensor (see above).  Stream ordering, staging and
+ * ownership as smol_preproc_run_compact: one DMA of the batch's byte range on
+ * the plan's copy stream, the index + decode kernels, then the fused kernel
+ * on `stream`; the arena must stay untouched until the call after next has
+ * returned (3 staging slots). */
+int32_t smol_preproc_run_jpeg(smol_preproc_plan_t* plan, const smol_jpeg_batch* batch, void* out,
+                              void* stream);
+
+/* Test-only: Huffman-decode every block of every image (no ROI, no plan)
+ * into caller-owned DEVICE planes: planes[3 i + c] = [blocks_h][blocks_w][64]
+ * int16, natural order, absolute DC (sizes from smol_jpeg_parse_header;
+ * NULL for the chroma of a grayscale file).  Synchronous; allocates and frees
+ * its own scratch. */
+int32_t smol_jpeg_decode_planes(const smol_jpeg_batch* batch, int16_t* const* planes, void* stream);
+
 /* Number of kernel launches one smol_preproc_run issues (for accounting): 1.
  * smol_preproc_run_host and smol_preproc_run_compact issue one more (the
- * gather or expand kernel before the fused kernel). */
+ * gather or expand kernel before the fused kernel), smol_preproc_run_jpeg two
+ * more (marker index + Huffman decode). */
 int32_t smol_preproc_launches_per_run(const smol_preproc_plan_t* plan);
 
 /* Host-only: geometry of one image under `params` (no CUDA needed). */

@@ -15,7 +15,8 @@ from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._native import (BatchDesc, CompactBatchDesc, CompactImage, Geometry, ImageDesc, Params,
+from ._native import (BatchDesc, CompactBatchDesc, CompactImage, Geometry, ImageDesc, JpegBatchDesc,
+                      JpegHeader, JpegImage, Params,
                       SmolError, build, check, lib,
                       SMOL_OUT_F16_NCHW, SMOL_OUT_F32_NCHW, SMOL_RESIZE_EXACT,
                       SMOL_RESIZE_SHORT_SIDE, SMOL_LAYOUT_DENSE64, SMOL_LAYOUT_PACKED, EXPORTS,
@@ -23,7 +24,8 @@ from ._native import (BatchDesc, CompactBatchDesc, CompactImage, Geometry, Image
                       LIB_PATH)
 from .layout import block_elems, pack_plane
 
-__all__ = ["make_params", "params_from_config", "geometry", "CoefBatch", "CompactBatch",
+__all__ = ["make_params", "params_from_config", "geometry", "CoefBatch", "CompactBatch", "JpegBatch",
+           "jpeg_header",
            "compact_encode", "Plan", "SmolError",
            "build", "lib", "EXPORTS", "LIB_PATH"]
 
@@ -253,6 +255,71 @@ class CompactBatch:
         self.desc.n_qtables = int(qtables.shape[0])
 
 
+def jpeg_header(data: bytes) -> dict:
+    """smol_jpeg_parse_header: the library's reading of a JPEG file's header."""
+    h = JpegHeader()
+    check(lib().smol_jpeg_parse_header(bytes(data), len(data), ctypes.byref(h)))
+    return {"width": h.width, "height": h.height, "subsampling": h.subsampling, "ncomp": h.ncomp,
+            "blocks_w": list(h.blocks_w)[:h.ncomp], "blocks_h": list(h.blocks_h)[:h.ncomp],
+            "mcus_x": h.mcus_x, "mcus_y": h.mcus_y, "restart_interval": h.restart_interval,
+            "n_segments": h.n_segments, "scan_offset": h.scan_offset}
+
+
+class JpegBatch:
+    """N JPEG files in one pinned host arena, for
+    smol_preproc_run_jpeg (headers parsed on the host, entropy decoding on the
+    GPU).  rois / roi_rects as for CompactBatch."""
+
+    def __init__(self, files: Sequence[bytes], rois: Optional[Sequence] = None,
+                 roi_rects: Optional[Sequence] = None):
+        import torch
+        self.n = len(files)
+        offs, o, seen = [], 0, {}
+        for f in files:                 # identical file objects share one copy
+            k = id(f)
+            if k not in seen:
+                seen[k] = o
+                o += (len(f) + 15) & ~15
+            offs.append(seen[k])
+        host = np.zeros(max(o, 16), np.uint8)
+        for f, oo in zip(files, offs):
+            host[oo:oo + len(f)] = np.frombuffer(f, np.uint8)
+        self.arena = torch.from_numpy(host).pin_memory()
+        self.arena_bytes = int(max(o, 16))
+        self.file_bytes = int(sum(len(f) for f in files))
+        self.images = (JpegImage * max(self.n, 1))()
+        for i, (f, oo) in enumerate(zip(files, offs)):
+            ji = JpegImage()
+            ji.offset, ji.size = oo, len(f)
+            roi = rois[i] if rois is not None else None
+            ji.roi_left, ji.roi_top = roi if roi is not None else (-1, -1)
+            if roi_rects is not None and roi_rects[i] is not None:
+                ji.roi_x, ji.roi_y, ji.roi_w, ji.roi_h = roi_rects[i]
+            self.images[i] = ji
+        self.desc = JpegBatchDesc()
+        self.desc.n_images = self.n
+        self.desc.images = ctypes.cast(self.images, ctypes.POINTER(JpegImage))
+        self.desc.arena = self.arena.data_ptr()
+        self.desc.arena_bytes = self.arena_bytes
+
+    def decode_planes(self, stream=None):
+        """smol_jpeg_decode_planes: every block of every file, Huffman-decoded
+        on the GPU -> per image a list of int16 device planes [bh][bw][64]."""
+        import torch
+        out, ptrs = [], []
+        for i in range(self.n):
+            f = bytes(self.arena[self.images[i].offset:self.images[i].offset + self.images[i].size].numpy())
+            h = jpeg_header(f)
+            pl = [torch.zeros((h["blocks_h"][c], h["blocks_w"][c], 64), dtype=torch.int16, device="cuda")
+                  for c in range(h["ncomp"])]
+            out.append(pl)
+            ptrs += [p.data_ptr() for p in pl] + [None] * (3 - len(pl))
+        arr = (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+        s = torch.cuda.current_stream() if stream is None else stream
+        check(lib().smol_jpeg_decode_planes(ctypes.byref(self.desc), arr, s.cuda_stream))
+        return out
+
+
 class Plan:
     """smol_preproc_plan on the current CUDA device."""
 
@@ -289,6 +356,10 @@ class Plan:
         if isinstance(batch, CompactBatch):
             check(lib().smol_preproc_run_compact(self._h, ctypes.byref(batch.desc), out.data_ptr(),
                                                  self._stream(stream)))
+            return out
+        if isinstance(batch, JpegBatch):
+            check(lib().smol_preproc_run_jpeg(self._h, ctypes.byref(batch.desc), out.data_ptr(),
+                                              self._stream(stream)))
             return out
         fn = lib().smol_preproc_run_host if batch.location == "pinned" else lib().smol_preproc_run
         check(fn(self._h, ctypes.byref(batch.desc), out.data_ptr(), self._stream(stream)))

@@ -33,7 +33,8 @@ SMOL_IDCT_BOX_MEAN, SMOL_IDCT_TRUNCATED = 0, 1
 EXPORTS = ["smol_preproc_plan", "smol_preproc_run", "smol_preproc_run_host", "smol_preproc_destroy",
            "smol_preproc_output_shape", "smol_preproc_launches_per_run", "smol_debug_geometry",
            "smol_debug_run", "smol_last_error", "smol_abi_version", "smol_compact_encode",
-           "smol_preproc_run_compact"]
+           "smol_preproc_run_compact", "smol_jpeg_parse_header", "smol_preproc_run_jpeg",
+           "smol_jpeg_decode_planes"]
 
 
 class Params(ctypes.Structure):
@@ -70,6 +71,25 @@ class CompactBatchDesc(ctypes.Structure):
     _fields_ = [("n_images", ctypes.c_int32), ("images", ctypes.POINTER(CompactImage)),
                 ("arena", ctypes.c_void_p), ("arena_bytes", ctypes.c_int64),
                 ("qtables", ctypes.c_void_p), ("n_qtables", ctypes.c_int32)]
+
+
+class JpegImage(ctypes.Structure):
+    _fields_ = [("offset", ctypes.c_int64), ("size", ctypes.c_int64),
+                ("roi_left", ctypes.c_int32), ("roi_top", ctypes.c_int32),
+                ("roi_x", ctypes.c_int32), ("roi_y", ctypes.c_int32),
+                ("roi_w", ctypes.c_int32), ("roi_h", ctypes.c_int32)]
+
+
+class JpegBatchDesc(ctypes.Structure):
+    _fields_ = [("n_images", ctypes.c_int32), ("images", ctypes.POINTER(JpegImage)),
+                ("arena", ctypes.c_void_p), ("arena_bytes", ctypes.c_int64)]
+
+
+class JpegHeader(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("subsampling", ctypes.c_int32),
+                ("ncomp", ctypes.c_int32), ("blocks_w", ctypes.c_int32 * 3), ("blocks_h", ctypes.c_int32 * 3),
+                ("mcus_x", ctypes.c_int32), ("mcus_y", ctypes.c_int32), ("restart_interval", ctypes.c_int32),
+                ("n_segments", ctypes.c_int32), ("scan_offset", ctypes.c_int32)]
 
 
 class BatchDesc(ctypes.Structure):
@@ -165,6 +185,9 @@ def lib():
         L.smol_abi_version.argtypes = []
         L.smol_compact_encode.argtypes = [P(Params), P(ImageDesc), vp, ctypes.c_int64, P(ctypes.c_int64)]
         L.smol_preproc_run_compact.argtypes = [vp, P(CompactBatchDesc), vp, vp]
+        L.smol_jpeg_parse_header.argtypes = [ctypes.c_char_p, ctypes.c_int64, P(JpegHeader)]
+        L.smol_preproc_run_jpeg.argtypes = [vp, P(JpegBatchDesc), vp, vp]
+        L.smol_jpeg_decode_planes.argtypes = [P(JpegBatchDesc), ctypes.POINTER(vp), vp]
         for name in EXPORTS:
             f = getattr(L, name)
             if f.restype is ctypes.c_int:           # ctypes default

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <mutex>
 #include <new>
@@ -22,6 +23,7 @@
 #include "smol_kernels.cuh"
 #include "smol_compact.cuh"
 #include "smol_thumb.cuh"
+#include "smol_jpeg.cuh"
 #include "smol_launch.h"
 
 using namespace smol;
@@ -165,6 +167,174 @@ int block_elems(int K, int layout, int def) {
   if (layout != SMOL_LAYOUT_PACKED || K == 1) return 64;
   if (def == SMOL_IDCT_TRUNCATED) return (8 / K) * (8 / K);
   return K == 2 ? 52 : K == 4 ? 28 : 1;
+}
+
+// ---- JPEG headers (T.81 Annex B) ----------------------
+constexpr int kMaxJpegQt = 64, kMaxHuffSets = 16;
+
+// Figure A.6 zig-zag order: position k -> natural index, built by walking
+// the anti-diagonals (even ones upwards).
+std::array<int, 64> zigzag_order() {
+  std::array<int, 64> z{};
+  int k = 0;
+  for (int s = 0; s < 15; ++s)
+    for (int i = 0; i < 8; ++i) {
+      const int v = (s % 2 == 0) ? std::min(s, 7) - i : std::max(0, s - 7) + i;   // row
+      const int u = s - v;
+      if (v < 0 || v > 7 || u < 0 || u > 7) continue;
+      z[k++] = v * 8 + u;
+    }
+  return z;
+}
+
+struct JpegHdr {
+  int32_t width = 0, height = 0, ncomp = 0, subsampling = 0;
+  int32_t h[3] = {}, v[3] = {}, tq[3] = {}, td[3] = {}, ta[3] = {};
+  int32_t ri = 0, scan_off = 0, mcus_x = 0, mcus_y = 0, nseg = 0;
+  int32_t blocks_w[3] = {}, blocks_h[3] = {};
+  uint16_t qt[4][64] = {};
+  bool qt_ok[4] = {};
+  // DHT contents per (class, id): BITS, HUFFVAL (kept raw for the table-set dedupe)
+  uint8_t bits[2][4][16] = {};
+  uint8_t vals[2][4][256] = {};
+  bool ht_ok[2][4] = {};
+};
+
+unsigned be16(const uint8_t* p) { return ((unsigned)p[0] << 8) | p[1]; }
+
+// T.81 Annex C code assignment (canonical: codes of one length consecutive,
+// next length = (last + 1) << 1); false if the counts overflow a prefix code.
+bool huff_valid(const uint8_t* bits) {
+  long long code = 0;
+  for (int l = 1; l <= 16; ++l) {
+    code += bits[l - 1];
+    if (code > (1LL << l)) return false;
+    code <<= 1;
+  }
+  return true;
+}
+
+void build_huff(const uint8_t* bits, const uint8_t* vals, HuffTable& t) {
+  memset(&t, 0, sizeof(t));
+  int code = 0, j = 0;
+  for (int l = 1; l <= 16; ++l) {
+    const int n = bits[l - 1];
+    if (n == 0) { t.maxcode[l] = -1; t.valoff[l] = 0; }
+    else {
+      t.valoff[l] = j - code;                   // HUFFVAL index = code + valoff (F.15: VALPTR - MINCODE)
+      for (int i = 0; i < n; ++i, ++code, ++j)
+        if (l <= kHuffLutBits)
+          for (int f = code << (kHuffLutBits - l); f < (code + 1) << (kHuffLutBits - l); ++f)
+            t.lut[f] = (uint16_t)(l << 8 | vals[j]);
+      t.maxcode[l] = code - 1;
+    }
+    code <<= 1;
+  }
+  t.maxcode[17] = INT_MAX;
+  memcpy(t.huffval, vals, 256);
+}
+
+// Header of one file; on error a status + message naming image idx.
+int32_t parse_jpeg(const uint8_t* d, int64_t size, int idx, JpegHdr& H) {
+  H = JpegHdr{};
+  static const std::array<int, 64> zz = zigzag_order();
+  if (size < 4 || d[0] != 0xFF || d[1] != 0xD8) return fail(SMOL_ERR_INVALID, "image %d: no SOI marker", idx);
+  int64_t i = 2;
+  bool sof = false;
+  while (true) {
+    if (i + 4 > size) return fail(SMOL_ERR_INVALID, "image %d: header runs past the file end", idx);
+    if (d[i] != 0xFF) return fail(SMOL_ERR_INVALID, "image %d: marker expected at byte %lld", idx, (long long)i);
+    const unsigned m = d[i + 1];
+    if (m == 0xFF) { ++i; continue; }
+    const unsigned len = be16(d + i + 2);
+    if (len < 2 || i + 2 + len > size) return fail(SMOL_ERR_INVALID, "image %d: segment length at byte %lld", idx, (long long)i);
+    const uint8_t* p = d + i + 4;
+    const int plen = (int)len - 2;
+    if (m == 0xDB) {                                               // DQT (B.2.4.1)
+      for (int o = 0; o < plen;) {
+        const int pq = p[o] >> 4, t = p[o] & 15;
+        if (pq != 0) return fail(SMOL_ERR_UNSUPPORTED, "image %d: 16-bit quantization table", idx);
+        if (t > 3 || o + 65 > plen) return fail(SMOL_ERR_INVALID, "image %d: bad DQT", idx);
+        for (int k = 0; k < 64; ++k) H.qt[t][zz[k]] = p[o + 1 + k];
+        H.qt_ok[t] = true;
+        o += 65;
+      }
+    } else if (m == 0xC4) {                                        // DHT (B.2.4.2)
+      for (int o = 0; o < plen;) {
+        if (o + 17 > plen) return fail(SMOL_ERR_INVALID, "image %d: bad DHT", idx);
+        const int tc = p[o] >> 4, th = p[o] & 15;
+        int nv = 0;
+        for (int k = 0; k < 16; ++k) nv += p[o + 1 + k];
+        if (tc > 1 || th > 3 || nv > 256 || o + 17 + nv > plen || !huff_valid(p + o + 1))
+          return fail(SMOL_ERR_INVALID, "image %d: bad DHT", idx);
+        memcpy(H.bits[tc][th], p + o + 1, 16);
+        memset(H.vals[tc][th], 0, 256);
+        memcpy(H.vals[tc][th], p + o + 17, (size_t)nv);
+        H.ht_ok[tc][th] = true;
+        o += 17 + nv;
+      }
+    } else if (m == 0xC0 || m == 0xC1) {                           // SOF0/1 (B.2.2)
+      if (plen < 6) return fail(SMOL_ERR_INVALID, "image %d: bad SOF", idx);
+      if (p[0] != 8) return fail(SMOL_ERR_UNSUPPORTED, "image %d: %d-bit samples", idx, p[0]);
+      H.height = (int32_t)be16(p + 1);
+      H.width = (int32_t)be16(p + 3);
+      H.ncomp = p[5];
+      if ((H.ncomp != 1 && H.ncomp != 3) || plen < 6 + 3 * H.ncomp)
+        return fail(SMOL_ERR_UNSUPPORTED, "image %d: %d components", idx, H.ncomp);
+      if (H.width <= 0 || H.height <= 0) return fail(SMOL_ERR_INVALID, "image %d: zero size (DNL)", idx);
+      for (int c = 0; c < H.ncomp; ++c) {
+        H.h[c] = p[7 + 3 * c] >> 4;
+        H.v[c] = p[7 + 3 * c] & 15;
+        H.tq[c] = p[8 + 3 * c];
+        if (H.tq[c] > 3) return fail(SMOL_ERR_INVALID, "image %d: bad Tq", idx);
+      }
+      sof = true;
+    } else if (m >= 0xC2 && m <= 0xCF && m != 0xC4 && m != 0xC8 && m != 0xCC) {
+      return fail(SMOL_ERR_UNSUPPORTED, "image %d: not baseline sequential Huffman (SOF 0x%02X)", idx, m);
+    } else if (m == 0xDD) {                                        // DRI (B.2.4.4)
+      if (plen < 2) return fail(SMOL_ERR_INVALID, "image %d: bad DRI", idx);
+      H.ri = (int32_t)be16(p);
+    } else if (m == 0xDA) {                                        // SOS (B.2.3)
+      if (!sof || plen < 1) return fail(SMOL_ERR_INVALID, "image %d: SOS before SOF", idx);
+      const int ns = p[0];
+      if (ns != H.ncomp || plen < 1 + 2 * ns + 3)
+        return fail(SMOL_ERR_UNSUPPORTED, "image %d: scan of %d of %d components", idx, ns, H.ncomp);
+      for (int j = 0; j < ns; ++j) {
+        H.td[j] = p[2 + 2 * j] >> 4;
+        H.ta[j] = p[2 + 2 * j] & 15;
+        if (H.td[j] > 3 || H.ta[j] > 3 || !H.ht_ok[0][H.td[j]] || !H.ht_ok[1][H.ta[j]])
+          return fail(SMOL_ERR_INVALID, "image %d: scan uses an undefined Huffman table", idx);
+      }
+      if (p[1 + 2 * ns] != 0 || p[2 + 2 * ns] != 63 || p[3 + 2 * ns] != 0)
+        return fail(SMOL_ERR_UNSUPPORTED, "image %d: not a baseline scan (Ss/Se/Ah/Al)", idx);
+      if (i + 2 + len > INT_MAX || size > INT_MAX) return fail(SMOL_ERR_UNSUPPORTED, "image %d: file >= 2 GiB", idx);
+      H.scan_off = (int32_t)(i + 2 + len);
+      break;
+    }
+    i += 2 + len;
+  }
+  for (int c = 0; c < H.ncomp; ++c)
+    if (!H.qt_ok[H.tq[c]]) return fail(SMOL_ERR_INVALID, "image %d: undefined quantization table", idx);
+  if (H.ncomp == 1) {
+    H.subsampling = 400;
+    H.blocks_w[0] = ceil_div(H.width, 8);                          // A.2.2: non-interleaved
+    H.blocks_h[0] = ceil_div(H.height, 8);
+    H.mcus_x = H.blocks_w[0];
+    H.mcus_y = H.blocks_h[0];
+  } else {
+    if (H.h[1] != 1 || H.v[1] != 1 || H.h[2] != 1 || H.v[2] != 1)
+      return fail(SMOL_ERR_UNSUPPORTED, "image %d: chroma sampling factors must be 1x1", idx);
+    if (H.h[0] == 2 && H.v[0] == 2) H.subsampling = 420;
+    else if (H.h[0] == 2 && H.v[0] == 1) H.subsampling = 422;
+    else if (H.h[0] == 1 && H.v[0] == 1) H.subsampling = 444;
+    else return fail(SMOL_ERR_UNSUPPORTED, "image %d: luma sampling %dx%d", idx, H.h[0], H.v[0]);
+    H.mcus_x = ceil_div(H.width, 8 * H.h[0]);                     // A.2.3: interleaved
+    H.mcus_y = ceil_div(H.height, 8 * H.v[0]);
+    for (int c = 0; c < 3; ++c) { H.blocks_w[c] = H.mcus_x * H.h[c]; H.blocks_h[c] = H.mcus_y * H.v[c]; }
+  }
+  const long long nmcu = (long long)H.mcus_x * H.mcus_y;
+  H.nseg = H.ri > 0 ? (int32_t)((nmcu + H.ri - 1) / H.ri) : 1;
+  return SMOL_OK;
 }
 
 // Per-image geometry (readings R4, R7, R11); fills the device descriptor's
@@ -421,6 +591,26 @@ struct smol_preproc_plan {
   cudaStream_t expand_stream = nullptr;
   cudaEvent_t stage_expanded[kStageMax] = {};
   int expand_own_stream = 1;               // SMOL_EXPAND_STREAM=0: expand on `stream` (A/B)
+  // run_jpeg: per staging slot the image descriptors,
+  // Huffman table sets, quantization tables and the segment index
+  JpegDesc* h_jdesc = nullptr;             // pinned [n_stage][max_images]
+  JpegDesc* d_jdesc = nullptr;
+  HuffSet* h_huff = nullptr;               // pinned [n_stage][kMaxHuffSets]
+  HuffSet* d_huff = nullptr;
+  uint16_t* h_jqt = nullptr;               // pinned [n_stage][kMaxJpegQt][64]
+  uint16_t* d_jqt = nullptr;
+  int32_t* d_seg[kStageMax] = {};          // [2][cap]: segment start byte, image
+  size_t seg_cap[kStageMax] = {};          // bytes
+  int8_t* d_zmap = nullptr;                // zig-zag position -> stored element of the layout (-1: dropped)
+  // host scratch of the current run_jpeg call
+  std::vector<JpegHdr> jhdr;               // distinct headers
+  std::vector<int> jimg_hdr;               // per image: header index
+  std::vector<smol_compact_image> jci;     // per image: descriptor for the common validation
+  std::vector<std::array<uint16_t, 64>> jqt;   // distinct quantization tables
+  std::vector<int> jhdr_set;               // per header: Huffman table set
+  std::vector<std::array<int, 3>> jhdr_qid; // per header: quantization table ids per component
+  std::vector<int> jset_hdr;               // per table set: a header holding it
+  int jnseg = 0;                           // restart intervals of the current batch
   int stage_slot = 0;
   bool fixed_stage = false;                // staging sized in plan (params.max_width/max_height)
   std::vector<std::pair<uintptr_t, uintptr_t>> pinned_ok;   // run_host: verified [lo, hi) allocations
@@ -536,6 +726,28 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_gather, sizeof(GatherDesc) * (size_t)max_images * nst);
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_expand, sizeof(ExpandDesc) * (size_t)max_images * nst);
   if (e == cudaSuccess) e = cudaMallocHost(&pl->h_expand, sizeof(ExpandDesc) * (size_t)max_images * nst);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_jdesc, sizeof(JpegDesc) * (size_t)max_images * nst);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_jdesc, sizeof(JpegDesc) * (size_t)max_images * nst);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_huff, sizeof(HuffSet) * kMaxHuffSets * nst);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_huff, sizeof(HuffSet) * kMaxHuffSets * nst);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_jqt, sizeof(uint16_t) * 64 * kMaxJpegQt * nst);
+  if (e == cudaSuccess) e = cudaMallocHost(&pl->h_jqt, sizeof(uint16_t) * 64 * kMaxJpegQt * nst);
+  if (e == cudaSuccess) {
+    // zig-zag position k (T.81 Figure A.6) -> element of the stored block:
+    // dense-64: the natural index; packed: the rank of the natural index
+    // among the elements the scale uses (row-major, as the PACKED layouts
+    // store them), dropped (-1) if unused
+    int8_t zm[64];
+    const std::array<int, 64> zz = zigzag_order();
+    const bool packed = params->layout == SMOL_LAYOUT_PACKED && params->scale_denom > 1;
+    const uint64_t use = used_mask(params->scale_denom, false, params->idct_def == SMOL_IDCT_TRUNCATED);
+    for (int k = 0; k < 64; ++k) {
+      const int nat = zz[k];
+      zm[k] = (int8_t)(!packed ? nat : ((use >> nat) & 1) ? __builtin_popcountll(use & ((1ull << nat) - 1)) : -1);
+    }
+    e = cudaMalloc(&pl->d_zmap, 64);
+    if (e == cudaSuccess) e = cudaMemcpy(pl->d_zmap, zm, 64, cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) pl->layouts.reserve(max_images);
   if (e == cudaSuccess) {
     pl->map_cap = pl->num_sms * 8;
@@ -559,6 +771,13 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
         pl->cbuf_cap[i] = rec_img * (size_t)max_images;
         e = cudaMalloc(&pl->cbuf[i], pl->cbuf_cap[i] + 256);
       }
+    }
+    // run_jpeg segment index: at most one restart interval per MCU (8x8 px
+    // worst case), 2 int32 each
+    const size_t seg_img = (size_t)8 * ceil_div(params->max_width, 8) * ceil_div(params->max_height, 8);
+    for (int i = 0; i < pl->n_stage && e == cudaSuccess; ++i) {
+      pl->seg_cap[i] = seg_img * (size_t)max_images;
+      e = cudaMalloc(&pl->d_seg[i], pl->seg_cap[i] + 256);
     }
     pl->fixed_stage = true;
   }
@@ -608,6 +827,15 @@ void smol_preproc_destroy(smol_preproc_plan_t* pl) {
     if (pl->stage[i]) cudaFree(pl->stage[i]);
     if (pl->cbuf[i]) cudaFree(pl->cbuf[i]);
   }
+  for (int i = 0; i < kStageMax; ++i)
+    if (pl->d_seg[i]) cudaFree(pl->d_seg[i]);
+  if (pl->d_jdesc) cudaFree(pl->d_jdesc);
+  if (pl->h_jdesc) cudaFreeHost(pl->h_jdesc);
+  if (pl->d_huff) cudaFree(pl->d_huff);
+  if (pl->h_huff) cudaFreeHost(pl->h_huff);
+  if (pl->d_jqt) cudaFree(pl->d_jqt);
+  if (pl->h_jqt) cudaFreeHost(pl->h_jqt);
+  if (pl->d_zmap) cudaFree(pl->d_zmap);
   if (pl->d_expand) cudaFree(pl->d_expand);
   if (pl->h_expand) cudaFreeHost(pl->h_expand);
   if (pl->d_gather) cudaFree(pl->d_gather);
@@ -644,7 +872,7 @@ int32_t smol_preproc_launches_per_run(const smol_preproc_plan_t* pl) {
 namespace {
 
 // Where the coefficient blocks come from.
-enum class Src { kDevice, kGather, kCompact };
+enum class Src { kDevice, kGather, kCompact, kJpeg };
 
 // Validate a compact image descriptor into its device descriptor (coefficient
 // pointers are set by the staging step).
@@ -709,14 +937,16 @@ int32_t grow(void** buf, size_t* cap, size_t need, cudaStream_t s, bool fixed, c
 
 int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, const uint16_t* qtables,
                  int n_qtables, void* out, void* stream_v, const KParams* dbg, Src src,
-                 const smol_compact_batch* cb = nullptr) {
-  g_last_error.clear();
+                 const smol_compact_batch* cb = nullptr, const smol_jpeg_batch* jb = nullptr) {
+  // (run_jpeg calls with its parsed descriptors and no g_last_error reset:
+  // its own messages so far are kept only on failure)
+  if (src != Src::kJpeg) g_last_error.clear();
   if (n_images < 0) return fail(SMOL_ERR_INVALID, "n_images=%d < 0", n_images);
   if (n_images == 0) return SMOL_OK;
   if (n_images > pl->max_images)
     return fail(SMOL_ERR_CAPACITY, "n_images=%d > plan capacity %d", n_images, pl->max_images);
   if (!images) return fail(SMOL_ERR_INVALID, "batch.images is NULL");
-  if (!qtables || n_qtables < 1 || n_qtables > 4)
+  if ((!qtables && src != Src::kJpeg) || n_qtables < 1 || n_qtables > (src == Src::kJpeg ? kMaxJpegQt : 4))
     return fail(SMOL_ERR_INVALID, "batch.qtables NULL or n_qtables=%d not in [1,4]", n_qtables);
   if (!out) return fail(SMOL_ERR_INVALID, "out is NULL");
   {
@@ -751,7 +981,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   int nk = 0;
   for (int i = 0; i < n_images; ++i) {
     int32_t rc = SMOL_OK;
-    if (src == Src::kCompact) {
+    if (src == Src::kCompact || src == Src::kJpeg) {
       const smol_compact_image* ci = static_cast<const smol_compact_image*>(images);
       const bool same = i > 0 && memcmp(&ci[i], &ci[i - 1], offsetof(smol_compact_image, offset)) == 0;
       if (!same) {
@@ -1044,7 +1274,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       if (ntap) SMOL_CUDA(cudaMemcpyAsync(dt, ht, sizeof(int4) * ntap, cudaMemcpyHostToDevice, pl->copy_stream));
       smol_gather_kernel<<<n_images, 256, 0, pl->copy_stream>>>(dg);
       SMOL_CUDA(cudaGetLastError());
-    } else {
+    } else if (src == Src::kCompact) {
       // records: bounds (and, for host arenas, header) checks, then one DMA of
       // the batch's byte range
       const smol_compact_image* ci = static_cast<const smol_compact_image*>(images);
@@ -1104,11 +1334,106 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       if (!on_device)
         SMOL_CUDA(cudaMemcpyAsync(pl->cbuf[sl], arena + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice,
                                   pl->copy_stream));
+    } else {
+      // JPEG files (N4): per image the decoder descriptor (staged ROI box
+      // from the expand descriptor, header fields, table set), the distinct
+      // quantization tables and Huffman table sets, then one DMA of the
+      // batch's byte range
+      const smol_jpeg_image* ji = jb->images;
+      const uint8_t* arena = static_cast<const uint8_t*>(jb->arena);
+      int64_t lo = INT64_MAX, hi = 0;
+      for (int i = 0; i < n_images; ++i) {
+        lo = std::min<int64_t>(lo, ji[i].offset);
+        hi = std::max<int64_t>(hi, ji[i].offset + ji[i].size);
+      }
+      void* cbuf = pl->cbuf[sl];
+      rc = grow(&cbuf, &pl->cbuf_cap[sl], (size_t)(hi - lo), pl->copy_stream, pl->fixed_stage, "JPEG files");
+      pl->cbuf[sl] = static_cast<uint8_t*>(cbuf);
+      if (rc) return rc;
+      JpegDesc* hj = pl->h_jdesc + (size_t)sl * pl->max_images;
+      JpegDesc* dj = pl->d_jdesc + (size_t)sl * pl->max_images;
+      HuffSet* hh = pl->h_huff + (size_t)sl * kMaxHuffSets;
+      HuffSet* dh = pl->d_huff + (size_t)sl * kMaxHuffSets;
+      uint16_t* hq = pl->h_jqt + (size_t)sl * kMaxJpegQt * 64;
+      uint16_t* dq = pl->d_jqt + (size_t)sl * kMaxJpegQt * 64;
+      const int nset = (int)pl->jset_hdr.size();
+      for (int t = 0; t < nset; ++t) {
+        const JpegHdr& H = pl->jhdr[pl->jset_hdr[t]];
+        for (int cl = 0; cl < 2; ++cl)
+          for (int id = 0; id < 4; ++id) {
+            HuffTable& T = cl ? hh[t].ac[id] : hh[t].dc[id];
+            if (H.ht_ok[cl][id]) build_huff(H.bits[cl][id], H.vals[cl][id], T);
+            else { memset(&T, 0, sizeof(T)); for (int l = 0; l < 18; ++l) T.maxcode[l] = -1; }
+          }
+      }
+      for (size_t t = 0; t < pl->jqt.size(); ++t) memcpy(hq + 64 * t, pl->jqt[t].data(), 128);
+      int64_t nseg_total = 0;
+      for (int i = 0; i < n_images; ++i) {
+        const JpegHdr& H = pl->jhdr[pl->jimg_hdr[i]];
+        const ExpandDesc& e = he[i];
+        JpegDesc& J = hj[i];
+        J.data = pl->cbuf[sl] + (ji[i].offset - lo);
+        J.tabs = dh + pl->jhdr_set[pl->jimg_hdr[i]];
+        J.size = (int32_t)ji[i].size;
+        J.scan_off = H.scan_off;
+        const TileLayout& L = Ls[hr[i].kind];
+        for (int c = 0; c < 3; ++c) {
+          J.dst[c] = e.dst[c];
+          J.dst_stride[c] = e.dst_stride[c];
+          J.nbx[c] = c < H.ncomp ? e.nbx[c] : 0;
+          J.nby[c] = c < H.ncomp ? e.nby[c] : 0;
+          J.bx0[c] = L.bx0[c];
+          J.by0[c] = L.by0[c];
+          J.h[c] = (uint8_t)H.h[c]; J.v[c] = (uint8_t)H.v[c];
+          J.td[c] = (uint8_t)H.td[c]; J.ta[c] = (uint8_t)H.ta[c];
+        }
+        J.mcus_x = H.mcus_x;
+        J.nmcu = H.mcus_x * H.mcus_y;
+        J.ri = H.ri > 0 ? H.ri : J.nmcu;
+        J.nseg = H.nseg;
+        J.seg_base = (int32_t)nseg_total;
+        J.E = E;
+        J.ncomp = (uint8_t)H.ncomp;
+        nseg_total += H.nseg;
+      }
+      if (nseg_total >= INT_MAX / 2) return fail(SMOL_ERR_CAPACITY, "%lld restart intervals in one batch", (long long)nseg_total);
+      void* segb = pl->d_seg[sl];
+      rc = grow(&segb, &pl->seg_cap[sl], (size_t)nseg_total * 8, pl->copy_stream, pl->fixed_stage, "segment index");
+      pl->d_seg[sl] = static_cast<int32_t*>(segb);
+      if (rc) return rc;
+      pl->jnseg = (int)nseg_total;
+      SMOL_CUDA(cudaMemcpyAsync(dj, hj, sizeof(JpegDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(dh, hh, sizeof(HuffSet) * nset, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(dq, hq, 128 * pl->jqt.size(), cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(d, h, sizeof(DevImage) * nk, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(dr, hr, sizeof(DevRef) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (nl) SMOL_CUDA(cudaMemcpyAsync(dl, hl, sizeof(TileLayout) * nl, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (ntap) SMOL_CUDA(cudaMemcpyAsync(dt, ht, sizeof(int4) * ntap, cudaMemcpyHostToDevice, pl->copy_stream));
+      SMOL_CUDA(cudaMemcpyAsync(pl->cbuf[sl], arena + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice, pl->copy_stream));
+      qtables = dq;
     }
     if (map_n)
       SMOL_CUDA(cudaMemcpyAsync(dm, hm, sizeof(int4) * map_n, cudaMemcpyHostToDevice, pl->copy_stream));
     SMOL_CUDA(cudaEventRecord(pl->stage_ready[sl], pl->copy_stream));
-    if (src == Src::kCompact) {
+    if (src == Src::kJpeg) {
+      // marker index (warp per image) + Huffman decode (thread per restart
+      // interval) on the expand stream, into the staged ROI planes
+      cudaStream_t es = pl->expand_own_stream ? pl->expand_stream : stream;
+      const int sl_ = sl;
+      JpegDesc* dj = pl->d_jdesc + (size_t)sl_ * pl->max_images;
+      int32_t* seg_start = pl->d_seg[sl_];
+      int32_t* seg_img = seg_start + pl->jnseg;
+      SMOL_CUDA(cudaStreamWaitEvent(es, pl->stage_ready[sl_], 0));
+      smol_jpeg_index_kernel<<<ceil_div(n_images, 4), 128, 0, es>>>(dj, n_images, seg_start, seg_img);
+      SMOL_CUDA(cudaGetLastError());
+      smol_jpeg_decode_kernel<<<ceil_div(pl->jnseg, kJpegThreads), kJpegThreads, 0, es>>>(dj, pl->jnseg, seg_start,
+                                                                                          seg_img, pl->d_zmap);
+      SMOL_CUDA(cudaGetLastError());
+      if (es != stream) {
+        SMOL_CUDA(cudaEventRecord(pl->stage_expanded[sl_], es));
+        SMOL_CUDA(cudaStreamWaitEvent(stream, pl->stage_expanded[sl_], 0));
+      }
+    } else if (src == Src::kCompact) {
       // expand on the plan's expand stream: the copy stream carries only
       // copies (batch k+1's transfer overlaps batch k's kernels) and the
       // expansion of batch k+1 runs in the tail of batch k's fused kernel
@@ -1310,6 +1635,212 @@ int32_t smol_preproc_run_compact(smol_preproc_plan_t* pl, const smol_compact_bat
   if (b->n_images > 0 && (!b->arena || reinterpret_cast<uintptr_t>(b->arena) % 16 || b->arena_bytes <= 0))
     return fail(SMOL_ERR_INVALID, "compact arena NULL, not 16-byte aligned or empty");
   return run_impl(pl, b->n_images, b->images, b->qtables, b->n_qtables, out, stream, nullptr, Src::kCompact, b);
+}
+
+int32_t smol_jpeg_parse_header(const void* data, int64_t size, smol_jpeg_header* out) {
+  g_last_error.clear();
+  if (!data || !out) return fail(SMOL_ERR_INVALID, "data/out is NULL");
+  JpegHdr H;
+  int32_t rc = parse_jpeg(static_cast<const uint8_t*>(data), size, 0, H);
+  if (rc) return rc;
+  memset(out, 0, sizeof(*out));
+  out->width = H.width; out->height = H.height; out->subsampling = H.subsampling; out->ncomp = H.ncomp;
+  for (int c = 0; c < 3; ++c) { out->blocks_w[c] = H.blocks_w[c]; out->blocks_h[c] = H.blocks_h[c]; }
+  out->mcus_x = H.mcus_x; out->mcus_y = H.mcus_y;
+  out->restart_interval = H.ri;
+  out->n_segments = H.nseg;
+  out->scan_offset = H.scan_off;
+  return SMOL_OK;
+}
+
+namespace {
+// Batch checks shared by run_jpeg and decode_planes: host-readable arena,
+// files inside it.
+int32_t check_jpeg_batch(const smol_jpeg_batch* b) {
+  if (!b) return fail(SMOL_ERR_INVALID, "batch is NULL");
+  if (b->n_images < 0) return fail(SMOL_ERR_INVALID, "n_images=%d < 0", b->n_images);
+  if (b->n_images == 0) return SMOL_OK;
+  if (!b->images || !b->arena || b->arena_bytes <= 0) return fail(SMOL_ERR_INVALID, "images/arena NULL or empty");
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, b->arena) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
+    cudaGetLastError();
+    return fail(SMOL_ERR_INVALID, "JPEG arena must be pinned host memory (headers are parsed on the host)");
+  }
+  for (int i = 0; i < b->n_images; ++i) {
+    const smol_jpeg_image& m = b->images[i];
+    if (m.offset < 0 || m.offset % 16 || m.size < 4 || m.offset + m.size > b->arena_bytes || m.size > INT_MAX)
+      return fail(SMOL_ERR_INVALID, "image %d: file [%lld, +%lld) not 16-B aligned or outside the arena of %lld B", i,
+                  (long long)m.offset, (long long)m.size, (long long)b->arena_bytes);
+  }
+  return SMOL_OK;
+}
+
+// Distinct headers of a batch (an image whose header bytes equal the previous
+// image's reuses its parse), their quantization tables and table sets.
+int32_t parse_jpeg_batch(smol_preproc_plan_t* pl, const smol_jpeg_batch* b) {
+  const uint8_t* arena = static_cast<const uint8_t*>(b->arena);
+  const int n = b->n_images;
+  pl->jhdr.clear(); pl->jhdr_set.clear(); pl->jset_hdr.clear(); pl->jqt.clear(); pl->jhdr_qid.clear();
+  pl->jimg_hdr.resize(n);
+  pl->jci.resize(n);
+  for (int i = 0; i < n; ++i) {
+    const smol_jpeg_image& m = b->images[i];
+    const uint8_t* data = arena + m.offset;
+    bool same = false;
+    if (i > 0) {
+      const JpegHdr& P = pl->jhdr[pl->jimg_hdr[i - 1]];
+      const uint8_t* pd = arena + b->images[i - 1].offset;
+      same = m.size > P.scan_off && memcmp(data, pd, (size_t)P.scan_off) == 0;
+    }
+    if (same) {
+      pl->jimg_hdr[i] = pl->jimg_hdr[i - 1];
+    } else {
+      pl->jhdr.emplace_back();
+      JpegHdr& H = pl->jhdr.back();
+      int32_t rc = parse_jpeg(data, m.size, i, H);
+      if (rc) return rc;
+      std::array<int, 3> qid{0, 0, 0};
+      for (int c = 0; c < H.ncomp; ++c) {
+        std::array<uint16_t, 64> q;
+        memcpy(q.data(), H.qt[H.tq[c]], 128);
+        int k = 0;
+        while (k < (int)pl->jqt.size() && pl->jqt[k] != q) ++k;
+        if (k == (int)pl->jqt.size()) {
+          if (k >= kMaxJpegQt) return fail(SMOL_ERR_CAPACITY, "more than %d distinct quantization tables", kMaxJpegQt);
+          pl->jqt.push_back(q);
+        }
+        qid[c] = k;
+      }
+      pl->jhdr_qid.push_back(qid);
+      int t = 0;
+      for (; t < (int)pl->jset_hdr.size(); ++t) {
+        const JpegHdr& O = pl->jhdr[pl->jset_hdr[t]];
+        if (!memcmp(O.ht_ok, H.ht_ok, sizeof(H.ht_ok)) && !memcmp(O.bits, H.bits, sizeof(H.bits)) &&
+            !memcmp(O.vals, H.vals, sizeof(H.vals)))
+          break;
+      }
+      if (t == (int)pl->jset_hdr.size()) {
+        if (t >= kMaxHuffSets) return fail(SMOL_ERR_CAPACITY, "more than %d distinct Huffman table sets", kMaxHuffSets);
+        pl->jset_hdr.push_back((int)pl->jhdr.size() - 1);
+      }
+      pl->jhdr_set.push_back(t);
+      pl->jimg_hdr[i] = (int)pl->jhdr.size() - 1;
+    }
+    const int hi = pl->jimg_hdr[i];
+    const JpegHdr& H = pl->jhdr[hi];
+    smol_compact_image& ci = pl->jci[i];
+    memset(&ci, 0, sizeof(ci));
+    ci.width = H.width; ci.height = H.height; ci.subsampling = H.subsampling;
+    for (int c = 0; c < 3; ++c) ci.qtable[c] = c < H.ncomp ? pl->jhdr_qid[hi][c] : 0;
+    ci.roi_left = m.roi_left; ci.roi_top = m.roi_top;
+    ci.roi_x = m.roi_x; ci.roi_y = m.roi_y; ci.roi_w = m.roi_w; ci.roi_h = m.roi_h;
+    ci.offset = 0;
+  }
+  return SMOL_OK;
+}
+}  // namespace
+
+int32_t smol_preproc_run_jpeg(smol_preproc_plan_t* pl, const smol_jpeg_batch* b, void* out, void* stream) {
+  g_last_error.clear();
+  if (!pl) return fail(SMOL_ERR_INVALID, "plan is NULL");
+  int32_t rc = check_jpeg_batch(b);
+  if (rc || b->n_images == 0) return rc;
+  if (b->n_images > pl->max_images)
+    return fail(SMOL_ERR_CAPACITY, "n_images=%d > plan capacity %d", b->n_images, pl->max_images);
+  if (pl->p.chroma_2s) return fail(SMOL_ERR_UNSUPPORTED, "run_jpeg with chroma_2s plans");
+  rc = parse_jpeg_batch(pl, b);
+  if (rc) return rc;
+  return run_impl(pl, b->n_images, pl->jci.data(), nullptr, (int)pl->jqt.size(), out, stream, nullptr, Src::kJpeg,
+                  nullptr, b);
+}
+
+int32_t smol_jpeg_decode_planes(const smol_jpeg_batch* b, int16_t* const* planes, void* stream_v) {
+  g_last_error.clear();
+  int32_t rc = check_jpeg_batch(b);
+  if (rc || b->n_images == 0) return rc;
+  if (!planes) return fail(SMOL_ERR_INVALID, "planes is NULL");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_v);
+  const int n = b->n_images;
+  std::vector<JpegHdr> hs(n);
+  std::vector<JpegDesc> js(n);
+  std::vector<HuffSet> sets(n);
+  int64_t lo = INT64_MAX, hi = 0, nseg = 0;
+  for (int i = 0; i < n; ++i) {
+    const smol_jpeg_image& m = b->images[i];
+    rc = parse_jpeg(static_cast<const uint8_t*>(b->arena) + m.offset, m.size, i, hs[i]);
+    if (rc) return rc;
+    lo = std::min<int64_t>(lo, m.offset);
+    hi = std::max<int64_t>(hi, m.offset + m.size);
+    nseg += hs[i].nseg;
+  }
+  const std::array<int, 64> zz = zigzag_order();
+  int8_t zm[64];
+  for (int k = 0; k < 64; ++k) zm[k] = (int8_t)zz[k];
+  uint8_t* dd = nullptr;
+  JpegDesc* dj = nullptr;
+  HuffSet* dh = nullptr;
+  int32_t* dseg = nullptr;
+  int8_t* dz = nullptr;
+  auto cleanup = [&] {
+    if (dd) cudaFree(dd);
+    if (dj) cudaFree(dj);
+    if (dh) cudaFree(dh);
+    if (dseg) cudaFree(dseg);
+    if (dz) cudaFree(dz);
+  };
+  cudaError_t e = cudaMalloc(&dd, (size_t)(hi - lo));
+  if (e == cudaSuccess) e = cudaMalloc(&dj, sizeof(JpegDesc) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&dh, sizeof(HuffSet) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&dseg, 8 * (size_t)nseg);
+  if (e == cudaSuccess) e = cudaMalloc(&dz, 64);
+  nseg = 0;
+  for (int i = 0; i < n && e == cudaSuccess; ++i) {
+    const JpegHdr& H = hs[i];
+    for (int cl = 0; cl < 2; ++cl)
+      for (int id = 0; id < 4; ++id) {
+        HuffTable& T = cl ? sets[i].ac[id] : sets[i].dc[id];
+        if (H.ht_ok[cl][id]) build_huff(H.bits[cl][id], H.vals[cl][id], T);
+        else { memset(&T, 0, sizeof(T)); for (int l = 0; l < 18; ++l) T.maxcode[l] = -1; }
+      }
+    JpegDesc& J = js[i];
+    memset(&J, 0, sizeof(J));
+    J.data = dd + (b->images[i].offset - lo);
+    J.tabs = dh + i;
+    J.size = (int32_t)b->images[i].size;
+    J.scan_off = H.scan_off;
+    for (int c = 0; c < H.ncomp; ++c) {
+      J.dst[c] = planes[3 * i + c];
+      if (!J.dst[c]) { e = cudaErrorInvalidValue; break; }
+      J.dst_stride[c] = H.blocks_w[c] * 64;
+      J.nbx[c] = H.blocks_w[c];
+      J.nby[c] = H.blocks_h[c];
+      J.h[c] = (uint8_t)H.h[c]; J.v[c] = (uint8_t)H.v[c];
+      J.td[c] = (uint8_t)H.td[c]; J.ta[c] = (uint8_t)H.ta[c];
+    }
+    J.mcus_x = H.mcus_x;
+    J.nmcu = H.mcus_x * H.mcus_y;
+    J.ri = H.ri > 0 ? H.ri : J.nmcu;
+    J.nseg = H.nseg;
+    J.seg_base = (int32_t)nseg;
+    J.E = 64;
+    J.ncomp = (uint8_t)H.ncomp;
+    nseg += H.nseg;
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dd, static_cast<const uint8_t*>(b->arena) + lo, (size_t)(hi - lo),
+                                            cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dj, js.data(), sizeof(JpegDesc) * n, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dh, sets.data(), sizeof(HuffSet) * n, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dz, zm, 64, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) {
+    smol_jpeg_index_kernel<<<ceil_div(n, 4), 128, 0, stream>>>(dj, n, dseg, dseg + nseg);
+    smol_jpeg_decode_kernel<<<(int)((nseg + kJpegThreads - 1) / kJpegThreads), kJpegThreads, 0, stream>>>(
+        dj, (int)nseg, dseg, dseg + nseg, dz);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  cleanup();
+  if (e != cudaSuccess) return fail(SMOL_ERR_CUDA, "jpeg decode: %s", cudaGetErrorString(e));
+  return SMOL_OK;
 }
 
 int32_t smol_compact_encode(const smol_preproc_params* p, const smol_image_desc* d, void* dst, int64_t capacity,

@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(native):
     assert declared == set(_native.EXPORTS)
     for name in declared:
         assert hasattr(native, name), name
-    assert native.smol_abi_version() == 2
+    assert native.smol_abi_version() == 3
 
 
 def test_library_is_sm100a(native):
