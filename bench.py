@@ -37,6 +37,7 @@ import subprocess
 import sys
 import threading
 import time
+from typing import Optional
 
 import numpy as np
 
@@ -75,6 +76,29 @@ def _traffic(cfg_name: str, layout: str):
         return None if t is None else float(t["read"] + t["write"])
     except Exception:
         return None
+
+
+def _warp_instr(cfg_name: str, layout: str):
+    """ncu warp instructions per launch of the config's kernel (profiles/traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(f"{cfg_name}/{layout}")
+        return None if t is None or "warp_instr" not in t else float(t["warp_instr"])
+    except Exception:
+        return None
+
+
+def _issue_roofline(cfg_name: str, layout: str, launch_ms: float, sm_mhz) -> Optional[dict]:
+    """Secondary roofline: warp instructions issued per second against the
+    issue peak (148 SMs x 4 schedulers x 1 instruction per clock at the
+    measured SM clock) -- the bound of a kernel that is not HBM-bound."""
+    wi = _warp_instr(cfg_name, layout)
+    if wi is None or not sm_mhz:
+        return None
+    peak = 148 * 4 * float(sm_mhz) * 1e6 / 1e9
+    achieved = wi / (launch_ms / 1e3) / 1e9
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "G warp-instr/s", "frac": achieved / peak,
+            "warp_instr_per_launch": wi, "source": "profiles/traffic.json (ncu smsp__inst_executed.sum)"}
 
 
 def _cpu_model() -> str:
@@ -638,6 +662,9 @@ def main():
         c = clk.summary()
         if c:
             line["clocks"] = c
+            iss = _issue_roofline(cfg.name, w.layout, step_ms, c.get("sm_mhz"))
+            if iss:
+                line["roofline"]["issue"] = iss
     # ---- Eq. 4 report (N = 1), the other configs, the CPU oracle ------------
     if line is not None and grp.world == 1 and not args.no_eq4:
         try:
@@ -656,6 +683,11 @@ def main():
                 del wx
                 torch.cuda.empty_cache()
         if line is not None:
+            mhz = (line.get("clocks") or {}).get("sm_mhz")
+            for name, ent in entries.items():
+                iss = _issue_roofline(name, ent["layout"], ent["ms_per_step"], mhz)
+                if iss:
+                    ent["issue"] = iss
             line["configs"] = entries
     if line is not None:
         if grp.world == 1 and not args.no_cpu_baseline:

@@ -16,7 +16,7 @@ HEADER = os.path.join(_ROOT, "include", "smol_preproc.h")
 _CSRC = os.path.join(_PKG, "csrc")
 # translation units (compiled in parallel, then linked) and the headers they include
 UNITS = ["smol_preproc.cu", "smol_inst_k1.cu", "smol_inst_k2.cu", "smol_inst_k4.cu", "smol_inst_k8.cu"]
-HEADERS = ["smol_kernels.cuh", "smol_geom.cuh", "smol_compact.cuh", "smol_thumb.cuh", "smol_launch.h"]
+HEADERS = ["smol_kernels.cuh", "smol_geom.cuh", "smol_compact.cuh", "smol_thumb.cuh", "smol_jpeg.cuh", "smol_launch.h"]
 SOURCES = [os.path.join(_CSRC, f) for f in UNITS + HEADERS]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-Xfatbin", "-compress-all"]

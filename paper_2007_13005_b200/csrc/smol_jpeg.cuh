@@ -14,10 +14,12 @@
 //      (dense-64 or packed-for-scale), which the fused kernel then reads as on
 //      the compact path.  Segments with no block inside the ROI are skipped:
 //      an interval is independently decodable.
-// Decoding per symbol: a 9-bit lookup (length, symbol) for short codes, the
-// T.81 F.16 MAXCODE walk for longer ones; bit buffer of 64 bits refilled a
-// byte at a time with 0xFF00 unstuffing (B.1.1.5); at a marker the reader
-// feeds zero bits (well-formed data never needs them).
+// Decoding: one flat loop, one symbol per iteration (DC or AC, any block), so
+// a warp's lanes stay on one code path; a 9-bit lookup (length, symbol) for
+// short codes, the T.81 F.16 MAXCODE walk for longer ones; a 64-bit bit
+// buffer refilled 4 raw bytes at a time when they hold no 0xFF, else byte by
+// byte with 0xFF00 unstuffing (B.1.1.5); at a marker the reader feeds zero
+// bits (well-formed data never needs them).
 #pragma once
 #include <stdint.h>
 
@@ -27,10 +29,12 @@ namespace smol {
 
 constexpr int kHuffLutBits = 9;
 
-// One Huffman table in the decoder's format (built on the host from a DHT).
-struct HuffTable {
+// One Huffman table in the decoder's format (built on the host from a DHT);
+// 16-B aligned so the LUT can be copied to shared memory with 16-B loads.
+struct alignas(16) HuffTable {
   uint16_t lut[1 << kHuffLutBits];   // code prefix -> length << 8 | symbol (length 0: longer code)
-  int32_t maxcode[18];               // per length l: largest code of length l (-1: none); [17] sentinel
+  uint32_t limit[17];                // per length l: codes of length <= l, left-justified to 16 bits, lie
+                                     // below limit[l] (canonical codes, T.81 C.2); no code: window >= limit[16]
   int32_t valoff[17];                // per length l: index of HUFFVAL for code c = c + valoff[l]
   uint8_t huffval[256];
 };
@@ -57,13 +61,32 @@ struct JpegDesc {
 constexpr int kJpegThreads = 128;
 constexpr int kJpegBlkStride = 68;   // int16 per thread block buffer (136 B: spreads the lanes' banks)
 
+// Does restart interval s of image d hold a block inside the ROI box?
+__device__ __forceinline__ bool seg_in_roi(const JpegDesc& d, int s) {
+  const int m0 = s * d.ri, m1 = min(d.nmcu, m0 + d.ri) - 1;
+  if (m1 < m0) return false;
+  const int my0 = m0 / d.mcus_x, my1 = m1 / d.mcus_x;
+  const int mxa = my0 == my1 ? m0 - my0 * d.mcus_x : 0;
+  const int mxb = my0 == my1 ? m1 - my1 * d.mcus_x : d.mcus_x - 1;
+  bool any = false;
+  for (int c = 0; c < d.ncomp; ++c) {
+    const int H = d.ncomp == 1 ? 1 : d.h[c], V = d.ncomp == 1 ? 1 : d.v[c];
+    const int r0 = my0 * V, r1 = my1 * V + V - 1, c0 = mxa * H, c1 = mxb * H + H - 1;
+    any |= r0 <= d.by0[c] + d.nby[c] - 1 && r1 >= d.by0[c] && c0 <= d.bx0[c] + d.nbx[c] - 1 && c1 >= d.bx0[c];
+  }
+  return any;
+}
+
 // warp per image: segment s > 0 starts after the s-th RST marker.  The
 // warp reads 512 B per step (16-byte loads, files 16-B aligned), four steps
 // in flight; a marker's second byte may sit in the next lane's (or step's)
 // first byte.
 constexpr int kIndexUnroll = 4;
+// Also appends the image's intervals that hold ROI blocks to the batch's
+// active list (the decode kernel's work: no lane idles on a skipped interval).
 __global__ void __launch_bounds__(128) smol_jpeg_index_kernel(const JpegDesc* ds, int n_images,
-                                                              int32_t* seg_start, int32_t* seg_img) {
+                                                              int32_t* seg_start, int32_t* seg_img,
+                                                              int32_t* active, int32_t* n_active) {
   const int lane = threadIdx.x & 31;
   const int img = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (img >= n_images) return;
@@ -71,9 +94,19 @@ __global__ void __launch_bounds__(128) smol_jpeg_index_kernel(const JpegDesc* ds
   const uint8_t* p = d.data;
   const int end = d.size, s0 = d.scan_off;
   const int base = d.seg_base, nseg = d.nseg;
-  for (int s = lane; s < nseg; s += 32) {         // defaults: segment 0 at the scan start,
-    seg_img[base + s] = img;                      // missing markers -> empty segments
-    seg_start[base + s] = s == 0 ? s0 : end;
+  for (int s0w = 0; s0w < nseg; s0w += 32) {      // defaults: segment 0 at the scan start,
+    const int s = s0w + lane;                     // missing markers -> empty segments
+    bool act = false;
+    if (s < nseg) {
+      seg_img[base + s] = img;
+      seg_start[base + s] = s == 0 ? s0 : end;
+      act = seg_in_roi(d, s);
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, act);
+    int at = 0;
+    if (lane == 0 && bal) at = atomicAdd(n_active, __popc(bal));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (act) active[at + __popc(bal & ((1u << lane) - 1))] = base + s;
   }
   __syncwarp();
   if (nseg <= 1) return;
@@ -135,25 +168,44 @@ struct BitReader {
   int nb;                    // valid bits in buf
   bool stop;                 // met a marker / the end: feed zeros
 
-  __device__ __forceinline__ void refill() {
-    while (nb <= 56) {
-      uint32_t b = 0;
-      if (!stop) {
-        if (p < pend) {
-          b = __ldg(p);
-          ++p;
-          if (b == 0xFFu) {
-            const uint32_t b2 = p < pend ? __ldg(p) : 0xD9u;
-            if (b2 == 0u) ++p;                    // stuffed 0xFF00 (B.1.1.5)
-            else { stop = true; b = 0; }          // a marker ends the interval
-          }
-        } else {
-          stop = true;
+  // one raw byte with 0xFF00 unstuffing (B.1.1.5); a marker or the end stops
+  __device__ __forceinline__ void put_byte() {
+    uint32_t b = 0;
+    if (!stop) {
+      if (p < pend) {
+        b = __ldg(p);
+        ++p;
+        if (b == 0xFFu) {
+          const uint32_t b2 = p < pend ? __ldg(p) : 0xD9u;
+          if (b2 == 0u) ++p;                      // stuffed 0xFF00
+          else { stop = true; b = 0; }            // a marker ends the interval
         }
+      } else {
+        stop = true;
       }
-      buf |= (uint64_t)b << (56 - nb);
-      nb += 8;
     }
+    buf |= (uint64_t)b << (56 - nb);
+    nb += 8;
+  }
+  // >= 33 valid bits afterwards (one code of <= 16 bits + <= 16 extra bits).
+  // Fast path: the next 4 raw bytes (two aligned 32-bit loads, funnel-shifted)
+  // hold no 0xFF: append them at once; else byte by byte.
+  __device__ __forceinline__ void refill() {
+    if (nb > 32) return;
+    if (!stop && p + 4 <= pend) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+      const uint32_t lo = __ldg(w), hi = __ldg(w + 1);
+      const uint32_t x = __funnelshift_r(lo, hi, 8 * (uint32_t)(a & 3));   // bytes p..p+3, p in the low byte
+      const uint32_t nx = ~x;
+      if (((nx - 0x01010101u) & ~nx & 0x80808080u) == 0u) {    // no 0xFF byte
+        buf |= (uint64_t)__byte_perm(x, 0u, 0x0123) << (32 - nb);
+        nb += 32;
+        p += 4;
+        return;
+      }
+    }
+    while (nb <= 56) put_byte();
   }
   __device__ __forceinline__ uint32_t peek16() const { return (uint32_t)(buf >> 48); }
   __device__ __forceinline__ void skip(int n) { buf <<= n; nb -= n; }
@@ -166,108 +218,159 @@ struct BitReader {
   }
 };
 
-// T.81 F.16 DECODE (needs >= 16 valid bits)
-__device__ __forceinline__ int huff_decode(BitReader& br, const HuffTable* t) {
+// T.81 F.16 DECODE (needs >= 16 valid bits).  Codes of <= 9 bits: one LUT
+// read; longer codes: the length is the number of left-justified limits the
+// 16-bit window reaches (branch-free, the same instructions for every lane).
+__device__ __forceinline__ int huff_decode(BitReader& br, const HuffTable* t, const uint16_t* slut = nullptr) {
   const uint32_t look = br.peek16();
-  const uint32_t e = __ldg(&t->lut[look >> (16 - kHuffLutBits)]);
+  const uint32_t e = slut ? slut[look >> (16 - kHuffLutBits)] : __ldg(&t->lut[look >> (16 - kHuffLutBits)]);
   if (e >> 8) {
     br.skip((int)(e >> 8));
     return (int)(e & 255u);
   }
   int l = kHuffLutBits + 1;
-  while (l <= 16 && (int32_t)(look >> (16 - l)) > __ldg(&t->maxcode[l])) ++l;
-  if (l > 16) { br.skip(16); return 0; }        // invalid code: read as EOB / zero
+#pragma unroll
+  for (int i = kHuffLutBits + 1; i < 16; ++i) l += look >= __ldg(&t->limit[i]) ? 1 : 0;
+  if (look >= __ldg(&t->limit[16])) { br.skip(16); return 0; }   // invalid code: read as EOB / zero
   br.skip(l);
   return (int)__ldg(&t->huffval[((int32_t)(look >> (16 - l)) + __ldg(&t->valoff[l])) & 255]);
 }
 
-// thread per restart interval
+// Thread per restart interval.  The decode is one flat loop, one symbol per
+// iteration whatever the lane's state (DC or AC, any block), so the lanes of
+// a warp stay converged on the same code path.  Blocks that end in an
+// iteration are stored by the whole warp together (one coalesced 4-byte store
+// per lane per block), then the lanes move on to their next block.
+// one_set: every image of the batch uses table set `set0`, whose 9-bit LUTs
+// of tables 0 and 1 are then read from shared memory.
 __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const JpegDesc* ds, int nseg_total,
                                                                         const int32_t* seg_start,
                                                                         const int32_t* seg_img,
-                                                                        const int8_t* dst_index) {
+                                                                        const int32_t* active,
+                                                                        const int32_t* n_active,
+                                                                        const int8_t* dst_index,
+                                                                        const HuffSet* set0, int one_set) {
   __shared__ __align__(16) int16_t blkbuf[kJpegThreads * kJpegBlkStride];
+  __shared__ __align__(16) uint16_t slut[4][1 << kHuffLutBits];   // DC0, DC1, AC0, AC1 of set0
   __shared__ uint8_t zmap[64];                    // zig-zag position -> stored element (255: dropped)
   if (threadIdx.x < 64) zmap[threadIdx.x] = (uint8_t)dst_index[threadIdx.x];
+  if (one_set) {
+    for (int i = threadIdx.x; i < 4 * (1 << kHuffLutBits) / 8; i += kJpegThreads) {
+      const int t = i / ((1 << kHuffLutBits) / 8), w = i % ((1 << kHuffLutBits) / 8);
+      const HuffTable& T = t == 0 ? set0->dc[0] : t == 1 ? set0->dc[1] : t == 2 ? set0->ac[0] : set0->ac[1];
+      reinterpret_cast<uint4*>(slut[t])[w] = __ldg(reinterpret_cast<const uint4*>(T.lut) + w);
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  int16_t* const wbuf = blkbuf + (threadIdx.x & ~31) * kJpegBlkStride;   // the warp's 32 block buffers
   int16_t* blk = blkbuf + threadIdx.x * kJpegBlkStride;
 #pragma unroll
   for (int i = 0; i < 16; ++i) reinterpret_cast<uint2*>(blk)[i] = make_uint2(0u, 0u);   // (8-B aligned buffers)
   __syncthreads();
-  const int g = blockIdx.x * kJpegThreads + threadIdx.x;
-  if (g >= nseg_total) return;
+  const int gi = blockIdx.x * kJpegThreads + threadIdx.x;
+  if (__all_sync(0xffffffffu, gi >= min(nseg_total, __ldg(n_active)))) return;   // (warp-uniform exit)
+  bool alive = gi < min(nseg_total, __ldg(n_active));
+  const int g = alive ? __ldg(active + gi) : __ldg(active);      // an interval holding ROI blocks
   const JpegDesc& d = ds[seg_img[g]];
   const int s = g - d.seg_base;
   const int m0 = s * d.ri, m1 = min(d.nmcu, m0 + d.ri) - 1;
   const int nc = d.ncomp;
-  // skip an interval none of whose blocks is inside the ROI box
-  {
-    const int my0 = m0 / d.mcus_x, my1 = m1 / d.mcus_x;
-    const int mxa = my0 == my1 ? m0 - my0 * d.mcus_x : 0;
-    const int mxb = my0 == my1 ? m1 - my1 * d.mcus_x : d.mcus_x - 1;
-    bool any = false;
-    for (int c = 0; c < nc; ++c) {
-      const int H = nc == 1 ? 1 : d.h[c], V = nc == 1 ? 1 : d.v[c];
-      const int r0 = my0 * V, r1 = my1 * V + V - 1, c0 = mxa * H, c1 = mxb * H + H - 1;
-      any |= r0 <= d.by0[c] + d.nby[c] - 1 && r1 >= d.by0[c] && c0 <= d.bx0[c] + d.nbx[c] - 1 && c1 >= d.bx0[c];
-    }
-    if (!any || m1 < m0) return;
-  }
   BitReader br;
   br.p = d.data + seg_start[g];
   br.pend = d.data + d.size;
   br.buf = 0;
   br.nb = 0;
   br.stop = false;
-  const int E = d.E;
+  const int E = d.E;                              // (uniform over a batch)
+  // block cursor: MCU (my, mx), component c, block (y, x) inside the MCU
+  int my = m0 / d.mcus_x, mx = m0 - my * d.mcus_x, m = m0;
+  int c = 0, y = 0, x = 0;
+  int H = nc == 1 ? 1 : d.h[0], V = nc == 1 ? 1 : d.v[0];
+  const HuffTable* tdc = &d.tabs->dc[d.td[0]];
+  const HuffTable* tac = &d.tabs->ac[d.ta[0]];
+  // shared-memory LUT rows of the current component's tables (-1: global)
+  int sdc = one_set && d.td[0] < 2 ? d.td[0] : -1, sac = one_set && d.ta[0] < 2 ? 2 + d.ta[0] : -1;
   int32_t pred0 = 0, pred1 = 0, pred2 = 0;        // DC predictors (reset per interval, F.2.1.3.1)
-  for (int m = m0; m <= m1; ++m) {
-    const int my = m / d.mcus_x, mx = m - my * d.mcus_x;
-    for (int c = 0; c < nc; ++c) {
-      const int H = nc == 1 ? 1 : d.h[c], V = nc == 1 ? 1 : d.v[c];
-      const HuffTable* tdc = &d.tabs->dc[d.td[c]];
-      const HuffTable* tac = &d.tabs->ac[d.ta[c]];
-      for (int y = 0; y < V; ++y)
-        for (int x = 0; x < H; ++x) {
-          // DC (F.2.2.1)
-          br.refill();
-          const int t = huff_decode(br, tdc);
-          const int32_t diff = br.receive_extend(t & 15);
-          int32_t& pred = c == 0 ? pred0 : c == 1 ? pred1 : pred2;
-          pred += diff;
-          const int by = my * V + y - d.by0[c], bx = mx * H + x - d.bx0[c];
-          const bool keep = by >= 0 && by < d.nby[c] && bx >= 0 && bx < d.nbx[c];
-          blk[0] = (int16_t)pred;                 // zig-zag 0 is stored element 0 in every layout
-          // AC (F.2.2.2, Figure F.13)
-          for (int k = 1; k < 64;) {
-            br.refill();
-            const int rs = huff_decode(br, tac);
-            const int ssss = rs & 15, r = rs >> 4;
-            if (ssss == 0) {
-              if (r != 15) break;                 // EOB
-              k += 16;                            // ZRL
-              continue;
-            }
-            k += r;
-            if (k > 63) break;                    // corrupt run: stop the block
-            const int32_t v = br.receive_extend(ssss);
-            const int e = zmap[k];
-            if (e != 255) blk[e] = (int16_t)v;
-            ++k;
-          }
-          if (keep) {
-            int16_t* out = (c == 0 ? d.dst[0] : c == 1 ? d.dst[1] : d.dst[2]) +
-                           (int64_t)by * (c == 0 ? d.dst_stride[0] : c == 1 ? d.dst_stride[1] : d.dst_stride[2]) +
-                           (int64_t)bx * E;
-            if (E == 1) {
-              *out = blk[0];
-            } else {
-              // E*2 bytes (a multiple of 8): 8-byte words
-              for (int w = 0; w < E / 4; ++w)
-                reinterpret_cast<uint2*>(out)[w] = reinterpret_cast<const uint2*>(blk)[w];
-            }
-          }
-          for (int w = 0; w < (E + 3) / 4; ++w) reinterpret_cast<uint2*>(blk)[w] = make_uint2(0u, 0u);
+  int k = 0;                                      // zig-zag position of the next coefficient
+  while (__any_sync(0xffffffffu, alive)) {
+    bool fin = false;
+    if (alive) {
+      br.refill();
+      // one symbol: the DC category (k == 0, F.2.2.1) or an AC run/size (F.13)
+      const int sl = k == 0 ? sdc : sac;
+      const int sym = huff_decode(br, k == 0 ? tdc : tac, sl >= 0 ? slut[sl] : nullptr);
+      const int ssss = sym & 15, r = k == 0 ? 0 : sym >> 4;
+      if (ssss == 0 && k > 0) {
+        k = r == 15 ? k + 16 : 64;                // ZRL / EOB
+      } else {
+        k += r;
+        int32_t v = br.receive_extend(ssss);
+        if (k == 0) {
+          const int32_t pv = c == 0 ? pred0 : c == 1 ? pred1 : pred2;
+          v += pv;
+          if (c == 0) pred0 = v; else if (c == 1) pred1 = v; else pred2 = v;
         }
+        if (k < 64) {
+          const int e = zmap[k];
+          if (e != 255) blk[e] = (int16_t)v;
+        }
+        ++k;
+      }
+      fin = k >= 64;
+    }
+    // ---- blocks that ended: destination (if inside the ROI box) ----------
+    int16_t* out = nullptr;
+    if (fin) {
+      const int by = my * V + y - (c == 0 ? d.by0[0] : c == 1 ? d.by0[1] : d.by0[2]);
+      const int bx = mx * H + x - (c == 0 ? d.bx0[0] : c == 1 ? d.bx0[1] : d.bx0[2]);
+      const int nby = c == 0 ? d.nby[0] : c == 1 ? d.nby[1] : d.nby[2];
+      const int nbx = c == 0 ? d.nbx[0] : c == 1 ? d.nbx[1] : d.nbx[2];
+      if (by >= 0 && by < nby && bx >= 0 && bx < nbx)
+        out = (c == 0 ? d.dst[0] : c == 1 ? d.dst[1] : d.dst[2]) +
+              (int64_t)by * (c == 0 ? d.dst_stride[0] : c == 1 ? d.dst_stride[1] : d.dst_stride[2]) +
+              (int64_t)bx * E;
+    }
+    // ---- the warp stores them together and clears their buffers ----------
+    uint32_t fm = __ballot_sync(0xffffffffu, fin);
+    __syncwarp();                                 // lanes' coefficient writes visible to the warp
+    while (fm) {
+      const int j = __ffs(fm) - 1;
+      fm &= fm - 1;
+      const unsigned long long oj = __shfl_sync(0xffffffffu, (unsigned long long)out, j);
+      int16_t* bj = wbuf + j * kJpegBlkStride;
+      if (E == 1) {
+        if (lane == 0) {
+          if (oj) *reinterpret_cast<int16_t*>(oj) = bj[0];
+          bj[0] = 0;
+        }
+      } else if (lane < E / 2) {                  // E even: E/2 4-byte words
+        uint32_t* b32 = reinterpret_cast<uint32_t*>(bj);
+        if (oj) reinterpret_cast<uint32_t*>(oj)[lane] = b32[lane];
+        b32[lane] = 0u;
+      }
+    }
+    __syncwarp();
+    if (!fin) continue;
+    // ---- next block of this lane's interval ------------------------------
+    k = 0;
+    if (++x == H) {
+      x = 0;
+      if (++y == V) {
+        y = 0;
+        if (++c == nc) {
+          c = 0;
+          if (++m > m1) { alive = false; continue; }
+          if (++mx == d.mcus_x) { mx = 0; ++my; }
+        }
+        H = nc == 1 ? 1 : (c == 0 ? d.h[0] : 1);
+        V = nc == 1 ? 1 : (c == 0 ? d.v[0] : 1);
+        const int td = c == 0 ? d.td[0] : c == 1 ? d.td[1] : d.td[2];
+        const int ta = c == 0 ? d.ta[0] : c == 1 ? d.ta[1] : d.ta[2];
+        tdc = &d.tabs->dc[td];
+        tac = &d.tabs->ac[ta];
+        sdc = one_set && td < 2 ? td : -1;
+        sac = one_set && ta < 2 ? 2 + ta : -1;
+      }
     }
   }
 }

@@ -889,8 +889,11 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
           }
         };
         int cur = -1;                     // ring byte offset of the current top row
+        // output pointer walks down the run (one 64-bit add per row instead of
+        // re-deriving the task's column per row)
+        OutT* ot = outb + (uint32_t)(ra * kp.OW + ox);
 #pragma unroll 1
-        for (int r = ra; r < rb; ++r) {
+        for (int r = ra; r < rb; ++r, ot += kp.OW) {
           const int2 ty = yt[r];
           const int ro = ty.x & 0xffff;
           if (ro != cur) {
@@ -914,7 +917,6 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
               y[ch][2 * e] = yn.x;
               y[ch][2 * e + 1] = yn.y;
             }
-          OutT* const ot = outb + (uint32_t)(r * kp.OW + ox);
           if (vst) {
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {

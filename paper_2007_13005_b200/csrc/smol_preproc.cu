@@ -219,19 +219,20 @@ void build_huff(const uint8_t* bits, const uint8_t* vals, HuffTable& t) {
   int code = 0, j = 0;
   for (int l = 1; l <= 16; ++l) {
     const int n = bits[l - 1];
-    if (n == 0) { t.maxcode[l] = -1; t.valoff[l] = 0; }
-    else {
-      t.valoff[l] = j - code;                   // HUFFVAL index = code + valoff (F.15: VALPTR - MINCODE)
-      for (int i = 0; i < n; ++i, ++code, ++j)
-        if (l <= kHuffLutBits)
-          for (int f = code << (kHuffLutBits - l); f < (code + 1) << (kHuffLutBits - l); ++f)
-            t.lut[f] = (uint16_t)(l << 8 | vals[j]);
-      t.maxcode[l] = code - 1;
-    }
+    t.valoff[l] = j - code;                     // HUFFVAL index = code + valoff (F.15: VALPTR - MINCODE)
+    for (int i = 0; i < n; ++i, ++code, ++j)
+      if (l <= kHuffLutBits)
+        for (int f = code << (kHuffLutBits - l); f < (code + 1) << (kHuffLutBits - l); ++f)
+          t.lut[f] = (uint16_t)(l << 8 | vals[j]);
+    t.limit[l] = (uint32_t)code << (16 - l);    // first code of length > l, left-justified
     code <<= 1;
   }
-  t.maxcode[17] = INT_MAX;
   memcpy(t.huffval, vals, 256);
+}
+
+// Decoder tables of an absent (never referenced) table: every window invalid.
+void empty_huff(HuffTable& t) {
+  memset(&t, 0, sizeof(t));
 }
 
 // Header of one file; on error a status + message naming image idx.
@@ -773,10 +774,10 @@ int32_t smol_preproc_plan(const smol_preproc_params* params, int32_t max_images,
       }
     }
     // run_jpeg segment index: at most one restart interval per MCU (8x8 px
-    // worst case), 2 int32 each
-    const size_t seg_img = (size_t)8 * ceil_div(params->max_width, 8) * ceil_div(params->max_height, 8);
+    // worst case), 3 int32 each (start, image, active list) + the counter
+    const size_t seg_img = (size_t)12 * ceil_div(params->max_width, 8) * ceil_div(params->max_height, 8);
     for (int i = 0; i < pl->n_stage && e == cudaSuccess; ++i) {
-      pl->seg_cap[i] = seg_img * (size_t)max_images;
+      pl->seg_cap[i] = seg_img * (size_t)max_images + 16;
       e = cudaMalloc(&pl->d_seg[i], pl->seg_cap[i] + 256);
     }
     pl->fixed_stage = true;
@@ -1075,10 +1076,11 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   for (int i = 0; i < nk && !c2s; ++i) c2s = h[i].ck != K;
   KernelFn fn = select_kernel(K, pl->p.out_dtype == SMOL_OUT_F16_NCHW, dbg != nullptr, packed, nt,
                               pl->p.idct_def == SMOL_IDCT_TRUNCATED, gc, c2s);
-  int occ = 768 / nt;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, smem) != cudaSuccess || occ < 1) {
+  const int cta_threads = nt;
+  int occ = 768 / cta_threads;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, cta_threads, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
-    occ = 768 / nt;
+    occ = 768 / cta_threads;
   }
   if (auto_rows && n_col_tiles == 1) {
     const int tr = auto_tile_rows(pl->OH, n_images, pl->num_sms * occ);
@@ -1363,7 +1365,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
           for (int id = 0; id < 4; ++id) {
             HuffTable& T = cl ? hh[t].ac[id] : hh[t].dc[id];
             if (H.ht_ok[cl][id]) build_huff(H.bits[cl][id], H.vals[cl][id], T);
-            else { memset(&T, 0, sizeof(T)); for (int l = 0; l < 18; ++l) T.maxcode[l] = -1; }
+            else empty_huff(T);
           }
       }
       for (size_t t = 0; t < pl->jqt.size(); ++t) memcpy(hq + 64 * t, pl->jqt[t].data(), 128);
@@ -1398,7 +1400,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       }
       if (nseg_total >= INT_MAX / 2) return fail(SMOL_ERR_CAPACITY, "%lld restart intervals in one batch", (long long)nseg_total);
       void* segb = pl->d_seg[sl];
-      rc = grow(&segb, &pl->seg_cap[sl], (size_t)nseg_total * 8, pl->copy_stream, pl->fixed_stage, "segment index");
+      rc = grow(&segb, &pl->seg_cap[sl], (size_t)nseg_total * 12 + 16, pl->copy_stream, pl->fixed_stage, "segment index");
       pl->d_seg[sl] = static_cast<int32_t*>(segb);
       if (rc) return rc;
       pl->jnseg = (int)nseg_total;
@@ -1423,11 +1425,16 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       JpegDesc* dj = pl->d_jdesc + (size_t)sl_ * pl->max_images;
       int32_t* seg_start = pl->d_seg[sl_];
       int32_t* seg_img = seg_start + pl->jnseg;
+      int32_t* active = seg_img + pl->jnseg;
+      int32_t* n_active = active + pl->jnseg;
       SMOL_CUDA(cudaStreamWaitEvent(es, pl->stage_ready[sl_], 0));
-      smol_jpeg_index_kernel<<<ceil_div(n_images, 4), 128, 0, es>>>(dj, n_images, seg_start, seg_img);
+      SMOL_CUDA(cudaMemsetAsync(n_active, 0, sizeof(int32_t), es));
+      smol_jpeg_index_kernel<<<ceil_div(n_images, 4), 128, 0, es>>>(dj, n_images, seg_start, seg_img, active,
+                                                                    n_active);
       SMOL_CUDA(cudaGetLastError());
-      smol_jpeg_decode_kernel<<<ceil_div(pl->jnseg, kJpegThreads), kJpegThreads, 0, es>>>(dj, pl->jnseg, seg_start,
-                                                                                          seg_img, pl->d_zmap);
+      smol_jpeg_decode_kernel<<<ceil_div(pl->jnseg, kJpegThreads), kJpegThreads, 0, es>>>(
+          dj, pl->jnseg, seg_start, seg_img, active, n_active, pl->d_zmap,
+          pl->d_huff + (size_t)sl_ * kMaxHuffSets, pl->jset_hdr.size() == 1 ? 1 : 0);
       SMOL_CUDA(cudaGetLastError());
       if (es != stream) {
         SMOL_CUDA(cudaEventRecord(pl->stage_expanded[sl_], es));
@@ -1508,7 +1515,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   const long long nblk = map_n ? (long long)map_n : (long long)ntiles * n_col_tiles * n_images;
   if (nblk >= INT_MAX) return fail(SMOL_ERR_CAPACITY, "%lld CTAs exceed the grid limit", nblk);
   dim3 grid((unsigned)nblk, 1);
-  fn<<<grid, nt, smem, stream>>>(kp);
+  fn<<<grid, cta_threads, smem, stream>>>(kp);
   SMOL_CUDA(cudaGetLastError());
   SMOL_CUDA(cudaEventRecord(pl->ev[slot], stream));
   if (sl_used >= 0) SMOL_CUDA(cudaEventRecord(pl->stage_free[sl_used], stream));
@@ -1788,10 +1795,10 @@ int32_t smol_jpeg_decode_planes(const smol_jpeg_batch* b, int16_t* const* planes
     if (dseg) cudaFree(dseg);
     if (dz) cudaFree(dz);
   };
-  cudaError_t e = cudaMalloc(&dd, (size_t)(hi - lo));
+  cudaError_t e = cudaMalloc(&dd, (size_t)(hi - lo) + 16);     // (the bit reader's 4-byte loads may read 7 B ahead)
   if (e == cudaSuccess) e = cudaMalloc(&dj, sizeof(JpegDesc) * n);
   if (e == cudaSuccess) e = cudaMalloc(&dh, sizeof(HuffSet) * n);
-  if (e == cudaSuccess) e = cudaMalloc(&dseg, 8 * (size_t)nseg);
+  if (e == cudaSuccess) e = cudaMalloc(&dseg, 12 * (size_t)nseg + 16);
   if (e == cudaSuccess) e = cudaMalloc(&dz, 64);
   nseg = 0;
   for (int i = 0; i < n && e == cudaSuccess; ++i) {
@@ -1800,7 +1807,7 @@ int32_t smol_jpeg_decode_planes(const smol_jpeg_batch* b, int16_t* const* planes
       for (int id = 0; id < 4; ++id) {
         HuffTable& T = cl ? sets[i].ac[id] : sets[i].dc[id];
         if (H.ht_ok[cl][id]) build_huff(H.bits[cl][id], H.vals[cl][id], T);
-        else { memset(&T, 0, sizeof(T)); for (int l = 0; l < 18; ++l) T.maxcode[l] = -1; }
+        else empty_huff(T);
       }
     JpegDesc& J = js[i];
     memset(&J, 0, sizeof(J));
@@ -1831,10 +1838,12 @@ int32_t smol_jpeg_decode_planes(const smol_jpeg_batch* b, int16_t* const* planes
   if (e == cudaSuccess) e = cudaMemcpyAsync(dj, js.data(), sizeof(JpegDesc) * n, cudaMemcpyHostToDevice, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dh, sets.data(), sizeof(HuffSet) * n, cudaMemcpyHostToDevice, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dz, zm, 64, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dseg + 3 * nseg, 0, sizeof(int32_t), stream);
   if (e == cudaSuccess) {
-    smol_jpeg_index_kernel<<<ceil_div(n, 4), 128, 0, stream>>>(dj, n, dseg, dseg + nseg);
+    smol_jpeg_index_kernel<<<ceil_div(n, 4), 128, 0, stream>>>(dj, n, dseg, dseg + nseg, dseg + 2 * nseg,
+                                                               dseg + 3 * nseg);
     smol_jpeg_decode_kernel<<<(int)((nseg + kJpegThreads - 1) / kJpegThreads), kJpegThreads, 0, stream>>>(
-        dj, (int)nseg, dseg, dseg + nseg, dz);
+        dj, (int)nseg, dseg, dseg + nseg, dseg + 2 * nseg, dseg + 3 * nseg, dz, dh, 0);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);

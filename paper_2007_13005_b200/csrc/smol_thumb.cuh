@@ -140,8 +140,9 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
         }
       };
       int c0 = -1, c1 = -1;                       // source rows of T and B
+      OutT* o = outn + (uint32_t)ra * OW + ox;    // walks down the run
 #pragma unroll 1
-      for (int oy = ra; oy < rb; ++oy) {
+      for (int oy = ra; oy < rb; ++oy, o += OW) {
         const int2 ty = S.yt[oy];
         const int i0 = ty.x & 0xffff, i1 = ty.x >> 16;
         if (i0 != c0 || i1 != c1) {
@@ -165,7 +166,6 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
             v[c][2 * e] = yn.x;
             v[c][2 * e + 1] = yn.y;
           }
-        OutT* const o = outn + (uint32_t)oy * OW + ox;
         if ((OW & 3) == 0 && kp.out_vec) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
