@@ -55,7 +55,7 @@ L2_BYTES = 126 * 2 ** 20
 LAYOUT = {"c1": "dense", "c2": "dense", "c3a": "packed", "c3b": "packed", "c4": "packed", "c5": "packed"}
 # distinct synthetic images per config (replicated into distinct buffers)
 N_DISTINCT = {"c5": 16}
-JPEG_RESTART_INTERVAL = 4          # MCUs per restart interval of the e2e JPEG files
+JPEG_RESTART_INTERVAL = 1          # MCUs per restart interval of the e2e JPEG files (the parallelism of the GPU decode)
 # PAPER.md context numbers (another machine's: AWS g4dn.xlarge, one T4 + 4 vCPUs)
 PAPER_CONTEXT = {
     "hardware": "AWS g4dn.xlarge: NVIDIA T4 GPU + 4 vCPU cores (PAPER.md P:384-392)",

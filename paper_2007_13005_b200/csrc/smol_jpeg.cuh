@@ -77,42 +77,16 @@ __device__ __forceinline__ bool seg_in_roi(const JpegDesc& d, int s) {
   return any;
 }
 
-// warp per image: segment s > 0 starts after the s-th RST marker.  The
-// warp reads 512 B per step (16-byte loads, files 16-B aligned), four steps
-// in flight; a marker's second byte may sit in the next lane's (or step's)
-// first byte.
-constexpr int kIndexUnroll = 4;
-// Also appends the image's intervals that hold ROI blocks to the batch's
-// active list (the decode kernel's work: no lane idles on a skipped interval).
-__global__ void __launch_bounds__(128) smol_jpeg_index_kernel(const JpegDesc* ds, int n_images,
-                                                              int32_t* seg_start, int32_t* seg_img,
-                                                              int32_t* active, int32_t* n_active) {
-  const int lane = threadIdx.x & 31;
-  const int img = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (img >= n_images) return;
-  const JpegDesc& d = ds[img];
-  const uint8_t* p = d.data;
-  const int end = d.size, s0 = d.scan_off;
-  const int base = d.seg_base, nseg = d.nseg;
-  for (int s0w = 0; s0w < nseg; s0w += 32) {      // defaults: segment 0 at the scan start,
-    const int s = s0w + lane;                     // missing markers -> empty segments
-    bool act = false;
-    if (s < nseg) {
-      seg_img[base + s] = img;
-      seg_start[base + s] = s == 0 ? s0 : end;
-      act = seg_in_roi(d, s);
-    }
-    const uint32_t bal = __ballot_sync(0xffffffffu, act);
-    int at = 0;
-    if (lane == 0 && bal) at = atomicAdd(n_active, __popc(bal));
-    at = __shfl_sync(0xffffffffu, at, 0);
-    if (act) active[at + __popc(bal & ((1u << lane) - 1))] = base + s;
-  }
-  __syncwarp();
-  if (nseg <= 1) return;
+// RST markers (0xFF then 0xD0..0xD7) at positions [clo, chi) of one file,
+// by one warp: 512 B per step (16-byte loads; files are 16-B aligned), four
+// steps in flight; a marker's second byte may sit in the next lane's (or
+// step's) first byte.  Counts them; with `write`, the idx-th marker of the
+// scan (idx from `first`) starts segment idx: seg_start[idx] = position + 2.
+constexpr int kIndexUnroll = 4, kIndexWarps = 8;
+__device__ __forceinline__ int scan_markers(const uint8_t* p, int clo, int chi, int s0, int end, int lane,
+                                            bool write, int first, int nseg, int32_t* seg_start) {
   int found = 0;                                  // markers seen so far (whole warp)
-  const int a0 = s0 & ~15;
-  for (int o = a0; o < end && found < nseg - 1; o += 512 * kIndexUnroll) {
+  for (int o = clo; o < chi; o += 512 * kIndexUnroll) {
     uint4 w[kIndexUnroll];
 #pragma unroll
     for (int u = 0; u < kIndexUnroll; ++u) {
@@ -133,14 +107,14 @@ __global__ void __launch_bounds__(128) smol_jpeg_index_kernel(const JpegDesc* ds
       const uint32_t nstep =
           u + 1 < kIndexUnroll ? (__shfl_sync(0xffffffffu, w[(u + 1) % kIndexUnroll].x, 0) & 0xFFu) : 0u;
       if (lane == 31) nxt = u + 1 < kIndexUnroll ? nstep : (q + 16 < end ? (uint32_t)__ldg(p + q + 16) : 0u);
-      // bit j: 0xFF at byte j and 0xD0..0xD7 at byte j + 1, at or after the scan start
+      // bit j: 0xFF at byte j and 0xD0..0xD7 at byte j + 1, inside [max(clo, s0), chi)
       const uint32_t wd[5] = {w[u].x, w[u].y, w[u].z, w[u].w, nxt};
       uint32_t hits = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const uint32_t b0 = (wd[j >> 2] >> (8 * (j & 3))) & 0xFFu;
         const uint32_t b1 = j == 15 ? nxt : (wd[(j + 1) >> 2] >> (8 * ((j + 1) & 3))) & 0xFFu;
-        if (b0 == 0xFFu && (b1 & 0xF8u) == 0xD0u && q + j >= s0 && q + j + 1 < end) hits |= 1u << j;
+        if (b0 == 0xFFu && (b1 & 0xF8u) == 0xD0u && q + j >= s0 && q + j < chi && q + j + 1 < end) hits |= 1u << j;
       }
       const int cnt = __popc(hits);
       int inc = cnt;                              // inclusive warp scan of the counts
@@ -149,16 +123,64 @@ __global__ void __launch_bounds__(128) smol_jpeg_index_kernel(const JpegDesc* ds
         const int t = __shfl_up_sync(0xffffffffu, inc, k);
         if (lane >= k) inc += t;
       }
-      int idx = found + inc - cnt;                // markers before this lane's first hit
-      while (hits) {
-        const int j = __ffs(hits) - 1;
-        hits &= hits - 1;
-        ++idx;                                    // the idx-th marker starts segment idx
-        if (idx < nseg) seg_start[base + idx] = q + j + 2;
+      if (write) {
+        int idx = first + found + inc - cnt;      // markers before this lane's first hit
+        while (hits) {
+          const int j = __ffs(hits) - 1;
+          hits &= hits - 1;
+          ++idx;                                  // the idx-th marker starts segment idx
+          if (idx < nseg) seg_start[idx] = q + j + 2;
+        }
       }
       found += __shfl_sync(0xffffffffu, inc, 31);
     }
   }
+  return found;
+}
+
+// CTA of kIndexWarps warps per image: segment s > 0 starts after the s-th RST
+// marker.  The scan is split into contiguous chunks, one per warp: each warp
+// counts its chunk's markers, a CTA prefix gives each chunk its first index,
+// then each warp rescans its chunk (L1 / L2 hits) writing the starts.  Also
+// appends the image's intervals that hold ROI blocks to the batch's active
+// list (the decode kernel's work: no lane idles on a skipped interval).
+__global__ void __launch_bounds__(32 * kIndexWarps) smol_jpeg_index_kernel(const JpegDesc* ds, int n_images,
+                                                                         int32_t* seg_start, int32_t* seg_img,
+                                                                         int32_t* active, int32_t* n_active) {
+  __shared__ int cnt_s[kIndexWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int img = blockIdx.x;
+  if (img >= n_images) return;
+  const JpegDesc& d = ds[img];
+  const uint8_t* p = d.data;
+  const int end = d.size, s0 = d.scan_off;
+  const int base = d.seg_base, nseg = d.nseg;
+  for (int s0w = warp * 32; s0w < nseg; s0w += 32 * kIndexWarps) {   // defaults: segment 0 at the scan
+    const int s = s0w + lane;                     // start, missing markers -> empty segments
+    bool act = false;
+    if (s < nseg) {
+      seg_img[base + s] = img;
+      seg_start[base + s] = s == 0 ? s0 : end;
+      act = seg_in_roi(d, s);
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, act);
+    int at = 0;
+    if (lane == 0 && bal) at = atomicAdd(n_active, __popc(bal));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (act) active[at + __popc(bal & ((1u << lane) - 1))] = base + s;
+  }
+  if (nseg <= 1) return;                          // (uniform over the CTA)
+  const int a0 = s0 & ~15;
+  const int span = end - a0;
+  const int L = ((span + kIndexWarps - 1) / kIndexWarps + 512 * kIndexUnroll - 1) / (512 * kIndexUnroll) *
+                (512 * kIndexUnroll);             // chunk: whole steps
+  const int clo = min(end, a0 + warp * L), chi = min(end, clo + L);
+  const int n = scan_markers(p, clo, chi, s0, end, lane, false, 0, nseg, nullptr);
+  if (lane == 0) cnt_s[warp] = n;
+  __syncthreads();                                // (after the segment defaults above, too)
+  int first = 0;
+  for (int w = 0; w < warp; ++w) first += cnt_s[w];
+  if (n > 0 && first < nseg - 1) scan_markers(p, clo, chi, s0, end, lane, true, first, nseg, seg_start + base);
 }
 
 struct BitReader {
@@ -218,9 +240,9 @@ struct BitReader {
   }
 };
 
-// T.81 F.16 DECODE (needs >= 16 valid bits).  Codes of <= 9 bits: one LUT
-// read; longer codes: the length is the number of left-justified limits the
-// 16-bit window reaches (branch-free, the same instructions for every lane).
+// T.81 F.16 DECODE (needs >= 16 valid bits): codes of <= 9 bits by one LUT
+// read, longer ones by the MAXCODE walk on left-justified limits (a short
+// divergent loop; the branch-free form measured slower, r02h)
 __device__ __forceinline__ int huff_decode(BitReader& br, const HuffTable* t, const uint16_t* slut = nullptr) {
   const uint32_t look = br.peek16();
   const uint32_t e = slut ? slut[look >> (16 - kHuffLutBits)] : __ldg(&t->lut[look >> (16 - kHuffLutBits)]);
@@ -229,18 +251,17 @@ __device__ __forceinline__ int huff_decode(BitReader& br, const HuffTable* t, co
     return (int)(e & 255u);
   }
   int l = kHuffLutBits + 1;
-#pragma unroll
-  for (int i = kHuffLutBits + 1; i < 16; ++i) l += look >= __ldg(&t->limit[i]) ? 1 : 0;
-  if (look >= __ldg(&t->limit[16])) { br.skip(16); return 0; }   // invalid code: read as EOB / zero
+  while (l <= 16 && look >= __ldg(&t->limit[l])) ++l;
+  if (l > 16) { br.skip(16); return 0; }        // invalid code: read as EOB / zero
   br.skip(l);
   return (int)__ldg(&t->huffval[((int32_t)(look >> (16 - l)) + __ldg(&t->valoff[l])) & 255]);
 }
 
 // Thread per restart interval.  The decode is one flat loop, one symbol per
 // iteration whatever the lane's state (DC or AC, any block), so the lanes of
-// a warp stay converged on the same code path.  Blocks that end in an
-// iteration are stored by the whole warp together (one coalesced 4-byte store
-// per lane per block), then the lanes move on to their next block.
+// a warp stay converged on the same code path; a block that ends stores its
+// coefficients (if inside the ROI box) and the lane moves to its next block
+// (warp-cooperative stores measured slower, r02h).
 // one_set: every image of the batch uses table set `set0`, whose 9-bit LUTs
 // of tables 0 and 1 are then read from shared memory.
 __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const JpegDesc* ds, int nseg_total,
@@ -261,16 +282,13 @@ __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const Jp
       reinterpret_cast<uint4*>(slut[t])[w] = __ldg(reinterpret_cast<const uint4*>(T.lut) + w);
     }
   }
-  const int lane = threadIdx.x & 31;
-  int16_t* const wbuf = blkbuf + (threadIdx.x & ~31) * kJpegBlkStride;   // the warp's 32 block buffers
   int16_t* blk = blkbuf + threadIdx.x * kJpegBlkStride;
 #pragma unroll
   for (int i = 0; i < 16; ++i) reinterpret_cast<uint2*>(blk)[i] = make_uint2(0u, 0u);   // (8-B aligned buffers)
   __syncthreads();
   const int gi = blockIdx.x * kJpegThreads + threadIdx.x;
-  if (__all_sync(0xffffffffu, gi >= min(nseg_total, __ldg(n_active)))) return;   // (warp-uniform exit)
-  bool alive = gi < min(nseg_total, __ldg(n_active));
-  const int g = alive ? __ldg(active + gi) : __ldg(active);      // an interval holding ROI blocks
+  if (gi >= min(nseg_total, __ldg(n_active))) return;
+  const int g = __ldg(active + gi);               // an interval holding ROI blocks
   const JpegDesc& d = ds[seg_img[g]];
   const int s = g - d.seg_base;
   const int m0 = s * d.ri, m1 = min(d.nmcu, m0 + d.ri) - 1;
@@ -292,66 +310,48 @@ __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const Jp
   int sdc = one_set && d.td[0] < 2 ? d.td[0] : -1, sac = one_set && d.ta[0] < 2 ? 2 + d.ta[0] : -1;
   int32_t pred0 = 0, pred1 = 0, pred2 = 0;        // DC predictors (reset per interval, F.2.1.3.1)
   int k = 0;                                      // zig-zag position of the next coefficient
-  while (__any_sync(0xffffffffu, alive)) {
-    bool fin = false;
-    if (alive) {
-      br.refill();
-      // one symbol: the DC category (k == 0, F.2.2.1) or an AC run/size (F.13)
-      const int sl = k == 0 ? sdc : sac;
-      const int sym = huff_decode(br, k == 0 ? tdc : tac, sl >= 0 ? slut[sl] : nullptr);
-      const int ssss = sym & 15, r = k == 0 ? 0 : sym >> 4;
-      if (ssss == 0 && k > 0) {
-        k = r == 15 ? k + 16 : 64;                // ZRL / EOB
-      } else {
-        k += r;
-        int32_t v = br.receive_extend(ssss);
-        if (k == 0) {
-          const int32_t pv = c == 0 ? pred0 : c == 1 ? pred1 : pred2;
-          v += pv;
-          if (c == 0) pred0 = v; else if (c == 1) pred1 = v; else pred2 = v;
-        }
-        if (k < 64) {
-          const int e = zmap[k];
-          if (e != 255) blk[e] = (int16_t)v;
-        }
-        ++k;
+  while (true) {
+    br.refill();
+    // one symbol: the DC category (k == 0, F.2.2.1) or an AC run/size (F.13)
+    const int sl = k == 0 ? sdc : sac;
+    const int sym = huff_decode(br, k == 0 ? tdc : tac, sl >= 0 ? slut[sl] : nullptr);
+    const int ssss = sym & 15, r = k == 0 ? 0 : sym >> 4;
+    if (ssss == 0 && k > 0) {
+      k = r == 15 ? k + 16 : 64;                  // ZRL / EOB
+    } else {
+      k += r;
+      int32_t v = br.receive_extend(ssss);
+      if (k == 0) {
+        const int32_t pv = c == 0 ? pred0 : c == 1 ? pred1 : pred2;
+        v += pv;
+        if (c == 0) pred0 = v; else if (c == 1) pred1 = v; else pred2 = v;
       }
-      fin = k >= 64;
+      if (k < 64) {
+        const int e = zmap[k];
+        if (e != 255) blk[e] = (int16_t)v;
+      }
+      ++k;
     }
-    // ---- blocks that ended: destination (if inside the ROI box) ----------
-    int16_t* out = nullptr;
-    if (fin) {
+    if (k < 64) continue;
+    // ---- block done: store it if inside the ROI box, clear, next block ----
+    {
       const int by = my * V + y - (c == 0 ? d.by0[0] : c == 1 ? d.by0[1] : d.by0[2]);
       const int bx = mx * H + x - (c == 0 ? d.bx0[0] : c == 1 ? d.bx0[1] : d.bx0[2]);
       const int nby = c == 0 ? d.nby[0] : c == 1 ? d.nby[1] : d.nby[2];
       const int nbx = c == 0 ? d.nbx[0] : c == 1 ? d.nbx[1] : d.nbx[2];
-      if (by >= 0 && by < nby && bx >= 0 && bx < nbx)
-        out = (c == 0 ? d.dst[0] : c == 1 ? d.dst[1] : d.dst[2]) +
-              (int64_t)by * (c == 0 ? d.dst_stride[0] : c == 1 ? d.dst_stride[1] : d.dst_stride[2]) +
-              (int64_t)bx * E;
-    }
-    // ---- the warp stores them together and clears their buffers ----------
-    uint32_t fm = __ballot_sync(0xffffffffu, fin);
-    __syncwarp();                                 // lanes' coefficient writes visible to the warp
-    while (fm) {
-      const int j = __ffs(fm) - 1;
-      fm &= fm - 1;
-      const unsigned long long oj = __shfl_sync(0xffffffffu, (unsigned long long)out, j);
-      int16_t* bj = wbuf + j * kJpegBlkStride;
-      if (E == 1) {
-        if (lane == 0) {
-          if (oj) *reinterpret_cast<int16_t*>(oj) = bj[0];
-          bj[0] = 0;
+      if (by >= 0 && by < nby && bx >= 0 && bx < nbx) {
+        int16_t* out = (c == 0 ? d.dst[0] : c == 1 ? d.dst[1] : d.dst[2]) +
+                       (int64_t)by * (c == 0 ? d.dst_stride[0] : c == 1 ? d.dst_stride[1] : d.dst_stride[2]) +
+                       (int64_t)bx * E;
+        if (E == 1) {
+          *out = blk[0];
+        } else {
+          for (int w = 0; w < E / 4; ++w)         // E*2 bytes (a multiple of 8): 8-byte words
+            reinterpret_cast<uint2*>(out)[w] = reinterpret_cast<const uint2*>(blk)[w];
         }
-      } else if (lane < E / 2) {                  // E even: E/2 4-byte words
-        uint32_t* b32 = reinterpret_cast<uint32_t*>(bj);
-        if (oj) reinterpret_cast<uint32_t*>(oj)[lane] = b32[lane];
-        b32[lane] = 0u;
       }
+      for (int w = 0; w < (E + 3) / 4; ++w) reinterpret_cast<uint2*>(blk)[w] = make_uint2(0u, 0u);
     }
-    __syncwarp();
-    if (!fin) continue;
-    // ---- next block of this lane's interval ------------------------------
     k = 0;
     if (++x == H) {
       x = 0;
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const Jp
         y = 0;
         if (++c == nc) {
           c = 0;
-          if (++m > m1) { alive = false; continue; }
+          if (++m > m1) break;
           if (++mx == d.mcus_x) { mx = 0; ++my; }
         }
         H = nc == 1 ? 1 : (c == 0 ? d.h[0] : 1);

@@ -1429,7 +1429,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       int32_t* n_active = active + pl->jnseg;
       SMOL_CUDA(cudaStreamWaitEvent(es, pl->stage_ready[sl_], 0));
       SMOL_CUDA(cudaMemsetAsync(n_active, 0, sizeof(int32_t), es));
-      smol_jpeg_index_kernel<<<ceil_div(n_images, 4), 128, 0, es>>>(dj, n_images, seg_start, seg_img, active,
+      smol_jpeg_index_kernel<<<n_images, 32 * kIndexWarps, 0, es>>>(dj, n_images, seg_start, seg_img, active,
                                                                     n_active);
       SMOL_CUDA(cudaGetLastError());
       smol_jpeg_decode_kernel<<<ceil_div(pl->jnseg, kJpegThreads), kJpegThreads, 0, es>>>(
@@ -1840,8 +1840,8 @@ int32_t smol_jpeg_decode_planes(const smol_jpeg_batch* b, int16_t* const* planes
   if (e == cudaSuccess) e = cudaMemcpyAsync(dz, zm, 64, cudaMemcpyHostToDevice, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(dseg + 3 * nseg, 0, sizeof(int32_t), stream);
   if (e == cudaSuccess) {
-    smol_jpeg_index_kernel<<<ceil_div(n, 4), 128, 0, stream>>>(dj, n, dseg, dseg + nseg, dseg + 2 * nseg,
-                                                               dseg + 3 * nseg);
+    smol_jpeg_index_kernel<<<n, 32 * kIndexWarps, 0, stream>>>(dj, n, dseg, dseg + nseg, dseg + 2 * nseg,
+                                                                dseg + 3 * nseg);
     smol_jpeg_decode_kernel<<<(int)((nseg + kJpegThreads - 1) / kJpegThreads), kJpegThreads, 0, stream>>>(
         dj, (int)nseg, dseg, dseg + nseg, dseg + 2 * nseg, dseg + 3 * nseg, dz, dh, 0);
     e = cudaGetLastError();
