@@ -62,8 +62,9 @@ constexpr int kJpegThreads = 128;
 constexpr int kJpegBlkStride = 68;   // int16 per thread block buffer (136 B: spreads the lanes' banks)
 
 // Does restart interval s of image d hold a block inside the ROI box?
-__device__ __forceinline__ bool seg_in_roi(const JpegDesc& d, int s) {
-  const int m0 = s * d.ri, m1 = min(d.nmcu, m0 + d.ri) - 1;
+// (host: the decode grid is sized from the count)
+__host__ __device__ __forceinline__ bool seg_in_roi(const JpegDesc& d, int s) {
+  const int m0 = s * d.ri, m1 = (d.nmcu < m0 + d.ri ? d.nmcu : m0 + d.ri) - 1;
   if (m1 < m0) return false;
   const int my0 = m0 / d.mcus_x, my1 = m1 / d.mcus_x;
   const int mxa = my0 == my1 ? m0 - my0 * d.mcus_x : 0;

@@ -612,6 +612,7 @@ struct smol_preproc_plan {
   std::vector<std::array<int, 3>> jhdr_qid; // per header: quantization table ids per component
   std::vector<int> jset_hdr;               // per table set: a header holding it
   int jnseg = 0;                           // restart intervals of the current batch
+  int jnact = 0;                           // of them holding ROI blocks (one decode thread each)
   int stage_slot = 0;
   bool fixed_stage = false;                // staging sized in plan (params.max_width/max_height)
   std::vector<std::pair<uintptr_t, uintptr_t>> pinned_ok;   // run_host: verified [lo, hi) allocations
@@ -1369,7 +1370,8 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
           }
       }
       for (size_t t = 0; t < pl->jqt.size(); ++t) memcpy(hq + 64 * t, pl->jqt[t].data(), 128);
-      int64_t nseg_total = 0;
+      int64_t nseg_total = 0, nact_total = 0;
+      int nact_img = 0;
       for (int i = 0; i < n_images; ++i) {
         const JpegHdr& H = pl->jhdr[pl->jimg_hdr[i]];
         const ExpandDesc& e = he[i];
@@ -1397,6 +1399,13 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
         J.E = E;
         J.ncomp = (uint8_t)H.ncomp;
         nseg_total += H.nseg;
+        // intervals holding ROI blocks (the decode grid; equal for
+        // consecutive images of one header and kind)
+        if (!(i > 0 && pl->jimg_hdr[i] == pl->jimg_hdr[i - 1] && hr[i].kind == hr[i - 1].kind)) {
+          nact_img = 0;
+          for (int sg = 0; sg < J.nseg; ++sg) nact_img += seg_in_roi(J, sg) ? 1 : 0;
+        }
+        nact_total += nact_img;
       }
       if (nseg_total >= INT_MAX / 2) return fail(SMOL_ERR_CAPACITY, "%lld restart intervals in one batch", (long long)nseg_total);
       void* segb = pl->d_seg[sl];
@@ -1404,6 +1413,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       pl->d_seg[sl] = static_cast<int32_t*>(segb);
       if (rc) return rc;
       pl->jnseg = (int)nseg_total;
+      pl->jnact = (int)nact_total;
       SMOL_CUDA(cudaMemcpyAsync(dj, hj, sizeof(JpegDesc) * n_images, cudaMemcpyHostToDevice, pl->copy_stream));
       SMOL_CUDA(cudaMemcpyAsync(dh, hh, sizeof(HuffSet) * nset, cudaMemcpyHostToDevice, pl->copy_stream));
       SMOL_CUDA(cudaMemcpyAsync(dq, hq, 128 * pl->jqt.size(), cudaMemcpyHostToDevice, pl->copy_stream));
@@ -1432,7 +1442,7 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
       smol_jpeg_index_kernel<<<n_images, 32 * kIndexWarps, 0, es>>>(dj, n_images, seg_start, seg_img, active,
                                                                     n_active);
       SMOL_CUDA(cudaGetLastError());
-      smol_jpeg_decode_kernel<<<ceil_div(pl->jnseg, kJpegThreads), kJpegThreads, 0, es>>>(
+      smol_jpeg_decode_kernel<<<ceil_div(std::max(pl->jnact, 1), kJpegThreads), kJpegThreads, 0, es>>>(
           dj, pl->jnseg, seg_start, seg_img, active, n_active, pl->d_zmap,
           pl->d_huff + (size_t)sl_ * kMaxHuffSets, pl->jset_hdr.size() == 1 ? 1 : 0);
       SMOL_CUDA(cudaGetLastError());
