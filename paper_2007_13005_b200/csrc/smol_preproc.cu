@@ -1123,9 +1123,10 @@ int32_t run_impl(smol_preproc_plan_t* pl, int n_images, const void* images, cons
   int map_n = 0;
   int4* hm = pl->h_map + (size_t)slot * pl->map_cap;
   int4* dm = pl->d_map + (size_t)slot * pl->map_cap;
-  // (scale 1 only: at 1/2..1/8 a tile spans few 16-row rolling steps and the
-  // extra tiles' halos cost more than the idle slots, measured r01m)
-  if (pl->cta_map_mode && auto_rows && n_col_tiles == 1 && K == 1 && !thumb) {
+  // (all scales: r02n c3a 0.0698 -> 0.0672 ms, c3b 0.0374 -> 0.0369, c5
+  // unchanged; round 1 had measured the halos costing more at 1/2..1/8,
+  // r01m, before the per-kind tile layouts and tap tables)
+  if (pl->cta_map_mode && auto_rows && n_col_tiles == 1 && !thumb) {
     const int S = pl->num_sms * occ;
     const long long base = (long long)n_images * ntiles;
     if (base < S && S <= pl->map_cap && ntiles + 1 <= pl->OH / 8) {
