@@ -270,3 +270,25 @@ def test_run_jpeg_corrupt_entropy_data_is_contained(k, layout):
     torch.cuda.synchronize()
     a, b = _run_pair(params, files)
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_run_jpeg_mixed_tables_in_one_batch():
+    """A batch whose files carry different quantization tables (q50 / q75 / q95)
+    and different Huffman tables (libjpeg's optimized per-image tables): several
+    table sets, so the decoder reads its LUTs from global memory; equal to run
+    on the oracle-decoded planes."""
+    from PIL import Image
+    rng = np.random.default_rng(12)
+    files = []
+    for q in (50, 75, 95):
+        qt = synth.quant_tables(q)
+        files.append(jpeg.encode(synth.make_image(rng, 200, 150, qt, "natural"), qt, 2))
+    for opt in (True, False):
+        buf = io.BytesIO()
+        Image.fromarray(synth.natural_rgb(rng, 200, 150)).save(buf, "JPEG", quality=80, optimize=opt,
+                                                                restart_marker_blocks=3)
+        files.append(buf.getvalue())
+    for name, layout in (("c3b", "packed"), ("c2", "dense")):
+        a, b = _run_pair(smol.params_from_config(synth.CONFIGS[name], layout=layout), files)
+        np.testing.assert_array_equal(a, b)
