@@ -136,13 +136,33 @@ def _coef_images(files):
     return imgs, np.stack(qts)
 
 
+def _per_image(plan, params, imgs, qt, rois, roi_rects):
+    """smol_preproc_run image by image, each with its own (<= 3) tables."""
+    import torch
+    outs = []
+    for i, im in enumerate(imgs):
+        ids = list(dict.fromkeys(im.qidx))
+        local = synth.CoefImage(im.width, im.height, im.coef, tuple(ids.index(t) for t in im.qidx),
+                                subsampling=im.subsampling)
+        outs.append(plan.run(smol.batch_for(params, [local], qt[ids],
+                                            rois=None if rois is None else [rois[i]],
+                                            roi_rects=None if roi_rects is None else [roi_rects[i]])))
+    return torch.cat(outs)
+
+
 def _run_pair(params, files, rois=None, roi_rects=None):
     """(run_jpeg output, run on the oracle-decoded planes)."""
     import torch
     imgs, qt = _coef_images(files)
     plan = smol.Plan(params, len(files))
     out_j = plan.run(smol.JpegBatch(files, rois=rois, roi_rects=roi_rects))
-    out_d = plan.run(smol.batch_for(params, imgs, qt, rois=rois, roi_rects=roi_rects))
+    if len(qt) <= 4:
+        out_d = plan.run(smol.batch_for(params, imgs, qt, rois=rois, roi_rects=roi_rects))
+    else:
+        # more distinct tables than smol_preproc_run's 4 (run_jpeg takes up
+        # to 64): the reference image by image (outputs do not depend on the
+        # batch -- shard invariance)
+        out_d = _per_image(plan, params, imgs, qt, rois, roi_rects)
     torch.cuda.synchronize()
     r = out_j.cpu().numpy(), out_d.cpu().numpy()
     plan.close()
