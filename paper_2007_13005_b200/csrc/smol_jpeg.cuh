@@ -59,7 +59,7 @@ struct JpegDesc {
 
 #if defined(__CUDACC__)
 constexpr int kJpegThreads = 128;
-constexpr int kJpegBlkStride = 68;   // int16 per thread block buffer (136 B: spreads the lanes' banks)
+constexpr int kJpegBlkStride = 72;   // int16 per thread block buffer (144 B: 16-B aligned for 16-byte copies)
 
 // Does restart interval s of image d hold a block inside the ROI box?
 // (host: the decode grid is sized from the count)
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const Jp
   }
   int16_t* blk = blkbuf + threadIdx.x * kJpegBlkStride;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) reinterpret_cast<uint2*>(blk)[i] = make_uint2(0u, 0u);   // (8-B aligned buffers)
+  for (int i = 0; i < 8; ++i) reinterpret_cast<uint4*>(blk)[i] = make_uint4(0u, 0u, 0u, 0u);   // (16-B aligned buffers)
   __syncthreads();
   const int gi = blockIdx.x * kJpegThreads + threadIdx.x;
   if (gi >= min(nseg_total, __ldg(n_active))) return;
@@ -344,14 +344,22 @@ __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const Jp
         int16_t* out = (c == 0 ? d.dst[0] : c == 1 ? d.dst[1] : d.dst[2]) +
                        (int64_t)by * (c == 0 ? d.dst_stride[0] : c == 1 ? d.dst_stride[1] : d.dst_stride[2]) +
                        (int64_t)bx * E;
-        if (E == 1) {
+        if (E == 64) {                            // dense blocks: 128 B, 16-B aligned
+#pragma unroll
+          for (int w = 0; w < 8; ++w) reinterpret_cast<uint4*>(out)[w] = reinterpret_cast<const uint4*>(blk)[w];
+        } else if (E == 1) {
           *out = blk[0];
         } else {
           for (int w = 0; w < E / 4; ++w)         // E*2 bytes (a multiple of 8): 8-byte words
             reinterpret_cast<uint2*>(out)[w] = reinterpret_cast<const uint2*>(blk)[w];
         }
       }
-      for (int w = 0; w < (E + 3) / 4; ++w) reinterpret_cast<uint2*>(blk)[w] = make_uint2(0u, 0u);
+      if (E == 64) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) reinterpret_cast<uint4*>(blk)[w] = make_uint4(0u, 0u, 0u, 0u);
+      } else {
+        for (int w = 0; w < (E + 3) / 4; ++w) reinterpret_cast<uint2*>(blk)[w] = make_uint2(0u, 0u);
+      }
     }
     k = 0;
     if (++x == H) {
