@@ -58,7 +58,10 @@ struct JpegDesc {
 };
 
 #if defined(__CUDACC__)
-constexpr int kJpegThreads = 128;
+#ifndef SMOL_JPEG_THREADS
+#define SMOL_JPEG_THREADS 128
+#endif
+constexpr int kJpegThreads = SMOL_JPEG_THREADS;   // decode CTA size
 constexpr int kJpegBlkStride = 72;   // int16 per thread block buffer (144 B: 16-B aligned for 16-byte copies)
 
 // Does restart interval s of image d hold a block inside the ROI box?
