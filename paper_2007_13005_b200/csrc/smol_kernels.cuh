@@ -26,9 +26,6 @@
 // scale 1 the output tasks share the phase with the next step's IDCT and are
 // grabbed dynamically, two per lane per grab, interleaved by the compiler; at
 // scales 1/2..1/8 that IDCT is small and a static stride wins.
-#ifndef SMOL_OUT_RUN_ROWS
-#define SMOL_OUT_RUN_ROWS(K) ((K) == 1 ? 4 : 8)   // rows per output run
-#endif
 #ifndef SMOL_OUT_PER_GRAB
 #define SMOL_OUT_PER_GRAB 2      // scale 1: output tasks per lane per work-counter grab
 #endif
@@ -486,7 +483,7 @@ struct KParams {
   void* out;
   int OW, OH, tile_rows, tile_cols, n_col_tiles, n_row_tiles;
   int out_vec;                     // out is 16-B (fp32) / 8-B (fp16) aligned: vector stores allowed
-  int rowrun;                      // output tasks walk runs of rows, reusing horizontal lerps (vertical magnification)
+  int rowrun;                      // > 0: output tasks walk runs of this many rows, reusing horizontal lerps (vertical magnification)
   const int4* cta_map;             // non-null: 1-D grid, CTA -> {image, oy0, oy1, 0}
   uint32_t magic;                  // 0x4B000000: bit pattern of 2^23 (byte -> float trick)
   float na[3], nb[3];              // y = x * na + nb = (x/255 - mean)/std
@@ -895,7 +892,7 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
     // one row lower keeps the old bottom lerp as the new top.  Bit-identical
     // to recomputing them (same operations on the same samples).
     {
-      constexpr int kRun = SMOL_OUT_RUN_ROWS(K);
+      const int kRun = kp.rowrun;        // rows per run (host: longer under stronger magnification)
       const int nrows = done - done_prev;
       const int ngr = (nrows + kRun - 1) / kRun;
       const int ntasko = ngr * nq4;

@@ -19,7 +19,10 @@ constexpr int kThumbWarps = 4;                 // images in flight per CTA
 constexpr int kThumbMaxFoot = 32;              // decoded luma footprint limit (px per side)
 constexpr int kThumbMaxOut = 128;              // output width / height limit
 constexpr int kThumbCP = kThumbMaxFoot / 2 + 2;   // chroma footprint pitch
-constexpr int kThumbRun = 8;                   // output rows per lane task (row-run reuse)
+#ifndef SMOL_THUMB_RUN
+#define SMOL_THUMB_RUN 8
+#endif
+constexpr int kThumbRun = SMOL_THUMB_RUN;       // output rows per lane task (row-run reuse)
 struct ThumbWarpSmem {
   uint32_t rgb[kThumbMaxFoot * kThumbMaxFoot + 1];  // RGBx of the luma footprint (+1: x0 + 1 read at the end)
   uint8_t y[kThumbMaxFoot * kThumbMaxFoot];
