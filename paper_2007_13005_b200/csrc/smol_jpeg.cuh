@@ -159,20 +159,29 @@ __global__ void __launch_bounds__(32 * kIndexWarps) smol_jpeg_index_kernel(const
   const uint8_t* p = d.data;
   const int end = d.size, s0 = d.scan_off;
   const int base = d.seg_base, nseg = d.nseg;
-  for (int s0w = warp * 32; s0w < nseg; s0w += 32 * kIndexWarps) {   // defaults: segment 0 at the scan
-    const int s = s0w + lane;                     // start, missing markers -> empty segments
-    bool act = false;
-    if (s < nseg) {
-      seg_img[base + s] = img;
-      seg_start[base + s] = s == 0 ? s0 : end;
-      act = seg_in_roi(d, s);
-    }
-    const uint32_t bal = __ballot_sync(0xffffffffu, act);
-    int at = 0;
-    if (lane == 0 && bal) at = atomicAdd(n_active, __popc(bal));
-    at = __shfl_sync(0xffffffffu, at, 0);
-    if (act) active[at + __popc(bal & ((1u << lane) - 1))] = base + s;
+  // defaults (segment 0 at the scan start, missing markers -> empty
+  // segments) and the image's intervals holding ROI blocks: counted per
+  // thread, one global atomic per CTA, then written at the CTA's offset
+  __shared__ int act_s[32 * kIndexWarps];
+  __shared__ int act_base;
+  int na = 0;
+  for (int s = threadIdx.x; s < nseg; s += 32 * kIndexWarps) {
+    seg_img[base + s] = img;
+    seg_start[base + s] = s == 0 ? s0 : end;
+    na += seg_in_roi(d, s) ? 1 : 0;
   }
+  act_s[threadIdx.x] = na;
+  __syncthreads();
+  if (threadIdx.x == 0) {                         // exclusive scan of the counts (256 values)
+    int acc = 0;
+    for (int i = 0; i < 32 * kIndexWarps; ++i) { const int t = act_s[i]; act_s[i] = acc; acc += t; }
+    act_base = acc ? atomicAdd(n_active, acc) : 0;
+  }
+  __syncthreads();
+  int at = act_base + act_s[threadIdx.x];
+  if (na)
+    for (int s = threadIdx.x; s < nseg; s += 32 * kIndexWarps)
+      if (seg_in_roi(d, s)) active[at++] = base + s;
   if (nseg <= 1) return;                          // (uniform over the CTA)
   const int a0 = s0 & ~15;
   const int span = end - a0;

@@ -312,3 +312,35 @@ def test_run_jpeg_mixed_tables_in_one_batch():
     for name, layout in (("c3b", "packed"), ("c2", "dense")):
         a, b = _run_pair(smol.params_from_config(synth.CONFIGS[name], layout=layout), files)
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_run_jpeg_errors():
+    """Batch-level refusals of smol_preproc_run_jpeg: status and message."""
+    import ctypes
+    import torch
+    _, _, files = _files("natural", [(64, 64)] * 3, 1, seed=2)
+    params = smol.params_from_config(synth.CONFIGS["c1"])
+    plan = smol.Plan(params, 2)
+    with pytest.raises(smol.SmolError) as e:               # more images than the plan holds
+        plan.run(smol.JpegBatch(files))
+    assert e.value.status == native.SMOL_ERR_CAPACITY
+    bad = list(files[:2])
+    bad[1] = bad[1][:2] + b"\xff\xc2" + bad[1][4:]          # image 1: progressive SOF marker first
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(smol.JpegBatch(bad))
+    assert "image 1" in str(e.value)
+    jb = smol.JpegBatch(files[:2])
+    jb.images[1].offset += 1                               # not 16-B aligned
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(jb)
+    assert e.value.status == native.SMOL_ERR_INVALID
+    jb = smol.JpegBatch(files[:2])
+    dev = jb.arena.cuda()                                  # device arena: headers cannot be parsed
+    jb.desc.arena = dev.data_ptr()
+    with pytest.raises(smol.SmolError) as e:
+        plan.run(jb)
+    assert e.value.status == native.SMOL_ERR_INVALID
+    out = plan.run(smol.JpegBatch(files[:2]))              # the plan still works
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
