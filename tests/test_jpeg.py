@@ -344,3 +344,20 @@ def test_run_jpeg_errors():
     out = plan.run(smol.JpegBatch(files[:2]))              # the plan still works
     torch.cuda.synchronize()
     assert torch.isfinite(out).all()
+
+
+@pytest.mark.gpu
+def test_run_jpeg_large_frames():
+    """Maximum sizes of the path through the JPEG input: 1080p frames (c5
+    params: 1/4 scale, packed) and a 12 MP photo at 1/8 with column tiles;
+    GPU entropy decode == oracle, run_jpeg == run on the decoded planes."""
+    qt = synth.quant_tables(75)
+    rng = np.random.default_rng(21)
+    hd = [jpeg.encode(synth.make_image(rng, 1920, 1080, qt, "natural"), qt, 4)]
+    _check_planes(hd)
+    a, b = _run_pair(smol.params_from_config(synth.CONFIGS["c5"], layout="packed"), hd)
+    np.testing.assert_array_equal(a, b)
+    big = [jpeg.encode(synth.make_image(rng, 4000, 3000, qt, "natural"), qt, 8)]
+    cfg = synth.Config("big8", 1, 4000, 3000, 8, "exact", resize_w=250, resize_h=188)
+    a, b = _run_pair(smol.params_from_config(cfg), big)
+    np.testing.assert_array_equal(a, b)
