@@ -227,7 +227,8 @@ struct BitReader {
   // hold no 0xFF: append them at once; else byte by byte.
   __device__ __forceinline__ void refill() {
     if (nb > 32) return;
-    if (!stop && p + 4 <= pend) {
+    if (stop) { nb = 64; return; }                // past a marker: the buffer's low bits are already zeros
+    if (p + 4 <= pend) {
       const uintptr_t a = reinterpret_cast<uintptr_t>(p);
       const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
       const uint32_t lo = __ldg(w), hi = __ldg(w + 1);
