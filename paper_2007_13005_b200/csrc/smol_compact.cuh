@@ -76,7 +76,7 @@ struct ExpandDesc {
 constexpr int kExpandWarps = 4;
 // per-lane block buffers are padded by 8 bytes (lane stride 2E + 8 bytes) so
 // the lanes' zeroing/scatter stores do not all land in one shared-memory bank
-constexpr int kExpandLanePad = 4;               // int16 elements
+constexpr int kExpandLanePad = 8;               // int16 elements (lane stride 2E + 16 B: 16-B aligned)
 constexpr int kExpandBlkBuf = 32 * (64 + kExpandLanePad);
 // dynamic shared memory per CTA: per warp a 32-block output buffer
 constexpr int kExpandSmem = kExpandWarps * kExpandBlkBuf * 2;
@@ -155,8 +155,13 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
         // 3. zero + scatter this lane's block (E*2 bytes, a multiple of 8)
         const int ls = E + kExpandLanePad;                 // lane stride (elements)
         int16_t* mine = blk + lane * ls;
-        uint2* m8 = reinterpret_cast<uint2*>(mine);
-        for (int q = 0; q < E / 4; ++q) m8[q] = make_uint2(0u, 0u);
+        if (E % 8 == 0) {                                   // (dense: 16-byte words)
+          uint4* m16 = reinterpret_cast<uint4*>(mine);
+          for (int q = 0; q < E / 8; ++q) m16[q] = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          uint2* m8 = reinterpret_cast<uint2*>(mine);
+          for (int q = 0; q < E / 4; ++q) m8[q] = make_uint2(0u, 0u);
+        }
         __syncwarp();                                       // staged entries visible
         for (int j = 0; j < cntc; ++j) {
           const uint16_t u = __ldg(ub + j);
@@ -165,13 +170,23 @@ __global__ void __launch_bounds__(kExpandWarps * 32) smol_expand_kernel(const Ex
           mine[u & 63] = v;
         }
         __syncwarp();
-        // 4. copy the nb blocks out (contiguous in the staged row): 8-byte
-        // word w of the chunk is word w % wpb of block w / wpb
-        const int wpb = E / 4;                              // 8-byte words per block
-        uint2* to8 = reinterpret_cast<uint2*>(drow + (int64_t)ch * E);
-        for (int w = lane; w < nb * wpb; w += 32) {
-          const int bb = wpb == 1 ? w : (int)__umulhi((uint32_t)w, fd_wpb);   // w / wpb (w < 2^16)
-          to8[w] = reinterpret_cast<const uint2*>(blk + bb * ls)[w - bb * wpb];
+        // 4. copy the nb blocks out (contiguous in the staged row): word w of
+        // the chunk is word w % wpb of block w / wpb; 16-byte words when the
+        // blocks are (dense: 128 B blocks, 16-B aligned rows), else 8-byte
+        if (E % 8 == 0) {
+          const int wpb = E / 8;                            // 16-byte words per block
+          uint4* to16 = reinterpret_cast<uint4*>(drow + (int64_t)ch * E);
+          for (int w = lane; w < nb * wpb; w += 32) {
+            const int bb = w / wpb;
+            to16[w] = reinterpret_cast<const uint4*>(blk + bb * ls)[w - bb * wpb];
+          }
+        } else {
+          const int wpb = E / 4;                            // 8-byte words per block
+          uint2* to8 = reinterpret_cast<uint2*>(drow + (int64_t)ch * E);
+          for (int w = lane; w < nb * wpb; w += 32) {
+            const int bb = wpb == 1 ? w : (int)__umulhi((uint32_t)w, fd_wpb);   // w / wpb (w < 2^16)
+            to8[w] = reinterpret_cast<const uint2*>(blk + bb * ls)[w - bb * wpb];
+          }
         }
       }
       __syncwarp();
