@@ -341,7 +341,11 @@ int32_t smol_jpeg_parse_header(const void* data, int64_t size, smol_jpeg_header*
 /* Files -> output tensor (see above).  Stream ordering, staging and
  * ownership as smol_preproc_run_compact: one DMA of the batch's byte range on
  * the plan's copy stream, the index + decode kernels, then the fused kernel
- * on `stream`; the arena must stay untouched until the call after next has
+ * on `stream`.  Errors: SMOL_ERR_CAPACITY (n_images > the plan's max_images,
+ * or too many distinct tables), SMOL_ERR_INVALID (arena not pinned host
+ * memory, a file outside it or at an offset not a multiple of 16, a bad
+ * header), SMOL_ERR_UNSUPPORTED (a non-baseline file, a chroma_2s plan); no
+ * work is queued when a check fails.  The arena must stay untouched until the call after next has
  * returned (3 staging slots). */
 int32_t smol_preproc_run_jpeg(smol_preproc_plan_t* plan, const smol_jpeg_batch* batch, void* out,
                               void* stream);
