@@ -61,6 +61,9 @@ struct JpegDesc {
 #ifndef SMOL_JPEG_THREADS
 #define SMOL_JPEG_THREADS 128
 #endif
+#ifndef SMOL_JPEG_SLUT
+#define SMOL_JPEG_SLUT 1     // 9-bit LUTs of a single table set in shared memory
+#endif
 constexpr int kJpegThreads = SMOL_JPEG_THREADS;   // decode CTA size
 constexpr int kJpegBlkStride = 72;   // int16 per thread block buffer (144 B: 16-B aligned for 16-byte copies)
 
@@ -86,7 +89,20 @@ __host__ __device__ __forceinline__ bool seg_in_roi(const JpegDesc& d, int s) {
 // steps in flight; a marker's second byte may sit in the next lane's (or
 // step's) first byte.  Counts them; with `write`, the idx-th marker of the
 // scan (idx from `first`) starts segment idx: seg_start[idx] = position + 2.
-constexpr int kIndexUnroll = 4, kIndexWarps = 8;
+// 4 warps per image at <= 32 registers (16 CTAs / SM): an index CTA fits
+// beside the fused kernel's four CTAs, so batch k+1's marker scan overlaps
+// batch k's fused kernel (r02bb: JPEG e2e 0.241-0.254 -> 0.223 ms; 8 warps
+// at 64 registers did not fit)
+#ifndef SMOL_INDEX_WARPS
+#define SMOL_INDEX_WARPS 4
+#endif
+#ifndef SMOL_INDEX_UNROLL
+#define SMOL_INDEX_UNROLL 2
+#endif
+#ifndef SMOL_INDEX_MINB
+#define SMOL_INDEX_MINB 16
+#endif
+constexpr int kIndexUnroll = SMOL_INDEX_UNROLL, kIndexWarps = SMOL_INDEX_WARPS;
 __device__ __forceinline__ int scan_markers(const uint8_t* p, int clo, int chi, int s0, int end, int lane,
                                             bool write, int first, int nseg, int32_t* seg_start) {
   int found = 0;                                  // markers seen so far (whole warp)
@@ -148,7 +164,7 @@ __device__ __forceinline__ int scan_markers(const uint8_t* p, int clo, int chi, 
 // then each warp rescans its chunk (L1 / L2 hits) writing the starts.  Also
 // appends the image's intervals that hold ROI blocks to the batch's active
 // list (the decode kernel's work: no lane idles on a skipped interval).
-__global__ void __launch_bounds__(32 * kIndexWarps) smol_jpeg_index_kernel(const JpegDesc* ds, int n_images,
+__global__ void __launch_bounds__(32 * kIndexWarps, SMOL_INDEX_MINB) smol_jpeg_index_kernel(const JpegDesc* ds, int n_images,
                                                                          int32_t* seg_start, int32_t* seg_img,
                                                                          int32_t* active, int32_t* n_active) {
   __shared__ int cnt_s[kIndexWarps];
@@ -286,7 +302,12 @@ __global__ void __launch_bounds__(kJpegThreads) smol_jpeg_decode_kernel(const Jp
                                                                         const int8_t* dst_index,
                                                                         const HuffSet* set0, int one_set) {
   __shared__ __align__(16) int16_t blkbuf[kJpegThreads * kJpegBlkStride];
+#if SMOL_JPEG_SLUT
   __shared__ __align__(16) uint16_t slut[4][1 << kHuffLutBits];   // DC0, DC1, AC0, AC1 of set0
+#else
+  uint16_t (*slut)[1 << kHuffLutBits] = nullptr;
+  one_set = 0;
+#endif
   __shared__ uint8_t zmap[64];                    // zig-zag position -> stored element (255: dropped)
   if (threadIdx.x < 64) zmap[threadIdx.x] = (uint8_t)dst_index[threadIdx.x];
   if (one_set) {
