@@ -19,6 +19,7 @@ constexpr int kThumbWarps = 4;                 // images in flight per CTA
 constexpr int kThumbMaxFoot = 32;              // decoded luma footprint limit (px per side)
 constexpr int kThumbMaxOut = 128;              // output width / height limit
 constexpr int kThumbCP = kThumbMaxFoot / 2 + 2;   // chroma footprint pitch
+constexpr int kThumbRun = 8;                   // output rows per lane task (row-run reuse; 16 / 32 no gain, r02t)
 struct ThumbWarpSmem {
   uint32_t rgb[kThumbMaxFoot * kThumbMaxFoot + 1];  // RGBx of the luma footprint (+1: x0 + 1 read at the end)
   uint8_t y[kThumbMaxFoot * kThumbMaxFoot];
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
     const int lx0 = S.L.lx0, ly0 = S.L.ly0, fw = S.L.lx1 - lx0 + 1, fh = S.L.ly1 - ly0 + 1;
     const int cx0 = S.L.cx0, cy0 = S.L.cy0, cw = S.L.cx1 - cx0 + 1, ch = S.L.cy1 - cy0 + 1;
     // magic-number divisions by the runtime widths (all operands < 2^16)
-    const FastDiv fd_fw = S.L.fd_fw, fd_cw = S.L.fd_cw;   // (precomputed with the layout)
+    const FastDiv fd_fw = S.L.fd_fw, fd_cw = S.L.fd_cw, fd_nq = S.L.fd_q4;   // (precomputed with the layout)
     // taps (reading R9: exact integers); a clamped upper tap gets weight 0
     // column taps per output pair, byte offsets of x0 in an RGB row; the
     // kernel always reads x0 + 1 (a clamped upper tap has weight 0, and the
@@ -105,90 +106,95 @@ __global__ void __launch_bounds__(kThumbWarps * 32) smol_thumb_kernel(const __gr
       S.rgb[r * kThumbMaxFoot + x] = colour(S.y[r * kThumbMaxFoot + x], cb, cr);
     }
     __syncwarp();
-    // bilinear (reading R8) + normalize: the warp walks the output rows
-    // together, lane l holding output pixel pairs l and l + 32 (2 pixels per
-    // packed FP32x2 instruction); u8 -> float by one PRMT into the 2^23
-    // magic (the bias cancels in b - a) -- the tiled kernel's formulation, so
-    // the outputs are bit-identical to it.  All lanes share each row's taps,
-    // so the horizontal lerps of a source row are recomputed only where the
-    // row taps move (thumbnails magnify: 21 -> 64 rows at c4), by the whole
-    // warp at once; the old bottom becomes the new top when they move down
-    // one row (bit-identical).
+    // bilinear (reading R8) + normalize, 4 consecutive output pixels per lane,
+    // two pixels per packed FP32x2 instruction; u8 -> float by one PRMT into
+    // the 2^23 magic (the bias cancels in b - a) -- the tiled kernel's
+    // formulation, so the outputs are bit-identical to it
     OutT* const outn = reinterpret_cast<OutT*>(kp.out) + (size_t)n * 3 * plane;
+    const int nq = (OW + 3) >> 2;
     const uint32_t magic = kp.magic;
     const float2 na0 = f2(kp.na[0]), na1 = f2(kp.na[1]), na2 = f2(kp.na[2]);
     const float2 nb0 = f2(kp.nb[0]), nb1 = f2(kp.nb[1]), nb2 = f2(kp.nb[2]);
-    const int npair = (OW + 1) >> 1;              // <= kThumbMaxOut / 2 = 64: two pairs per lane at most
-    const bool has1 = lane + 32 < npair;
-    const int4 tx0 = S.xp[min(lane, npair - 1)];
-    const int4 tx1 = S.xp[min(lane + 32, npair - 1)];
-    float2 T0[3], B0[3], T1[3], B1[3];            // horizontal lerps of the top / bottom source rows [ch]
-    auto hlerp = [&](int row, const int4& tx, float2 (&H)[3]) {
-      const uint8_t* base = reinterpret_cast<const uint8_t*>(S.rgb + row * kThumbMaxFoot);
-      const float2 wx = make_float2(__int_as_float(tx.z), __int_as_float(tx.w));
-      const uint32_t p0 = lds_u32(base + tx.x), p1 = lds_u32(base + tx.x + 4);
-      const uint32_t q0 = lds_u32(base + tx.y), q1 = lds_u32(base + tx.y + 4);
+    // a lane walks one 4-pixel column quad down a run of kThumbRun rows:
+    // the horizontal lerps of a source row are reused while the row taps
+    // stay put (thumbnails magnify: 21 -> 64 rows at c4), the old bottom
+    // becomes the new top when they move down one row (bit-identical)
+    const int ngr = (OH + kThumbRun - 1) / kThumbRun;
+    for (int t = lane; t < nq * ngr; t += 32) {
+      const int g = (int)fdiv((uint32_t)t, fd_nq), q = t - g * nq, ox = 4 * q;
+      const int ra = g * kThumbRun, rb = min(ra + kThumbRun, OH);
+      const int4 txa = S.xp[min(ox >> 1, ((OW + 1) >> 1) - 1)];
+      const int4 txb = S.xp[min((ox + 2) >> 1, ((OW + 1) >> 1) - 1)];
+      float2 T[3][2], B[3][2];
+      auto hlerp = [&](int row, float2 (&H)[3][2]) {
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(S.rgb + row * kThumbMaxFoot);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int sel = 0x7540 + c;
-        const float2 fa = make_float2(__uint_as_float(__byte_perm(p0, magic, sel)), __uint_as_float(__byte_perm(q0, magic, sel)));
-        const float2 fb = make_float2(__uint_as_float(__byte_perm(p1, magic, sel)), __uint_as_float(__byte_perm(q1, magic, sel)));
-        H[c] = __ffma2_rn(wx, __ffma2_rn(fa, f2(-1.f), fb), __fadd2_rn(fa, f2(-8388608.f)));
-      }
-    };
-    const bool vec = (OW & 1) == 0 && kp.out_vec;  // pixel pairs 8-B (f32) / 4-B (f16) aligned
-    auto store = [&](OutT* o, const float2 (&T)[3], const float2 (&B)[3], float2 wy2, int x) {
-      float2 v[3];
+        for (int e = 0; e < 2; ++e) {
+          const int4 tx = e == 0 ? txa : txb;
+          const float2 wx = make_float2(__int_as_float(tx.z), __int_as_float(tx.w));
+          const uint32_t p0 = lds_u32(base + tx.x), p1 = lds_u32(base + tx.x + 4);
+          const uint32_t q0 = lds_u32(base + tx.y), q1 = lds_u32(base + tx.y + 4);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float2 vv = __ffma2_rn(wy2, __ffma2_rn(T[c], f2(-1.f), B[c]), T[c]);
-        v[c] = __ffma2_rn(vv, c == 0 ? na0 : c == 1 ? na1 : na2, c == 0 ? nb0 : c == 1 ? nb1 : nb2);
-      }
-      if (vec) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if constexpr (F16) {
-            const __half2 h = __floats2half2_rn(v[c].x, v[c].y);
-            __stcs(reinterpret_cast<uint32_t*>(o + c * plane), *reinterpret_cast<const uint32_t*>(&h));
-          } else {
-            __stcs(reinterpret_cast<float2*>(o + c * plane), v[c]);
+          for (int c = 0; c < 3; ++c) {
+            const int sel = 0x7540 + c;
+            const float2 fa = make_float2(__uint_as_float(__byte_perm(p0, magic, sel)), __uint_as_float(__byte_perm(q0, magic, sel)));
+            const float2 fb = make_float2(__uint_as_float(__byte_perm(p1, magic, sel)), __uint_as_float(__byte_perm(q1, magic, sel)));
+            H[c][e] = __ffma2_rn(wx, __ffma2_rn(fa, f2(-1.f), fb), __fadd2_rn(fa, f2(-8388608.f)));
           }
         }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if constexpr (F16) {
-            o[c * plane] = __float2half_rn(v[c].x);
-            if (x + 1 < OW) o[1 + c * plane] = __float2half_rn(v[c].y);
-          } else {
-            o[c * plane] = v[c].x;
-            if (x + 1 < OW) o[1 + c * plane] = v[c].y;
-          }
-        }
-      }
-    };
-    int c0 = -1, c1 = -1;                         // source rows of T and B (uniform over the warp)
-    const bool has0 = lane < npair;
+      };
+      int c0 = -1, c1 = -1;                       // source rows of T and B
+      OutT* o = outn + (uint32_t)ra * OW + ox;    // walks down the run
 #pragma unroll 1
-    for (int oy = 0; oy < OH; ++oy) {
-      const int2 ty = S.yt[oy];
-      const int i0 = ty.x & 0xffff, i1 = ty.x >> 16;
-      if (i0 != c0 || i1 != c1) {
-        if (i0 == c1) {
+      for (int oy = ra; oy < rb; ++oy, o += OW) {
+        const int2 ty = S.yt[oy];
+        const int i0 = ty.x & 0xffff, i1 = ty.x >> 16;
+        if (i0 != c0 || i1 != c1) {
+          if (i0 == c1) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) { T0[c] = B0[c]; T1[c] = B1[c]; }
-        } else {
-          hlerp(i0, tx0, T0);
-          if (has1) hlerp(i0, tx1, T1);
+            for (int c = 0; c < 3; ++c) { T[c][0] = B[c][0]; T[c][1] = B[c][1]; }
+          } else {
+            hlerp(i0, T);
+          }
+          hlerp(i1, B);
+          c0 = i0; c1 = i1;
         }
-        hlerp(i1, tx0, B0);
-        if (has1) hlerp(i1, tx1, B1);
-        c0 = i0; c1 = i1;
+        const float2 wy2 = f2(__int_as_float(ty.y));
+        float v[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float2 vv = __ffma2_rn(wy2, __ffma2_rn(T[c][e], f2(-1.f), B[c][e]), T[c][e]);
+            const float2 yn = __ffma2_rn(vv, c == 0 ? na0 : c == 1 ? na1 : na2, c == 0 ? nb0 : c == 1 ? nb1 : nb2);
+            v[c][2 * e] = yn.x;
+            v[c][2 * e + 1] = yn.y;
+          }
+        if ((OW & 3) == 0 && kp.out_vec) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if constexpr (F16) {
+              const __half2 h0 = __floats2half2_rn(v[c][0], v[c][1]), h1 = __floats2half2_rn(v[c][2], v[c][3]);
+              uint2 u;
+              u.x = *reinterpret_cast<const uint32_t*>(&h0);
+              u.y = *reinterpret_cast<const uint32_t*>(&h1);
+              __stcs(reinterpret_cast<uint2*>(o + c * plane), u);
+            } else {
+              __stcs(reinterpret_cast<float4*>(o + c * plane), make_float4(v[c][0], v[c][1], v[c][2], v[c][3]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (ox + e >= OW) break;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              if constexpr (F16) o[e + c * plane] = __float2half_rn(v[c][e]);
+              else o[e + c * plane] = v[c][e];
+            }
+          }
+        }
       }
-      const float2 wy2 = f2(__int_as_float(ty.y));
-      OutT* const orow = outn + (uint32_t)oy * OW;
-      if (has0) store(orow + 2 * lane, T0, B0, wy2, 2 * lane);
-      if (has1) store(orow + 2 * (lane + 32), T1, B1, wy2, 2 * (lane + 32));
     }
     __syncwarp();                                 // smem reused by the warp's next image
   }
