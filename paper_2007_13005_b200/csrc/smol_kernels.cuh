@@ -19,6 +19,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 #include <type_traits>
+#include <cstddef>
 
 #include "smol_geom.cuh"
 
@@ -537,17 +538,29 @@ __device__ __forceinline__ void smol_tile(const KParams& kp, const int n, const 
   __shared__ DevImage im;
   __shared__ TileLayout L;
   __shared__ int ctr[2];                   // dynamic work counter of the output phase (ctr[1])
-  if (tid == 0) {
-    const DevRef r = kp.refs[n];
-    im = kp.kinds[r.kind];
-    im.coef[0] = r.coef[0]; im.coef[1] = r.coef[1]; im.coef[2] = r.coef[2];
-    // the tile's layout: precomputed by the host per (image kind, tile), or
-    // computed here when the table did not fit
-    if (kp.lays) L = kp.lays[r.kind * kp.lay_stride + lay_local];
-    else tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP, GC);
-    ctr[1] = 0;
+  // the image's descriptor (its kind, with the coefficient pointers of its
+  // reference: the first 6 words of both) and the tile's layout, precomputed
+  // by the host per (image kind, tile): copied in by all threads, a word each
+  {
+    static_assert(offsetof(DevImage, coef) == 0 && offsetof(DevRef, coef) == 0, "coef pointers lead both");
+    static_assert(sizeof(DevImage) % 4 == 0 && sizeof(TileLayout) % 4 == 0, "word copies");
+    const int kind = kp.refs[n].kind;
+    const uint32_t* sr = reinterpret_cast<const uint32_t*>(kp.refs + n);
+    const uint32_t* sk = reinterpret_cast<const uint32_t*>(kp.kinds + kind);
+    uint32_t* di = reinterpret_cast<uint32_t*>(&im);
+    for (int i = tid; i < (int)(sizeof(DevImage) / 4); i += kThreads) di[i] = i < 6 ? __ldg(sr + i) : __ldg(sk + i);
+    if (kp.lays) {
+      const uint32_t* sl = reinterpret_cast<const uint32_t*>(kp.lays + kind * kp.lay_stride + lay_local);
+      uint32_t* dl = reinterpret_cast<uint32_t*>(&L);
+      for (int i = tid; i < (int)(sizeof(TileLayout) / 4); i += kThreads) dl[i] = __ldg(sl + i);
+    }
+    if (tid == 0) ctr[1] = 0;
   }
   __syncthreads();
+  if (!kp.lays) {                          // (uniform) the table did not fit: computed here
+    if (tid == 0) tile_layout(im, K, oy0, oy1, ox0, ox1, L, kYP, GC);
+    __syncthreads();
+  }
   // chroma rings: 4:2:0 kernels (GC = false) keep 16 rows of half-width
   // chroma; generic-chroma kernels 32 rows of full width (4:2:2, 4:4:4)
   constexpr int kCP = c_pitch(kYP, GC);     // chroma ring pitch
